@@ -1,0 +1,866 @@
+// sm_100a kernels of the ASADMM iteration loop.
+//
+// Data layout in HBM:
+//   * A_q        complex64, column-major, leading dimension ld_q =
+//                roundup(rows_q, 64) (zero-padded rows), so every pixel's
+//                column is a 512-B aligned contiguous run.  Never moved:
+//                elimination compacts the index list J_q instead and every
+//                matvec streams only the active columns A(:, J_q).
+//   * G_q        complex128 inverse of the rows x rows capacitance
+//                beta I + mu A_J A_J^H (dual form) or of the N_q x N_q
+//                Gram mu A_J^H A_J + beta I (primal form), column-major.
+//   * solver state (x_full, x_hat, rhs, data, s, x_G, sigma, gap) complex128;
+//     screening ring of |x_k - x_{k-1}|, W x N doubles per sensor.
+// Arithmetic: A is promoted to fp64 in registers; all products and sums are
+// fp64 (the fp64 oracle sees the very same complex64 operator values).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace radmm_dev {
+
+constexpr int kWarp = 32;
+constexpr int kMaxBatch = 64;
+
+// Per-sensor job descriptors travel as __grid_constant__ kernel parameters
+// (no device-side descriptor arrays, no extra copies per launch).
+template <typename T>
+struct Pack {
+  T j[kMaxBatch];
+};
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_scale(double2 a, double s) {
+  return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s));
+}
+__device__ __forceinline__ double c_abs(double2 a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ double c_norm2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// acc += conj(a) * v  (4 DFMA)
+__device__ __forceinline__ void cfma_conj(double& re, double& im, double ar, double ai, double2 v) {
+  re = fma(ar, v.x, re);
+  re = fma(ai, v.y, re);
+  im = fma(ar, v.y, im);
+  im = fma(-ai, v.x, im);
+}
+// acc += a * c  (4 DFMA)
+__device__ __forceinline__ void cfma(double& re, double& im, double ar, double ai, double2 c) {
+  re = fma(ar, c.x, re);
+  re = fma(-ai, c.y, re);
+  im = fma(ar, c.y, im);
+  im = fma(ai, c.x, im);
+}
+
+// ---------------------------------------------------------------------------
+// Column-dot kernel: out_i = sum_r conj(M[r, col_i]) * vec[r] for the active
+// columns, with a per-use epilogue.  One warp per column: each lane streams
+// 16-B vector loads down the contiguous column, the vector sits in shared
+// memory, and the warp reduces with shuffles.  Used for
+//   * the adjoint matvec A_J^H w fused with the x-update (EPI_XDUAL),
+//   * the capacitance/Gram-inverse apply G v (EPI_STORE, G Hermitian),
+//   * the primal x-update Hinv rhs (EPI_XPRIMAL),
+//   * the data term mu A_J^H y_eff on rebuild (EPI_STORE, scale mu).
+// ---------------------------------------------------------------------------
+enum { EPI_STORE = 0, EPI_XDUAL = 1, EPI_XPRIMAL = 2 };
+
+struct ColDotJob {
+  const void* M;       // float2* (A) or double2* (G / Hinv)
+  int64_t ld;          // leading dimension in complex elements (multiple of 64 / 32)
+  int len;             // rows participating (<= ld); vec is zero-padded to ld
+  int n_out;           // number of output columns
+  const int* cols;     // matrix column of output i (nullptr: identity)
+  const int* pix;      // pixel index of output i for the x-update epilogue
+  const double2* vec;  // input vector (len entries)
+  double2* out;        // EPI_STORE destination
+  double scale;        // EPI_STORE scale
+  const double2* rhs;  // EPI_XDUAL: rhs_i
+  double2* x_hat;      // x-update outputs (compacted)
+  double2* x_full;     // x-update scatter target (N)
+  double* ring_slot;   // screening ring row for this update (N doubles)
+};
+
+template <typename T>
+struct ColLoad;
+
+template <>
+struct ColLoad<float2> {
+  // a lane covers 2 complex per step; a warp 64 rows.
+  static constexpr int kRowsPerStep = 64;
+  __device__ static __forceinline__ void dot(const void* base, int64_t ld, int col, int steps,
+                                             const double2* __restrict__ sv, int lane,
+                                             double& re, double& im) {
+    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(base) + (int64_t)col * ld) + lane;
+    double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
+    const double2* v = sv + 2 * lane;
+    int s = 0;
+#pragma unroll 1
+    for (; s + 4 <= steps; s += 4) {
+      float4 a0 = __ldg(p + (s + 0) * 32);
+      float4 a1 = __ldg(p + (s + 1) * 32);
+      float4 a2 = __ldg(p + (s + 2) * 32);
+      float4 a3 = __ldg(p + (s + 3) * 32);
+      cfma_conj(r0, i0, a0.x, a0.y, v[(s + 0) * 64]);
+      cfma_conj(r1, i1, a0.z, a0.w, v[(s + 0) * 64 + 1]);
+      cfma_conj(r0, i0, a1.x, a1.y, v[(s + 1) * 64]);
+      cfma_conj(r1, i1, a1.z, a1.w, v[(s + 1) * 64 + 1]);
+      cfma_conj(r0, i0, a2.x, a2.y, v[(s + 2) * 64]);
+      cfma_conj(r1, i1, a2.z, a2.w, v[(s + 2) * 64 + 1]);
+      cfma_conj(r0, i0, a3.x, a3.y, v[(s + 3) * 64]);
+      cfma_conj(r1, i1, a3.z, a3.w, v[(s + 3) * 64 + 1]);
+    }
+    for (; s < steps; ++s) {
+      float4 a0 = __ldg(p + s * 32);
+      cfma_conj(r0, i0, a0.x, a0.y, v[s * 64]);
+      cfma_conj(r1, i1, a0.z, a0.w, v[s * 64 + 1]);
+    }
+    re = r0 + r1;
+    im = i0 + i1;
+  }
+};
+
+template <>
+struct ColLoad<double2> {
+  static constexpr int kRowsPerStep = 32;
+  __device__ static __forceinline__ void dot(const void* base, int64_t ld, int col, int steps,
+                                             const double2* __restrict__ sv, int lane,
+                                             double& re, double& im) {
+    const double2* p = reinterpret_cast<const double2*>(base) + (int64_t)col * ld + lane;
+    double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
+    const double2* v = sv + lane;
+    int s = 0;
+#pragma unroll 1
+    for (; s + 4 <= steps; s += 4) {
+      double2 a0 = __ldg(p + (s + 0) * 32);
+      double2 a1 = __ldg(p + (s + 1) * 32);
+      double2 a2 = __ldg(p + (s + 2) * 32);
+      double2 a3 = __ldg(p + (s + 3) * 32);
+      cfma_conj(r0, i0, a0.x, a0.y, v[(s + 0) * 32]);
+      cfma_conj(r1, i1, a1.x, a1.y, v[(s + 1) * 32]);
+      cfma_conj(r0, i0, a2.x, a2.y, v[(s + 2) * 32]);
+      cfma_conj(r1, i1, a3.x, a3.y, v[(s + 3) * 32]);
+    }
+    for (; s < steps; ++s) {
+      double2 a0 = __ldg(p + s * 32);
+      cfma_conj(r0, i0, a0.x, a0.y, v[s * 32]);
+    }
+    re = r0 + r1;
+    im = i0 + i1;
+  }
+};
+
+template <typename T, int EPI>
+__global__ void __launch_bounds__(256) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
+  extern __shared__ double2 sv[];
+  const ColDotJob& jb = jobs.j[blockIdx.y];
+  const int n_out = jb.n_out;
+  if ((int)blockIdx.x * 8 >= n_out) return;
+  const int64_t ld = jb.ld;
+  for (int r = threadIdx.x; r < ld; r += blockDim.x) sv[r] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int steps = (int)((jb.len + ColLoad<T>::kRowsPerStep - 1) / ColLoad<T>::kRowsPerStep);
+  for (int i = blockIdx.x * 8 + warp; i < n_out; i += gridDim.x * 8) {
+    const int col = jb.cols ? jb.cols[i] : i;
+    double re, im;
+    ColLoad<T>::dot(jb.M, ld, col, steps, sv, lane, re, im);
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) {
+      if (EPI == EPI_STORE) {
+        jb.out[i] = make_double2(__dmul_rn(jb.scale, re), __dmul_rn(jb.scale, im));
+      } else {
+        double2 xh;
+        if (EPI == EPI_XDUAL) {
+          // x = (rhs - mu * A^H w) / beta  (Woodbury form of solver_core.hpp:47-51)
+          const double2 r = jb.rhs[i];
+          xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re)), beta),
+                            __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im)), beta));
+        } else {
+          xh = make_double2(re, im);
+        }
+        const int p = jb.pix[i];
+        const double2 old = jb.x_full[p];
+        jb.ring_slot[p] = c_abs(c_sub(xh, old));  // |hist[h][j] - hist[h-1][j]| (admm.hpp:143)
+        jb.x_full[p] = xh;                        // admm.hpp:121-122
+        jb.x_hat[i] = xh;                         // admm.hpp:120
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward kernel: v = sum_i A[:, J_i] * coef_i over a chunk of active columns
+// (rows in 512-row tiles, 2 complex per thread via float4), with the
+// coefficient prologue fused:
+//   MODE_RHS:    coef_i = data_i + beta gap[J_i] + beta x_hat_i - sigma[J_i]
+//                (rhs of admm.hpp:114-119, also written out for the x-update)
+//   MODE_GATHER: coef_i = src[J_i]  (frozen-echo update of y_eff, admm.hpp:174-176)
+// Partial sums per chunk are reduced by reduce_parts_kernel in fixed order.
+// ---------------------------------------------------------------------------
+enum { MODE_RHS = 0, MODE_GATHER = 1 };
+
+struct FwdJob {
+  const float2* A;
+  int64_t ld;
+  int n;               // columns in the list
+  const int* J;        // column (pixel) list
+  const double2* data; // MODE_RHS
+  const double2* x_hat;
+  double2* rhs_out;
+  const double2* src;  // MODE_GATHER
+  double2* part;       // [n_chunks][ld]
+  int n_chunks;
+  int chunk_len;
+};
+
+constexpr int kFwdThreads = 256;
+constexpr int kFwdTile = 2 * kFwdThreads;
+
+template <int MODE>
+__global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant__ Pack<FwdJob> jobs,
+                                                          const double2* __restrict__ gap,
+                                                          const double2* __restrict__ sigma, double beta) {
+  extern __shared__ unsigned char smem_raw[];
+  const FwdJob& jb = jobs.j[blockIdx.z];
+  const int chunk = blockIdx.x;
+  if (chunk >= jb.n_chunks) return;
+  const int64_t row0 = (int64_t)blockIdx.y * kFwdTile;
+  if (row0 >= jb.ld) return;
+  const int i0 = chunk * jb.chunk_len;
+  const int cnt = min(jb.chunk_len, jb.n - i0);
+  double2* coef = reinterpret_cast<double2*>(smem_raw);
+  int* cidx = reinterpret_cast<int*>(coef + jb.chunk_len);
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const int i = i0 + t;
+    const int c = jb.J[i];
+    double2 v;
+    if (MODE == MODE_RHS) {
+      const double2 d = jb.data[i], g = gap[c], xh = jb.x_hat[i], sg = sigma[c];
+      v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+      v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+      if (blockIdx.y == 0) jb.rhs_out[i] = v;
+    } else {
+      v = jb.src[c];
+    }
+    coef[t] = v;
+    cidx[t] = c;
+  }
+  __syncthreads();
+  const int64_t r = row0 + 2 * threadIdx.x;
+  double a0r = 0, a0i = 0, a1r = 0, a1i = 0;
+  double b0r = 0, b0i = 0, b1r = 0, b1i = 0;
+  if (r < jb.ld) {
+    const float2* A = jb.A + r;
+    int t = 0;
+#pragma unroll 1
+    for (; t + 4 <= cnt; t += 4) {
+      const float4 x0 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 0] * jb.ld));
+      const float4 x1 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 1] * jb.ld));
+      const float4 x2 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 2] * jb.ld));
+      const float4 x3 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 3] * jb.ld));
+      const double2 c0 = coef[t + 0], c1 = coef[t + 1], c2 = coef[t + 2], c3 = coef[t + 3];
+      cfma(a0r, a0i, x0.x, x0.y, c0); cfma(a1r, a1i, x0.z, x0.w, c0);
+      cfma(b0r, b0i, x1.x, x1.y, c1); cfma(b1r, b1i, x1.z, x1.w, c1);
+      cfma(a0r, a0i, x2.x, x2.y, c2); cfma(a1r, a1i, x2.z, x2.w, c2);
+      cfma(b0r, b0i, x3.x, x3.y, c3); cfma(b1r, b1i, x3.z, x3.w, c3);
+    }
+    for (; t < cnt; ++t) {
+      const float4 x0 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t] * jb.ld));
+      const double2 c0 = coef[t];
+      cfma(a0r, a0i, x0.x, x0.y, c0); cfma(a1r, a1i, x0.z, x0.w, c0);
+    }
+    double2* out = jb.part + (int64_t)chunk * jb.ld + r;
+    out[0] = make_double2(a0r + b0r, a0i + b0i);
+    out[1] = make_double2(a1r + b1r, a1i + b1i);
+  }
+}
+
+// out[r] = base[r] + sign * sum_c part[c][r]   (fixed chunk order)
+struct ReduceJob {
+  const double2* part;
+  int n_chunks;
+  int64_t ld;
+  int len;
+  const double2* base;  // may be nullptr
+  double2* out;
+  double sign;
+};
+
+__global__ void reduce_parts_kernel(const __grid_constant__ Pack<ReduceJob> jobs) {
+  const ReduceJob& jb = jobs.j[blockIdx.y];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= jb.ld) return;
+  double sr = 0, si = 0;
+  if (r < jb.len) {
+    for (int c = 0; c < jb.n_chunks; ++c) {
+      const double2 v = jb.part[(int64_t)c * jb.ld + r];
+      sr += v.x;
+      si += v.y;
+    }
+  }
+  double2 o;
+  if (jb.base) {
+    const double2 b = (r < jb.len) ? jb.base[r] : make_double2(0, 0);
+    o = make_double2(b.x + jb.sign * sr, b.y + jb.sign * si);
+  } else {
+    o = make_double2(jb.sign * sr, jb.sign * si);
+  }
+  jb.out[r] = (r < jb.len) ? o : make_double2(0, 0);
+}
+
+// rhs_i = data_i + beta gap[J_i] + beta x_hat_i - sigma[J_i] (primal sensors)
+struct RhsJob {
+  int n;
+  const int* J;
+  const double2* data;
+  const double2* x_hat;
+  double2* rhs;
+};
+
+__global__ void rhs_kernel(const __grid_constant__ Pack<RhsJob> jobs, const double2* __restrict__ gap,
+                           const double2* __restrict__ sigma, double beta) {
+  const RhsJob& jb = jobs.j[blockIdx.y];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= jb.n) return;
+  const int c = jb.J[i];
+  const double2 d = jb.data[i], g = gap[c], xh = jb.x_hat[i], sg = sigma[c];
+  double2 v;
+  v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+  v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+  jb.rhs[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Fusion: FusionCore::round (admm.hpp:236-258) for N pixels, then the five
+// squared norms reduced deterministically (per-block partials, last block
+// sums them in fixed order) and the stopping rule evaluated on the device.
+// ---------------------------------------------------------------------------
+struct FusionScalars {
+  double pri_res, dual_res, eps_pri, eps_dual;
+  double sq[5];
+  int trigger, converged;
+  int iteration;
+  int pad;
+};
+
+struct FusionArgs {
+  const double2* const* contrib;  // Q sensor images x_q (mirror == x_full)
+  int Q;
+  int N;
+  double2* s;
+  double2* xg;
+  double2* sigma;
+  double2* sigma_pre;
+  double2* gap;
+  double beta, kappa;
+  double root_n_eps_abs, eps_rel;
+  int has_prev;
+  int iteration;
+  double* partials;        // [gridDim.x * 5]
+  unsigned int* counter;
+  FusionScalars* out_dev;
+  FusionScalars* out_host; // mapped pinned memory
+};
+
+constexpr int kFusionThreads = 256;
+
+__device__ __forceinline__ double2 soft_threshold1(double2 v, double kappa) {
+  const double mag = c_abs(v);  // std::abs(complex) (solver_core.hpp:18)
+  if (mag > kappa) {
+    const double f = __dsub_rn(1.0, __ddiv_rn(kappa, mag));
+    return make_double2(__dmul_rn(v.x, f), __dmul_rn(v.y, f));
+  }
+  return make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
+  __shared__ double red[5][kFusionThreads / 32];
+  __shared__ bool last;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double q[5] = {0, 0, 0, 0, 0};
+  if (j < a.N) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < a.Q; ++k) s = c_add(s, a.contrib[k][j]);  // fixed sensor order
+    s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
+    const double2 xgp = a.xg[j];
+    const double2 sg = a.sigma[j];
+    a.sigma_pre[j] = sg;
+    const double2 v = make_double2(__dadd_rn(s.x, __ddiv_rn(sg.x, a.beta)), __dadd_rn(s.y, __ddiv_rn(sg.y, a.beta)));
+    const double2 xg = soft_threshold1(v, a.kappa);
+    const double2 eta = c_sub(s, xg);
+    const double2 dx = c_sub(xg, xgp);
+    const double2 sn = make_double2(__dadd_rn(sg.x, __dmul_rn(a.beta, eta.x)), __dadd_rn(sg.y, __dmul_rn(a.beta, eta.y)));
+    a.s[j] = s;
+    a.xg[j] = xg;
+    a.sigma[j] = sn;
+    a.gap[j] = c_sub(xg, s);
+    q[0] = c_norm2(eta);
+    q[1] = c_norm2(dx);
+    q[2] = c_norm2(s);
+    q[3] = c_norm2(xg);
+    q[4] = c_norm2(sn);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const double w = warp_sum(q[t]);
+    if (lane == 0) red[t][warp] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double acc = 0;
+    for (int w = 0; w < kFusionThreads / 32; ++w) acc += red[threadIdx.x][w];
+    a.partials[blockIdx.x * 5 + threadIdx.x] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 5) {
+    double acc = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) acc += ((volatile double*)a.partials)[b * 5 + threadIdx.x];
+    red[threadIdx.x][0] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FusionScalars f;
+    for (int t = 0; t < 5; ++t) f.sq[t] = red[t][0];
+    f.pri_res = sqrt(f.sq[0]);
+    f.dual_res = a.beta * sqrt(f.sq[1]);
+    f.eps_pri = a.root_n_eps_abs + a.eps_rel * fmax(sqrt(f.sq[2]), sqrt(f.sq[3]));
+    f.eps_dual = a.root_n_eps_abs + a.eps_rel * sqrt(f.sq[4]);
+    f.trigger = f.pri_res <= f.eps_pri;
+    f.converged = a.has_prev && f.trigger && f.dual_res <= f.eps_dual;
+    f.iteration = a.iteration;
+    f.pad = 0;
+    *a.out_dev = f;
+    if (a.out_host) {
+      volatile FusionScalars* h = a.out_host;
+      h->pri_res = f.pri_res; h->dual_res = f.dual_res; h->eps_pri = f.eps_pri; h->eps_dual = f.eps_dual;
+      for (int t = 0; t < 5; ++t) h->sq[t] = f.sq[t];
+      h->trigger = f.trigger; h->converged = f.converged;
+      __threadfence_system();
+      h->iteration = f.iteration;
+    }
+    *a.counter = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Screening (SensorCore::screen, admm.hpp:134-159) as a warp-ballot /
+// prefix-sum stream compaction of the active list.
+//   zeta_i = (1/W) sum_{t=0}^{W-1} ring[(upd-W+t) mod W][J_i]  (oldest first)
+//   keep   = zeta_i >= tol
+// ---------------------------------------------------------------------------
+constexpr int kScanBlock = 1024;
+
+struct ScreenJob {
+  int n;
+  const int* J;
+  const double* ring;     // W x N
+  int64_t ring_stride;    // N
+  int first_slot;         // (upd - W) mod W
+  unsigned char* keep;    // n flags
+  int* block_counts;      // ceil(n / kScanBlock)
+  int* block_offsets;
+  int* totals;            // [0] = kept
+  int* Jnew;
+  int* keep_pos;          // old compacted index of kept entry
+  int* rem_pix;           // removed pixel indices (in order)
+  int* rem_pos;           // removed old compacted positions
+  const double2* x_hat;
+  double2* x_hat_new;
+};
+
+__global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int W, double tol) {
+  const ScreenJob& jb = jobs.j[blockIdx.y];
+  __shared__ int wc[kScanBlock / 32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  if ((int)blockIdx.x * kScanBlock >= jb.n) return;
+  bool k = false;
+  if (i < jb.n) {
+    const int c = jb.J[i];
+    double z = 0.0;
+    for (int t = 0; t < W; ++t) {
+      const int slot = (jb.first_slot + t) % W;
+      z += jb.ring[(int64_t)slot * jb.ring_stride + c];
+    }
+    z = z / (double)W;
+    k = z >= tol;
+    jb.keep[i] = k ? 1 : 0;
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, k);
+  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) s += wc[w];
+    jb.block_counts[blockIdx.x] = s;
+  }
+}
+
+__global__ void screen_scan_kernel(const __grid_constant__ Pack<ScreenJob> jobs) {
+  const ScreenJob& jb = jobs.j[blockIdx.x];
+  if (threadIdx.x != 0) return;
+  const int nb = (jb.n + kScanBlock - 1) / kScanBlock;
+  int s = 0;
+  for (int b = 0; b < nb; ++b) {
+    jb.block_offsets[b] = s;
+    s += jb.block_counts[b];
+  }
+  jb.totals[0] = s;
+}
+
+__global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid_constant__ Pack<ScreenJob> jobs) {
+  const ScreenJob& jb = jobs.j[blockIdx.y];
+  __shared__ int woff[kScanBlock / 32];
+  if ((int)blockIdx.x * kScanBlock >= jb.n) return;
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const bool valid = i < jb.n;
+  const bool k = valid && jb.keep[i];
+  const unsigned b = __ballot_sync(0xffffffffu, k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) woff[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) {
+      const int c = woff[w];
+      woff[w] = s;
+      s += c;
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  const int kept_before = jb.block_offsets[blockIdx.x] + woff[warp] + __popc(b & ((1u << lane) - 1u));
+  if (k) {
+    jb.Jnew[kept_before] = jb.J[i];
+    jb.keep_pos[kept_before] = i;
+    jb.x_hat_new[kept_before] = jb.x_hat[i];  // x_full[J_new] (admm.hpp:153-156)
+  } else {
+    const int rpos = i - kept_before;
+    jb.rem_pix[rpos] = jb.J[i];
+    jb.rem_pos[rpos] = i;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 complex GEMM, SIMT tiles (64 x 64 x 8, 256 threads, 4 x 4 per thread):
+//   C = alpha * op(A) op(B) + beta0 * C  (+ diag) with gathered operands.
+// op(M)(i, k): (r, c) = trans ? (k, i) : (i, k); r = ridx ? ridx[r] : r;
+// c = cidx ? cidx[c] : c; value M[r + c*ld] (complex64 promoted or
+// complex128), conjugated if conj.  Drives the factor builds and
+// downdates of LocalSolveCache (solver_core.hpp:34-45) and the
+// Gauss-Jordan inverse.
+// ---------------------------------------------------------------------------
+struct MatRef {
+  const void* p;
+  int64_t ld;
+  const int* ridx;
+  const int* cidx;
+  int c64;
+  int trans;
+  int conj;
+};
+
+enum { GEPI_PLAIN = 0, GEPI_GJ = 1 };
+
+struct GemmJob {
+  int m, n, k;
+  MatRef a, b;
+  double2* c;
+  int64_t ldc;
+  double alpha, beta0;
+  double diag_add;  // C[i,i] += diag_add
+  int k0, kb;       // GEPI_GJ: pivot block rows/cols [k0, k0+kb); b = R' (kb x n)
+};
+
+__device__ __forceinline__ double2 mat_load(const MatRef& m, int i, int k) {
+  int r = m.trans ? k : i;
+  int c = m.trans ? i : k;
+  if (m.ridx) r = m.ridx[r];
+  if (m.cidx) c = m.cidx[c];
+  double2 v;
+  if (m.c64) {
+    const float2 f = reinterpret_cast<const float2*>(m.p)[r + (int64_t)c * m.ld];
+    v = make_double2((double)f.x, (double)f.y);
+  } else {
+    v = reinterpret_cast<const double2*>(m.p)[r + (int64_t)c * m.ld];
+  }
+  if (m.conj) v.y = -v.y;
+  return v;
+}
+
+constexpr int kGB = 64, kGK = 8;
+constexpr int kGjSmem = (64 * 65 + 128) * 16;
+
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  const GemmJob& jb = jobs.j[blockIdx.z];
+  const int m0 = blockIdx.y * kGB, n0 = blockIdx.x * kGB;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  __shared__ double2 As[2][kGK][kGB];
+  __shared__ double2 Bs[2][kGK][kGB];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc_r[4][4], acc_i[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc_r[a][b] = acc_i[a][b] = 0.0;
+
+  const MatRef A = jb.a, B = jb.b;
+  auto load_tile = [&](int buf, int kk0) {
+    // A tile: kGB (i) x kGK (k)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int e = tid + t * 256;
+      int ii, kk;
+      if (!A.trans) { ii = e & 63; kk = e >> 6; } else { kk = e & 7; ii = e >> 3; }
+      const int gi = m0 + ii, gk = kk0 + kk;
+      As[buf][kk][ii] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+    // B tile: kGK (k) x kGB (j)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int e = tid + t * 256;
+      int kk, jj;
+      if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e & 63; kk = e >> 6; }
+      const int gj = n0 + jj, gk = kk0 + kk;
+      Bs[buf][kk][jj] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+
+  const int nk = (jb.k + kGK - 1) / kGK;
+  if (nk > 0) load_tile(0, 0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) load_tile(cur ^ 1, (t + 1) * kGK);
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[cur][kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[cur][kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          acc_r[a][b] = fma(av[a].x, bv[b].x, acc_r[a][b]);
+          acc_r[a][b] = fma(-av[a].y, bv[b].y, acc_r[a][b]);
+          acc_i[a][b] = fma(av[a].x, bv[b].y, acc_i[a][b]);
+          acc_i[a][b] = fma(av[a].y, bv[b].x, acc_i[a][b]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = m0 + ty + 16 * a;
+    if (i >= jb.m) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = n0 + tx + 16 * b;
+      if (j >= jb.n) continue;
+      double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+      if (EPI == GEPI_PLAIN) {
+        double2 o = make_double2(jb.alpha * acc_r[a][b], jb.alpha * acc_i[a][b]);
+        if (jb.beta0 != 0.0) {
+          const double2 c0 = *cp;
+          o.x += jb.beta0 * c0.x;
+          o.y += jb.beta0 * c0.y;
+        }
+        if (i == j) o.x += jb.diag_add;
+        *cp = o;
+      } else {
+        // Gauss-Jordan sweep of pivot block K = [k0, k0+kb):
+        //   i in K:      M[i,j] = R'[i-k0, j]
+        //   i not in K:  M[i,j] = (j in K ? 0 : M[i,j]) - (F R')[i,j]
+        const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+        if (iK) {
+          *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+        } else {
+          const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+          const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+          *cp = make_double2(c0.x - acc_r[a][b], c0.y - acc_i[a][b]);
+        }
+      }
+    }
+  }
+}
+
+// In-place Gauss-Jordan inverse of one kb x kb HPD pivot block (kb <= 64)
+// in shared memory: writes P = inv(M_KK) to P (ld = ldp) and raises *fail
+// if a pivot is not a positive finite real (the Cholesky-failure analogue of
+// solver_core.hpp:42-43).
+struct DiagJob {
+  const double2* M;
+  int64_t ld;
+  int n;          // matrix order
+  int k0, kb;     // pivot block
+  double2* P;     // kb x kb, ld = ldp
+  int64_t ldp;
+  double2* F;     // copy of M[:, K] (n x kb), ld = ldf
+  int64_t ldf;
+  double2* R;     // row panel R' (kb x n), ld = ldr
+  int64_t ldr;
+  int* fail;
+};
+
+__global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.x];
+  if (jb.k0 >= jb.n) return;
+  extern __shared__ double2 gj_smem[];
+  double2 (*S)[65] = reinterpret_cast<double2 (*)[65]>(gj_smem);
+  double2* prow = gj_smem + 64 * 65;
+  double2* pcol = prow + 64;
+  const int kb = jb.kb;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e % kb, c = e / kb;
+    S[r][c] = jb.M[(jb.k0 + r) + (int64_t)(jb.k0 + c) * jb.ld];
+  }
+  __syncthreads();
+  for (int p = 0; p < kb; ++p) {
+    const double2 piv = S[p][p];
+    if (threadIdx.x == 0 && !(piv.x > 0.0 && isfinite(piv.x) && isfinite(piv.y))) atomicExch(jb.fail, 1);
+    const double den = piv.x * piv.x + piv.y * piv.y;
+    const double2 ip = make_double2(piv.x / den, -piv.y / den);
+    if (threadIdx.x < kb) {
+      const int c = threadIdx.x;
+      const double2 v = S[p][c];
+      prow[c] = (c == p) ? ip : make_double2(v.x * ip.x - v.y * ip.y, v.x * ip.y + v.y * ip.x);
+      pcol[c] = S[c][p];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+      const int r = e % kb, c = e / kb;
+      if (r == p) {
+        S[r][c] = prow[c];
+      } else {
+        const double2 f = pcol[r];
+        const double2 pr = prow[c];
+        const double2 base = (c == p) ? make_double2(0.0, 0.0) : S[r][c];
+        S[r][c] = make_double2(base.x - (f.x * pr.x - f.y * pr.y), base.y - (f.x * pr.y + f.y * pr.x));
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e % kb, c = e / kb;
+    jb.P[r + (int64_t)c * jb.ldp] = S[r][c];
+  }
+}
+
+// F = M[:, K] (pivot column panel), grid-stride over n*kb per job.
+__global__ void gj_panel_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.y];
+  if (jb.k0 >= jb.n) return;
+  const int64_t total = (int64_t)jb.n * jb.kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % jb.n), c = (int)(e / jb.n);
+    jb.F[r + (int64_t)c * jb.ldf] = jb.M[r + (int64_t)(jb.k0 + c) * jb.ld];
+  }
+}
+
+// R'[:, K] = P (overwrite the pivot columns of the row panel).
+__global__ void gj_fix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.x];
+  if (jb.k0 >= jb.n) return;
+  for (int e = threadIdx.x; e < jb.kb * jb.kb; e += blockDim.x) {
+    const int r = e % jb.kb, c = e / jb.kb;
+    jb.R[r + (int64_t)(jb.k0 + c) * jb.ldr] = jb.P[r + (int64_t)c * jb.ldp];
+  }
+}
+
+// out[i + j*ldo] = M[ridx[i] + cidx[j]*ld] (submatrix gather, grid-stride)
+struct SubJob {
+  const double2* M;
+  int64_t ld;
+  const int* ridx;
+  const int* cidx;
+  int m, n;
+  double2* out;
+  int64_t ldo;
+};
+
+__global__ void gather_sub_kernel(const __grid_constant__ Pack<SubJob> jobs) {
+  const SubJob& jb = jobs.j[blockIdx.y];
+  const int64_t total = (int64_t)jb.m * jb.n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % jb.m), j = (int)(e / jb.m);
+    jb.out[i + (int64_t)j * jb.ldo] = jb.M[jb.ridx[i] + (int64_t)jb.cidx[j] * jb.ld];
+  }
+}
+
+// Utility kernels -----------------------------------------------------------
+__global__ void c128_to_c64_kernel(const double2* __restrict__ src, int64_t lds, float2* __restrict__ dst,
+                                   int64_t ldd, int rows, int cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)rows * cols) return;
+  const int r = (int)(e % rows);
+  const int64_t c = e / rows;
+  const double2 v = src[r + c * lds];
+  dst[r + c * ldd] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+}
+
+__global__ void soft_threshold_kernel(const double2* __restrict__ v, int64_t n, double kappa, double2* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = soft_threshold1(v[i], kappa);
+}
+
+__global__ void abs_kernel(const double2* __restrict__ v, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = c_abs(v[i]);
+}
+
+__global__ void iota_kernel(int* __restrict__ J, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) J[i] = i;
+}
+
+// Gather x_full[J] -> x_hat (and zero a vector) etc.
+__global__ void gather_kernel(const double2* __restrict__ src, const int* __restrict__ idx, int n, double2* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+// BASELINE dechirped-LFM operator generator (mirrors scenario.baseline_operator
+// operation by operation, no FMA contraction).
+__global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K, int N,
+                               const double* __restrict__ pix, const double* __restrict__ tx,
+                               const double* __restrict__ rx, const double* __restrict__ phi,
+                               double alpha, double fc, double t_step, double c_light, double two_pi) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = M * K;
+  if (e >= (int64_t)rows * N) return;
+  const int r = (int)(e % rows);
+  const int n = (int)(e / rows);
+  const int m = r / K, k = r % K;
+  const double px = pix[3 * n], py = pix[3 * n + 1], pz = pix[3 * n + 2];
+  double dx = __dsub_rn(tx[0], px), dy = __dsub_rn(tx[1], py), dz = __dsub_rn(tx[2], pz);
+  const double dtx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  dx = __dsub_rn(rx[3 * m], px); dy = __dsub_rn(rx[3 * m + 1], py); dz = __dsub_rn(rx[3 * m + 2], pz);
+  const double drx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  const double tau = __ddiv_rn(__dadd_rn(dtx, drx), c_light);
+  const double tk = __dmul_rn((double)k, t_step);
+  double cyc = __dadd_rn(__dmul_rn(__dmul_rn(alpha, tau), tk), __dmul_rn(fc, tau));
+  cyc = __dsub_rn(cyc, floor(cyc));
+  const double ang = __dadd_rn(__dmul_rn(two_pi, cyc), phi[n]);
+  double s, c;
+  sincos(ang, &s, &c);
+  A[r + (int64_t)n * ld] = make_float2(__double2float_rn(c), __double2float_rn(s));
+}
+
+}  // namespace radmm_dev

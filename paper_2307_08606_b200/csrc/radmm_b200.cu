@@ -1,0 +1,1315 @@
+// Host runtime of the B200-native ASADMM iteration loop: owns device state,
+// drives the sm_100a kernels of kernels.cuh, and exports the C ABI declared
+// in include/radmm_b200.h.
+//
+// Reference mapping (paths under /root/reference/proj/include/radmm):
+//   radmm_run            <- run()                  admm.hpp:357-445
+//   Sensor::* state      <- SensorCore             admm.hpp:88-192
+//   fusion_kernel        <- FusionCore::round      admm.hpp:236-258
+//   refactor()/GJ        <- LocalSolveCache        solver_core.hpp:30-58
+//   screen_all()         <- SensorCore::screen     admm.hpp:134-159
+//   NCCL exchange        <- run_inproc/run_tcp gather+broadcast (runtime.hpp:362-766)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/radmm_b200.h"
+#include "kernels.cuh"
+
+using namespace radmm_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure : std::exception {
+  int code;
+  std::string msg;
+  Failure(int c, std::string m) : code(c), msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure(code, msg); }
+
+void check_cuda(cudaError_t e, const char* what, int line) {
+  if (e == cudaSuccess) return;
+  const int code = (e == cudaErrorMemoryAllocation) ? RADMM_OUT_OF_MEMORY : RADMM_CUDA;
+  fail(code, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " (radmm_b200.cu:" +
+                 std::to_string(line) + ")");
+}
+#define CK(x) check_cuda((x), #x, __LINE__)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RADMM_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return RADMM_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RADMM_CUDA;
+  }
+}
+
+template <typename T>
+struct DArr {
+  T* p = nullptr;
+  size_t n = 0;
+  DArr() = default;
+  DArr(const DArr&) = delete;
+  DArr& operator=(const DArr&) = delete;
+  DArr(DArr&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DArr& operator=(DArr&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DArr() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count, bool zero = true) {
+    release();
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+    if (zero) CK(cudaMemset(p, 0, count * sizeof(T)));
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+};
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (only sharded contexts need it).
+// ---------------------------------------------------------------------------
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm;
+struct Nccl {
+  void* h = nullptr;
+  int (*GetUniqueId)(nccl_uid*) = nullptr;
+  int (*CommInitRank)(nccl_comm*, int, nccl_uid, int) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(nccl_comm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  void load() {
+    if (h) return;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) fail(RADMM_TRANSPORT, "cannot load libnccl.so.2");
+    GetUniqueId = (int (*)(nccl_uid*))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+    AllGather = (int (*)(const void*, void*, size_t, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllGather");
+    CommDestroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy)
+      fail(RADMM_TRANSPORT, "libnccl is missing required symbols");
+  }
+  void check(int r, const char* what) {
+    if (r != 0)
+      fail(RADMM_TRANSPORT, std::string("NCCL error in ") + what + ": " +
+                                (GetErrorString ? GetErrorString(r) : std::to_string(r)));
+  }
+};
+Nccl g_nccl;
+constexpr int kNcclDouble = 8;  // ncclFloat64
+
+// ---------------------------------------------------------------------------
+// Device state
+// ---------------------------------------------------------------------------
+struct Sensor {
+  int rows = 0;
+  int64_t ld = 0;  // roundup(rows, 64)
+  bool has_op = false, has_y = false;
+  DArr<float2> A;
+  DArr<double2> y, y_eff;
+  // active set + SensorCore state
+  int n_act = 0;
+  bool primal = false;
+  bool stalled = false;
+  DArr<int> J, Jnew, keep_pos, rem_pix, rem_pos, blk_cnt, blk_off, totals;
+  DArr<unsigned char> keep;
+  DArr<double2> x_full, x_hat, x_hat_new, data, rhs;
+  DArr<double> ring;
+  // cached inverse of the capacitance (dual) or Gram (primal) matrix
+  DArr<double2> G, G2;
+  int64_t ldg = 0;
+  int g_n = 0;
+  // forward partials / KM-space vectors
+  DArr<double2> part, v, w;
+  int part_chunks = 0;  // capacity of part in chunks of ld
+  int removed_now = 0;
+};
+
+struct Scratch {
+  DArr<char> buf;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    const size_t bytes = round_up((int64_t)(count * sizeof(T)), 256);
+    if (off + bytes > buf.n) fail(RADMM_OUT_OF_MEMORY, "scratch arena exhausted");
+    T* p = reinterpret_cast<T*>(buf.p + off);
+    off += bytes;
+    return p;
+  }
+  void reserve(size_t bytes) {
+    if (bytes > buf.n) {
+      CK(cudaDeviceSynchronize());
+      buf.alloc(bytes, false);
+    }
+    off = 0;
+  }
+};
+
+}  // namespace
+
+struct radmm_ctx {
+  int device = 0;
+  int N = 0;
+  int Q = 0;        // local sensors
+  int Q_total = 0;
+  int q_begin = 0;
+  int rank = 0, world = 1;
+  int q_max_local = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::vector<Sensor> sensors;
+  DArr<double2> s, xg, sigma, sigma_pre, gap;
+  DArr<double> fpart;
+  DArr<unsigned int> fcounter;
+  DArr<FusionScalars> fs_dev;
+  FusionScalars* fs_host = nullptr;
+  FusionScalars* fs_host_dev = nullptr;
+  DArr<const double2*> contrib;
+  int* h_totals = nullptr;   // pinned, per local sensor
+  int* h_flags = nullptr;    // pinned, kMaxBatch
+  Scratch scratch;
+  DArr<int> fail_flags;
+  // sharded exchange
+  nccl_comm comm = nullptr;
+  DArr<double2> send_buf, gathered;
+  DArr<double> size_send, size_recv;
+  // results of the last run
+  std::vector<radmm_iteration_record> records;
+  std::vector<int32_t> active_log;
+  std::vector<int32_t> removal_log;
+  radmm_run_summary summary{};
+  bool have_result = false;
+  int64_t launches = 0;
+  int64_t rebuilds = 0, downdates = 0;
+  int W = 5;
+  int upd = 0;  // local updates performed in the current run
+
+  ~radmm_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+    if (fs_host) cudaFreeHost(fs_host);
+    if (h_totals) cudaFreeHost(h_totals);
+    if (h_flags) cudaFreeHost(h_flags);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+constexpr int kCtasPerSmTarget = 8;
+
+void set_device(radmm_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
+  c->device = device;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    fail(RADMM_CUDA, "radmm_b200 requires an sm_100 (Blackwell) GPU; found " + std::string(prop.name));
+  c->sm_count = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->N = n_pixels;
+  c->Q = q_local;
+  c->sensors.resize(q_local);
+  const int N = n_pixels;
+  c->s.alloc(N); c->xg.alloc(N); c->sigma.alloc(N); c->sigma_pre.alloc(N); c->gap.alloc(N);
+  const int fblocks = (N + kFusionThreads - 1) / kFusionThreads;
+  c->fpart.alloc((size_t)fblocks * 5);
+  c->fcounter.alloc(1);
+  c->fs_dev.alloc(1);
+  CK(cudaHostAlloc(&c->fs_host, sizeof(FusionScalars), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
+  CK(cudaHostAlloc(&c->h_totals, sizeof(int) * std::max(1, q_local), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&c->h_flags, sizeof(int) * kMaxBatch, cudaHostAllocDefault));
+  c->fail_flags.alloc(kMaxBatch);
+  for (int q = 0; q < q_local; ++q) {
+    Sensor& S = c->sensors[q];
+    S.J.alloc(N); S.Jnew.alloc(N); S.keep_pos.alloc(N); S.rem_pix.alloc(N); S.rem_pos.alloc(N);
+    S.keep.alloc(N);
+    const int nb = (N + kScanBlock - 1) / kScanBlock;
+    S.blk_cnt.alloc(nb); S.blk_off.alloc(nb); S.totals.alloc(1);
+    S.x_full.alloc(N); S.x_hat.alloc(N); S.x_hat_new.alloc(N); S.data.alloc(N); S.rhs.alloc(N);
+  }
+}
+
+Sensor& sensor_at(radmm_ctx* c, int q) {
+  if (!c) fail(RADMM_INVALID_ARGUMENT, "null context");
+  if (q < 0 || q >= c->Q) fail(RADMM_INVALID_ARGUMENT, "sensor index out of range");
+  return c->sensors[q];
+}
+
+void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
+  if (rows < 1) fail(RADMM_INVALID_ARGUMENT, "ForwardOperator: rows must be >= 1");
+  S.rows = rows;
+  S.ld = round_up(rows, 64);
+  S.A.alloc((size_t)S.ld * c->N);  // zero padding rows
+  S.y_eff.alloc(S.ld);
+  S.v.alloc(S.ld);
+  S.w.alloc(S.ld);
+  const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
+  S.part_chunks = std::max(1, c->sm_count * kCtasPerSmTarget / tiles) + 1;
+  S.part.alloc((size_t)S.part_chunks * S.ld, false);
+  S.has_op = true;
+  S.has_y = false;
+}
+
+#define LAUNCH(c, kern, grid, block, smem, ...)                              \
+  do {                                                                        \
+    kern<<<(grid), (block), (smem), (c)->stream>>>(__VA_ARGS__);              \
+    CK(cudaGetLastError());                                                   \
+    ++(c)->launches;                                                          \
+  } while (0)
+
+// ---- column-dot launches --------------------------------------------------
+template <typename T, int EPI>
+void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double beta) {
+  if (jobs.empty()) return;
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<ColDotJob> pk;
+    int64_t ld_max = 0;
+    int n_max = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = jobs[b0 + i];
+      ld_max = std::max(ld_max, pk.j[i].ld);
+      n_max = std::max(n_max, pk.j[i].n_out);
+    }
+    if (n_max == 0) continue;
+    const size_t smem = (size_t)ld_max * sizeof(double2);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(coldot_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    if (smem > 227 * 1024) fail(RADMM_INVALID_ARGUMENT, "operator rows exceed the shared-memory vector budget");
+    const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
+    const int target = c->sm_count * per_sm;
+    int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
+    dim3 grid(gx, (unsigned)nb);
+    LAUNCH(c, (coldot_kernel<T, EPI>), grid, 256, smem, pk, mu, beta);
+  }
+}
+
+// ---- forward (axpy) launches ------------------------------------------------
+template <int MODE>
+void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<ReduceJob>& red, double beta) {
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<FwdJob> pk;
+    Pack<ReduceJob> rp;
+    int max_chunks = 0, max_len = 0;
+    int64_t ld_max = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = jobs[b0 + i];
+      rp.j[i] = red[b0 + i];
+      max_chunks = std::max(max_chunks, pk.j[i].n_chunks);
+      max_len = std::max(max_len, pk.j[i].chunk_len);
+      ld_max = std::max(ld_max, pk.j[i].ld);
+    }
+    if (max_chunks > 0) {
+      const size_t smem = (size_t)max_len * (sizeof(double2) + sizeof(int));
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(fwd_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      dim3 grid(max_chunks, (unsigned)((ld_max + kFwdTile - 1) / kFwdTile), (unsigned)nb);
+      LAUNCH(c, fwd_kernel<MODE>, grid, kFwdThreads, smem, pk, c->gap.p, c->sigma.p, beta);
+    }
+    dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
+    LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp);
+  }
+}
+
+// chunking so one forward launch fills the GPU: ~kCtasPerSmTarget CTAs/SM
+void plan_chunks(radmm_ctx* c, const Sensor& S, int n, int batch, int& n_chunks, int& chunk_len) {
+  const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
+  const int target = c->sm_count * kCtasPerSmTarget;
+  const int chunks = std::min(S.part_chunks, std::max(1, target / std::max(1, tiles * batch)));
+  chunk_len = (int)round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8);
+  n_chunks = (n + chunk_len - 1) / chunk_len;
+}
+
+// ---- GEMM launches -----------------------------------------------------------
+template <int EPI>
+void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<GemmJob> pk;
+    int mm = 0, nn = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = jobs[b0 + i];
+      mm = std::max(mm, pk.j[i].m);
+      nn = std::max(nn, pk.j[i].n);
+    }
+    if (mm == 0 || nn == 0) continue;
+    dim3 grid((nn + kGB - 1) / kGB, (mm + kGB - 1) / kGB, (unsigned)nb);
+    LAUNCH(c, gemm_kernel<EPI>, grid, 256, 0, pk);
+  }
+}
+
+MatRef mref(const void* p, int64_t ld, bool c64, bool trans = false, bool conj = false,
+            const int* ridx = nullptr, const int* cidx = nullptr) {
+  MatRef m;
+  m.p = p; m.ld = ld; m.ridx = ridx; m.cidx = cidx;
+  m.c64 = c64 ? 1 : 0; m.trans = trans ? 1 : 0; m.conj = conj ? 1 : 0;
+  return m;
+}
+
+GemmJob gjob(int m, int n, int k, MatRef a, MatRef b, double2* cp, int64_t ldc, double alpha,
+             double beta0, double diag_add = 0.0) {
+  GemmJob g;
+  g.m = m; g.n = n; g.k = k; g.a = a; g.b = b; g.c = cp; g.ldc = ldc;
+  g.alpha = alpha; g.beta0 = beta0; g.diag_add = diag_add; g.k0 = 0; g.kb = 0;
+  return g;
+}
+
+// ---- batched in-place Gauss-Jordan inverse of HPD matrices --------------------
+struct InvTarget {
+  double2* M;
+  int64_t ld;
+  int n;
+};
+
+constexpr int kGJB = 64;
+
+// Inverts every target in place; raises RADMM_NUMERICAL if a pivot fails.
+void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* what) {
+  if (targets.empty()) return;
+  if (targets.size() > kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many matrices in one batch");
+  const size_t T = targets.size();
+  // scratch: P (64x64), F (n x 64), R (64 x n) per target
+  size_t need = 0;
+  for (const auto& t : targets) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 3 * 256;
+  Scratch& sc = c->scratch;
+  const size_t base_off = sc.off;
+  if (sc.off + need > sc.buf.n) {
+    // grow: preserve nothing (callers take scratch before gj only for inputs they own)
+    fail(RADMM_OUT_OF_MEMORY, "scratch arena too small for Gauss-Jordan inverse");
+  }
+  std::vector<double2*> P(T), F(T), R(T);
+  std::vector<int64_t> ldf(T);
+  int n_max = 0;
+  for (size_t i = 0; i < T; ++i) {
+    const int64_t nn = round_up(targets[i].n, 64);
+    P[i] = sc.take<double2>(64 * 64);
+    F[i] = sc.take<double2>((size_t)nn * 64);
+    R[i] = sc.take<double2>((size_t)nn * 64);
+    ldf[i] = nn;
+    n_max = std::max(n_max, targets[i].n);
+  }
+  CK(cudaMemsetAsync(c->fail_flags.p, 0, sizeof(int) * kMaxBatch, c->stream));
+  for (int k0 = 0; k0 < n_max; k0 += kGJB) {
+    Pack<DiagJob> dj;
+    std::vector<GemmJob> rjobs, ujobs;
+    int live = 0;
+    int64_t panel_max = 0;
+    for (size_t i = 0; i < T; ++i) {
+      DiagJob d;
+      d.M = targets[i].M; d.ld = targets[i].ld; d.n = targets[i].n; d.k0 = k0;
+      d.kb = std::max(0, std::min(kGJB, targets[i].n - k0));
+      d.P = P[i]; d.ldp = 64; d.F = F[i]; d.ldf = ldf[i]; d.R = R[i]; d.ldr = 64;
+      d.fail = c->fail_flags.p + i;
+      dj.j[i] = d;
+      if (d.kb <= 0) continue;
+      ++live;
+      panel_max = std::max<int64_t>(panel_max, (int64_t)d.n * d.kb);
+      // R' = P * M[K, :]
+      rjobs.push_back(gjob(d.kb, d.n, d.kb, mref(P[i], 64, false),
+                           mref(targets[i].M + k0, targets[i].ld, false), R[i], 64, 1.0, 0.0));
+      GemmJob u = gjob(d.n, d.n, d.kb, mref(F[i], ldf[i], false), mref(R[i], 64, false),
+                       targets[i].M, targets[i].ld, 1.0, 0.0);
+      u.k0 = k0;
+      u.kb = d.kb;
+      ujobs.push_back(u);
+    }
+    if (!live) break;
+    CK(cudaFuncSetAttribute(gj_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjSmem));
+    LAUNCH(c, gj_diag_kernel, dim3((unsigned)T), 1024, kGjSmem, dj);
+    const int pblocks = (int)std::min<int64_t>(1024, (panel_max + 255) / 256);
+    LAUNCH(c, gj_panel_kernel, dim3(pblocks, (unsigned)T), 256, 0, dj);
+    gemm<GEPI_PLAIN>(c, rjobs);
+    LAUNCH(c, gj_fix_kernel, dim3((unsigned)T), 256, 0, dj);
+    gemm<GEPI_GJ>(c, ujobs);
+  }
+  CK(cudaMemcpyAsync(c->h_flags, c->fail_flags.p, sizeof(int) * T, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t i = 0; i < T; ++i)
+    if (c->h_flags[i]) fail(RADMM_NUMERICAL, std::string(what) + ": Cholesky failed");
+  sc.off = base_off;
+}
+
+// ---------------------------------------------------------------------------
+// Factorization: LocalSolveCache (solver_core.hpp:34-45) realised as the
+// explicit inverse of the smaller of the two equivalent systems.
+// ---------------------------------------------------------------------------
+void ensure_g(Sensor& S, int dim, int64_t ld) {
+  const size_t need = (size_t)ld * dim;
+  if (S.G.n < need) S.G.alloc(need);
+}
+
+// Full rebuild for the listed sensors (batched): data term + factor.
+void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
+  if (qs.empty()) return;
+  std::vector<GemmJob> jobs;
+  std::vector<InvTarget> inv;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    S.primal = S.n_act <= S.rows;
+    const int dim = S.primal ? S.n_act : S.rows;
+    const int64_t ldg = S.primal ? round_up(dim, 32) : S.ld;
+    ensure_g(S, dim, ldg);
+    S.ldg = ldg;
+    S.g_n = dim;
+    CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)ldg * dim, c->stream));
+    if (S.primal) {
+      // Gram mu A_J^H A_J + beta I (solver_core.hpp:39-40)
+      jobs.push_back(gjob(dim, dim, S.rows, mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p),
+                          mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
+    } else {
+      // capacitance beta I + mu A_J A_J^H (Woodbury form of the same system)
+      jobs.push_back(gjob(dim, dim, S.n_act, mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p),
+                          mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
+    }
+    inv.push_back({S.G.p, ldg, dim});
+    ++c->rebuilds;
+  }
+  gemm<GEPI_PLAIN>(c, jobs);
+  size_t need = 0;
+  for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
+  c->scratch.reserve(need);
+  gj_invert(c, inv, "factorize");
+}
+
+// Data term mu A_J^H y_eff for the listed sensors (admm.hpp:177).
+void data_terms(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  std::vector<ColDotJob> jobs;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    ColDotJob j{};
+    j.M = S.A.p; j.ld = S.ld; j.len = S.rows; j.n_out = S.n_act; j.cols = S.J.p;
+    j.vec = S.y_eff.p; j.out = S.data.p; j.scale = mu;
+    jobs.push_back(j);
+  }
+  coldot<float2, EPI_STORE>(c, jobs, mu, 1.0);
+}
+
+// Low-rank downdates after screening removed rem_q columns.
+//   dual:   G <- G + mu P (I - mu R^H P)^{-1} P^H,  P = G R   (Woodbury)
+//   primal: Hinv_KK <- Hinv_KK - Hinv_KD inv(Hinv_DD) Hinv_DK (inverse of a
+//           principal submatrix), written compacted into G2 then swapped.
+void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  if (qs.empty()) return;
+  size_t need = 0;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    const size_t r = S.removed_now;
+    const size_t dimr = round_up(r, 64);
+    if (S.primal) need += (dimr * dimr + (size_t)round_up(S.n_act, 64) * dimr) * sizeof(double2);
+    else need += (2 * (size_t)S.ld * dimr + dimr * dimr) * sizeof(double2);
+    need += (64 * 64 + 2 * dimr * 64) * sizeof(double2) + 4096;
+  }
+  c->scratch.reserve(need);
+  std::vector<GemmJob> st1, st2, st3, st4;
+  std::vector<InvTarget> inv;
+  Pack<SubJob> sub;
+  int nsub = 0;
+  int64_t sub_max = 0;
+  std::vector<double2*> Pm(qs.size()), Tm(qs.size()), Sm(qs.size());
+  for (size_t t = 0; t < qs.size(); ++t) {
+    Sensor& S = c->sensors[qs[t]];
+    const int r = S.removed_now;
+    const int64_t ldr = round_up(r, 32);
+    Sm[t] = c->scratch.take<double2>((size_t)ldr * r);
+    CK(cudaMemsetAsync(Sm[t], 0, sizeof(double2) * (size_t)ldr * r, c->stream));
+    if (!S.primal) {
+      const int m = S.rows;
+      Pm[t] = c->scratch.take<double2>((size_t)S.ld * r);
+      Tm[t] = c->scratch.take<double2>((size_t)S.ld * r);
+      // P = G R
+      st1.push_back(gjob(m, r, m, mref(S.G.p, S.ldg, false),
+                         mref(S.A.p, S.ld, true, false, false, nullptr, S.rem_pix.p), Pm[t], S.ld, 1.0, 0.0));
+      // S = I - mu R^H P
+      st2.push_back(gjob(r, r, m, mref(S.A.p, S.ld, true, true, true, nullptr, S.rem_pix.p),
+                         mref(Pm[t], S.ld, false), Sm[t], ldr, -mu, 0.0, 1.0));
+      inv.push_back({Sm[t], ldr, r});
+      // T = P Sinv
+      st3.push_back(gjob(m, r, r, mref(Pm[t], S.ld, false), mref(Sm[t], ldr, false), Tm[t], S.ld, 1.0, 0.0));
+      // G += mu T P^H
+      st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
+                         S.ldg, mu, 1.0));
+    } else {
+      const int nn = S.n_act;  // kept
+      const int64_t ld_new = round_up(nn, 32);
+      if (S.G2.n < (size_t)ld_new * nn) S.G2.alloc((size_t)ld_new * nn);
+      CK(cudaMemsetAsync(S.G2.p, 0, sizeof(double2) * (size_t)ld_new * nn, c->stream));
+      Tm[t] = c->scratch.take<double2>((size_t)round_up(nn, 64) * r);
+      // S = Hinv[D, D]
+      SubJob sj;
+      sj.M = S.G.p; sj.ld = S.ldg; sj.ridx = S.rem_pos.p; sj.cidx = S.rem_pos.p; sj.m = r; sj.n = r;
+      sj.out = Sm[t]; sj.ldo = ldr;
+      sub.j[nsub++] = sj;
+      sub_max = std::max<int64_t>(sub_max, (int64_t)r * r);
+      SubJob sk;
+      sk.M = S.G.p; sk.ld = S.ldg; sk.ridx = S.keep_pos.p; sk.cidx = S.keep_pos.p; sk.m = nn; sk.n = nn;
+      sk.out = S.G2.p; sk.ldo = ld_new;
+      sub.j[nsub++] = sk;
+      sub_max = std::max<int64_t>(sub_max, (int64_t)nn * nn);
+      inv.push_back({Sm[t], ldr, r});
+      // T = Hinv[K, D] Sinv
+      st3.push_back(gjob(nn, r, r, mref(S.G.p, S.ldg, false, false, false, S.keep_pos.p, S.rem_pos.p),
+                         mref(Sm[t], ldr, false), Tm[t], round_up(nn, 64), 1.0, 0.0));
+      // G2 -= T Hinv[D, K]
+      st4.push_back(gjob(nn, nn, r, mref(Tm[t], round_up(nn, 64), false),
+                         mref(S.G.p, S.ldg, false, false, false, S.rem_pos.p, S.keep_pos.p), S.G2.p, ld_new,
+                         -1.0, 1.0));
+    }
+    ++c->downdates;
+  }
+  if (nsub) {
+    const int blocks = (int)std::min<int64_t>(2048, (sub_max + 255) / 256);
+    LAUNCH(c, gather_sub_kernel, dim3(std::max(1, blocks), nsub), 256, 0, sub);
+  }
+  gemm<GEPI_PLAIN>(c, st1);
+  gemm<GEPI_PLAIN>(c, st2);
+  gj_invert(c, inv, "factorize");
+  gemm<GEPI_PLAIN>(c, st3);
+  gemm<GEPI_PLAIN>(c, st4);
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    if (S.primal) {
+      std::swap(S.G, S.G2);
+      S.ldg = round_up(S.n_act, 32);
+      S.g_n = S.n_act;
+    }
+  }
+}
+
+
+// Frozen-echo update y_eff -= A[:, removed] x_full[removed] (admm.hpp:174-176;
+// incremental: frozen values never change once frozen).
+void update_y_eff(radmm_ctx* c, const std::vector<int>& qs) {
+  std::vector<FwdJob> jobs;
+  std::vector<ReduceJob> red;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    FwdJob f{};
+    f.A = S.A.p; f.ld = S.ld; f.n = S.removed_now; f.J = S.rem_pix.p; f.src = S.x_full.p;
+    f.part = S.part.p;
+    plan_chunks(c, S, S.removed_now, (int)qs.size(), f.n_chunks, f.chunk_len);
+    jobs.push_back(f);
+    ReduceJob r{S.part.p, f.n_chunks, S.ld, S.rows, S.y_eff.p, S.y_eff.p, -1.0};
+    red.push_back(r);
+  }
+  forward<MODE_GATHER>(c, jobs, red, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// One run
+// ---------------------------------------------------------------------------
+void validate_hyper(const radmm_hyperparams* h) {
+  if (!h) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: null");
+  if (!(h->mu > 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: mu must be > 0");
+  if (!(h->lambda >= 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: lambda must be >= 0");
+  if (!(h->beta > 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: beta must be > 0");
+  if (!(h->eps_abs > 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: eps_abs must be > 0");
+  if (!(h->eps_rel > 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: eps_rel must be > 0");
+  if (h->screening_window < 2)
+    fail(RADMM_INVALID_ARGUMENT, "Hyperparams: screening_window needs at least one successive pair");
+  if (!(h->screening_tol >= 0.0)) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: screening_tol must be >= 0");
+  if (h->max_iter < 1) fail(RADMM_INVALID_ARGUMENT, "Hyperparams: max_iter must be >= 1");
+}
+
+size_t contribution_size(size_t n) { return 1 + 4 + 8 + 4 + n * (4 + 16); }  // wire.hpp:54-56
+size_t notice_size(size_t n) { return 1 + 4 + 8 + 4 + n * (4 + 16); }        // wire.hpp:60-62
+
+void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
+  const int N = c->N;
+  c->W = h->screening_window;
+  c->upd = 0;
+  std::vector<int> all;
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    if (!S.has_op) fail(RADMM_INVALID_ARGUMENT, "Problem: sensor " + std::to_string(q) + " has no operator");
+    if (!S.has_y) fail(RADMM_INVALID_ARGUMENT, "Problem: measurement length mismatch");
+    S.n_act = N;
+    S.stalled = false;
+    S.removed_now = 0;
+    LAUNCH(c, iota_kernel, dim3((N + 255) / 256), 256, 0, S.J.p, N);
+    CK(cudaMemsetAsync(S.x_full.p, 0, sizeof(double2) * N, c->stream));
+    CK(cudaMemsetAsync(S.x_hat.p, 0, sizeof(double2) * N, c->stream));
+    if (S.ring.n != (size_t)c->W * N) S.ring.alloc((size_t)c->W * N);
+    CK(cudaMemsetAsync(S.ring.p, 0, sizeof(double) * S.ring.n, c->stream));
+    CK(cudaMemsetAsync(S.y_eff.p, 0, sizeof(double2) * S.ld, c->stream));
+    CK(cudaMemcpyAsync(S.y_eff.p, S.y.p, sizeof(double2) * S.rows, cudaMemcpyDeviceToDevice, c->stream));
+    all.push_back(q);
+  }
+  for (DArr<double2>* v : {&c->s, &c->xg, &c->sigma, &c->sigma_pre, &c->gap})
+    CK(cudaMemsetAsync(v->p, 0, sizeof(double2) * N, c->stream));
+  CK(cudaMemsetAsync(c->fcounter.p, 0, sizeof(unsigned), c->stream));
+  data_terms(c, all, h->mu);
+  full_rebuild(c, all, h->mu, h->beta);
+}
+
+// One synchronous Jacobi sweep of local updates (admm.hpp:389-390).
+void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
+  const int slot = c->upd % c->W;
+  std::vector<FwdJob> fj;
+  std::vector<ReduceJob> rj;
+  std::vector<ColDotJob> gj, aj, pj;
+  Pack<RhsJob> rh;
+  int n_rhs = 0, rhs_max = 0;
+  int n_dual = 0;
+  for (int q = 0; q < c->Q; ++q) if (!c->sensors[q].primal) ++n_dual;
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    double* ring_slot = S.ring.p + (size_t)slot * c->N;
+    if (!S.primal) {
+      FwdJob f{};
+      f.A = S.A.p; f.ld = S.ld; f.n = S.n_act; f.J = S.J.p; f.data = S.data.p; f.x_hat = S.x_hat.p;
+      f.rhs_out = S.rhs.p; f.part = S.part.p;
+      plan_chunks(c, S, S.n_act, n_dual, f.n_chunks, f.chunk_len);
+      fj.push_back(f);
+      rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0});
+      ColDotJob g{};
+      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
+      gj.push_back(g);
+      ColDotJob a{};
+      a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = S.n_act; a.cols = S.J.p; a.pix = S.J.p;
+      a.vec = S.w.p; a.rhs = S.rhs.p; a.x_hat = S.x_hat.p; a.x_full = S.x_full.p; a.ring_slot = ring_slot;
+      aj.push_back(a);
+    } else {
+      if (n_rhs >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many primal sensors in one batch");
+      rh.j[n_rhs++] = RhsJob{S.n_act, S.J.p, S.data.p, S.x_hat.p, S.rhs.p};
+      rhs_max = std::max(rhs_max, S.n_act);
+      ColDotJob p{};
+      p.M = S.G.p; p.ld = S.ldg; p.len = S.n_act; p.n_out = S.n_act; p.pix = S.J.p; p.vec = S.rhs.p;
+      p.x_hat = S.x_hat.p; p.x_full = S.x_full.p; p.ring_slot = ring_slot;
+      pj.push_back(p);
+    }
+  }
+  if (!fj.empty()) {
+    forward<MODE_RHS>(c, fj, rj, h->beta);
+    coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+    coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta);
+  }
+  if (n_rhs) {
+    LAUNCH(c, rhs_kernel, dim3((rhs_max + 255) / 256, n_rhs), 256, 0, rh, c->gap.p, c->sigma.p, h->beta);
+    coldot<double2, EPI_XPRIMAL>(c, pj, h->mu, h->beta);
+  }
+  ++c->upd;
+}
+
+// Sharded runs: every rank receives every sensor image (fixed global order),
+// plus per-sensor active sizes / stalled flags and the rank's notice bytes.
+void exchange(radmm_ctx* c, double notice_bytes) {
+  if (c->world <= 1) return;
+  const size_t N = c->N;
+  for (int q = 0; q < c->Q; ++q)
+    CK(cudaMemcpyAsync(c->send_buf.p + (size_t)q * N, c->sensors[q].x_full.p, sizeof(double2) * N,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  std::vector<double> meta(2 * c->q_max_local + 1, 0.0);
+  for (int q = 0; q < c->Q; ++q) {
+    meta[2 * q] = c->sensors[q].n_act;
+    meta[2 * q + 1] = c->sensors[q].stalled ? 1.0 : 0.0;
+  }
+  meta[2 * c->q_max_local] = notice_bytes;
+  CK(cudaMemcpyAsync(c->size_send.p, meta.data(), sizeof(double) * meta.size(), cudaMemcpyHostToDevice, c->stream));
+  g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble, c->comm,
+                                c->stream), "ncclAllGather(contributions)");
+  g_nccl.check(g_nccl.AllGather(c->size_send.p, c->size_recv.p, meta.size(), kNcclDouble, c->comm, c->stream),
+               "ncclAllGather(meta)");
+  c->launches += 2;
+}
+
+void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  FusionArgs a;
+  a.contrib = c->contrib.p;
+  a.Q = c->Q_total;
+  a.N = c->N;
+  a.s = c->s.p; a.xg = c->xg.p; a.sigma = c->sigma.p; a.sigma_pre = c->sigma_pre.p; a.gap = c->gap.p;
+  a.beta = h->beta;
+  a.kappa = h->lambda / h->beta;
+  a.root_n_eps_abs = std::sqrt((double)c->N) * h->eps_abs;
+  a.eps_rel = h->eps_rel;
+  a.has_prev = k > 1 ? 1 : 0;
+  a.iteration = k;
+  a.partials = c->fpart.p;
+  a.counter = c->fcounter.p;
+  a.out_dev = c->fs_dev.p;
+  a.out_host = c->fs_host_dev;
+  LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
+}
+
+// SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386).
+// Returns the notice bytes of this round.
+uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  if (c->upd < c->W) return 0;  // history shorter than W+1 (admm.hpp:137)
+  Pack<ScreenJob> pk;
+  int n_max = 0;
+  if (c->Q > kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors per GPU for screening batch");
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    ScreenJob j;
+    j.n = S.n_act; j.J = S.J.p; j.ring = S.ring.p; j.ring_stride = c->N; j.first_slot = c->upd % c->W;
+    j.keep = S.keep.p; j.block_counts = S.blk_cnt.p; j.block_offsets = S.blk_off.p; j.totals = S.totals.p;
+    j.Jnew = S.Jnew.p; j.keep_pos = S.keep_pos.p; j.rem_pix = S.rem_pix.p; j.rem_pos = S.rem_pos.p;
+    j.x_hat = S.x_hat.p; j.x_hat_new = S.x_hat_new.p;
+    pk.j[q] = j;
+    n_max = std::max(n_max, S.n_act);
+  }
+  const int nb = (n_max + kScanBlock - 1) / kScanBlock;
+  LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol);
+  LAUNCH(c, screen_scan_kernel, dim3(c->Q), 32, 0, pk);
+  LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk);
+  for (int q = 0; q < c->Q; ++q)
+    CK(cudaMemcpyAsync(c->h_totals + q, c->sensors[q].totals.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  uint64_t notice = 0;
+  std::vector<int> changed;
+  std::vector<int> pix;
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    const int kept = c->h_totals[q];
+    const int removed = S.n_act - kept;
+    if (removed == 0) continue;
+    if (kept == 0) {  // admm.hpp:148-151
+      S.stalled = true;
+      continue;
+    }
+    S.removed_now = removed;
+    std::swap(S.J, S.Jnew);
+    std::swap(S.x_hat, S.x_hat_new);
+    S.n_act = kept;
+    changed.push_back(q);
+    notice += notice_size((size_t)removed);
+    pix.resize(removed);
+    CK(cudaMemcpy(pix.data(), S.rem_pix.p, sizeof(int) * removed, cudaMemcpyDeviceToHost));
+    for (int p : pix) {
+      c->removal_log.push_back(k);
+      c->removal_log.push_back(c->q_begin + q);
+      c->removal_log.push_back(p);
+    }
+  }
+  if (changed.empty()) return notice;
+  // rebuild() (admm.hpp:171-179): frozen echo, data term, factor
+  update_y_eff(c, changed);
+  data_terms(c, changed, h->mu);
+  std::vector<int> rebuild, down;
+  for (int q : changed) {
+    Sensor& S = c->sensors[q];
+    const bool now_primal = S.n_act <= S.rows;
+    if (S.primal) {
+      (S.removed_now <= S.n_act ? down : rebuild).push_back(q);
+    } else if (now_primal) {
+      rebuild.push_back(q);
+    } else {
+      (S.removed_now <= S.rows ? down : rebuild).push_back(q);
+    }
+  }
+  full_rebuild(c, rebuild, h->mu, h->beta);
+  downdate(c, down, h->mu);
+  return notice;
+}
+
+void build_contrib(radmm_ctx* c) {
+  std::vector<const double2*> ptrs(c->Q_total);
+  if (c->world <= 1) {
+    for (int q = 0; q < c->Q; ++q) ptrs[q] = c->sensors[q].x_full.p;
+  } else {
+    for (int g = 0; g < c->Q_total; ++g) {
+      int r = 0;
+      while (r + 1 < c->world && (int64_t)(r + 1) * c->Q_total / c->world <= g) ++r;
+      const int begin = (int)((int64_t)r * c->Q_total / c->world);
+      ptrs[g] = c->gathered.p + ((size_t)r * c->q_max_local + (g - begin)) * c->N;
+    }
+  }
+  if (c->contrib.n != ptrs.size()) c->contrib.alloc(ptrs.size());
+  CK(cudaMemcpy(c->contrib.p, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
+}
+
+void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o, radmm_run_summary* out) {
+  validate_hyper(h);
+  set_device(c);
+  const bool asadmm = o && o->mode == RADMM_MODE_ASADMM;
+  const bool disable = o && o->disable_screening;
+  const bool fixed = o && o->fixed_iterations;
+  c->records.clear();
+  c->active_log.clear();
+  c->removal_log.clear();
+  c->have_result = false;
+  c->launches = 0;
+  c->rebuilds = c->downdates = 0;
+  radmm_run_summary sm{};
+  const auto t0 = std::chrono::steady_clock::now();
+  build_contrib(c);
+  begin_run(c, h);
+  CK(cudaStreamSynchronize(c->stream));
+  const auto t1 = std::chrono::steady_clock::now();
+  sm.setup_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  std::vector<double> hx, hs, hsig;
+  std::vector<int32_t> sizes(c->Q_total);
+  std::vector<double> meta_all;
+  if (o && o->observer) { hx.resize(2 * (size_t)c->N); hs.resize(2 * (size_t)c->N); hsig.resize(2 * (size_t)c->N); }
+  bool staged_trigger = false;
+  FusionScalars f{};
+  for (int k = 1; k <= h->max_iter; ++k) {
+    uint64_t notice = 0;
+    if (asadmm && !disable && staged_trigger) notice = screen_all(c, h, k);
+    local_updates(c, h);
+    exchange(c, (double)notice);
+    run_fusion(c, h, k);
+    CK(cudaStreamSynchronize(c->stream));
+    f = *c->fs_host;
+    radmm_iteration_record rec{};
+    rec.iteration = k;
+    rec.pri_res = f.pri_res;
+    rec.dual_res = f.dual_res;
+    rec.eps_pri = f.eps_pri;
+    rec.eps_dual = f.eps_dual;
+    uint64_t bytes = notice;
+    bool stalled_any = false;
+    if (c->world <= 1) {
+      for (int q = 0; q < c->Q; ++q) {
+        sizes[q] = c->sensors[q].n_act;
+        stalled_any = stalled_any || c->sensors[q].stalled;
+      }
+    } else {
+      const int stride = 2 * c->q_max_local + 1;
+      meta_all.resize((size_t)stride * c->world);
+      CK(cudaMemcpy(meta_all.data(), c->size_recv.p, sizeof(double) * meta_all.size(), cudaMemcpyDeviceToHost));
+      bytes = 0;
+      for (int r = 0; r < c->world; ++r) {
+        const int begin = (int)((int64_t)r * c->Q_total / c->world);
+        const int end = (int)((int64_t)(r + 1) * c->Q_total / c->world);
+        for (int g = begin; g < end; ++g) {
+          sizes[g] = (int32_t)meta_all[(size_t)r * stride + 2 * (g - begin)];
+          stalled_any = stalled_any || meta_all[(size_t)r * stride + 2 * (g - begin) + 1] != 0.0;
+        }
+        bytes += (uint64_t)meta_all[(size_t)r * stride + 2 * c->q_max_local];
+      }
+    }
+    int max_active = 0;
+    for (int g = 0; g < c->Q_total; ++g) {
+      const size_t cb = contribution_size((size_t)sizes[g]);
+      bytes += cb;
+      max_active = std::max(max_active, sizes[g]);
+      sm.total_active_solves += (uint64_t)sizes[g];
+      c->active_log.push_back(sizes[g]);
+    }
+    rec.bytes_sent = bytes;
+    rec.active_fraction = (double)max_active / c->N;
+    rec.ms_elapsed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+    sm.total_bytes += bytes;
+    c->records.push_back(rec);
+    sm.screening_stalled = stalled_any ? 1 : 0;
+    if (o && o->observer) {
+      CK(cudaMemcpy(hx.data(), c->xg.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hs.data(), c->s.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hsig.data(), c->sigma.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
+      radmm_iteration_view view{k, hx.data(), hs.data(), hsig.data(), sizes.data(), f.converged, f.trigger};
+      o->observer(o->observer_user, &view);
+    }
+    sm.iterations = k;
+    if (f.converged && !fixed) {
+      sm.converged = 1;
+      break;
+    }
+    staged_trigger = f.trigger != 0;
+  }
+  if (fixed) sm.converged = f.converged;
+  const auto t2 = std::chrono::steady_clock::now();
+  sm.solve_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  sm.kernel_launches = c->launches;
+  sm.rebuilds = c->rebuilds;
+  sm.downdates = c->downdates;
+  c->summary = sm;
+  c->have_result = true;
+  if (out) *out = sm;
+}
+
+void copy_out(radmm_ctx* c, const void* dev, void* host, size_t bytes) {
+  if (!host) fail(RADMM_INVALID_ARGUMENT, "null output buffer");
+  set_device(c);
+  CK(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost));
+}
+
+void need_result(radmm_ctx* c) {
+  if (!c) fail(RADMM_INVALID_ARGUMENT, "null context");
+  if (!c->have_result) fail(RADMM_INVALID_ARGUMENT, "no completed run on this context");
+}
+
+}  // namespace
+
+struct radmm_solve_cache {
+  radmm_ctx* ctx = nullptr;
+  double mu = 0, beta = 0;
+  int rows = 0, cols = 0;
+  DArr<double2> x, tmp;
+  DArr<double> ring;
+  ~radmm_solve_cache() { delete ctx; }
+};
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* radmm_last_error(void) { return g_last_error.c_str(); }
+int radmm_version(void) { return 1; }
+
+int radmm_hyperparams_default(radmm_hyperparams* out) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    *out = radmm_hyperparams{3.0, 20.0, 100.0, 1e-4, 1e-2, 5, 1e-5, 1000};
+  });
+}
+
+int radmm_hyperparams_validate(const radmm_hyperparams* h) {
+  return guarded([&] { validate_hyper(h); });
+}
+
+int radmm_ctx_create(int device, int n_pixels, int n_sensors, radmm_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    if (n_sensors < 1) fail(RADMM_INVALID_ARGUMENT, "Problem: needs at least one sensor");
+    if (n_pixels < 1) fail(RADMM_INVALID_ARGUMENT, "Problem: needs at least one pixel");
+    auto c = std::make_unique<radmm_ctx>();
+    init_ctx(c.get(), device, n_pixels, n_sensors);
+    c->Q_total = n_sensors;
+    c->q_begin = 0;
+    c->q_max_local = n_sensors;
+    *out = c.release();
+  });
+}
+
+int radmm_ctx_destroy(radmm_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int64_t lda, int ptr_kind) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!a) fail(RADMM_INVALID_ARGUMENT, "null operator");
+    if (lda < rows) fail(RADMM_INVALID_ARGUMENT, "lda < rows");
+    set_device(ctx);
+    prepare_operator(ctx, S, rows);
+    CK(cudaMemcpy2DAsync(S.A.p, S.ld * sizeof(float2), a, lda * sizeof(float2), rows * sizeof(float2), ctx->N,
+                         ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int radmm_set_operator_c128(radmm_ctx* ctx, int q, int rows, const double* a, int64_t lda, int ptr_kind) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!a) fail(RADMM_INVALID_ARGUMENT, "null operator");
+    if (lda < rows) fail(RADMM_INVALID_ARGUMENT, "lda < rows");
+    set_device(ctx);
+    prepare_operator(ctx, S, rows);
+    const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (rows * (int64_t)sizeof(double2)));
+    DArr<double2> stage;
+    stage.alloc((size_t)rows * std::min<int64_t>(chunk, ctx->N), false);
+    for (int64_t c0 = 0; c0 < ctx->N; c0 += chunk) {
+      const int64_t nc = std::min<int64_t>(chunk, ctx->N - c0);
+      CK(cudaMemcpy2DAsync(stage.p, rows * sizeof(double2), a + 2 * c0 * lda, lda * sizeof(double2),
+                           rows * sizeof(double2), nc,
+                           ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           ctx->stream));
+      const int64_t total = rows * nc;
+      LAUNCH(ctx, c128_to_c64_kernel, dim3((unsigned)((total + 255) / 256)), 256, 0, stage.p, (int64_t)rows,
+             S.A.p + c0 * S.ld, S.ld, rows, (int)nc);
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!S.has_op) fail(RADMM_INVALID_ARGUMENT, "set the operator before the measurement");
+    if (!y) fail(RADMM_INVALID_ARGUMENT, "null measurement");
+    set_device(ctx);
+    S.y.alloc(S.ld);
+    CK(cudaMemcpy(S.y.p, y, sizeof(double2) * S.rows,
+                  ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    S.has_y = true;
+  });
+}
+
+int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const double* pix, const double* tx,
+                                    const double* rx, const double* phi, double fc, double bw, double pulse) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (M < 1 || K < 1 || !pix || !tx || !rx || !phi) fail(RADMM_INVALID_ARGUMENT, "bad generator arguments");
+    set_device(ctx);
+    prepare_operator(ctx, S, M * K);
+    const int N = ctx->N;
+    DArr<double> dpix, dtx, drx, dphi;
+    dpix.alloc(3 * (size_t)N, false); dtx.alloc(3, false); drx.alloc(3 * (size_t)M, false); dphi.alloc(N, false);
+    CK(cudaMemcpy(dpix.p, pix, sizeof(double) * 3 * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dtx.p, tx, sizeof(double) * 3, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(drx.p, rx, sizeof(double) * 3 * M, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dphi.p, phi, sizeof(double) * N, cudaMemcpyHostToDevice));
+    const int64_t total = (int64_t)M * K * N;
+    const double pi = 3.141592653589793238462643383279502884;
+    LAUNCH(ctx, dechirp_kernel, dim3((unsigned)((total + 255) / 256)), 256, 0, S.A.p, S.ld, M, K, N, dpix.p, dtx.p,
+           drx.p, dphi.p, bw / pulse, fc, pulse / K, 299792458.0, 2.0 * pi);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int radmm_get_operator_c64(radmm_ctx* ctx, int q, float* out) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!S.has_op || !out) fail(RADMM_INVALID_ARGUMENT, "no operator");
+    set_device(ctx);
+    CK(cudaMemcpy2D(out, S.rows * sizeof(float2), S.A.p, S.ld * sizeof(float2), S.rows * sizeof(float2), ctx->N,
+                    cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_run(radmm_ctx* ctx, const radmm_hyperparams* hyper, const radmm_run_options* opts,
+              radmm_run_summary* summary) {
+  return guarded([&] {
+    if (!ctx) fail(RADMM_INVALID_ARGUMENT, "null context");
+    do_run(ctx, hyper, opts, summary);
+  });
+}
+
+int radmm_get_image(radmm_ctx* ctx, double* out) {
+  return guarded([&] {
+    need_result(ctx);
+    DArr<double> img;
+    img.alloc(ctx->N, false);
+    LAUNCH(ctx, abs_kernel, dim3((ctx->N + 255) / 256), 256, 0, ctx->xg.p, ctx->N, img.p);
+    CK(cudaStreamSynchronize(ctx->stream));
+    copy_out(ctx, img.p, out, sizeof(double) * ctx->N);
+  });
+}
+
+int radmm_get_vector(radmm_ctx* ctx, radmm_vector which, double* out) {
+  return guarded([&] {
+    need_result(ctx);
+    const double2* src = nullptr;
+    switch (which) {
+      case RADMM_VEC_X_GLOBAL: src = ctx->xg.p; break;
+      case RADMM_VEC_S: src = ctx->s.p; break;
+      case RADMM_VEC_SIGMA: src = ctx->sigma.p; break;
+      case RADMM_VEC_SIGMA_PRE_GLOBAL: src = ctx->sigma_pre.p; break;
+      case RADMM_VEC_GAP: src = ctx->gap.p; break;
+      default: fail(RADMM_INVALID_ARGUMENT, "unknown vector");
+    }
+    copy_out(ctx, src, out, sizeof(double2) * ctx->N);
+  });
+}
+
+int radmm_get_sensor_image(radmm_ctx* ctx, int q, double* out) {
+  return guarded([&] {
+    need_result(ctx);
+    Sensor& S = sensor_at(ctx, q);
+    copy_out(ctx, S.x_full.p, out, sizeof(double2) * ctx->N);
+  });
+}
+
+int radmm_get_record_count(radmm_ctx* ctx, int* count) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!count) fail(RADMM_INVALID_ARGUMENT, "null output");
+    *count = (int)ctx->records.size();
+  });
+}
+
+int radmm_get_records(radmm_ctx* ctx, radmm_iteration_record* out, int capacity) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!out || capacity < (int)ctx->records.size()) fail(RADMM_INVALID_ARGUMENT, "output too small");
+    std::memcpy(out, ctx->records.data(), sizeof(radmm_iteration_record) * ctx->records.size());
+  });
+}
+
+int radmm_get_active_sizes(radmm_ctx* ctx, int32_t* out, int capacity) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!out || capacity < (int)ctx->active_log.size()) fail(RADMM_INVALID_ARGUMENT, "output too small");
+    std::memcpy(out, ctx->active_log.data(), sizeof(int32_t) * ctx->active_log.size());
+  });
+}
+
+int radmm_get_active_set(radmm_ctx* ctx, int q, int32_t* out, int* count) {
+  return guarded([&] {
+    need_result(ctx);
+    Sensor& S = sensor_at(ctx, q);
+    if (!count) fail(RADMM_INVALID_ARGUMENT, "null output");
+    *count = S.n_act;
+    if (out) copy_out(ctx, S.J.p, out, sizeof(int) * S.n_act);
+  });
+}
+
+int radmm_get_removal_log_size(radmm_ctx* ctx, int* entries) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!entries) fail(RADMM_INVALID_ARGUMENT, "null output");
+    *entries = (int)(ctx->removal_log.size() / 3);
+  });
+}
+
+int radmm_get_removal_log(radmm_ctx* ctx, int32_t* out, int capacity) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!out || capacity < (int)(ctx->removal_log.size() / 3)) fail(RADMM_INVALID_ARGUMENT, "output too small");
+    std::memcpy(out, ctx->removal_log.data(), sizeof(int32_t) * ctx->removal_log.size());
+  });
+}
+
+int radmm_factorize(int device, int rows, int cols, const double* a_hat, double mu, double beta,
+                    radmm_solve_cache** out) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    if (!(mu > 0.0)) fail(RADMM_INVALID_ARGUMENT, "factorize: mu must be > 0");
+    if (!(beta > 0.0)) fail(RADMM_INVALID_ARGUMENT, "factorize: beta must be > 0");
+    if (rows < 1 || cols < 1 || !a_hat) fail(RADMM_INVALID_ARGUMENT, "factorize: empty matrix");
+    for (int64_t i = 0; i < 2ll * rows * cols; ++i)
+      if (!std::isfinite(a_hat[i])) fail(RADMM_INVALID_ARGUMENT, "factorize: matrix has non-finite entries");
+    auto sc = std::make_unique<radmm_solve_cache>();
+    sc->ctx = new radmm_ctx();
+    radmm_ctx* c = sc->ctx;
+    init_ctx(c, device, cols, 1);
+    c->Q_total = 1;
+    c->q_max_local = 1;
+    Sensor& S = c->sensors[0];
+    int st = radmm_set_operator_c128(c, 0, rows, a_hat, rows, RADMM_PTR_HOST);
+    if (st != RADMM_OK) fail(st, g_last_error);
+    S.n_act = cols;
+    LAUNCH(c, iota_kernel, dim3((cols + 255) / 256), 256, 0, S.J.p, cols);
+    full_rebuild(c, {0}, mu, beta);
+    sc->mu = mu; sc->beta = beta; sc->rows = rows; sc->cols = cols;
+    sc->x.alloc(cols); sc->tmp.alloc(cols); sc->ring.alloc(cols);
+    *out = sc.release();
+  });
+}
+
+int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
+  return guarded([&] {
+    if (!sc || !rhs || !x) fail(RADMM_INVALID_ARGUMENT, "solve_local: null argument");
+    radmm_ctx* c = sc->ctx;
+    set_device(c);
+    Sensor& S = c->sensors[0];
+    CK(cudaMemcpy(S.rhs.p, rhs, sizeof(double2) * sc->cols, cudaMemcpyHostToDevice));
+    if (S.primal) {
+      ColDotJob j{};
+      j.M = S.G.p; j.ld = S.ldg; j.len = sc->cols; j.n_out = sc->cols; j.vec = S.rhs.p; j.out = sc->x.p; j.scale = 1.0;
+      coldot<double2, EPI_STORE>(c, {j}, sc->mu, sc->beta);
+    } else {
+      FwdJob f{};
+      f.A = S.A.p; f.ld = S.ld; f.n = sc->cols; f.J = S.J.p; f.src = S.rhs.p; f.part = S.part.p;
+      plan_chunks(c, S, sc->cols, 1, f.n_chunks, f.chunk_len);
+      forward<MODE_GATHER>(c, {f}, {ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0}}, 0.0);
+      ColDotJob g{};
+      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
+      coldot<double2, EPI_STORE>(c, {g}, sc->mu, sc->beta);
+      ColDotJob a{};
+      a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = sc->cols; a.cols = S.J.p; a.pix = S.J.p; a.vec = S.w.p;
+      a.rhs = S.rhs.p; a.x_hat = sc->x.p; a.x_full = sc->tmp.p; a.ring_slot = sc->ring.p;
+      coldot<float2, EPI_XDUAL>(c, {a}, sc->mu, sc->beta);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(x, sc->x.p, sizeof(double2) * sc->cols, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_solve_cache_destroy(radmm_solve_cache* sc) {
+  return guarded([&] { delete sc; });
+}
+
+int radmm_soft_threshold(int device, const double* v, int64_t n, double kappa, double* out) {
+  return guarded([&] {
+    if (!(kappa >= 0.0)) fail(RADMM_INVALID_ARGUMENT, "soft_threshold: kappa must be >= 0");
+    if (n < 0 || (n > 0 && (!v || !out))) fail(RADMM_INVALID_ARGUMENT, "soft_threshold: null buffer");
+    if (n == 0) return;
+    CK(cudaSetDevice(device));
+    DArr<double2> dv, dout;
+    dv.alloc(n, false);
+    dout.alloc(n, false);
+    CK(cudaMemcpy(dv.p, v, sizeof(double2) * n, cudaMemcpyHostToDevice));
+    soft_threshold_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dv.p, n, kappa, dout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    g_nccl.load();
+    nccl_uid id;
+    g_nccl.check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, 128);
+  });
+}
+
+int radmm_ctx_create_sharded(int device, int n_pixels, int q_total, int q_begin, int q_end, int rank,
+                             int world_size, const uint8_t nccl_id[128], radmm_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    if (world_size < 1 || rank < 0 || rank >= world_size) fail(RADMM_INVALID_ARGUMENT, "bad rank / world size");
+    if (q_total < world_size) fail(RADMM_INVALID_ARGUMENT, "fewer sensors than ranks");
+    const int b = (int)((int64_t)rank * q_total / world_size);
+    const int e = (int)((int64_t)(rank + 1) * q_total / world_size);
+    if (q_begin != b || q_end != e)
+      fail(RADMM_INVALID_ARGUMENT, "sensor range must be the contiguous block [r*Q/G, (r+1)*Q/G)");
+    auto c = std::make_unique<radmm_ctx>();
+    init_ctx(c.get(), device, n_pixels, e - b);
+    c->Q_total = q_total;
+    c->q_begin = b;
+    c->rank = rank;
+    c->world = world_size;
+    c->q_max_local = (q_total + world_size - 1) / world_size;
+    if (world_size > 1) {
+      if (!nccl_id) fail(RADMM_INVALID_ARGUMENT, "null NCCL id");
+      g_nccl.load();
+      nccl_uid id;
+      std::memcpy(id.internal, nccl_id, 128);
+      g_nccl.check(g_nccl.CommInitRank(&c->comm, world_size, id, rank), "ncclCommInitRank");
+      c->send_buf.alloc((size_t)c->q_max_local * n_pixels);
+      c->gathered.alloc((size_t)c->q_max_local * n_pixels * world_size);
+      c->size_send.alloc(2 * (size_t)c->q_max_local + 1);
+      c->size_recv.alloc((2 * (size_t)c->q_max_local + 1) * world_size);
+    }
+    *out = c.release();
+  });
+}
+
+}  // extern "C"
