@@ -81,6 +81,14 @@ def notice_size(n: int) -> int:  # wire.hpp:60-62
     return 1 + 4 + 8 + 4 + n * (4 + 16)
 
 
+def cdiv(v: np.ndarray, d: float) -> np.ndarray:
+    """complex / real the way std::complex<double> / double does it: each
+    component divided by d.  (NumPy's complex division multiplies by the
+    reciprocal, which is not the reference's rounding.)"""
+    v = np.ascontiguousarray(v, dtype=np.complex128)
+    return (v.view(np.float64) / d).view(np.complex128)
+
+
 def soft_threshold(v: np.ndarray, kappa: float) -> np.ndarray:
     """out_i = mag > kappa ? v_i (1 - kappa/mag) : 0  (solver_core.hpp:14-23)."""
     if not kappa >= 0.0:
@@ -123,7 +131,7 @@ class LocalSolve:
             return sla.cho_solve(self.fac, rhs, check_finite=False)
         v = self.a_hat @ rhs
         w = sla.cho_solve(self.fac, v, check_finite=False)
-        return (rhs - self.mu * (self.a_hat.conj().T @ w)) / self.beta
+        return cdiv(rhs - self.mu * (self.a_hat.conj().T @ w), self.beta)
 
 
 class SensorRef:
@@ -225,11 +233,11 @@ class FusionRef:
         s = np.zeros(self.n, dtype=np.complex128)
         for c in self.contrib:            # fixed sensor order
             s = s + c
-        s = s / float(len(self.contrib))
+        s = cdiv(s, float(len(self.contrib)))
         self.s = s
         self.x_g_prev = self.x_g
         self.sigma_pre = self.sigma
-        self.x_g = soft_threshold(s + self.sigma / h.beta, h.lambda_ / h.beta)
+        self.x_g = soft_threshold(s + cdiv(self.sigma, h.beta), h.lambda_ / h.beta)
         eta = s - self.x_g
         self.pri = float(np.linalg.norm(eta))
         self.dual = h.beta * float(np.linalg.norm(self.x_g - self.x_g_prev))
@@ -408,7 +416,7 @@ def straight_line_sadmm(ops, ys, mu, lam, beta, eps_abs, eps_rel, max_iter):
         x = nxt
         s = sum(x) / q_count
         x_prev = x_g
-        x_g = soft_threshold(s + sigma / beta, lam / beta)
+        x_g = soft_threshold(s + cdiv(sigma, beta), lam / beta)
         pri = np.linalg.norm(s - x_g)
         dual = beta * np.linalg.norm(x_g - x_prev)
         sigma = sigma + beta * (s - x_g)

@@ -155,22 +155,40 @@ struct ColLoad<double2> {
   }
 };
 
-template <typename T, int EPI>
+// Fallback dot for vectors too long for shared memory (rows > ~14k, e.g. the
+// reference desk scenario's 24568-row operators): the vector is read through
+// L1/L2 with a bounds check.  Only used on rebuild paths.
+template <typename T>
+__device__ __forceinline__ void dot_global(const void* base, int64_t ld, int col, int len, const double2* __restrict__ vec,
+                                           int lane, double& re, double& im) {
+  re = 0.0;
+  im = 0.0;
+  const T* p = reinterpret_cast<const T*>(base) + (int64_t)col * ld;
+  for (int r = lane; r < len; r += 32) {
+    const T a = p[r];
+    cfma_conj(re, im, (double)a.x, (double)a.y, __ldg(vec + r));
+  }
+}
+
+template <typename T, int EPI, bool SMEM_VEC>
 __global__ void __launch_bounds__(256) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
   extern __shared__ double2 sv[];
   const ColDotJob& jb = jobs.j[blockIdx.y];
   const int n_out = jb.n_out;
   if ((int)blockIdx.x * 8 >= n_out) return;
   const int64_t ld = jb.ld;
-  for (int r = threadIdx.x; r < ld; r += blockDim.x) sv[r] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
-  __syncthreads();
+  if (SMEM_VEC) {
+    for (int r = threadIdx.x; r < ld; r += blockDim.x) sv[r] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int steps = (int)((jb.len + ColLoad<T>::kRowsPerStep - 1) / ColLoad<T>::kRowsPerStep);
   for (int i = blockIdx.x * 8 + warp; i < n_out; i += gridDim.x * 8) {
     const int col = jb.cols ? jb.cols[i] : i;
     double re, im;
-    ColLoad<T>::dot(jb.M, ld, col, steps, sv, lane, re, im);
+    if (SMEM_VEC) ColLoad<T>::dot(jb.M, ld, col, steps, sv, lane, re, im);
+    else dot_global<T>(jb.M, ld, col, jb.len, jb.vec, lane, re, im);
     re = warp_sum(re);
     im = warp_sum(im);
     if (lane == 0) {

@@ -233,6 +233,7 @@ struct radmm_ctx {
 namespace {
 
 constexpr int kCtasPerSmTarget = 8;
+constexpr size_t kColdotSmemMax = 200 * 1024;
 
 void set_device(radmm_ctx* c) { CK(cudaSetDevice(c->device)); }
 
@@ -313,14 +314,21 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
     }
     if (n_max == 0) continue;
     const size_t smem = (size_t)ld_max * sizeof(double2);
-    if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(coldot_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    if (smem > 227 * 1024) fail(RADMM_INVALID_ARGUMENT, "operator rows exceed the shared-memory vector budget");
-    const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
-    const int target = c->sm_count * per_sm;
-    int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
-    dim3 grid(gx, (unsigned)nb);
-    LAUNCH(c, (coldot_kernel<T, EPI>), grid, 256, smem, pk, mu, beta);
+    if (smem <= kColdotSmemMax) {
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(coldot_kernel<T, EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024));
+      const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
+      const int target = c->sm_count * per_sm;
+      int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
+      dim3 grid(gx, (unsigned)nb);
+      LAUNCH(c, (coldot_kernel<T, EPI, true>), grid, 256, smem, pk, mu, beta);
+    } else {
+      const int target = c->sm_count * 8;
+      int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
+      dim3 grid(gx, (unsigned)nb);
+      LAUNCH(c, (coldot_kernel<T, EPI, false>), grid, 256, 0, pk, mu, beta);
+    }
   }
 }
 

@@ -161,12 +161,14 @@ def test_converged_state_contracts():
         last = r.report.iterations[-1]
         assert np.linalg.norm(r.s - r.x_global) <= last.eps_pri
         assert last.pri_res <= last.eps_pri and last.dual_res <= last.eps_dual
-        assert np.array_equal(api.soft_threshold(r.s + r.sigma_pre_global / h.beta, h.lambda_ / h.beta),
-                              r.x_global)
+        # x_G is exactly the threshold of what it saw (test_admm.cpp:316-319)
+        assert np.array_equal(api.soft_threshold(r.s + admm_ref.cdiv(r.sigma_pre_global, h.beta),
+                                                 h.lambda_ / h.beta), r.x_global)
+        # the aggregate is the average of the sensor images (test_admm.cpp:320-324)
         total = np.zeros_like(r.s)
         for xq in r.sensor_images:
             total = total + xq
-        assert np.array_equal(total / len(r.sensor_images), r.s)
+        assert np.array_equal(admm_ref.cdiv(total, len(r.sensor_images)), r.s)
 
 
 def test_iteration_cap_and_csv():
