@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: ASADMM iterations/s on the BASELINE config-2 workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--no-cpu-baseline] [--ttt]
+
+A step is one ASADMM iteration of the whole problem: staged screening
+(+ compaction and factor downdate when pixels freeze), the Q sensor local
+updates (forward matvec, capacitance-inverse apply, adjoint matvec fused with
+the x-update), the exchange (N > 1) and the fusion / stopping rule.
+
+Workload (BASELINE.json configs[1]): Q=8 sensors, M=8, K=256 (KM=2048),
+128x128 grid (N=16384), dechirped-LFM complex64 operators generated on the
+GPU from seeded geometry/phases (268 MB per sensor, 2.15 GB total -- inputs
+far larger than the 126 MB L2, so no L2 flush is needed between steps),
+60 seeded targets, 20 dB AWGN (bit-exact reference noise stream),
+mu=1, beta=rho=1, lambda = 0.05 max|A^H y|, eps_rel=1e-5, eps_abs=1e-12.
+
+One JSON line (rank 0): value = whole-job iterations/s over K timed
+iterations after W warm-up iterations, device-timed with CUDA events on the
+library stream (max over ranks); e2e = the same metric through the public
+API with host (pinned) buffers, H2D of the operators + setup + the solve +
+D2H of the results inside the timed region; roofline = the dominant kernel's
+algorithmic bytes / its average device time vs the measured HBM peak;
+cpu_baseline = the fp64 CPU oracle on a bounded sample of the same workload.
+--impl reference times the CPU reference path (the oracle restatement;
+the reference itself cannot be built here).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--ttt", action="store_true", help="also run to tolerance (time-to-tolerance)")
+    p.add_argument("--ttt-max-iter", type=int, default=3000)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for n, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(phase: str, config: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    entry = d.get(config, {}).get(phase)
+    return None if entry is None else entry.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def build_workload(cfg, solver, q_begin: int, q_end: int, dist=None):
+    """Operators on the device; scene + bit-exact noise on the host; y = A x + w
+    via the device forward operator; lambda = frac * max |A^H y| (all ranks)."""
+    from paper_2307_08606_b200 import scenario
+    from paper_2307_08606_b200.rng import ComplexGaussian, mix_seed
+    pix, tx, rx = scenario.baseline_geometry(cfg)
+    per_sensor = scenario.baseline_scene(cfg)
+    ys = []
+    lam_local = 0.0
+    for q in range(q_begin, q_end):
+        solver.generate_dechirp_operator(q - q_begin, cfg.M, cfg.K, pix, tx[q], rx[q],
+                                         scenario.baseline_phases(cfg, q), cfg.fc, cfg.bw, cfg.pulse)
+        y = solver.apply(q - q_begin, per_sensor[q].astype(np.complex128))
+        power = float(np.vdot(y, y).real)
+        sigma = math.sqrt(power / (cfg.KM * 10.0 ** (cfg.snr_db / 10.0)))
+        y = y + sigma * ComplexGaussian(mix_seed(cfg.seed, q + 1)).draw(cfg.KM)
+        solver.set_measurement(q - q_begin, y)
+        ys.append(y)
+        lam_local = max(lam_local, float(np.abs(solver.apply_adjoint(q - q_begin, y)).max()))
+    if dist is not None:
+        import torch
+        t = torch.tensor([lam_local], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lam_local = float(t.item())
+    return ys, cfg.lambda_frac * lam_local
+
+
+def algorithmic_bytes_per_iteration(cfg, sizes):
+    """Dual form: 2 passes over the active columns + the KM^2 capacitance
+    inverse (c128) + O(N) vectors."""
+    km = cfg.KM
+    return sum(2.0 * km * n * 8 + km * km * 16 for n in sizes) + 12.0 * cfg.N * 16
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle; bounded sample)
+# ---------------------------------------------------------------------------
+def cpu_sample(cfg, iters: int, sample_sensors: int = 2):
+    """fp64 oracle (NumPy/SciPy, all BLAS threads) on `sample_sensors` of the Q
+    sensors: time `iters` local updates + the fusion round; extrapolate the
+    per-sensor cost x Q (the Jacobi sweep is a sum of independent per-sensor
+    solves, admm.hpp:389-390).  Setup (Woodbury factor) is excluded."""
+    from oracle import admm_ref
+    from paper_2307_08606_b200 import scenario
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
+    except Exception:
+        cores = os.cpu_count() or 1
+    per_sensor = scenario.baseline_scene(cfg)
+    h = admm_ref.Hyper(mu=cfg.mu, lambda_=1.0, beta=cfg.beta, eps_abs=cfg.eps_abs, eps_rel=cfg.eps_rel,
+                       max_iter=iters)
+    sensors = []
+    for q in range(sample_sensors):
+        a = scenario.baseline_operator(cfg, q).astype(np.complex128)
+        y = scenario.simulate_measurement(a, per_sensor[q], cfg.snr_db,
+                                          scenario.mix_seed(cfg.seed, q + 1))[0]
+        sensors.append(admm_ref.SensorRef(a, y, h))
+    fusion = admm_ref.FusionRef(cfg.N, cfg.Q, h)
+    t_local = 0.0
+    t_fusion = 0.0
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        for s in sensors:
+            s.local_update(fusion.gap, fusion.sigma)
+        t1 = time.perf_counter()
+        for q, s in enumerate(sensors):
+            fusion.set_contribution(q + 1, s.active, s.x_hat)
+        fusion.round()
+        t2 = time.perf_counter()
+        t_local += t1 - t0
+        t_fusion += t2 - t1
+    per_iter = (t_local / sample_sensors) * cfg.Q / iters + t_fusion / iters
+    return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": int(cores), "kind": "port",
+            "sample": (f"fp64 NumPy/SciPy oracle (Woodbury form), {sample_sensors} of {cfg.Q} sensors x {iters} "
+                       f"iterations timed, per-sensor local-update time x{cfg.Q} + fusion; "
+                       f"setup excluded; {cfg.name} shapes")}
+
+
+def reference_arm(args, cfg):
+    from paper_2307_08606_b200.distributed import env_rank_world
+    rank, world, _ = env_rank_world()
+    if world > 1 and rank != 0:
+        return
+    base = cpu_sample(cfg, max(1, args.steps))
+    v = base["value"]
+    out = {"metric": "ASADMM iterations/s", "value": v, "unit": "iterations/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64 complex)", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"BASELINE {cfg.name}: Q={cfg.Q} KM={cfg.KM} N={cfg.N}",
+                      "parallelism": "host BLAS threads"},
+           "cpu_baseline": {"kind": base["kind"], "cores": base["cores"], "sample": base["sample"], "value": v,
+                            "unit": "iterations/s"},
+           "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def ours(args, cfg):
+    import torch
+    from paper_2307_08606_b200 import api, distributed as D
+    import __graft_entry__
+    __graft_entry__.build()
+    rank, world, local = D.env_rank_world()
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo")
+        dist = tdist
+    torch.cuda.set_device(local)
+    uid = D.broadcast_unique_id(rank, world)
+    q0, q1 = D.shard_range(cfg.Q, rank, world)
+    solver = D.sharded_solver(cfg.N, cfg.Q, rank, world, local, uid) if world > 1 else api.Solver(cfg.N, cfg.Q, local)
+    ys, lam = build_workload(cfg, solver, q0, q1, dist)
+    W, K = args.warmup, args.steps
+    hyper = api.Hyperparams(mu=cfg.mu, lambda_=lam, beta=cfg.beta, eps_abs=cfg.eps_abs, eps_rel=cfg.eps_rel,
+                            screening_window=5, screening_tol=1e-5, max_iter=W + K)
+
+    # ---- timed run: W warm-up + K timed iterations, device-timed ----------
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    res = solver.run(hyper, api.Mode.ASADMM, fixed_iterations=True, fetch=False)
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    it_ms, it_launch = solver.iteration_stats(res.iterations)
+    timed_ms = float(np.sum(it_ms[W:W + K]))
+    launches = int(np.sum(it_launch[W:W + K]))
+    if dist is not None:
+        t = torch.tensor([timed_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        timed_ms = float(t.item())
+    value = K / (timed_ms / 1000.0)
+
+    # ---- profiling pass: per-phase device time + algorithmic bytes ----------
+    solver.set_profiling(True)
+    solver.run(hyper, api.Mode.ASADMM, fixed_iterations=True, fetch=False)
+    phases = solver.phase_stats()
+    solver.set_profiling(False)
+    peak, peak_kind = measured_peaks()
+    kern = max(("forward", "adjoint", "gapply", "primal"), key=lambda p: phases[p]["ms"])
+    ph = phases[kern]
+    per_launch_ms = ph["ms"] / max(1, ph["calls"])
+    per_launch_bytes = ph["bytes"] / max(1, ph["calls"])
+    achieved = per_launch_bytes / (per_launch_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_kind,
+                "traffic": ncu_traffic(kern, cfg.name),
+                "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_ms": per_launch_ms,
+                "phases": {k: {"ms_per_call": v["ms"] / max(1, v["calls"]),
+                               "GBps": (v["bytes"] / (v["ms"] / 1000.0) / 1e9) if v["ms"] > 0 else None,
+                               "share": v["ms"] / max(1e-9, sum(p["ms"] for p in phases.values()))}
+                           for k, v in phases.items() if v["calls"]}}
+
+    # ---- time to tolerance ------------------------------------------------
+    ttt = None
+    if args.ttt:
+        h2 = api.Hyperparams(**{**hyper.__dict__, "max_iter": args.ttt_max_iter})
+        r2 = solver.run(h2, api.Mode.ASADMM, fetch=False)
+        ms2, _ = solver.iteration_stats(r2.iterations)
+        ttt = {"converged": r2.converged, "iterations": r2.iterations, "solve_s_device": float(np.sum(ms2)) / 1e3,
+               "setup_s": r2.setup_ms / 1e3, "max_iter": args.ttt_max_iter}
+    solver.close()
+
+    # ---- e2e through the public API with pinned host buffers ---------------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = e2e_run(cfg, hyper, ys)
+
+    # ---- CPU baseline ------------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg, 3)
+
+    bytes_iter = algorithmic_bytes_per_iteration(cfg, [cfg.N] * cfg.Q)
+    if rank == 0:
+        out = {"metric": "ASADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
+               "steps": K, "warmup": W, "ms_per_step": timed_ms / K, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "c64 operator, fp64 arithmetic",
+               "data": "synthetic (seeded BASELINE dechirp operators generated on device)",
+               "config": {"workload": f"BASELINE {cfg.name}: Q={cfg.Q} M={cfg.M} K={cfg.K} KM={cfg.KM} "
+                                      f"N={cfg.N} (128x128), {cfg.n_targets} targets, {cfg.snr_db} dB",
+                          "global_batch": cfg.Q, "parallelism": f"sensor-sharded x{world}",
+                          "l2": "inputs 2.15 GB >> 126 MB L2 (no flush needed)",
+                          "hyper": {"mu": cfg.mu, "beta": cfg.beta, "lambda": lam, "eps_rel": cfg.eps_rel,
+                                    "eps_abs": cfg.eps_abs, "W": 5, "tol": 1e-5}},
+               "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+               "iteration_GBps_algorithmic": bytes_iter * value / 1e9,
+               "cpu_baseline": cpu, "e2e": e2e, "time_to_tolerance": ttt,
+               "active_sizes_end": None}
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_run(cfg, hyper, ys):
+    """The public call a user makes (api.run on host numpy arrays), with the
+    operators in pinned host memory: H2D of A + y, initial factorization,
+    W+K iterations and D2H of every RunResult field, timed with CUDA events."""
+    import torch
+    from paper_2307_08606_b200 import api, scenario
+    pinned = torch.empty((cfg.Q, cfg.N, cfg.KM), dtype=torch.complex64, pin_memory=True)
+    gen = api.Solver(cfg.N, cfg.Q)
+    pix, tx, rx = scenario.baseline_geometry(cfg)
+    for q in range(cfg.Q):
+        gen.generate_dechirp_operator(q, cfg.M, cfg.K, pix, tx[q], rx[q], scenario.baseline_phases(cfg, q),
+                                      cfg.fc, cfg.bw, cfg.pulse)
+        pinned[q].numpy()[:] = gen.get_operator(q).T
+    gen.close()
+    ops = [api.ForwardOperator.from_matrix(pinned[q].numpy().T) for q in range(cfg.Q)]  # F-contiguous views
+    prob = api.Problem(ops, ys)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = api.run(prob, hyper, api.Mode.ASADMM, fixed_iterations=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    h2d = sum(a.matrix().nbytes for a in ops) + sum(np.asarray(y).nbytes for y in ys)
+    d2h = (r.image.nbytes + 4 * r.x_global.nbytes + sum(x.nbytes for x in r.sensor_images)
+           + sum(a.nbytes for a in r.active_sets))
+    return {"value": r.iterations / (ms / 1000.0), "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "step": f"one api.run call of {r.iterations} iterations",
+            "ms": ms, "setup_ms": r.setup_ms, "solve_ms": r.solve_ms}
+
+
+def main():
+    args = parse()
+    from paper_2307_08606_b200 import scenario
+    cfg = scenario.baseline_config(args.config)
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -182,6 +182,41 @@ int radmm_solve_local(radmm_solve_cache* cache, const double* rhs, double* x);
 int radmm_solve_cache_destroy(radmm_solve_cache* cache);
 int radmm_soft_threshold(int device, const double* v, int64_t n, double kappa, double* out);
 
+/* ---- operator application (forward_model.hpp:147-177) ------------------ */
+/* y = A_q x (x: N complex128, y: rows complex128), host buffers. */
+int radmm_apply_operator(radmm_ctx* ctx, int q, const double* x, double* y);
+/* x = A_q^H y (y: rows complex128, x: N complex128), host buffers. */
+int radmm_apply_adjoint(radmm_ctx* ctx, int q, const double* y, double* x);
+
+/* ---- device-side measurement ------------------------------------------- */
+/* Phases of one iteration, timed with CUDA events on the context's stream
+ * when profiling is enabled; bytes are ALGORITHMIC bytes. */
+typedef enum {
+  RADMM_PHASE_FORWARD = 0,   /* v = A_J rhs (+ rhs prologue, partial reduce) */
+  RADMM_PHASE_GAPPLY = 1,    /* w = G v (capacitance inverse apply)          */
+  RADMM_PHASE_ADJOINT = 2,   /* x = (rhs - mu A_J^H w)/beta + scatter/ring   */
+  RADMM_PHASE_PRIMAL = 3,    /* x = Hinv rhs (primal form sensors)           */
+  RADMM_PHASE_EXCHANGE = 4,  /* NCCL all-gather of sensor images             */
+  RADMM_PHASE_FUSION = 5,    /* average, threshold, dual, norms, stop rule   */
+  RADMM_PHASE_SCREEN = 6,    /* zeta + ballot/prefix-sum compaction          */
+  RADMM_PHASE_REFACTOR = 7,  /* frozen echo, data term, downdate / rebuild   */
+  RADMM_PHASE_COUNT = 8
+} radmm_phase;
+
+typedef struct {
+  int64_t calls;     /* times the phase ran */
+  int64_t launches;  /* kernels launched by it */
+  double total_ms;   /* device time (CUDA events) */
+  double bytes;      /* algorithmic bytes moved */
+} radmm_phase_stat;
+
+int radmm_set_profiling(radmm_ctx* ctx, int enabled);
+/* out[RADMM_PHASE_COUNT], accumulated over the last run. */
+int radmm_get_phase_stats(radmm_ctx* ctx, radmm_phase_stat* out);
+/* Device time (CUDA events) and kernel launches of each iteration of the
+ * last run (screening + refactor + local updates + exchange + fusion). */
+int radmm_get_iteration_stats(radmm_ctx* ctx, double* device_ms, int64_t* launches, int capacity);
+
 /* ---- sharded runs over NCCL (runtime.hpp:768-775 analogue) ------------- */
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
 int radmm_nccl_unique_id(uint8_t out[128]);

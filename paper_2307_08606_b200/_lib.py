@@ -79,6 +79,13 @@ class Summary(C.Structure):
                 ("rebuilds", C.c_int64), ("downdates", C.c_int64)]
 
 
+class PhaseStat(C.Structure):
+    _fields_ = [("calls", C.c_int64), ("launches", C.c_int64), ("total_ms", C.c_double), ("bytes", C.c_double)]
+
+
+PHASES = ["forward", "gapply", "adjoint", "primal", "exchange", "fusion", "screen", "refactor"]
+
+
 # Every symbol include/radmm_b200.h declares, with its argument types.
 _VP = C.c_void_p
 _DP = C.POINTER(C.c_double)
@@ -111,6 +118,11 @@ SIGNATURES = {
     "radmm_solve_local": (C.c_int, [_VP, _DP, _DP]),
     "radmm_solve_cache_destroy": (C.c_int, [_VP]),
     "radmm_soft_threshold": (C.c_int, [C.c_int, _DP, C.c_int64, C.c_double, _DP]),
+    "radmm_apply_operator": (C.c_int, [_VP, C.c_int, _DP, _DP]),
+    "radmm_apply_adjoint": (C.c_int, [_VP, C.c_int, _DP, _DP]),
+    "radmm_set_profiling": (C.c_int, [_VP, C.c_int]),
+    "radmm_get_phase_stats": (C.c_int, [_VP, C.POINTER(PhaseStat)]),
+    "radmm_get_iteration_stats": (C.c_int, [_VP, _DP, C.POINTER(C.c_int64), C.c_int]),
     "radmm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "radmm_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(C.c_uint8), C.POINTER(_VP)]),

@@ -294,6 +294,40 @@ class Solver:
         _lib.check(_lib.lib().radmm_get_operator_c64(self._h, q, out.ctypes.data_as(C.c_void_p)))
         return out.T
 
+    def apply(self, q: int, x) -> np.ndarray:
+        """ForwardOperator::apply (forward_model.hpp:147-160) on the GPU."""
+        x = _c128(x)
+        if x.shape[0] != self.N:
+            raise InvalidArgument(_lib.INVALID_ARGUMENT, "ForwardOperator::apply: size mismatch")
+        y = np.empty(self.rows[q], dtype=np.complex128)
+        _lib.check(_lib.lib().radmm_apply_operator(self._h, q, _dptr(x), _dptr(y)))
+        return y
+
+    def apply_adjoint(self, q: int, y) -> np.ndarray:
+        """ForwardOperator::apply_adjoint (forward_model.hpp:162-177) on the GPU."""
+        y = _c128(y)
+        if y.shape[0] != self.rows[q]:
+            raise InvalidArgument(_lib.INVALID_ARGUMENT, "ForwardOperator::apply_adjoint: size mismatch")
+        x = np.empty(self.N, dtype=np.complex128)
+        _lib.check(_lib.lib().radmm_apply_adjoint(self._h, q, _dptr(y), _dptr(x)))
+        return x
+
+    def set_profiling(self, enabled: bool) -> None:
+        _lib.check(_lib.lib().radmm_set_profiling(self._h, int(bool(enabled))))
+
+    def phase_stats(self) -> dict:
+        arr = (_lib.PhaseStat * len(_lib.PHASES))()
+        _lib.check(_lib.lib().radmm_get_phase_stats(self._h, arr))
+        return {name: dict(calls=int(a.calls), launches=int(a.launches), ms=float(a.total_ms),
+                           bytes=float(a.bytes)) for name, a in zip(_lib.PHASES, arr)}
+
+    def iteration_stats(self, iterations: int):
+        ms = np.empty(max(1, iterations))
+        ln = np.empty(max(1, iterations), dtype=np.int64)
+        _lib.check(_lib.lib().radmm_get_iteration_stats(self._h, _dptr(ms), ln.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                        ms.size))
+        return ms[:iterations], ln[:iterations]
+
     # ---- run -----------------------------------------------------------
     def run(self, hyper: Hyperparams, mode: Mode = Mode.ASADMM, observer=None,
             disable_screening: bool = False, fixed_iterations: bool = False,

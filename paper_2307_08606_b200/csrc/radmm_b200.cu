@@ -219,9 +219,26 @@ struct radmm_ctx {
   int64_t rebuilds = 0, downdates = 0;
   int W = 5;
   int upd = 0;  // local updates performed in the current run
+  // device timing: per-iteration CUDA events (always), per-phase events
+  // (profiling mode) -- all on this context's stream.
+  cudaEvent_t ev_it0 = nullptr, ev_it1 = nullptr;
+  std::vector<double> iter_ms;
+  std::vector<int64_t> iter_launches;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;  // events handed out since the last flush
+  struct Mark { int cat; int ev0, ev1; double bytes; int64_t launches; };
+  std::vector<Mark> marks;
+  double prof_ms[RADMM_PHASE_COUNT] = {};
+  double prof_bytes[RADMM_PHASE_COUNT] = {};
+  int64_t prof_launches[RADMM_PHASE_COUNT] = {};
+  int64_t prof_calls[RADMM_PHASE_COUNT] = {};
 
   ~radmm_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    if (ev_it0) cudaEventDestroy(ev_it0);
+    if (ev_it1) cudaEventDestroy(ev_it1);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     if (fs_host) cudaFreeHost(fs_host);
     if (h_totals) cudaFreeHost(h_totals);
@@ -234,6 +251,56 @@ namespace {
 
 constexpr int kCtasPerSmTarget = 8;
 constexpr size_t kColdotSmemMax = 200 * 1024;
+
+// ---- device-time accounting (CUDA events on the context stream) -------------
+cudaEvent_t take_event(radmm_ctx* c, int& idx) {
+  if (c->ev_used >= (int)c->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  idx = c->ev_used++;
+  return c->ev_pool[idx];
+}
+
+struct PhaseScope {
+  radmm_ctx* c;
+  int cat;
+  double bytes;
+  int e0 = -1;
+  int64_t l0 = 0;
+  PhaseScope(radmm_ctx* ctx, int category, double algorithmic_bytes) : c(ctx), cat(category), bytes(algorithmic_bytes) {
+    if (!c->profiling) return;
+    CK(cudaEventRecord(take_event(c, e0), c->stream));
+    l0 = c->launches;
+  }
+  ~PhaseScope() {
+    if (!c->profiling || e0 < 0) return;
+    int e1;
+    if (c->ev_used >= (int)c->ev_pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      c->ev_pool.push_back(e);
+    }
+    e1 = c->ev_used++;
+    if (cudaEventRecord(c->ev_pool[e1], c->stream) != cudaSuccess) return;
+    c->marks.push_back({cat, e0, e1, bytes, c->launches - l0});
+  }
+};
+
+// Called after a stream synchronize: fold the recorded phases into the stats.
+void flush_marks(radmm_ctx* c) {
+  for (const auto& m : c->marks) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_pool[m.ev0], c->ev_pool[m.ev1]));
+    c->prof_ms[m.cat] += ms;
+    c->prof_bytes[m.cat] += m.bytes;
+    c->prof_launches[m.cat] += m.launches;
+    c->prof_calls[m.cat] += 1;
+  }
+  c->marks.clear();
+  c->ev_used = 0;
+}
 
 void set_device(radmm_ctx* c) { CK(cudaSetDevice(c->device)); }
 
@@ -727,12 +794,24 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
       pj.push_back(p);
     }
   }
+  double a_bytes = 0, g_bytes = 0, p_bytes = 0;
+  for (const auto& a : aj) a_bytes += 8.0 * a.len * a.n_out;
+  for (const auto& g : gj) g_bytes += 16.0 * g.len * g.n_out;
+  for (const auto& p : pj) p_bytes += 16.0 * p.len * p.n_out;
   if (!fj.empty()) {
-    forward<MODE_RHS>(c, fj, rj, h->beta);
-    coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+    {
+      PhaseScope ps(c, RADMM_PHASE_FORWARD, a_bytes);
+      forward<MODE_RHS>(c, fj, rj, h->beta);
+    }
+    {
+      PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
+      coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+    }
+    PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
     coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta);
   }
   if (n_rhs) {
+    PhaseScope ps(c, RADMM_PHASE_PRIMAL, p_bytes);
     LAUNCH(c, rhs_kernel, dim3((rhs_max + 255) / 256, n_rhs), 256, 0, rh, c->gap.p, c->sigma.p, h->beta);
     coldot<double2, EPI_XPRIMAL>(c, pj, h->mu, h->beta);
   }
@@ -744,6 +823,7 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
 void exchange(radmm_ctx* c, double notice_bytes) {
   if (c->world <= 1) return;
   const size_t N = c->N;
+  PhaseScope ps(c, RADMM_PHASE_EXCHANGE, 16.0 * N * c->q_max_local * c->world);
   for (int q = 0; q < c->Q; ++q)
     CK(cudaMemcpyAsync(c->send_buf.p + (size_t)q * N, c->sensors[q].x_full.p, sizeof(double2) * N,
                        cudaMemcpyDeviceToDevice, c->stream));
@@ -777,6 +857,7 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   a.counter = c->fcounter.p;
   a.out_dev = c->fs_dev.p;
   a.out_host = c->fs_host_dev;
+  PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
   LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
 
@@ -798,9 +879,14 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     n_max = std::max(n_max, S.n_act);
   }
   const int nb = (n_max + kScanBlock - 1) / kScanBlock;
-  LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol);
-  LAUNCH(c, screen_scan_kernel, dim3(c->Q), 32, 0, pk);
-  LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk);
+  {
+    double sb = 0;
+    for (int q = 0; q < c->Q; ++q) sb += (double)c->sensors[q].n_act * (8.0 * c->W + 4 + 1 + 4 + 4 + 32);
+    PhaseScope ps(c, RADMM_PHASE_SCREEN, sb);
+    LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol);
+    LAUNCH(c, screen_scan_kernel, dim3(c->Q), 32, 0, pk);
+    LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk);
+  }
   for (int q = 0; q < c->Q; ++q)
     CK(cudaMemcpyAsync(c->h_totals + q, c->sensors[q].totals.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -832,6 +918,12 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   }
   if (changed.empty()) return notice;
   // rebuild() (admm.hpp:171-179): frozen echo, data term, factor
+  double rb = 0;
+  for (int q : changed) {
+    const Sensor& S = c->sensors[q];
+    rb += 8.0 * S.rows * (S.n_act + S.removed_now) + (S.primal ? 32.0 * S.n_act * S.n_act : 48.0 * S.rows * S.rows);
+  }
+  PhaseScope ps(c, RADMM_PHASE_REFACTOR, rb);
   update_y_eff(c, changed);
   data_terms(c, changed, h->mu);
   std::vector<int> rebuild, down;
@@ -879,6 +971,18 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   c->have_result = false;
   c->launches = 0;
   c->rebuilds = c->downdates = 0;
+  c->iter_ms.clear();
+  c->iter_launches.clear();
+  c->marks.clear();
+  c->ev_used = 0;
+  for (int i = 0; i < RADMM_PHASE_COUNT; ++i) {
+    c->prof_ms[i] = c->prof_bytes[i] = 0;
+    c->prof_launches[i] = c->prof_calls[i] = 0;
+  }
+  if (!c->ev_it0) {
+    CK(cudaEventCreate(&c->ev_it0));
+    CK(cudaEventCreate(&c->ev_it1));
+  }
   radmm_run_summary sm{};
   const auto t0 = std::chrono::steady_clock::now();
   build_contrib(c);
@@ -894,11 +998,21 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   FusionScalars f{};
   for (int k = 1; k <= h->max_iter; ++k) {
     uint64_t notice = 0;
+    const int64_t l0 = c->launches;
+    CK(cudaEventRecord(c->ev_it0, c->stream));
     if (asadmm && !disable && staged_trigger) notice = screen_all(c, h, k);
     local_updates(c, h);
     exchange(c, (double)notice);
     run_fusion(c, h, k);
+    CK(cudaEventRecord(c->ev_it1, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev_it0, c->ev_it1));
+      c->iter_ms.push_back(ms);
+      c->iter_launches.push_back(c->launches - l0);
+    }
+    flush_marks(c);
     f = *c->fs_host;
     radmm_iteration_record rec{};
     rec.iteration = k;
@@ -1275,6 +1389,73 @@ int radmm_soft_threshold(int device, const double* v, int64_t n, double kappa, d
     soft_threshold_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dv.p, n, kappa, dout.p);
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_apply_operator(radmm_ctx* ctx, int q, const double* x, double* y) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!S.has_op || !x || !y) fail(RADMM_INVALID_ARGUMENT, "ForwardOperator::apply: size mismatch");
+    set_device(ctx);
+    const int N = ctx->N;
+    DArr<double2> dx;
+    DArr<int> idx;
+    dx.alloc(N, false);
+    idx.alloc(N, false);
+    CK(cudaMemcpy(dx.p, x, sizeof(double2) * N, cudaMemcpyHostToDevice));
+    LAUNCH(ctx, iota_kernel, dim3((N + 255) / 256), 256, 0, idx.p, N);
+    FwdJob f{};
+    f.A = S.A.p; f.ld = S.ld; f.n = N; f.J = idx.p; f.src = dx.p; f.part = S.part.p;
+    plan_chunks(ctx, S, N, 1, f.n_chunks, f.chunk_len);
+    forward<MODE_GATHER>(ctx, {f}, {ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0}}, 0.0);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(y, S.v.p, sizeof(double2) * S.rows, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_apply_adjoint(radmm_ctx* ctx, int q, const double* y, double* x) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (!S.has_op || !x || !y) fail(RADMM_INVALID_ARGUMENT, "ForwardOperator::apply_adjoint: size mismatch");
+    set_device(ctx);
+    const int N = ctx->N;
+    DArr<double2> dy, dx;
+    DArr<int> idx;
+    dy.alloc(S.ld);
+    dx.alloc(N, false);
+    idx.alloc(N, false);
+    CK(cudaMemcpy(dy.p, y, sizeof(double2) * S.rows, cudaMemcpyHostToDevice));
+    LAUNCH(ctx, iota_kernel, dim3((N + 255) / 256), 256, 0, idx.p, N);
+    ColDotJob j{};
+    j.M = S.A.p; j.ld = S.ld; j.len = S.rows; j.n_out = N; j.cols = idx.p; j.vec = dy.p; j.out = dx.p; j.scale = 1.0;
+    coldot<float2, EPI_STORE>(ctx, {j}, 1.0, 1.0);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(x, dx.p, sizeof(double2) * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_set_profiling(radmm_ctx* ctx, int enabled) {
+  return guarded([&] {
+    if (!ctx) fail(RADMM_INVALID_ARGUMENT, "null context");
+    ctx->profiling = enabled != 0;
+  });
+}
+
+int radmm_get_phase_stats(radmm_ctx* ctx, radmm_phase_stat* out) {
+  return guarded([&] {
+    need_result(ctx);
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    for (int i = 0; i < RADMM_PHASE_COUNT; ++i)
+      out[i] = radmm_phase_stat{ctx->prof_calls[i], ctx->prof_launches[i], ctx->prof_ms[i], ctx->prof_bytes[i]};
+  });
+}
+
+int radmm_get_iteration_stats(radmm_ctx* ctx, double* device_ms, int64_t* launches, int capacity) {
+  return guarded([&] {
+    need_result(ctx);
+    if (capacity < (int)ctx->iter_ms.size()) fail(RADMM_INVALID_ARGUMENT, "output too small");
+    if (device_ms) std::memcpy(device_ms, ctx->iter_ms.data(), sizeof(double) * ctx->iter_ms.size());
+    if (launches) std::memcpy(launches, ctx->iter_launches.data(), sizeof(int64_t) * ctx->iter_launches.size());
   });
 }
 
