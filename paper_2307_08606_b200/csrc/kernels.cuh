@@ -86,76 +86,107 @@ struct ColDotJob {
   double* ring_slot;   // screening ring row for this update (N doubles)
 };
 
-template <typename T>
+// Columns per warp (CPW): each vector element fetched from shared memory
+// feeds CPW columns (CPW x fewer LDS per HBM byte) and each lane keeps
+// 2*CPW independent 16-B loads in flight.
+constexpr int kCPW = 4;  // upper bound (ColDot launch picks 1, 2 or 4)
+
+template <typename T, int CPW>
 struct ColLoad;
 
-template <>
-struct ColLoad<float2> {
-  // a lane covers 2 complex per step; a warp 64 rows.
+// complex64 operator columns.  The shared vector is stored split by row
+// parity (sv_e[i] = vec[2i], sv_o[i] = vec[2i+1]) so a lane's two complex
+// values for its float4 are two conflict-free 16-B loads.
+template <int CPW>
+struct ColLoad<float2, CPW> {
   static constexpr int kRowsPerStep = 64;
-  __device__ static __forceinline__ void dot(const void* base, int64_t ld, int col, int steps,
-                                             const double2* __restrict__ sv, int lane,
-                                             double& re, double& im) {
-    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(base) + (int64_t)col * ld) + lane;
-    double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
-    const double2* v = sv + 2 * lane;
+  __device__ static __forceinline__ void dot(const void* base, int64_t ld, const int (&col)[CPW], int steps,
+                                             const double2* __restrict__ sv, int64_t half, int lane,
+                                             double (&re)[CPW], double (&im)[CPW]) {
+    const float4* p[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      p[c] = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(base) + (int64_t)col[c] * ld) + lane;
+      re[c] = 0.0;
+      im[c] = 0.0;
+    }
+    const double2* ve = sv + lane;
+    const double2* vo = sv + half + lane;
     int s = 0;
 #pragma unroll 1
-    for (; s + 4 <= steps; s += 4) {
-      float4 a0 = __ldg(p + (s + 0) * 32);
-      float4 a1 = __ldg(p + (s + 1) * 32);
-      float4 a2 = __ldg(p + (s + 2) * 32);
-      float4 a3 = __ldg(p + (s + 3) * 32);
-      cfma_conj(r0, i0, a0.x, a0.y, v[(s + 0) * 64]);
-      cfma_conj(r1, i1, a0.z, a0.w, v[(s + 0) * 64 + 1]);
-      cfma_conj(r0, i0, a1.x, a1.y, v[(s + 1) * 64]);
-      cfma_conj(r1, i1, a1.z, a1.w, v[(s + 1) * 64 + 1]);
-      cfma_conj(r0, i0, a2.x, a2.y, v[(s + 2) * 64]);
-      cfma_conj(r1, i1, a2.z, a2.w, v[(s + 2) * 64 + 1]);
-      cfma_conj(r0, i0, a3.x, a3.y, v[(s + 3) * 64]);
-      cfma_conj(r1, i1, a3.z, a3.w, v[(s + 3) * 64 + 1]);
+    for (; s + 2 <= steps; s += 2) {
+      float4 a0[CPW], a1[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) a0[c] = __ldg(p[c] + (s + 0) * 32);
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) a1[c] = __ldg(p[c] + (s + 1) * 32);
+      const double2 e0 = ve[(s + 0) * 32], o0 = vo[(s + 0) * 32];
+      const double2 e1 = ve[(s + 1) * 32], o1 = vo[(s + 1) * 32];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        cfma_conj(re[c], im[c], a0[c].x, a0[c].y, e0);
+        cfma_conj(re[c], im[c], a0[c].z, a0[c].w, o0);
+        cfma_conj(re[c], im[c], a1[c].x, a1[c].y, e1);
+        cfma_conj(re[c], im[c], a1[c].z, a1[c].w, o1);
+      }
     }
     for (; s < steps; ++s) {
-      float4 a0 = __ldg(p + s * 32);
-      cfma_conj(r0, i0, a0.x, a0.y, v[s * 64]);
-      cfma_conj(r1, i1, a0.z, a0.w, v[s * 64 + 1]);
+      const double2 e0 = ve[s * 32], o0 = vo[s * 32];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const float4 a0 = __ldg(p[c] + s * 32);
+        cfma_conj(re[c], im[c], a0.x, a0.y, e0);
+        cfma_conj(re[c], im[c], a0.z, a0.w, o0);
+      }
     }
-    re = r0 + r1;
-    im = i0 + i1;
   }
+  // smem layout: even rows then odd rows
+  __device__ static __forceinline__ int64_t slot(int64_t r, int64_t half) { return (r & 1) ? half + (r >> 1) : (r >> 1); }
 };
 
-template <>
-struct ColLoad<double2> {
+// complex128 matrices (capacitance inverse G, primal Hinv).
+template <int CPW>
+struct ColLoad<double2, CPW> {
   static constexpr int kRowsPerStep = 32;
-  __device__ static __forceinline__ void dot(const void* base, int64_t ld, int col, int steps,
-                                             const double2* __restrict__ sv, int lane,
-                                             double& re, double& im) {
-    const double2* p = reinterpret_cast<const double2*>(base) + (int64_t)col * ld + lane;
-    double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
+  __device__ static __forceinline__ void dot(const void* base, int64_t ld, const int (&col)[CPW], int steps,
+                                             const double2* __restrict__ sv, int64_t /*half*/, int lane,
+                                             double (&re)[CPW], double (&im)[CPW]) {
+    const double2* p[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      p[c] = reinterpret_cast<const double2*>(base) + (int64_t)col[c] * ld + lane;
+      re[c] = 0.0;
+      im[c] = 0.0;
+    }
     const double2* v = sv + lane;
     int s = 0;
 #pragma unroll 1
-    for (; s + 4 <= steps; s += 4) {
-      double2 a0 = __ldg(p + (s + 0) * 32);
-      double2 a1 = __ldg(p + (s + 1) * 32);
-      double2 a2 = __ldg(p + (s + 2) * 32);
-      double2 a3 = __ldg(p + (s + 3) * 32);
-      cfma_conj(r0, i0, a0.x, a0.y, v[(s + 0) * 32]);
-      cfma_conj(r1, i1, a1.x, a1.y, v[(s + 1) * 32]);
-      cfma_conj(r0, i0, a2.x, a2.y, v[(s + 2) * 32]);
-      cfma_conj(r1, i1, a3.x, a3.y, v[(s + 3) * 32]);
+    for (; s + 2 <= steps; s += 2) {
+      double2 a0[CPW], a1[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) a0[c] = __ldg(p[c] + (s + 0) * 32);
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) a1[c] = __ldg(p[c] + (s + 1) * 32);
+      const double2 v0 = v[(s + 0) * 32], v1 = v[(s + 1) * 32];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        cfma_conj(re[c], im[c], a0[c].x, a0[c].y, v0);
+        cfma_conj(re[c], im[c], a1[c].x, a1[c].y, v1);
+      }
     }
     for (; s < steps; ++s) {
-      double2 a0 = __ldg(p + s * 32);
-      cfma_conj(r0, i0, a0.x, a0.y, v[s * 32]);
+      const double2 v0 = v[s * 32];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const double2 a0 = __ldg(p[c] + s * 32);
+        cfma_conj(re[c], im[c], a0.x, a0.y, v0);
+      }
     }
-    re = r0 + r1;
-    im = i0 + i1;
   }
+  __device__ static __forceinline__ int64_t slot(int64_t r, int64_t) { return r; }
 };
 
-// Fallback dot for vectors too long for shared memory (rows > ~14k, e.g. the
+// Fallback dot for vectors too long for shared memory (rows > ~12k, e.g. the
 // reference desk scenario's 24568-row operators): the vector is read through
 // L1/L2 with a bounds check.  Only used on rebuild paths.
 template <typename T>
@@ -170,45 +201,76 @@ __device__ __forceinline__ void dot_global(const void* base, int64_t ld, int col
   }
 }
 
-template <typename T, int EPI, bool SMEM_VEC>
+template <int EPI>
+__device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, double re, double im, double mu,
+                                                double beta) {
+  if (EPI == EPI_STORE) {
+    jb.out[i] = make_double2(__dmul_rn(jb.scale, re), __dmul_rn(jb.scale, im));
+  } else {
+    double2 xh;
+    if (EPI == EPI_XDUAL) {
+      // x = (rhs - mu * A^H w) / beta  (Woodbury form of solver_core.hpp:47-51)
+      const double2 r = jb.rhs[i];
+      xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re)), beta),
+                        __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im)), beta));
+    } else {
+      xh = make_double2(re, im);
+    }
+    const int p = jb.pix[i];
+    const double2 old = jb.x_full[p];
+    jb.ring_slot[p] = c_abs(c_sub(xh, old));  // |hist[h][j] - hist[h-1][j]| (admm.hpp:143)
+    jb.x_full[p] = xh;                        // admm.hpp:121-122
+    jb.x_hat[i] = xh;                         // admm.hpp:120
+  }
+}
+
+template <typename T, int EPI, bool SMEM_VEC, int CPW>
 __global__ void __launch_bounds__(256) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
   extern __shared__ double2 sv[];
   const ColDotJob& jb = jobs.j[blockIdx.y];
   const int n_out = jb.n_out;
-  if ((int)blockIdx.x * 8 >= n_out) return;
+  // balanced contiguous column range per warp (sizes differ by <= 1)
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  const int i_begin = (int)(gw * n_out / nw);
+  const int i_end = (int)((gw + 1) * n_out / nw);
+  if ((int)((int64_t)blockIdx.x * 8 * n_out / nw) >= n_out) return;  // whole CTA idle
   const int64_t ld = jb.ld;
+  const int64_t half = ld >> 1;
   if (SMEM_VEC) {
-    for (int r = threadIdx.x; r < ld; r += blockDim.x) sv[r] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
+    for (int r = threadIdx.x; r < ld; r += blockDim.x)
+      sv[ColLoad<T, CPW>::slot(r, half)] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int steps = (int)((jb.len + ColLoad<T>::kRowsPerStep - 1) / ColLoad<T>::kRowsPerStep);
-  for (int i = blockIdx.x * 8 + warp; i < n_out; i += gridDim.x * 8) {
-    const int col = jb.cols ? jb.cols[i] : i;
-    double re, im;
-    if (SMEM_VEC) ColLoad<T>::dot(jb.M, ld, col, steps, sv, lane, re, im);
-    else dot_global<T>(jb.M, ld, col, jb.len, jb.vec, lane, re, im);
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) {
-      if (EPI == EPI_STORE) {
-        jb.out[i] = make_double2(__dmul_rn(jb.scale, re), __dmul_rn(jb.scale, im));
-      } else {
-        double2 xh;
-        if (EPI == EPI_XDUAL) {
-          // x = (rhs - mu * A^H w) / beta  (Woodbury form of solver_core.hpp:47-51)
-          const double2 r = jb.rhs[i];
-          xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re)), beta),
-                            __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im)), beta));
-        } else {
-          xh = make_double2(re, im);
-        }
-        const int p = jb.pix[i];
-        const double2 old = jb.x_full[p];
-        jb.ring_slot[p] = c_abs(c_sub(xh, old));  // |hist[h][j] - hist[h-1][j]| (admm.hpp:143)
-        jb.x_full[p] = xh;                        // admm.hpp:121-122
-        jb.x_hat[i] = xh;                         // admm.hpp:120
+  const int steps = (int)((jb.len + ColLoad<T, CPW>::kRowsPerStep - 1) / ColLoad<T, CPW>::kRowsPerStep);
+  for (int i0 = i_begin; i0 < i_end; i0 += CPW) {
+    if (SMEM_VEC) {
+      int col[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const int i = min(i0 + c, i_end - 1);
+        col[c] = jb.cols ? jb.cols[i] : i;
+      }
+      double re[CPW], im[CPW];
+      ColLoad<T, CPW>::dot(jb.M, ld, col, steps, sv, half, lane, re, im);
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        re[c] = warp_sum(re[c]);
+        im[c] = warp_sum(im[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < CPW; ++c)
+        if (lane == c && i0 + c < i_end) coldot_epilogue<EPI>(jb, i0 + c, re[c], im[c], mu, beta);
+    } else {
+      for (int c = 0; c < CPW && i0 + c < i_end; ++c) {
+        const int i = i0 + c;
+        const int col = jb.cols ? jb.cols[i] : i;
+        double re, im;
+        dot_global<T>(jb.M, ld, col, jb.len, jb.vec, lane, re, im);
+        re = warp_sum(re);
+        im = warp_sum(im);
+        if (lane == 0) coldot_epilogue<EPI>(jb, i, re, im, mu, beta);
       }
     }
   }
@@ -279,16 +341,16 @@ __global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant_
     const float2* A = jb.A + r;
     int t = 0;
 #pragma unroll 1
-    for (; t + 4 <= cnt; t += 4) {
-      const float4 x0 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 0] * jb.ld));
-      const float4 x1 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 1] * jb.ld));
-      const float4 x2 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 2] * jb.ld));
-      const float4 x3 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + 3] * jb.ld));
-      const double2 c0 = coef[t + 0], c1 = coef[t + 1], c2 = coef[t + 2], c3 = coef[t + 3];
-      cfma(a0r, a0i, x0.x, x0.y, c0); cfma(a1r, a1i, x0.z, x0.w, c0);
-      cfma(b0r, b0i, x1.x, x1.y, c1); cfma(b1r, b1i, x1.z, x1.w, c1);
-      cfma(a0r, a0i, x2.x, x2.y, c2); cfma(a1r, a1i, x2.z, x2.w, c2);
-      cfma(b0r, b0i, x3.x, x3.y, c3); cfma(b1r, b1i, x3.z, x3.w, c3);
+    for (; t + 8 <= cnt; t += 8) {
+      float4 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t + u] * jb.ld));
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const double2 c0 = coef[t + u], c1 = coef[t + u + 1];
+        cfma(a0r, a0i, x[u].x, x[u].y, c0); cfma(a1r, a1i, x[u].z, x[u].w, c0);
+        cfma(b0r, b0i, x[u + 1].x, x[u + 1].y, c1); cfma(b1r, b1i, x[u + 1].z, x[u + 1].w, c1);
+      }
     }
     for (; t < cnt; ++t) {
       const float4 x0 = __ldg(reinterpret_cast<const float4*>(A + (int64_t)cidx[t] * jb.ld));

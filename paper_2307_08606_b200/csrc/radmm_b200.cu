@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -192,6 +193,7 @@ struct radmm_ctx {
   int rank = 0, world = 1;
   int q_max_local = 0;
   int sm_count = 148;
+  int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API)
   cudaStream_t stream = nullptr;
   std::vector<Sensor> sensors;
   DArr<double2> s, xg, sigma, sigma_pre, gap;
@@ -249,8 +251,8 @@ struct radmm_ctx {
 
 namespace {
 
-constexpr int kCtasPerSmTarget = 8;
 constexpr size_t kColdotSmemMax = 200 * 1024;
+constexpr int kDefaultCpw = 2;
 
 // ---- device-time accounting (CUDA events on the context stream) -------------
 cudaEvent_t take_event(radmm_ctx* c, int& idx) {
@@ -312,6 +314,8 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   if (prop.major < 10)
     fail(RADMM_CUDA, "radmm_b200 requires an sm_100 (Blackwell) GPU; found " + std::string(prop.name));
   c->sm_count = prop.multiProcessorCount;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS>, kFwdThreads, 16 * 1024));
+  c->fwd_per_sm = std::max(1, c->fwd_per_sm);
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->N = n_pixels;
   c->Q = q_local;
@@ -352,7 +356,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.v.alloc(S.ld);
   S.w.alloc(S.ld);
   const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
-  S.part_chunks = std::max(1, c->sm_count * kCtasPerSmTarget / tiles) + 1;
+  S.part_chunks = std::max(1, c->sm_count * c->fwd_per_sm / tiles) + 1;
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
   S.has_y = false;
@@ -366,6 +370,30 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   } while (0)
 
 // ---- column-dot launches --------------------------------------------------
+// One full wave of resident CTAs split evenly over the batch (occupancy API);
+// every warp then owns a balanced contiguous range of columns.
+template <typename T, int EPI, bool SMEM, int CPW>
+void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
+                   double beta) {
+  auto kern = coldot_kernel<T, EPI, SMEM, CPW>;
+  if (SMEM && smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  int per_sm = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, SMEM ? smem : 0));
+  const int target = c->sm_count * std::max(1, per_sm);
+  const int gx = std::max(1, std::min((n_max + 8 * CPW - 1) / (8 * CPW), (int)((target + nb - 1) / nb)));
+  LAUNCH(c, kern, dim3(gx, (unsigned)nb), 256, SMEM ? smem : 0, pk, mu, beta);
+}
+
+int coldot_cpw() {
+  static int v = [] {
+    const char* e = std::getenv("RADMM_CPW");
+    const int x = e ? std::atoi(e) : 0;
+    return (x == 1 || x == 2 || x == 4) ? x : 0;
+  }();
+  return v;
+}
+
 template <typename T, int EPI>
 void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double beta) {
   if (jobs.empty()) return;
@@ -381,21 +409,14 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
     }
     if (n_max == 0) continue;
     const size_t smem = (size_t)ld_max * sizeof(double2);
-    if (smem <= kColdotSmemMax) {
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(coldot_kernel<T, EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024));
-      const int per_sm = std::max(1, std::min(8, (int)((228 * 1024) / (smem + 1024))));
-      const int target = c->sm_count * per_sm;
-      int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
-      dim3 grid(gx, (unsigned)nb);
-      LAUNCH(c, (coldot_kernel<T, EPI, true>), grid, 256, smem, pk, mu, beta);
-    } else {
-      const int target = c->sm_count * 8;
-      int gx = std::max(1, std::min((n_max + 7) / 8, (int)((target + nb - 1) / nb)));
-      dim3 grid(gx, (unsigned)nb);
-      LAUNCH(c, (coldot_kernel<T, EPI, false>), grid, 256, 0, pk, mu, beta);
+    if (smem > kColdotSmemMax) {
+      coldot_launch<T, EPI, false, 1>(c, pk, nb, n_max, 0, mu, beta);
+      continue;
     }
+    const int cpw = coldot_cpw() ? coldot_cpw() : kDefaultCpw;
+    if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta);
+    else if (cpw == 2) coldot_launch<T, EPI, true, 2>(c, pk, nb, n_max, smem, mu, beta);
+    else coldot_launch<T, EPI, true, 4>(c, pk, nb, n_max, smem, mu, beta);
   }
 }
 
@@ -427,10 +448,10 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
   }
 }
 
-// chunking so one forward launch fills the GPU: ~kCtasPerSmTarget CTAs/SM
+// chunking so one forward launch is exactly one full wave of resident CTAs
 void plan_chunks(radmm_ctx* c, const Sensor& S, int n, int batch, int& n_chunks, int& chunk_len) {
   const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
-  const int target = c->sm_count * kCtasPerSmTarget;
+  const int target = c->sm_count * c->fwd_per_sm;
   const int chunks = std::min(S.part_chunks, std::max(1, target / std::max(1, tiles * batch)));
   chunk_len = (int)round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8);
   n_chunks = (n + chunk_len - 1) / chunk_len;
