@@ -200,7 +200,8 @@ typedef enum {
   RADMM_PHASE_FUSION = 5,    /* average, threshold, dual, norms, stop rule   */
   RADMM_PHASE_SCREEN = 6,    /* zeta + ballot/prefix-sum compaction          */
   RADMM_PHASE_REFACTOR = 7,  /* frozen echo, data term, downdate / rebuild   */
-  RADMM_PHASE_COUNT = 8
+  RADMM_PHASE_SWEEP = 8,     /* fused adjoint(k) + fusion(k) + forward(k+1)  */
+  RADMM_PHASE_COUNT = 9
 } radmm_phase;
 
 typedef struct {

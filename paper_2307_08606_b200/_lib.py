@@ -83,7 +83,7 @@ class PhaseStat(C.Structure):
     _fields_ = [("calls", C.c_int64), ("launches", C.c_int64), ("total_ms", C.c_double), ("bytes", C.c_double)]
 
 
-PHASES = ["forward", "gapply", "adjoint", "primal", "exchange", "fusion", "screen", "refactor"]
+PHASES = ["forward", "gapply", "adjoint", "primal", "exchange", "fusion", "screen", "refactor", "sweep"]
 
 
 # Every symbol include/radmm_b200.h declares, with its argument types.

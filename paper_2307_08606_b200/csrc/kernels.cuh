@@ -461,34 +461,42 @@ __device__ __forceinline__ double2 soft_threshold1(double2 v, double kappa) {
   return make_double2(0.0, 0.0);
 }
 
-__global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
-  __shared__ double red[5][kFusionThreads / 32];
+// FusionCore::round for one pixel j; accumulates the five squared norms.
+// contrib(k) returns sensor k's image value at j.
+template <typename Contrib>
+__device__ __forceinline__ void fusion_pixel(const FusionArgs& a, int j, Contrib contrib, double (&q)[5]) {
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = 0; k < a.Q; ++k) s = c_add(s, contrib(k));  // fixed sensor order (admm.hpp:239)
+  s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
+  const double2 xgp = a.xg[j];
+  const double2 sg = a.sigma[j];
+  a.sigma_pre[j] = sg;
+  const double2 v = make_double2(__dadd_rn(s.x, __ddiv_rn(sg.x, a.beta)), __dadd_rn(s.y, __ddiv_rn(sg.y, a.beta)));
+  const double2 xg = soft_threshold1(v, a.kappa);
+  const double2 eta = c_sub(s, xg);
+  const double2 dx = c_sub(xg, xgp);
+  const double2 sn = make_double2(__dadd_rn(sg.x, __dmul_rn(a.beta, eta.x)), __dadd_rn(sg.y, __dmul_rn(a.beta, eta.y)));
+  a.s[j] = s;
+  a.xg[j] = xg;
+  a.sigma[j] = sn;
+  a.gap[j] = c_sub(xg, s);
+  q[0] += c_norm2(eta);
+  q[1] += c_norm2(dx);
+  q[2] += c_norm2(s);
+  q[3] += c_norm2(xg);
+  q[4] += c_norm2(sn);
+}
+
+// Block-reduce the five partial sums, publish them, and let the last block of
+// the grid reduce all blocks in fixed order and evaluate the stopping rule
+// (admm.hpp:244-256).  Deterministic for a fixed grid.
+__device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5]) {
+  __shared__ double red[5][32];
   __shared__ bool last;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  double q[5] = {0, 0, 0, 0, 0};
-  if (j < a.N) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int k = 0; k < a.Q; ++k) s = c_add(s, a.contrib[k][j]);  // fixed sensor order
-    s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
-    const double2 xgp = a.xg[j];
-    const double2 sg = a.sigma[j];
-    a.sigma_pre[j] = sg;
-    const double2 v = make_double2(__dadd_rn(s.x, __ddiv_rn(sg.x, a.beta)), __dadd_rn(s.y, __ddiv_rn(sg.y, a.beta)));
-    const double2 xg = soft_threshold1(v, a.kappa);
-    const double2 eta = c_sub(s, xg);
-    const double2 dx = c_sub(xg, xgp);
-    const double2 sn = make_double2(__dadd_rn(sg.x, __dmul_rn(a.beta, eta.x)), __dadd_rn(sg.y, __dmul_rn(a.beta, eta.y)));
-    a.s[j] = s;
-    a.xg[j] = xg;
-    a.sigma[j] = sn;
-    a.gap[j] = c_sub(xg, s);
-    q[0] = c_norm2(eta);
-    q[1] = c_norm2(dx);
-    q[2] = c_norm2(s);
-    q[3] = c_norm2(xg);
-    q[4] = c_norm2(sn);
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  const int nblocks = gridDim.x * gridDim.y * gridDim.z;
+  const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
 #pragma unroll
   for (int t = 0; t < 5; ++t) {
     const double w = warp_sum(q[t]);
@@ -497,18 +505,18 @@ __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
   __syncthreads();
   if (threadIdx.x < 5) {
     double acc = 0;
-    for (int w = 0; w < kFusionThreads / 32; ++w) acc += red[threadIdx.x][w];
-    a.partials[blockIdx.x * 5 + threadIdx.x] = acc;
+    for (int w = 0; w < nwarps; ++w) acc += red[threadIdx.x][w];
+    a.partials[bid * 5 + threadIdx.x] = acc;
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) last = (atomicAdd(a.counter, 1u) == (unsigned)nblocks - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
   if (threadIdx.x < 5) {
     double acc = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) acc += ((volatile double*)a.partials)[b * 5 + threadIdx.x];
+    for (int b = 0; b < nblocks; ++b) acc += ((volatile double*)a.partials)[b * 5 + threadIdx.x];
     red[threadIdx.x][0] = acc;
   }
   __syncthreads();
@@ -534,6 +542,13 @@ __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
     }
     *a.counter = 0u;
   }
+}
+
+__global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double q[5] = {0, 0, 0, 0, 0};
+  if (j < a.N) fusion_pixel(a, j, [&](int k) { return a.contrib[k][j]; }, q);
+  fusion_finish(a, q);
 }
 
 // ---------------------------------------------------------------------------
@@ -663,6 +678,7 @@ struct GemmJob {
   double alpha, beta0;
   double diag_add;  // C[i,i] += diag_add
   int k0, kb;       // GEPI_GJ: pivot block rows/cols [k0, k0+kb); b = R' (kb x n)
+  int herm;         // result is Hermitian: compute tiles with m0 >= n0, mirror conj
 };
 
 __device__ __forceinline__ double2 mat_load(const MatRef& m, int i, int k) {
@@ -689,6 +705,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
   const GemmJob& jb = jobs.j[blockIdx.z];
   const int m0 = blockIdx.y * kGB, n0 = blockIdx.x * kGB;
   if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 < n0) return;  // upper tiles come from the mirror
   __shared__ double2 As[2][kGK][kGB];
   __shared__ double2 Bs[2][kGK][kGB];
   const int tid = threadIdx.x;
@@ -762,8 +779,13 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
           o.x += jb.beta0 * c0.x;
           o.y += jb.beta0 * c0.y;
         }
-        if (i == j) o.x += jb.diag_add;
+        if (i == j) {
+          o.x += jb.diag_add;
+          if (jb.herm) o.y = 0.0;  // exact real diagonal of a Hermitian matrix
+        }
+        if (jb.herm && i < j) continue;  // written (bit-exactly) as the mirror of (j, i)
         *cp = o;
+        if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
       } else {
         // Gauss-Jordan sweep of pivot block K = [k0, k0+kb):
         //   i in K:      M[i,j] = R'[i-k0, j]
@@ -941,6 +963,245 @@ __global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K,
   double s, c;
   sincos(ang, &s, &c);
   A[r + (int64_t)n * ld] = make_float2(__double2float_rn(c), __double2float_rn(s));
+}
+
+}  // namespace radmm_dev
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// Single-pass fused sweep (one GPU, all sensors in the dual form, Q <= 8).
+//
+// The two matvecs of consecutive iterations read the same operator columns:
+// the adjoint of iteration k (x-update) and the forward of iteration k+1
+// (v = A_J rhs).  Between them sits the fusion round, which couples all
+// sensors at each pixel.  A thread-block cluster holds one CTA per sensor over
+// a shared pixel range; per pixel tile:
+//   (a) CTA q: u_i = A_q(:,J_i)^H w_q for its active columns of the tile and
+//       the x-update epilogue (x_hat, x_full scatter, screening ring)   [HBM]
+//   (b) cluster barrier (release/acquire); CTA q runs FusionCore::round on a
+//       1/Q slice of the tile's pixels, reading every sensor's x_full (L2)
+//   (c) cluster barrier; CTA q forms rhs_{k+1} for its tile columns
+//   (d) CTA q accumulates v_{k+1} += A_q(:,J_i) rhs_i in registers     [L2]
+// A is streamed from HBM once per iteration; the second touch hits L2.  Each
+// CTA finally writes its KM-length partial of v_{k+1} (fixed-order reduce),
+// and the grid's last block finishes the fusion norms / stopping rule.
+// ---------------------------------------------------------------------------
+struct SweepJob {
+  const float2* A;
+  int64_t ld;
+  int n_act;
+  const int* J;
+  const double2* w;
+  const double2* data;
+  double2* rhs;
+  double2* x_hat;
+  double2* x_full;
+  double* ring_slot;
+  double2* part;  // [n_clusters][ld]
+};
+
+constexpr int kSweepThreads = 256;
+constexpr int kSweepTile = 64;
+
+__device__ __forceinline__ void cluster_sync_acqrel() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ int lower_bound_dev(const int* J, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (J[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// u = A(:,col)^H w for two columns, 8 float4 loads in flight per lane.
+__device__ __forceinline__ void sweep_dot2(const float2* __restrict__ A, int64_t ld, int c0, int c1, int steps,
+                                           const double2* __restrict__ sv, int64_t half, int lane,
+                                           double (&re)[2], double (&im)[2]) {
+  const float4* p0 = reinterpret_cast<const float4*>(A + (int64_t)c0 * ld) + lane;
+  const float4* p1 = reinterpret_cast<const float4*>(A + (int64_t)c1 * ld) + lane;
+  const double2* ve = sv + lane;
+  const double2* vo = sv + half + lane;
+  re[0] = re[1] = im[0] = im[1] = 0.0;
+  int s = 0;
+#pragma unroll 1
+  for (; s + 4 <= steps; s += 4) {
+    float4 a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = __ldg(p0 + (s + u) * 32);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = __ldg(p1 + (s + u) * 32);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 e = ve[(s + u) * 32], o = vo[(s + u) * 32];
+      cfma_conj(re[0], im[0], a[u].x, a[u].y, e);
+      cfma_conj(re[0], im[0], a[u].z, a[u].w, o);
+      cfma_conj(re[1], im[1], b[u].x, b[u].y, e);
+      cfma_conj(re[1], im[1], b[u].z, b[u].w, o);
+    }
+  }
+  for (; s < steps; ++s) {
+    const float4 a = __ldg(p0 + s * 32), b = __ldg(p1 + s * 32);
+    const double2 e = ve[s * 32], o = vo[s * 32];
+    cfma_conj(re[0], im[0], a.x, a.y, e);
+    cfma_conj(re[0], im[0], a.z, a.w, o);
+    cfma_conj(re[1], im[1], b.x, b.y, e);
+    cfma_conj(re[1], im[1], b.z, b.w, o);
+  }
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int RPT>  // float4 row-chunks per thread in the axpy: ld <= RPT * 512
+__global__ void __launch_bounds__(kSweepThreads) fused_sweep_kernel(const __grid_constant__ Pack<SweepJob> jobs,
+                                                                    const __grid_constant__ FusionArgs fa, double mu,
+                                                                    double beta, int n_clusters, int range, int tile,
+                                                                    int prefetch) {
+  extern __shared__ double2 sweep_smem[];
+  __shared__ int s_lo, s_hi, s_hi2;
+  const int q = (int)cluster_ctarank();
+  const int cl = blockIdx.x / fa.Q;
+  const SweepJob& jb = jobs.j[q];
+  const int64_t ld = jb.ld;
+  const int64_t half = ld >> 1;
+  double2* sv = sweep_smem;
+  double2* coef = sweep_smem + ld;
+  int* cidx = reinterpret_cast<int*>(coef + kSweepTile);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int r = tid; r < ld; r += kSweepThreads) sv[(r & 1) ? half + (r >> 1) : (r >> 1)] = jb.w[r];
+  const int p0 = cl * range, p1 = min(fa.N, p0 + range);
+  if (tid == 0) s_hi = lower_bound_dev(jb.J, jb.n_act, p0);
+  __syncthreads();
+  const int steps = (int)(ld >> 6);
+  const int slice = (tile + fa.Q - 1) / fa.Q;
+  double acc[RPT][4];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+  double qn[5] = {0, 0, 0, 0, 0};
+  for (int t0 = p0; t0 < p1; t0 += tile) {
+    const int t1 = min(p1, t0 + tile);
+    if (tid == 0) {
+      int lo = s_hi, hi = lo;
+      while (hi < jb.n_act && jb.J[hi] < t1) ++hi;
+      int hi2 = hi;
+      const int t2 = min(p1, t1 + tile);
+      while (hi2 < jb.n_act && jb.J[hi2] < t2) ++hi2;
+      s_lo = lo;
+      s_hi = hi;
+      s_hi2 = hi2;
+    }
+    __syncthreads();
+    const int lo = s_lo, hi = s_hi;
+    // stage the next tile's columns into L2 with TMA bulk prefetches so the
+    // HBM stream keeps running through the cluster barriers below
+    if (prefetch && tid < s_hi2 - hi)
+      prefetch_l2_bulk(jb.A + (int64_t)jb.J[hi + tid] * ld, (unsigned)(ld * sizeof(float2)));
+    // (a) adjoint dots + x-update for this sensor's active columns in the tile
+    for (int i0 = lo + 2 * warp; i0 < hi; i0 += 2 * (kSweepThreads / 32)) {
+      const int i1 = min(i0 + 1, hi - 1);
+      double re[2], im[2];
+      sweep_dot2(jb.A, ld, jb.J[i0], jb.J[i1], steps, sv, half, lane, re, im);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        re[c] = warp_sum(re[c]);
+        im[c] = warp_sum(im[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int i = i0 + c;
+        if (lane == c && i < hi) {
+          const double2 r = jb.rhs[i];
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re[c])), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im[c])), beta));
+          const int p = jb.J[i];
+          const double2 old = jb.x_full[p];
+          jb.ring_slot[p] = c_abs(c_sub(xh, old));
+          jb.x_full[p] = xh;
+          jb.x_hat[i] = xh;
+        }
+      }
+    }
+    cluster_sync_acqrel();
+    // (b) fusion for this CTA's slice of the tile's pixels
+    {
+      const int j = t0 + q * slice + tid;
+      if (tid < slice && j < t1 && j < t0 + (q + 1) * slice)
+        fusion_pixel(fa, j, [&](int k) { return __ldcg(jobs.j[k].x_full + j); }, qn);
+    }
+    cluster_sync_acqrel();
+    // (c) rhs_{k+1} = data + beta gap + beta x_hat - sigma (admm.hpp:114-119)
+    for (int i = lo + tid; i < hi; i += kSweepThreads) {
+      const int c = jb.J[i];
+      const double2 d = jb.data[i], g = __ldcg(fa.gap + c), xh = jb.x_hat[i], sg = __ldcg(fa.sigma + c);
+      double2 v;
+      v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+      v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+      jb.rhs[i] = v;
+      coef[i - lo] = v;
+      cidx[i - lo] = c;
+    }
+    __syncthreads();
+    // (d) v_{k+1} += A(:, J_i) rhs_i  -- the tile's columns are L2-hot
+    const int cnt = hi - lo;
+    int c = 0;
+#pragma unroll 1
+    for (; c + 2 <= cnt; c += 2) {
+      float4 x0[RPT], x1[RPT];
+      const float2* col0 = jb.A + (int64_t)cidx[c] * ld;
+      const float2* col1 = jb.A + (int64_t)cidx[c + 1] * ld;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t r = 2 * tid + 512 * u;
+        x0[u] = r < ld ? __ldg(reinterpret_cast<const float4*>(col0 + r)) : make_float4(0, 0, 0, 0);
+        x1[u] = r < ld ? __ldg(reinterpret_cast<const float4*>(col1 + r)) : make_float4(0, 0, 0, 0);
+      }
+      const double2 k0 = coef[c], k1 = coef[c + 1];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        cfma(acc[u][0], acc[u][1], x0[u].x, x0[u].y, k0);
+        cfma(acc[u][2], acc[u][3], x0[u].z, x0[u].w, k0);
+        cfma(acc[u][0], acc[u][1], x1[u].x, x1[u].y, k1);
+        cfma(acc[u][2], acc[u][3], x1[u].z, x1[u].w, k1);
+      }
+    }
+    for (; c < cnt; ++c) {
+      const float2* col0 = jb.A + (int64_t)cidx[c] * ld;
+      const double2 k0 = coef[c];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t r = 2 * tid + 512 * u;
+        if (r < ld) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(col0 + r));
+          cfma(acc[u][0], acc[u][1], x.x, x.y, k0);
+          cfma(acc[u][2], acc[u][3], x.z, x.w, k0);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // partial v_{k+1} of this CTA (rows owned by this thread)
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int64_t r = 2 * tid + 512 * u;
+    if (r < ld) {
+      double2* out = jb.part + (int64_t)cl * ld + r;
+      out[0] = make_double2(acc[u][0], acc[u][1]);
+      out[1] = make_double2(acc[u][2], acc[u][3]);
+    }
+  }
+  fusion_finish(fa, qn);
 }
 
 }  // namespace radmm_dev

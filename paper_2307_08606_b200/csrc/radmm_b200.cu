@@ -160,6 +160,7 @@ struct Sensor {
   DArr<double2> part, v, w;
   int part_chunks = 0;  // capacity of part in chunks of ld
   int removed_now = 0;
+  bool v_ready = false;  // v = A_J rhs for the coming iteration left by the fused sweep
 };
 
 struct Scratch {
@@ -194,6 +195,7 @@ struct radmm_ctx {
   int q_max_local = 0;
   int sm_count = 148;
   int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API)
+  int sweep_clusters = 0;  // clusters of the last fused sweep (= partial chunks it left)
   cudaStream_t stream = nullptr;
   std::vector<Sensor> sensors;
   DArr<double2> s, xg, sigma, sigma_pre, gap;
@@ -224,7 +226,9 @@ struct radmm_ctx {
   // device timing: per-iteration CUDA events (always), per-phase events
   // (profiling mode) -- all on this context's stream.
   cudaEvent_t ev_it0 = nullptr, ev_it1 = nullptr;
-  std::vector<double> iter_ms;
+  std::vector<double> iter_ms;       // per-step device wall time (incl. host round trip)
+  std::vector<double> iter_busy_ms;  // per-step device time from first to last kernel
+  std::vector<cudaEvent_t> ev_steps;
   std::vector<int64_t> iter_launches;
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -241,6 +245,7 @@ struct radmm_ctx {
     if (ev_it0) cudaEventDestroy(ev_it0);
     if (ev_it1) cudaEventDestroy(ev_it1);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_steps) cudaEventDestroy(e);
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     if (fs_host) cudaFreeHost(fs_host);
     if (h_totals) cudaFreeHost(h_totals);
@@ -487,7 +492,7 @@ GemmJob gjob(int m, int n, int k, MatRef a, MatRef b, double2* cp, int64_t ldc, 
              double beta0, double diag_add = 0.0) {
   GemmJob g;
   g.m = m; g.n = n; g.k = k; g.a = a; g.b = b; g.c = cp; g.ldc = ldc;
-  g.alpha = alpha; g.beta0 = beta0; g.diag_add = diag_add; g.k0 = 0; g.kb = 0;
+  g.alpha = alpha; g.beta0 = beta0; g.diag_add = diag_add; g.k0 = 0; g.kb = 0; g.herm = 0;
   return g;
 }
 
@@ -598,6 +603,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
       jobs.push_back(gjob(dim, dim, S.n_act, mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p),
                           mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
     }
+    jobs.back().herm = 1;  // Gram / capacitance are Hermitian: lower tiles + mirror
     inv.push_back({S.G.p, ldg, dim});
     ++c->rebuilds;
   }
@@ -762,6 +768,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
     S.n_act = N;
     S.stalled = false;
     S.removed_now = 0;
+    S.v_ready = false;
     LAUNCH(c, iota_kernel, dim3((N + 255) / 256), 256, 0, S.J.p, N);
     CK(cudaMemsetAsync(S.x_full.p, 0, sizeof(double2) * N, c->stream));
     CK(cudaMemsetAsync(S.x_hat.p, 0, sizeof(double2) * N, c->stream));
@@ -781,6 +788,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
 // One synchronous Jacobi sweep of local updates (admm.hpp:389-390).
 void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
   const int slot = c->upd % c->W;
+  for (Sensor& S : c->sensors) S.v_ready = false;  // partial buffers are reused below
   std::vector<FwdJob> fj;
   std::vector<ReduceJob> rj;
   std::vector<ColDotJob> gj, aj, pj;
@@ -862,22 +870,10 @@ void exchange(radmm_ctx* c, double notice_bytes) {
   c->launches += 2;
 }
 
+FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k);
+
 void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k) {
-  FusionArgs a;
-  a.contrib = c->contrib.p;
-  a.Q = c->Q_total;
-  a.N = c->N;
-  a.s = c->s.p; a.xg = c->xg.p; a.sigma = c->sigma.p; a.sigma_pre = c->sigma_pre.p; a.gap = c->gap.p;
-  a.beta = h->beta;
-  a.kappa = h->lambda / h->beta;
-  a.root_n_eps_abs = std::sqrt((double)c->N) * h->eps_abs;
-  a.eps_rel = h->eps_rel;
-  a.has_prev = k > 1 ? 1 : 0;
-  a.iteration = k;
-  a.partials = c->fpart.p;
-  a.counter = c->fcounter.p;
-  a.out_dev = c->fs_dev.p;
-  a.out_host = c->fs_host_dev;
+  const FusionArgs a = fusion_args(c, h, k);
   PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
   LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
@@ -924,6 +920,7 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
       continue;
     }
     S.removed_now = removed;
+    S.v_ready = false;  // the speculative v was formed over the old active set
     std::swap(S.J, S.Jnew);
     std::swap(S.x_hat, S.x_hat_new);
     S.n_act = kept;
@@ -962,6 +959,142 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   full_rebuild(c, rebuild, h->mu, h->beta);
   downdate(c, down, h->mu);
   return notice;
+}
+
+// ---- single-pass fused sweep (one GPU, all sensors dual, Q <= 8) ------------
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+constexpr int kDefaultSweepTile = 16;
+
+bool fused_enabled() {
+  static int v = [] {
+    const char* e = std::getenv("RADMM_FUSED");
+    return e ? std::atoi(e) : 0;  // experimental: see DESIGN.md section 9
+  }();
+  return v != 0;
+}
+
+bool fused_eligible(radmm_ctx* c) {
+  if (!fused_enabled() || c->world > 1 || c->Q < 1 || c->Q > 8) return false;
+  for (const Sensor& S : c->sensors)
+    if (S.primal || S.ld > 4 * 512) return false;
+  return true;
+}
+
+template <int RPT>
+void launch_sweep(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa, const radmm_hyperparams* h,
+                  size_t smem) {
+  auto kern = fused_sweep_kernel<RPT>;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c->Q;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kSweepThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)c->Q);
+  int clusters = 0;
+  CK(cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg));
+  clusters = std::max(1, clusters);
+  const int cap = env_int("RADMM_SWEEP_CLUSTERS", 0);
+  if (cap > 0) clusters = std::min(clusters, cap);
+  for (const Sensor& S : c->sensors) clusters = std::min(clusters, S.part_chunks);
+  const int tile = std::max(8, std::min(kSweepTile, env_int("RADMM_SWEEP_TILE", kDefaultSweepTile)));
+  const int prefetch = env_int("RADMM_SWEEP_PREFETCH", 1);
+  const int range = (int)round_up((c->N + clusters - 1) / clusters, tile);
+  clusters = (c->N + range - 1) / range;
+  cfg.gridDim = dim3((unsigned)(c->Q * clusters));
+  // the fusion partials hold one slot per block of the grid
+  if (c->fpart.n < (size_t)5 * c->Q * clusters) c->fpart.alloc((size_t)5 * c->Q * clusters);
+  FusionArgs a = fa;
+  a.partials = c->fpart.p;
+  CK(cudaLaunchKernelEx(&cfg, kern, pk, a, h->mu, h->beta, clusters, range, tile, prefetch));
+  ++c->launches;
+  c->sweep_clusters = clusters;
+}
+
+FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  FusionArgs a;
+  a.contrib = c->contrib.p;
+  a.Q = c->Q_total;
+  a.N = c->N;
+  a.s = c->s.p; a.xg = c->xg.p; a.sigma = c->sigma.p; a.sigma_pre = c->sigma_pre.p; a.gap = c->gap.p;
+  a.beta = h->beta;
+  a.kappa = h->lambda / h->beta;
+  a.root_n_eps_abs = std::sqrt((double)c->N) * h->eps_abs;
+  a.eps_rel = h->eps_rel;
+  a.has_prev = k > 1 ? 1 : 0;
+  a.iteration = k;
+  a.partials = c->fpart.p;
+  a.counter = c->fcounter.p;
+  a.out_dev = c->fs_dev.p;
+  a.out_host = c->fs_host_dev;
+  return a;
+}
+
+// One iteration on the fused path: v for every sensor (left by the previous
+// sweep, or a fresh forward pass after an active-set change / at k = 1), the
+// capacitance-inverse apply, then the sweep (x-update, fusion, next forward).
+void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  const int slot = c->upd % c->W;
+  std::vector<FwdJob> fj;
+  std::vector<ReduceJob> rj_fwd;
+  Pack<ReduceJob> rj_sweep;
+  int n_ready = 0;
+  int64_t ld_max = 0;
+  std::vector<ColDotJob> gj;
+  Pack<SweepJob> sp;
+  double a_bytes = 0, g_bytes = 0, f_bytes = 0;
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    ld_max = std::max(ld_max, S.ld);
+    if (!S.v_ready) {
+      FwdJob f{};
+      f.A = S.A.p; f.ld = S.ld; f.n = S.n_act; f.J = S.J.p; f.data = S.data.p; f.x_hat = S.x_hat.p;
+      f.rhs_out = S.rhs.p; f.part = S.part.p;
+      plan_chunks(c, S, S.n_act, c->Q, f.n_chunks, f.chunk_len);
+      fj.push_back(f);
+      rj_fwd.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0});
+      f_bytes += 8.0 * S.rows * S.n_act;
+    } else {
+      rj_sweep.j[n_ready++] = ReduceJob{S.part.p, c->sweep_clusters, S.ld, S.rows, nullptr, S.v.p, 1.0};
+    }
+    ColDotJob g{};
+    g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
+    gj.push_back(g);
+    g_bytes += 16.0 * S.rows * S.rows;
+    a_bytes += 8.0 * S.rows * S.n_act;
+    sp.j[q] = SweepJob{S.A.p, S.ld, S.n_act, S.J.p, S.w.p, S.data.p, S.rhs.p, S.x_hat.p, S.x_full.p,
+                       S.ring.p + (size_t)slot * c->N, S.part.p};
+  }
+  {
+    PhaseScope ps(c, RADMM_PHASE_FORWARD, f_bytes);
+    if (!fj.empty()) forward<MODE_RHS>(c, fj, rj_fwd, h->beta);
+    if (n_ready)
+      LAUNCH(c, reduce_parts_kernel, dim3((unsigned)((ld_max + 255) / 256), n_ready), 256, 0, rj_sweep);
+  }
+  {
+    PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
+    coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+  }
+  {
+    PhaseScope ps(c, RADMM_PHASE_SWEEP, a_bytes + 16.0 * c->N * (c->Q + 7));
+    const size_t smem = (size_t)ld_max * sizeof(double2) + kSweepTile * (sizeof(double2) + sizeof(int));
+    const FusionArgs fa = fusion_args(c, h, k);
+    if (ld_max <= 512) launch_sweep<1>(c, sp, fa, h, smem);
+    else if (ld_max <= 1024) launch_sweep<2>(c, sp, fa, h, smem);
+    else launch_sweep<4>(c, sp, fa, h, smem);
+  }
+  for (Sensor& S : c->sensors) S.v_ready = true;
+  ++c->upd;
 }
 
 void build_contrib(radmm_ctx* c) {
@@ -1017,20 +1150,34 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   if (o && o->observer) { hx.resize(2 * (size_t)c->N); hs.resize(2 * (size_t)c->N); hsig.resize(2 * (size_t)c->N); }
   bool staged_trigger = false;
   FusionScalars f{};
+  // step boundaries: ev_steps[k-1] is recorded when iteration k starts, so
+  // elapsed(ev_steps[k-1], ev_steps[k]) is the device-clock wall time of
+  // iteration k including the host round trip before iteration k+1.
+  while (c->ev_steps.size() < (size_t)h->max_iter + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->ev_steps.push_back(e);
+  }
+  c->iter_busy_ms.clear();
   for (int k = 1; k <= h->max_iter; ++k) {
     uint64_t notice = 0;
     const int64_t l0 = c->launches;
+    CK(cudaEventRecord(c->ev_steps[k - 1], c->stream));
     CK(cudaEventRecord(c->ev_it0, c->stream));
     if (asadmm && !disable && staged_trigger) notice = screen_all(c, h, k);
-    local_updates(c, h);
-    exchange(c, (double)notice);
-    run_fusion(c, h, k);
+    if (fused_eligible(c)) {
+      fused_iteration(c, h, k);
+    } else {
+      local_updates(c, h);
+      exchange(c, (double)notice);
+      run_fusion(c, h, k);
+    }
     CK(cudaEventRecord(c->ev_it1, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev_it0, c->ev_it1));
-      c->iter_ms.push_back(ms);
+      c->iter_busy_ms.push_back(ms);
       c->iter_launches.push_back(c->launches - l0);
     }
     flush_marks(c);
@@ -1092,6 +1239,13 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     staged_trigger = f.trigger != 0;
   }
   if (fixed) sm.converged = f.converged;
+  CK(cudaEventRecord(c->ev_steps[sm.iterations], c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < sm.iterations; ++k) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_steps[k], c->ev_steps[k + 1]));
+    c->iter_ms.push_back(ms);
+  }
   const auto t2 = std::chrono::steady_clock::now();
   sm.solve_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
   sm.kernel_launches = c->launches;
