@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--config", default="c2")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--ttt", action="store_true", help="also run to tolerance (time-to-tolerance)")
+    p.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance run")
     p.add_argument("--ttt-max-iter", type=int, default=3000)
     return p.parse_args()
 
@@ -293,12 +293,8 @@ def ours(args, cfg):
 
     # ---- time to tolerance ------------------------------------------------
     ttt = None
-    if args.ttt:
-        h2 = api.Hyperparams(**{**hyper.__dict__, "max_iter": args.ttt_max_iter})
-        r2 = solver.run(h2, api.Mode.ASADMM, fetch=False)
-        ms2, _ = solver.iteration_stats(r2.iterations)
-        ttt = {"converged": r2.converged, "iterations": r2.iterations, "solve_s_device": float(np.sum(ms2)) / 1e3,
-               "setup_s": r2.setup_ms / 1e3, "max_iter": args.ttt_max_iter}
+    if not args.no_ttt:
+        ttt = time_to_tolerance(solver, hyper, args.ttt_max_iter)
     solver.close()
 
     # ---- e2e through the public API with pinned host buffers ---------------
@@ -330,6 +326,30 @@ def ours(args, cfg):
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def time_to_tolerance(solver, hyper, max_iter):
+    """Time-to-tolerance for "ASADMM to rel. residual 1e-5" (BASELINE config 2).
+
+    With the literal mapping (eps_rel = 1e-5, eps_abs = 1e-12) the degenerate
+    BASELINE problem (x_G = 0) never meets the stopping
+    rule, so the residual is read as relative to the first iteration's:
+    eps_abs is set so that sqrt(N) eps_abs = 1e-5 * pri_res(1), i.e. the run
+    stops once the primal residual has dropped 1e5-fold (the reference's own
+    stopping rule, admm.hpp:248-255, then applies unchanged)."""
+    from paper_2307_08606_b200 import api
+    first = solver.run(api.Hyperparams(**{**hyper.__dict__, "max_iter": 1}), api.Mode.ASADMM, fetch=True)
+    pri1 = first.report.iterations[0].pri_res
+    eps_abs = 1e-5 * pri1 / math.sqrt(solver.N)
+    h2 = api.Hyperparams(**{**hyper.__dict__, "max_iter": max_iter, "eps_abs": eps_abs})
+    r2 = solver.run(h2, api.Mode.ASADMM, fetch=True)
+    ms2, _ = solver.iteration_stats(r2.iterations)
+    last = r2.report.iterations[-1]
+    return {"converged": r2.converged, "iterations": r2.iterations, "solve_s_device": float(np.sum(ms2)) / 1e3,
+            "setup_s": r2.setup_ms / 1e3, "time_to_tolerance_s": float(np.sum(ms2)) / 1e3 + r2.setup_ms / 1e3,
+            "rule": "pri_res <= 1e-5 * pri_res(1) (eps_abs = %.3e, eps_rel = %g)" % (eps_abs, hyper.eps_rel),
+            "final_pri_res": last.pri_res, "max_iter": max_iter,
+            "active_sizes_end": last.active_sizes}
 
 
 def e2e_run(cfg, hyper, ys):

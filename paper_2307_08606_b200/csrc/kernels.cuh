@@ -224,17 +224,20 @@ __device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, doub
   }
 }
 
-template <typename T, int EPI, bool SMEM_VEC, int CPW>
-__global__ void __launch_bounds__(256) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
+// THREADS = 256 normally; 1024 when the shared vector is so large (KM = 8192:
+// 128 KB) that only one CTA fits per SM, to keep enough loads in flight.
+template <typename T, int EPI, bool SMEM_VEC, int CPW, int THREADS>
+__global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
   extern __shared__ double2 sv[];
+  constexpr int kWarps = THREADS / 32;
   const ColDotJob& jb = jobs.j[blockIdx.y];
   const int n_out = jb.n_out;
   // balanced contiguous column range per warp (sizes differ by <= 1)
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * 8;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
   const int i_begin = (int)(gw * n_out / nw);
   const int i_end = (int)((gw + 1) * n_out / nw);
-  if ((int)((int64_t)blockIdx.x * 8 * n_out / nw) >= n_out) return;  // whole CTA idle
+  if ((int)((int64_t)blockIdx.x * kWarps * n_out / nw) >= n_out) return;  // whole CTA idle
   const int64_t ld = jb.ld;
   const int64_t half = ld >> 1;
   if (SMEM_VEC) {

@@ -258,6 +258,8 @@ namespace {
 
 constexpr size_t kColdotSmemMax = 200 * 1024;
 constexpr int kDefaultCpw = 2;
+constexpr size_t kColdotBigSmem = 96 * 1024;
+constexpr int kMaxChunk = 2048;  // forward columns per CTA (shared-memory coefficient slab)
 
 // ---- device-time accounting (CUDA events on the context stream) -------------
 cudaEvent_t take_event(radmm_ctx* c, int& idx) {
@@ -361,7 +363,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.v.alloc(S.ld);
   S.w.alloc(S.ld);
   const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
-  S.part_chunks = std::max(1, c->sm_count * c->fwd_per_sm / tiles) + 1;
+  S.part_chunks = std::max(std::max(1, c->sm_count * c->fwd_per_sm / tiles), (c->N + kMaxChunk - 1) / kMaxChunk) + 1;
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
   S.has_y = false;
@@ -377,17 +379,19 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
 // ---- column-dot launches --------------------------------------------------
 // One full wave of resident CTAs split evenly over the batch (occupancy API);
 // every warp then owns a balanced contiguous range of columns.
-template <typename T, int EPI, bool SMEM, int CPW>
+template <typename T, int EPI, bool SMEM, int CPW, int THREADS = 256>
 void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
                    double beta) {
-  auto kern = coldot_kernel<T, EPI, SMEM, CPW>;
+  auto kern = coldot_kernel<T, EPI, SMEM, CPW, THREADS>;
   if (SMEM && smem > 48 * 1024)
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   int per_sm = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, SMEM ? smem : 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM ? smem : 0));
   const int target = c->sm_count * std::max(1, per_sm);
-  const int gx = std::max(1, std::min((n_max + 8 * CPW - 1) / (8 * CPW), (int)((target + nb - 1) / nb)));
-  LAUNCH(c, kern, dim3(gx, (unsigned)nb), 256, SMEM ? smem : 0, pk, mu, beta);
+  constexpr int kWarps = THREADS / 32;
+  const int gx =
+      std::max(1, std::min((n_max + kWarps * CPW - 1) / (kWarps * CPW), (int)((target + nb - 1) / nb)));
+  LAUNCH(c, kern, dim3(gx, (unsigned)nb), THREADS, SMEM ? smem : 0, pk, mu, beta);
 }
 
 int coldot_cpw() {
@@ -419,6 +423,10 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
       continue;
     }
     const int cpw = coldot_cpw() ? coldot_cpw() : kDefaultCpw;
+    if (smem > kColdotBigSmem) {  // one CTA per SM: go wide
+      coldot_launch<T, EPI, true, 2, 1024>(c, pk, nb, n_max, smem, mu, beta);
+      continue;
+    }
     if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta);
     else if (cpw == 2) coldot_launch<T, EPI, true, 2>(c, pk, nb, n_max, smem, mu, beta);
     else coldot_launch<T, EPI, true, 4>(c, pk, nb, n_max, smem, mu, beta);
@@ -458,7 +466,7 @@ void plan_chunks(radmm_ctx* c, const Sensor& S, int n, int batch, int& n_chunks,
   const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
   const int target = c->sm_count * c->fwd_per_sm;
   const int chunks = std::min(S.part_chunks, std::max(1, target / std::max(1, tiles * batch)));
-  chunk_len = (int)round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8);
+  chunk_len = (int)std::min<int64_t>(kMaxChunk, round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8));
   n_chunks = (n + chunk_len - 1) / chunk_len;
 }
 
