@@ -1208,3 +1208,212 @@ __global__ void __launch_bounds__(kSweepThreads) fused_sweep_kernel(const __grid
 }
 
 }  // namespace radmm_dev
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// Fused sweep v2: asynchronous, warp-specialised, one cluster = Q CTAs (one
+// per sensor) over a shared pixel range, one CTA per SM.  Roles per CTA:
+//   dot warps    stream the active columns of each pixel tile from HBM and
+//                run the adjoint x-update (u = A^H w, x = (rhs - mu u)/beta)
+//   fusion warp  when all Q CTAs finished tile T (DSMEM mbarrier), runs
+//                FusionCore::round on its slice of T and tells the peers
+//   axpy warps   when the whole cluster fused tile T, form rhs_{k+1} and
+//                accumulate v_{k+1} += A(:,J_i) rhs_i, re-reading the tile's
+//                columns while they are still L2-resident; then free the
+//                tile slot for the dot warps (bounded lag = L2 footprint)
+// Tiles flow through a DEPTH-deep ring of mbarriers; no role waits for a
+// cluster-wide barrier, so the HBM stream of the dot warps never drains.
+// ---------------------------------------------------------------------------
+constexpr int kS2Dot = 8;        // dot warps
+constexpr int kS2Fuse = 4;       // fusion warps (tile T handled by warp T % kS2Fuse)
+constexpr int kS2Axpy = 4;       // axpy warps
+constexpr int kS2Threads = (kS2Dot + kS2Fuse + kS2Axpy) * 32;
+constexpr int kS2Depth = 8;      // tiles in flight per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, unsigned cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(b)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int RPT>  // float4 row chunks per axpy thread: ld <= RPT * 256
+__global__ void __launch_bounds__(kS2Threads, 1) fused_sweep2_kernel(const __grid_constant__ Pack<SweepJob> jobs,
+                                                                     const __grid_constant__ FusionArgs fa, double mu,
+                                                                     double beta, int range, int tile) {
+  extern __shared__ double2 s2_smem[];
+  __shared__ uint64_t bar_dots[kS2Depth], bar_xhat[kS2Depth], bar_fused[kS2Depth], bar_free[kS2Depth];
+  __shared__ double2 s_coef[64];
+  __shared__ int s_col[64];
+  const int Q = fa.Q;
+  const int q = (int)cluster_ctarank();
+  const int cl = blockIdx.x / Q;
+  const SweepJob& jb = jobs.j[q];
+  const int64_t ld = jb.ld;
+  const int64_t half = ld >> 1;
+  double2* sv = s2_smem;                                   // w_q, split by row parity
+  int* tlo = reinterpret_cast<int*>(s2_smem + ld);         // tile -> first active index
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p0 = cl * range, p1 = min(fa.N, p0 + range);
+  const int ntiles = p1 > p0 ? (p1 - p0 + tile - 1) / tile : 0;
+  for (int r = tid; r < ld; r += kS2Threads) sv[(r & 1) ? half + (r >> 1) : (r >> 1)] = jb.w[r];
+  for (int t = tid; t <= ntiles; t += kS2Threads) tlo[t] = lower_bound_dev(jb.J, jb.n_act, min(p1, p0 + t * tile));
+  if (tid == 0) {
+    for (int b = 0; b < kS2Depth; ++b) {
+      mbar_init(&bar_dots[b], kS2Dot);
+      mbar_init(&bar_xhat[b], Q);
+      mbar_init(&bar_fused[b], Q);
+      mbar_init(&bar_free[b], kS2Axpy);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_acqrel();  // peers' barriers are initialised before anyone arrives remotely
+  double qn[5] = {0, 0, 0, 0, 0};
+  if (warp < kS2Dot) {
+    // ---------------- dot warps ----------------
+    const int steps = (int)(ld >> 6);
+    for (int T = 0; T < ntiles; ++T) {
+      const int b = T % kS2Depth;
+      if (T >= kS2Depth) mbar_wait_cluster(&bar_free[b], ((T / kS2Depth) - 1) & 1);
+      const int lo = tlo[T], hi = tlo[T + 1];
+      for (int i0 = lo + 2 * warp; i0 < hi; i0 += 2 * kS2Dot) {
+        const int i1 = min(i0 + 1, hi - 1);
+        double re[2], im[2];
+        sweep_dot2(jb.A, ld, jb.J[i0], jb.J[i1], steps, sv, half, lane, re, im);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          re[c] = warp_sum(re[c]);
+          im[c] = warp_sum(im[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int i = i0 + c;
+          if (lane == c && i < hi) {
+            const double2 r = jb.rhs[i];
+            const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re[c])), beta),
+                                            __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im[c])), beta));
+            const int p = jb.J[i];
+            const double2 old = jb.x_full[p];
+            jb.ring_slot[p] = c_abs(c_sub(xh, old));
+            jb.x_full[p] = xh;
+            jb.x_hat[i] = xh;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&bar_dots[b]);
+    }
+  } else if (warp < kS2Dot + kS2Fuse) {
+    // ---------------- fusion warps ----------------
+    const int slice = (tile + Q - 1) / Q;
+    for (int T = warp - kS2Dot; T < ntiles; T += kS2Fuse) {
+      const int b = T % kS2Depth;
+      const unsigned par = (T / kS2Depth) & 1;
+      mbar_wait_cluster(&bar_dots[b], par);  // this CTA's x-updates of tile T are written
+      if (lane == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        for (int k = 0; k < Q; ++k) mbar_arrive_remote(&bar_xhat[b], (unsigned)k);
+      }
+      mbar_wait_cluster(&bar_xhat[b], par);  // every sensor's x-updates of tile T are written
+      const int t0 = p0 + T * tile, t1 = min(p1, t0 + tile);
+      for (int j = t0 + q * slice + lane; j < min(t1, t0 + (q + 1) * slice); j += 32)
+        fusion_pixel(fa, j, [&](int k) { return __ldcg(jobs.j[k].x_full + j); }, qn);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        for (int k = 0; k < Q; ++k) mbar_arrive_remote(&bar_fused[b], (unsigned)k);
+      }
+    }
+  } else {
+    // ---------------- axpy warps ----------------
+    const int at = tid - (kS2Dot + kS2Fuse) * 32;  // 0 .. 32*kS2Axpy-1
+    double acc[RPT][4];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+    for (int T = 0; T < ntiles; ++T) {
+      const int b = T % kS2Depth;
+      mbar_wait_cluster(&bar_fused[b], (T / kS2Depth) & 1);
+      const int lo = tlo[T], hi = tlo[T + 1];
+      // rhs_{k+1} = data + beta gap + beta x_hat - sigma (admm.hpp:114-119), one column per thread
+      for (int i = lo + at; i < hi; i += 32 * kS2Axpy) {
+        const int c = jb.J[i];
+        const double2 d = jb.data[i], g = __ldcg(fa.gap + c), xh = __ldcg(jb.x_hat + i), sg = __ldcg(fa.sigma + c);
+        double2 v;
+        v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+        v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+        jb.rhs[i] = v;
+        s_coef[i - lo] = v;
+        s_col[i - lo] = c;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kS2Axpy) : "memory");
+      const int cnt = hi - lo;
+      int t = 0;
+      for (; t + 2 <= cnt; t += 2) {
+        const float2* c0 = jb.A + (int64_t)s_col[t] * ld;
+        const float2* c1 = jb.A + (int64_t)s_col[t + 1] * ld;
+        float4 x0[RPT], x1[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int64_t r = 2 * (at + 32 * kS2Axpy * u);
+          x0[u] = r < ld ? __ldg(reinterpret_cast<const float4*>(c0 + r)) : make_float4(0, 0, 0, 0);
+          x1[u] = r < ld ? __ldg(reinterpret_cast<const float4*>(c1 + r)) : make_float4(0, 0, 0, 0);
+        }
+        const double2 v0 = s_coef[t], v1 = s_coef[t + 1];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          cfma(acc[u][0], acc[u][1], x0[u].x, x0[u].y, v0);
+          cfma(acc[u][2], acc[u][3], x0[u].z, x0[u].w, v0);
+          cfma(acc[u][0], acc[u][1], x1[u].x, x1[u].y, v1);
+          cfma(acc[u][2], acc[u][3], x1[u].z, x1[u].w, v1);
+        }
+      }
+      if (t < cnt) {
+        const float2* c0 = jb.A + (int64_t)s_col[t] * ld;
+        const double2 v0 = s_coef[t];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int64_t r = 2 * (at + 32 * kS2Axpy * u);
+          if (r < ld) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(c0 + r));
+            cfma(acc[u][0], acc[u][1], x.x, x.y, v0);
+            cfma(acc[u][2], acc[u][3], x.z, x.w, v0);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kS2Axpy) : "memory");  // s_coef reused next tile
+      if (lane == 0) mbar_arrive_local(&bar_free[b]);
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t r = 2 * (at + 32 * kS2Axpy * u);
+      if (r < ld) {
+        double2* out = jb.part + (int64_t)cl * ld + r;
+        out[0] = make_double2(acc[u][0], acc[u][1]);
+        out[1] = make_double2(acc[u][2], acc[u][3]);
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync_acqrel();  // no CTA leaves while a peer may still arrive on its barriers
+  fusion_finish(fa, qn);
+}
+
+}  // namespace radmm_dev

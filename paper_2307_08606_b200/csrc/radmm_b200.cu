@@ -977,13 +977,17 @@ int env_int(const char* name, int dflt) {
 
 constexpr int kDefaultSweepTile = 16;
 
-bool fused_enabled() {
+// RADMM_FUSED: 0 = two-pass local updates (default), 1 = synchronous cluster
+// sweep (v1), 2 = asynchronous warp-specialised sweep (v2).
+int fused_version() {
   static int v = [] {
     const char* e = std::getenv("RADMM_FUSED");
     return e ? std::atoi(e) : 0;  // experimental: see DESIGN.md section 9
   }();
-  return v != 0;
+  return v;
 }
+
+bool fused_enabled() { return fused_version() != 0; }
 
 bool fused_eligible(radmm_ctx* c) {
   if (!fused_enabled() || c->world > 1 || c->Q < 1 || c->Q > 8) return false;
@@ -1024,7 +1028,54 @@ void launch_sweep(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa, 
   if (c->fpart.n < (size_t)5 * c->Q * clusters) c->fpart.alloc((size_t)5 * c->Q * clusters);
   FusionArgs a = fa;
   a.partials = c->fpart.p;
+  if (env_int("RADMM_DEBUG", 0))
+    std::fprintf(stderr, "[radmm] sweep1: clusters=%d grid=%d smem=%zu range=%d tile=%d\n", clusters,
+                 c->Q * clusters, smem, range, tile);
   CK(cudaLaunchKernelEx(&cfg, kern, pk, a, h->mu, h->beta, clusters, range, tile, prefetch));
+  ++c->launches;
+  c->sweep_clusters = clusters;
+}
+
+template <int RPT>
+void launch_sweep2(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa, const radmm_hyperparams* h,
+                   int64_t ld_max) {
+  auto kern = fused_sweep2_kernel<RPT>;
+  const int tile = std::max(2, std::min(64, env_int("RADMM_SWEEP_TILE", 16)));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c->Q;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kS2Threads);
+  cfg.stream = c->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)c->Q);
+  // smem: w (ld complex) + tile table of the largest range (one cluster: N)
+  size_t smem = (size_t)ld_max * sizeof(double2) + sizeof(int) * ((size_t)c->N / tile + 2);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(smem, 200 * 1024)));
+  cfg.dynamicSmemBytes = std::min<size_t>(smem, 200 * 1024);
+  int clusters = 0;
+  CK(cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg));
+  clusters = std::max(1, clusters);
+  const int cap = env_int("RADMM_SWEEP_CLUSTERS", 0);
+  if (cap > 0) clusters = std::min(clusters, cap);
+  for (const Sensor& S : c->sensors) clusters = std::min(clusters, S.part_chunks);
+  const int range = (int)round_up((c->N + clusters - 1) / clusters, tile);
+  clusters = (c->N + range - 1) / range;
+  smem = (size_t)ld_max * sizeof(double2) + sizeof(int) * ((size_t)range / tile + 2);
+  if (smem > 200 * 1024) fail(RADMM_INVALID_ARGUMENT, "fused sweep: tile table exceeds shared memory");
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3((unsigned)(c->Q * clusters));
+  if (c->fpart.n < (size_t)5 * c->Q * clusters) c->fpart.alloc((size_t)5 * c->Q * clusters);
+  FusionArgs a = fa;
+  a.partials = c->fpart.p;
+  if (env_int("RADMM_DEBUG", 0))
+    std::fprintf(stderr, "[radmm] sweep2: clusters=%d grid=%d block=%d smem=%zu range=%d tile=%d\n", clusters,
+                 c->Q * clusters, kS2Threads, smem, range, tile);
+  CK(cudaLaunchKernelEx(&cfg, kern, pk, a, h->mu, h->beta, range, tile));
   ++c->launches;
   c->sweep_clusters = clusters;
 }
@@ -1097,9 +1148,18 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     PhaseScope ps(c, RADMM_PHASE_SWEEP, a_bytes + 16.0 * c->N * (c->Q + 7));
     const size_t smem = (size_t)ld_max * sizeof(double2) + kSweepTile * (sizeof(double2) + sizeof(int));
     const FusionArgs fa = fusion_args(c, h, k);
-    if (ld_max <= 512) launch_sweep<1>(c, sp, fa, h, smem);
-    else if (ld_max <= 1024) launch_sweep<2>(c, sp, fa, h, smem);
-    else launch_sweep<4>(c, sp, fa, h, smem);
+    if (fused_version() == 2) {
+      if (ld_max <= 256) launch_sweep2<1>(c, sp, fa, h, ld_max);
+      else if (ld_max <= 512) launch_sweep2<2>(c, sp, fa, h, ld_max);
+      else if (ld_max <= 1024) launch_sweep2<4>(c, sp, fa, h, ld_max);
+      else launch_sweep2<8>(c, sp, fa, h, ld_max);
+    } else if (ld_max <= 512) {
+      launch_sweep<1>(c, sp, fa, h, smem);
+    } else if (ld_max <= 1024) {
+      launch_sweep<2>(c, sp, fa, h, smem);
+    } else {
+      launch_sweep<4>(c, sp, fa, h, smem);
+    }
   }
   for (Sensor& S : c->sensors) S.v_ready = true;
   ++c->upd;
