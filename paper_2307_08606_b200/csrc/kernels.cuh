@@ -227,7 +227,9 @@ __device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, doub
 // THREADS = 256 normally; 1024 when the shared vector is so large (KM = 8192:
 // 128 KB) that only one CTA fits per SM, to keep enough loads in flight.
 template <typename T, int EPI, bool SMEM_VEC, int CPW, int THREADS>
-__global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta) {
+__global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
+                                                         const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ double2 sv[];
   constexpr int kWarps = THREADS / 32;
   const ColDotJob& jb = jobs.j[blockIdx.y];
@@ -310,7 +312,9 @@ constexpr int kFwdTile = 2 * kFwdThreads;
 template <int MODE>
 __global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant__ Pack<FwdJob> jobs,
                                                           const double2* __restrict__ gap,
-                                                          const double2* __restrict__ sigma, double beta) {
+                                                          const double2* __restrict__ sigma, double beta,
+                                                          const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ unsigned char smem_raw[];
   const FwdJob& jb = jobs.j[blockIdx.z];
   const int chunk = blockIdx.x;
@@ -377,7 +381,8 @@ struct ReduceJob {
   double sign;
 };
 
-__global__ void reduce_parts_kernel(const __grid_constant__ Pack<ReduceJob> jobs) {
+__global__ void reduce_parts_kernel(const __grid_constant__ Pack<ReduceJob> jobs, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   const ReduceJob& jb = jobs.j[blockIdx.y];
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= jb.ld) return;
@@ -409,7 +414,8 @@ struct RhsJob {
 };
 
 __global__ void rhs_kernel(const __grid_constant__ Pack<RhsJob> jobs, const double2* __restrict__ gap,
-                           const double2* __restrict__ sigma, double beta) {
+                           const double2* __restrict__ sigma, double beta, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   const RhsJob& jb = jobs.j[blockIdx.y];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= jb.n) return;
@@ -451,6 +457,12 @@ struct FusionArgs {
   unsigned int* counter;
   FusionScalars* out_dev;
   FusionScalars* out_host; // mapped pinned memory
+  // device-guarded speculation: this round runs only if *go != 0; it then
+  // decides whether the next (already enqueued) round may run
+  const int* go;
+  int* go_next;
+  int stop_on_converge;     // !fixed_iterations
+  int screen_next_possible; // ASADMM, screening enabled, history full after this round
 };
 
 constexpr int kFusionThreads = 256;
@@ -532,6 +544,8 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
     f.eps_dual = a.root_n_eps_abs + a.eps_rel * sqrt(f.sq[4]);
     f.trigger = f.pri_res <= f.eps_pri;
     f.converged = a.has_prev && f.trigger && f.dual_res <= f.eps_dual;
+    if (a.go_next)
+      *a.go_next = !((a.stop_on_converge && f.converged) || (a.screen_next_possible && f.trigger));
     f.iteration = a.iteration;
     f.pad = 0;
     *a.out_dev = f;
@@ -548,6 +562,7 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
 }
 
 __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
+  if (a.go && __ldg(a.go) == 0) return;  // cancelled speculative iteration
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double q[5] = {0, 0, 0, 0, 0};
   if (j < a.N) fusion_pixel(a, j, [&](int k) { return a.contrib[k][j]; }, q);

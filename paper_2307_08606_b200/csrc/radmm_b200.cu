@@ -229,6 +229,8 @@ struct radmm_ctx {
   std::vector<double> iter_ms;       // per-step device wall time (incl. host round trip)
   std::vector<double> iter_busy_ms;  // per-step device time from first to last kernel
   std::vector<cudaEvent_t> ev_steps;
+  std::vector<cudaEvent_t> ev_ends;  // recorded after each round's fusion
+  DArr<int> go_flags;                // speculation guards, alternating per round
   std::vector<int64_t> iter_launches;
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -246,6 +248,7 @@ struct radmm_ctx {
     if (ev_it1) cudaEventDestroy(ev_it1);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_steps) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_ends) cudaEventDestroy(e);
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
     if (fs_host) cudaFreeHost(fs_host);
     if (h_totals) cudaFreeHost(h_totals);
@@ -333,7 +336,9 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   c->fpart.alloc((size_t)fblocks * 5);
   c->fcounter.alloc(1);
   c->fs_dev.alloc(1);
-  CK(cudaHostAlloc(&c->fs_host, sizeof(FusionScalars), cudaHostAllocMapped));
+  CK(cudaHostAlloc(&c->fs_host, 2 * sizeof(FusionScalars), cudaHostAllocMapped));
+  std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
+  c->go_flags.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
   CK(cudaHostAlloc(&c->h_totals, sizeof(int) * std::max(1, q_local), cudaHostAllocDefault));
   CK(cudaHostAlloc(&c->h_flags, sizeof(int) * kMaxBatch, cudaHostAllocDefault));
@@ -381,7 +386,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
 // every warp then owns a balanced contiguous range of columns.
 template <typename T, int EPI, bool SMEM, int CPW, int THREADS = 256>
 void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
-                   double beta) {
+                   double beta, const int* go) {
   auto kern = coldot_kernel<T, EPI, SMEM, CPW, THREADS>;
   if (SMEM && smem > 48 * 1024)
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -391,7 +396,7 @@ void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max
   constexpr int kWarps = THREADS / 32;
   const int gx =
       std::max(1, std::min((n_max + kWarps * CPW - 1) / (kWarps * CPW), (int)((target + nb - 1) / nb)));
-  LAUNCH(c, kern, dim3(gx, (unsigned)nb), THREADS, SMEM ? smem : 0, pk, mu, beta);
+  LAUNCH(c, kern, dim3(gx, (unsigned)nb), THREADS, SMEM ? smem : 0, pk, mu, beta, go);
 }
 
 int coldot_cpw() {
@@ -404,7 +409,7 @@ int coldot_cpw() {
 }
 
 template <typename T, int EPI>
-void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double beta) {
+void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double beta, const int* go = nullptr) {
   if (jobs.empty()) return;
   for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
     const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
@@ -419,23 +424,24 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
     if (n_max == 0) continue;
     const size_t smem = (size_t)ld_max * sizeof(double2);
     if (smem > kColdotSmemMax) {
-      coldot_launch<T, EPI, false, 1>(c, pk, nb, n_max, 0, mu, beta);
+      coldot_launch<T, EPI, false, 1>(c, pk, nb, n_max, 0, mu, beta, go);
       continue;
     }
     const int cpw = coldot_cpw() ? coldot_cpw() : kDefaultCpw;
     if (smem > kColdotBigSmem) {  // one CTA per SM: go wide
-      coldot_launch<T, EPI, true, 2, 1024>(c, pk, nb, n_max, smem, mu, beta);
+      coldot_launch<T, EPI, true, 2, 1024>(c, pk, nb, n_max, smem, mu, beta, go);
       continue;
     }
-    if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta);
-    else if (cpw == 2) coldot_launch<T, EPI, true, 2>(c, pk, nb, n_max, smem, mu, beta);
-    else coldot_launch<T, EPI, true, 4>(c, pk, nb, n_max, smem, mu, beta);
+    if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta, go);
+    else if (cpw == 2) coldot_launch<T, EPI, true, 2>(c, pk, nb, n_max, smem, mu, beta, go);
+    else coldot_launch<T, EPI, true, 4>(c, pk, nb, n_max, smem, mu, beta, go);
   }
 }
 
 // ---- forward (axpy) launches ------------------------------------------------
 template <int MODE>
-void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<ReduceJob>& red, double beta) {
+void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<ReduceJob>& red, double beta,
+             const int* go = nullptr) {
   for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
     const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
     Pack<FwdJob> pk;
@@ -454,10 +460,10 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
       if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(fwd_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       dim3 grid(max_chunks, (unsigned)((ld_max + kFwdTile - 1) / kFwdTile), (unsigned)nb);
-      LAUNCH(c, fwd_kernel<MODE>, grid, kFwdThreads, smem, pk, c->gap.p, c->sigma.p, beta);
+      LAUNCH(c, fwd_kernel<MODE>, grid, kFwdThreads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
     dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
-    LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp);
+    LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp, go);
   }
 }
 
@@ -794,7 +800,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
 }
 
 // One synchronous Jacobi sweep of local updates (admm.hpp:389-390).
-void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
+void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nullptr) {
   const int slot = c->upd % c->W;
   for (Sensor& S : c->sensors) S.v_ready = false;  // partial buffers are reused below
   std::vector<FwdJob> fj;
@@ -838,19 +844,19 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h) {
   if (!fj.empty()) {
     {
       PhaseScope ps(c, RADMM_PHASE_FORWARD, a_bytes);
-      forward<MODE_RHS>(c, fj, rj, h->beta);
+      forward<MODE_RHS>(c, fj, rj, h->beta, go);
     }
     {
       PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
-      coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+      coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta, go);
     }
     PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
-    coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta);
+    coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta, go);
   }
   if (n_rhs) {
     PhaseScope ps(c, RADMM_PHASE_PRIMAL, p_bytes);
-    LAUNCH(c, rhs_kernel, dim3((rhs_max + 255) / 256, n_rhs), 256, 0, rh, c->gap.p, c->sigma.p, h->beta);
-    coldot<double2, EPI_XPRIMAL>(c, pj, h->mu, h->beta);
+    LAUNCH(c, rhs_kernel, dim3((rhs_max + 255) / 256, n_rhs), 256, 0, rh, c->gap.p, c->sigma.p, h->beta, go);
+    coldot<double2, EPI_XPRIMAL>(c, pj, h->mu, h->beta, go);
   }
   ++c->upd;
 }
@@ -880,8 +886,13 @@ void exchange(radmm_ctx* c, double notice_bytes) {
 
 FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k);
 
-void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k) {
-  const FusionArgs a = fusion_args(c, h, k);
+void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go = nullptr,
+                int* go_next = nullptr, int stop_on_converge = 1, int screen_next_possible = 0) {
+  FusionArgs a = fusion_args(c, h, k);
+  a.go = go;
+  a.go_next = go_next;
+  a.stop_on_converge = stop_on_converge;
+  a.screen_next_possible = screen_next_possible;
   PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
   LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
@@ -1095,7 +1106,11 @@ FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   a.partials = c->fpart.p;
   a.counter = c->fcounter.p;
   a.out_dev = c->fs_dev.p;
-  a.out_host = c->fs_host_dev;
+  a.out_host = c->fs_host_dev + (k & 1);  // two slots: round k+1 may finish before the host reads round k
+  a.go = nullptr;
+  a.go_next = nullptr;
+  a.stop_on_converge = 1;
+  a.screen_next_possible = 0;
   return a;
 }
 
@@ -1138,7 +1153,7 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     PhaseScope ps(c, RADMM_PHASE_FORWARD, f_bytes);
     if (!fj.empty()) forward<MODE_RHS>(c, fj, rj_fwd, h->beta);
     if (n_ready)
-      LAUNCH(c, reduce_parts_kernel, dim3((unsigned)((ld_max + 255) / 256), n_ready), 256, 0, rj_sweep);
+      LAUNCH(c, reduce_parts_kernel, dim3((unsigned)((ld_max + 255) / 256), n_ready), 256, 0, rj_sweep, nullptr);
   }
   {
     PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
@@ -1227,29 +1242,68 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     c->ev_steps.push_back(e);
   }
   c->iter_busy_ms.clear();
-  for (int k = 1; k <= h->max_iter; ++k) {
-    uint64_t notice = 0;
-    const int64_t l0 = c->launches;
-    CK(cudaEventRecord(c->ev_steps[k - 1], c->stream));
-    CK(cudaEventRecord(c->ev_it0, c->stream));
-    if (asadmm && !disable && staged_trigger) notice = screen_all(c, h, k);
+  while (c->ev_ends.size() < (size_t)h->max_iter + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->ev_ends.push_back(e);
+  }
+  // Device-guarded speculation: while iteration k runs, iteration k+1 is
+  // already enqueued; its kernels run only if fusion_k set go[(k+1)&1] (not
+  // converged, and no screening staged).  Otherwise they exit at entry and
+  // the host re-issues k+1 after screening.  Off for observers / profiling /
+  // sharded or fused runs.
+  const bool spec = !(o && o->observer) && c->world <= 1 && !fused_enabled() && !c->profiling &&
+                    env_int("RADMM_SPECULATE", 1) != 0;
+  auto screen_next_possible = [&]() { return (asadmm && !disable && c->upd >= c->W) ? 1 : 0; };
+  // issue one round: local updates (+ exchange) + fusion; go == nullptr = unconditional
+  auto issue = [&](int kk, const int* go, uint64_t notice) {
+    int* go_next = spec ? c->go_flags.p + ((kk + 1) & 1) : nullptr;
     if (fused_eligible(c)) {
-      fused_iteration(c, h, k);
+      fused_iteration(c, h, kk);
     } else {
-      local_updates(c, h);
+      local_updates(c, h, go);
       exchange(c, (double)notice);
-      run_fusion(c, h, k);
+      run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, screen_next_possible());
     }
-    CK(cudaEventRecord(c->ev_it1, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, c->ev_it0, c->ev_it1));
-      c->iter_busy_ms.push_back(ms);
-      c->iter_launches.push_back(c->launches - l0);
+    CK(cudaEventRecord(c->ev_ends[kk], c->stream));
+  };
+  bool k_launched = false;   // iteration k already enqueued (speculatively)
+  int64_t l_k = 0;           // launch counter when iteration k was enqueued
+  uint64_t notice_k = 0;
+  for (int k = 1; k <= h->max_iter; ++k) {
+    if (!k_launched) {
+      l_k = c->launches;
+      CK(cudaEventRecord(c->ev_steps[k - 1], c->stream));
+      notice_k = 0;
+      if (asadmm && !disable && staged_trigger) notice_k = screen_all(c, h, k);
+      issue(k, nullptr, notice_k);
     }
+    const uint64_t notice = notice_k;
+    const int64_t l0 = l_k;
+    const int64_t l_end = c->launches;
+    bool spec_next = spec && k < h->max_iter;
+    int upd_before_next = c->upd;
+    if (spec_next) {
+      l_k = c->launches;
+      CK(cudaEventRecord(c->ev_steps[k], c->stream));
+      issue(k + 1, c->go_flags.p + ((k + 1) & 1), 0);
+    }
+    CK(cudaEventSynchronize(c->ev_ends[k]));
+    c->iter_launches.push_back(l_end - l0);
     flush_marks(c);
-    f = *c->fs_host;
+    f = c->fs_host[k & 1];
+    k_launched = false;
+    if (spec_next) {
+      const bool cancelled = (!fixed && f.converged) || (f.trigger && asadmm && !disable && upd_before_next >= c->W);
+      if (cancelled) {
+        CK(cudaStreamSynchronize(c->stream));
+        c->upd = upd_before_next;  // the no-op round consumed no update
+        for (Sensor& S : c->sensors) S.v_ready = false;
+      } else {
+        k_launched = true;
+        notice_k = 0;
+      }
+    }
     radmm_iteration_record rec{};
     rec.iteration = k;
     rec.pri_res = f.pri_res;
