@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Summarise ncu captures into profiles/ (tracked evidence).
 
-    python tools/ncu_summarize.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv \
-        --config c2 --out profiles/r01_ncu_c2
+    python tools/ncu_summarize.py --rep gpurun_out/a.ncu-rep gpurun_out/b.ncu-rep \
+        --launches gpurun_out/launches.csv --config c2 --out profiles/r01_ncu_c2
 
 Writes <out>.md (human-readable) and merges per-phase DRAM bytes per launch
 into profiles/ncu_summary.json (read by bench.py for roofline.traffic).
@@ -15,14 +15,13 @@ import json
 import os
 import subprocess
 
-PHASE_OF = {  # kernel (mangled fragment) -> bench phase name
+PHASE_OF = {  # kernel name fragment (mangled or demangled) -> bench phase name
     "coldot_kernelI6float2Li1": "adjoint",
     "fwd_kernelILi0": "forward",
     "coldot_kernelI7double2Li0": "gapply",
     "coldot_kernelI7double2Li2": "primal",
     "fusion_kernel": "fusion",
-    "fused_sweep_kernel": "adjoint_forward_fused",
-    # demangled spellings (ncu raw page)
+    "fused_sweep2_kernel": "sweep",
     "coldot_kernel<float2, 1": "adjoint",
     "fwd_kernel<0>": "forward",
     "coldot_kernel<double2, 0": "gapply",
@@ -33,7 +32,6 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "lts__t_sector_hit_rate.pct"]
-UNIT = {"dram__bytes_read.sum": "Gbyte?", "dram__bytes_write.sum": "Gbyte?"}
 
 
 def raw(rep):
@@ -55,9 +53,29 @@ def launches(path):
     return agg
 
 
+def capture_rows(rep):
+    h, rows = raw(rep)
+    out = []
+    for r in rows:
+        d = {m: r[h.index(m)] for m in METRICS if m in h}
+        d["name"] = r[h.index("Kernel Name")]
+        d["rep"] = os.path.basename(rep)
+        st = {}
+        for i, col in enumerate(h):
+            if col.startswith("smsp__pcsamp_warps_issue_stalled_") and not col.endswith("not_issued"):
+                try:
+                    st[col.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(r[i].replace(",", ""))
+                except ValueError:
+                    pass
+        tot = sum(st.values()) or 1.0
+        d["stalls"] = {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:4]}
+        out.append(d)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--rep")
+    ap.add_argument("--rep", nargs="*", default=[])
     ap.add_argument("--launches")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--out", required=True)
@@ -75,25 +93,14 @@ def main():
             md.append(f"| `{n}` | {c} | {v / 1e6:.3f} | {100 * v / tot:.1f}% |")
         md.append("")
     if a.rep:
-        h, rows = raw(a.rep)
         md += ["## full-set captures", ""]
         per = collections.defaultdict(list)
-        for r in rows:
-            mangled = r[h.index("Kernel Name")]
-            d = {m: r[h.index(m)] for m in METRICS if m in h}
-            d["name"] = mangled
-            st = {}
-            for i, col in enumerate(h):
-                if col.startswith("smsp__pcsamp_warps_issue_stalled_") and not col.endswith("not_issued"):
-                    try:
-                        st[col.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(r[i].replace(",", ""))
-                    except ValueError:
-                        pass
-            tot = sum(st.values()) or 1.0
-            d["stalls"] = {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:4]}
-            for frag, phase in PHASE_OF.items():
-                if frag in mangled:
-                    per[phase].append(d)
+        for rep in a.rep:
+            for d in capture_rows(rep):
+                for frag, phase in PHASE_OF.items():
+                    if frag in d["name"]:
+                        per[phase].append(d)
+                        break
         for phase, ds in per.items():
             rd = [float(x["dram__bytes_read.sum"]) for x in ds]
             wr = [float(x["dram__bytes_write.sum"]) for x in ds]
@@ -101,17 +108,18 @@ def main():
             traffic = (sum(rd) + sum(wr)) / len(ds)
             summary.setdefault(a.config, {})[phase] = {
                 "dram_bytes_per_launch": traffic, "duration_ns": sum(dur) / len(dur), "captures": len(ds),
-                "source": os.path.basename(a.rep)}
+                "source": ds[0]["rep"]}
             md += [f"### {phase} (`{ds[0]['name'][:90]}`)", "",
-                   f"- launches captured: {len(ds)}; mean duration {sum(dur) / len(dur) / 1e3:.1f} us (ncu, clocks uncontrolled)",
-                   f"- DRAM read {sum(rd) / len(ds) / 1e9:.3f} GB + write {sum(wr) / len(ds) / 1e9:.4f} GB per launch",
-                   f"- DRAM throughput {ds[0].get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')}% of peak; "
-                   f"warps active {ds[0].get('sm__warps_active.avg.pct_of_peak_sustained_active')}%; "
+                   f"- launches captured: {len(ds)}; mean duration {sum(dur) / len(dur) / 1e3:.1f} us "
+                   f"(ncu, clocks uncontrolled)",
+                   f"- DRAM read {sum(rd) / len(ds) / 1e9:.4f} GB + write {sum(wr) / len(ds) / 1e9:.4f} GB per launch",
+                   f"- DRAM throughput {ds[0].get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')}% of "
+                   f"peak; warps active {ds[0].get('sm__warps_active.avg.pct_of_peak_sustained_active')}%; "
                    f"regs {ds[0].get('launch__registers_per_thread')}; grid {ds[0].get('launch__grid_size')} x "
                    f"{ds[0].get('launch__block_size')}",
                    f"- fp64 pipe {ds[0].get('sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active')}%; "
-                   f"smem ld bank conflicts {ds[0].get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum')}; "
-                   f"L2 hit {ds[0].get('lts__t_sector_hit_rate.pct')}%",
+                   f"smem ld bank conflicts {ds[0].get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum')};"
+                   f" L2 hit {ds[0].get('lts__t_sector_hit_rate.pct')}%",
                    f"- top stalls: {ds[0]['stalls']}", ""]
     with open(a.out + ".md", "w") as f:
         f.write("\n".join(md) + "\n")
