@@ -303,3 +303,61 @@ def test_c1_fixed_iterations_parity():
     assert bad == 0
     for k in ("sensor_images", "s", "sigma", "x_global"):
         assert errs[k] < NORTH_STAR_TOL, errs
+
+
+# ---- event paths: downdates, form switch, rebuild, sharded context ------------------
+def _small_c1(**kw):
+    cfg = scenario.baseline_config("c1", **kw)
+    ops, ys, _, hyper = scenario.baseline_problem(cfg)
+    return ops, ys, hyper
+
+
+@pytest.mark.parametrize("nside,K,tol,iters", [(16, 16, 1e-3, 150), (12, 8, 3e-3, 150), (16, 64, 1e-3, 120)])
+def test_elimination_event_paths_match_oracle(nside, K, tol, iters):
+    """Aggressive screening drives the active sets through low-rank downdates,
+    dual->primal form switches and large-removal rebuilds; masks and states
+    must track the oracle at every step."""
+    ops, ys, hyper = _small_c1(nside=nside, K=K, n_targets=4, max_iter=iters)
+    hyper = dict(hyper, screening_tol=tol)
+    g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
+    print(f"nside={nside} K={K}: rebuilds={g.rebuilds} downdates={g.downdates} "
+          f"final sizes={g.report.iterations[-1].active_sizes} rows={ops[0].shape[0]}")
+    assert g.downdates + g.rebuilds > len(ops)  # events beyond the initial factorisations
+    bad, near = compare_masks(g, o, tol, 5)
+    assert bad == 0, (bad, near)
+    for rg, ro in zip(g.report.iterations, o.records):
+        assert rg.active_sizes == ro.active_sizes
+    errs = state_errors(g, o)
+    assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-6, errs
+
+
+def test_sharded_context_world1_equals_plain():
+    from paper_2307_08606_b200 import distributed as D
+    ops, ys, hyper = _small_c1(nside=16, K=16, max_iter=40)
+    h = api.Hyperparams(**hyper)
+    plain = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    s = D.sharded_solver(ops[0].shape[1], len(ops), 0, 1, 0, None)
+    for q, (a, y) in enumerate(zip(ops, ys)):
+        s.set_operator(q, a)
+        s.set_measurement(q, y)
+    r = s.run(h, api.Mode.ASADMM, fixed_iterations=True)
+    s.close()
+    assert np.array_equal(r.x_global, plain.x_global) and np.array_equal(r.sigma, plain.sigma)
+
+
+def test_apply_and_adjoint_match_host():
+    ops, ys, hyper = _small_c1(nside=16, K=16)
+    s = api.Solver(ops[0].shape[1], len(ops))
+    rng = np.random.default_rng(3)
+    for q, a in enumerate(ops):
+        s.set_operator(q, a)
+        x = rng.normal(size=a.shape[1]) + 1j * rng.normal(size=a.shape[1])
+        y = rng.normal(size=a.shape[0]) + 1j * rng.normal(size=a.shape[0])
+        a128 = a.astype(np.complex128)
+        assert rel(s.apply(q, x), a128 @ x) < 1e-13
+        assert rel(s.apply_adjoint(q, y), a128.conj().T @ y) < 1e-13
+        # adjoint identity <Ax, y> = <x, A^H y> (forward_model tests, 1e-10)
+        lhs, rhs = np.vdot(y, s.apply(q, x)), np.vdot(s.apply_adjoint(q, y), x)
+        assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(a128 @ x) * np.linalg.norm(y)
+    s.close()
