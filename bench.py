@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance run")
     p.add_argument("--ttt-max-iter", type=int, default=3000)
+    p.add_argument("--stress", action="store_true", help="BASELINE config 4 elimination-stress report")
+    p.add_argument("--stress-iters", type=int, default=400)
     return p.parse_args()
 
 
@@ -390,9 +392,54 @@ def e2e_run(cfg, hyper, ys, to_tolerance=True):
             "ms": ms, "setup_ms": r.setup_ms, "solve_ms": r.solve_ms}
 
 
+def stress(args):
+    """BASELINE config 4 (elimination stress): config-2 geometry at 0.1% and 5%
+    scene density, SADMM vs ASADMM on the same seed.  Fixed iteration count
+    (the degenerate BASELINE objective meets its stopping rule exactly when the
+    screening trigger first fires, so elimination is only
+    observable past it).  Reports active-set sizes over the run, the
+    compaction / refactor cost, and iterations/s of both modes.  One JSON line
+    per density (auxiliary output, not the headline line)."""
+    import __graft_entry__
+    from paper_2307_08606_b200 import api, scenario
+    __graft_entry__.build()
+    iters = args.stress_iters
+    for which in ("c4_sparse", "c4_dense"):
+        cfg = scenario.baseline_config(which)
+        s = api.Solver(cfg.N, cfg.Q)
+        ys, lam = build_workload(cfg, s, 0, cfg.Q)
+        h = api.Hyperparams(mu=cfg.mu, lambda_=lam, beta=cfg.beta, eps_abs=1e-4, eps_rel=1e-2, max_iter=iters)
+        out = {"config": which, "n_targets": cfg.n_targets, "iterations": iters,
+               "hyper": {"eps_abs": 1e-4, "eps_rel": 1e-2, "W": 5, "tol": 1e-5, "lambda": lam}}
+        for mode in (api.Mode.SADMM, api.Mode.ASADMM):
+            s.set_profiling(True)
+            r = s.run(h, mode, fixed_iterations=True)
+            ph = s.phase_stats()
+            ms, _ = s.iteration_stats(r.iterations)
+            trig = next((rec.iteration for rec in r.report.iterations if rec.pri_res <= rec.eps_pri), None)
+            sizes = [rec.active_sizes for rec in r.report.iterations]
+            pick = sorted({1, trig or 1, iters // 4, iters // 2, iters})
+            out[api.mode_name(mode)] = {
+                "iterations_per_s": r.iterations / (float(np.sum(ms)) / 1e3),
+                "solve_s_device": float(np.sum(ms)) / 1e3, "setup_s": r.setup_ms / 1e3,
+                "first_trigger_iteration": trig, "rebuilds": r.rebuilds, "downdates": r.downdates,
+                "active_sizes": {str(k): sizes[k - 1] for k in pick},
+                "total_active_solves": r.report.total_active_solves,
+                "compaction_ms_total": ph["screen"]["ms"], "refactor_ms_total": ph["refactor"]["ms"],
+                "screen_calls": ph["screen"]["calls"], "refactor_calls": ph["refactor"]["calls"]}
+        s.close()
+        a, p = out["asadmm"], out["sadmm"]
+        out["asadmm_vs_sadmm_solve_ratio"] = a["total_active_solves"] / max(1, p["total_active_solves"])
+        out["asadmm_vs_sadmm_time_ratio"] = a["solve_s_device"] / max(1e-12, p["solve_s_device"])
+        print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     from paper_2307_08606_b200 import scenario
+    if args.stress:
+        stress(args)
+        return
     cfg = scenario.baseline_config(args.config)
     if args.impl == "reference":
         reference_arm(args, cfg)
