@@ -593,6 +593,8 @@ struct ScreenJob {
   int* rem_pos;           // removed old compacted positions
   const double2* x_hat;
   double2* x_hat_new;
+  const double2* data;  // compacted with J: the (possibly lagged) data term
+  double2* data_new;
 };
 
 __global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int W, double tol) {
@@ -660,6 +662,7 @@ __global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid
     jb.Jnew[kept_before] = jb.J[i];
     jb.keep_pos[kept_before] = i;
     jb.x_hat_new[kept_before] = jb.x_hat[i];  // x_full[J_new] (admm.hpp:153-156)
+    jb.data_new[kept_before] = jb.data[i];
   } else {
     const int rpos = i - kept_before;
     jb.rem_pix[rpos] = jb.J[i];
@@ -686,7 +689,7 @@ struct MatRef {
   int conj;
 };
 
-enum { GEPI_PLAIN = 0, GEPI_GJ = 1 };
+enum { GEPI_PLAIN = 0, GEPI_GJ = 1, GEPI_SPLIT = 2 };
 
 struct GemmJob {
   int m, n, k;
@@ -718,15 +721,24 @@ __device__ __forceinline__ double2 mat_load(const MatRef& m, int i, int k) {
 constexpr int kGB = 64, kGK = 8;
 constexpr int kGjSmem = (64 * 65 + 128) * 16;
 
+// GEPI_SPLIT: split-K for skinny products (the rank-r downdates, r << KM):
+// blockIdx.z = job * nsplit + split; each split accumulates its K range and
+// stores the raw partial tile to ws[split][m][n]; gemm_split_reduce applies
+// alpha / beta0 / diag in fixed split order.
 template <int EPI>
-__global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
-  const GemmJob& jb = jobs.j[blockIdx.z];
+__global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
+                                                   double2* __restrict__ ws, int64_t ws_stride) {
+  const int split = blockIdx.z % nsplit;
+  const GemmJob& jb = jobs.j[blockIdx.z / nsplit];
   const int m0 = blockIdx.y * kGB, n0 = blockIdx.x * kGB;
   if (m0 >= jb.m || n0 >= jb.n) return;
   if (EPI == GEPI_PLAIN && jb.herm && m0 < n0) return;  // upper tiles come from the mirror
   __shared__ double2 As[2][kGK][kGB];
   __shared__ double2 Bs[2][kGK][kGB];
   const int tid = threadIdx.x;
+  // thread (tx, ty) owns rows m0 + tx + 16a and columns n0 + ty + 16b: a warp
+  // covers 16 consecutive rows of 2 columns, so the column-major epilogue
+  // (the rank-r updates are read-modify-write bound) is coalesced.
   const int tx = tid & 15, ty = tid >> 4;
   double acc_r[4][4], acc_i[4][4];
 #pragma unroll
@@ -756,19 +768,22 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
     }
   };
 
-  const int nk = (jb.k + kGK - 1) / kGK;
-  if (nk > 0) load_tile(0, 0);
+  const int nk_all = (jb.k + kGK - 1) / kGK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per;
+  const int nk = max(0, min(nk_all, t0 + per) - t0);
+  if (nk > 0) load_tile(0, t0 * kGK);
   __syncthreads();
   for (int t = 0; t < nk; ++t) {
     const int cur = t & 1;
-    if (t + 1 < nk) load_tile(cur ^ 1, (t + 1) * kGK);
+    if (t + 1 < nk) load_tile(cur ^ 1, (t0 + t + 1) * kGK);
 #pragma unroll
     for (int kk = 0; kk < kGK; ++kk) {
       double2 av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = As[cur][kk][ty + 16 * a];
+      for (int a = 0; a < 4; ++a) av[a] = As[cur][kk][tx + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = Bs[cur][kk][tx + 16 * b];
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[cur][kk][ty + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -781,21 +796,33 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
     }
     __syncthreads();
   }
+  // read the C tile first (all 16 loads in flight) when it is accumulated into
+  double2 cold[4][4];
+  if (EPI == GEPI_PLAIN && jb.beta0 != 0.0) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = m0 + tx + 16 * a, j = n0 + ty + 16 * b;
+        cold[a][b] = (i < jb.m && j < jb.n) ? jb.c[i + (int64_t)j * jb.ldc] : make_double2(0.0, 0.0);
+      }
+  }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int i = m0 + ty + 16 * a;
+    const int i = m0 + tx + 16 * a;
     if (i >= jb.m) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int j = n0 + tx + 16 * b;
+      const int j = n0 + ty + 16 * b;
       if (j >= jb.n) continue;
       double2* cp = jb.c + i + (int64_t)j * jb.ldc;
-      if (EPI == GEPI_PLAIN) {
+      if (EPI == GEPI_SPLIT) {
+        ws[(int64_t)blockIdx.z * ws_stride + (int64_t)j * jb.m + i] = make_double2(acc_r[a][b], acc_i[a][b]);
+      } else if (EPI == GEPI_PLAIN) {
         double2 o = make_double2(jb.alpha * acc_r[a][b], jb.alpha * acc_i[a][b]);
         if (jb.beta0 != 0.0) {
-          const double2 c0 = *cp;
-          o.x += jb.beta0 * c0.x;
-          o.y += jb.beta0 * c0.y;
+          o.x += jb.beta0 * cold[a][b].x;
+          o.y += jb.beta0 * cold[a][b].y;
         }
         if (i == j) {
           o.x += jb.diag_add;
@@ -819,6 +846,30 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
       }
     }
   }
+}
+
+// C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
+__global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
+                                  const double2* __restrict__ ws, int64_t ws_stride) {
+  const GemmJob& jb = jobs.j[blockIdx.y];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)jb.m * jb.n) return;
+  const int i = (int)(e % jb.m), j = (int)(e / jb.m);
+  double sr = 0.0, si = 0.0;
+  for (int s = 0; s < nsplit; ++s) {
+    const double2 v = ws[(int64_t)(blockIdx.y * nsplit + s) * ws_stride + (int64_t)j * jb.m + i];
+    sr += v.x;
+    si += v.y;
+  }
+  double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+  double2 o = make_double2(jb.alpha * sr, jb.alpha * si);
+  if (jb.beta0 != 0.0) {
+    const double2 c0 = *cp;
+    o.x += jb.beta0 * c0.x;
+    o.y += jb.beta0 * c0.y;
+  }
+  if (i == j) o.x += jb.diag_add;
+  *cp = o;
 }
 
 // In-place Gauss-Jordan inverse of one kb x kb HPD pivot block (kb <= 64)
@@ -943,6 +994,26 @@ __global__ void soft_threshold_kernel(const double2* __restrict__ v, int64_t n, 
 __global__ void abs_kernel(const double2* __restrict__ v, int n, double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = c_abs(v[i]);
+}
+
+// out = beta * (a - b): the accumulated frozen echo z = y_eff_s - y_eff,
+// scaled, that is folded into v when the stored data term lags (see
+// local_updates in radmm_b200.cu).
+__global__ void scaled_diff_kernel(double2* __restrict__ out, const double2* __restrict__ a,
+                                   const double2* __restrict__ b, double beta, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double2(beta * (a[i].x - b[i].x), beta * (a[i].y - b[i].y));
+}
+
+// Rb[:, t] = A[:, rem_pix[t]] promoted to complex128 (zero-padded to ld).
+__global__ void gather_cols_c128_kernel(const float2* __restrict__ A, int64_t ld, const int* __restrict__ pix,
+                                        int r, double2* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ld * r) return;
+  const int t = (int)(e / ld);
+  const int64_t row = e % ld;
+  const float2 v = A[row + (int64_t)pix[t] * ld];
+  out[e] = make_double2((double)v.x, (double)v.y);
 }
 
 __global__ void iota_kernel(int* __restrict__ J, int n) {

@@ -150,7 +150,7 @@ struct Sensor {
   bool stalled = false;
   DArr<int> J, Jnew, keep_pos, rem_pix, rem_pos, blk_cnt, blk_off, totals;
   DArr<unsigned char> keep;
-  DArr<double2> x_full, x_hat, x_hat_new, data, rhs;
+  DArr<double2> x_full, x_hat, x_hat_new, data, data_new, rhs;
   DArr<double> ring;
   // cached inverse of the capacitance (dual) or Gram (primal) matrix
   DArr<double2> G, G2;
@@ -161,6 +161,12 @@ struct Sensor {
   int part_chunks = 0;  // capacity of part in chunks of ld
   int removed_now = 0;
   bool v_ready = false;  // v = A_J rhs for the coming iteration left by the fused sweep
+  // Lagged data term (dual form): data holds mu A_J^H y_eff_s; the true data
+  // term is data - mu A_J^H z with z = y_eff_s - y_eff (frozen echo since the
+  // snapshot).  Then w = G (v_s + beta z) and x = (rhs_s - mu A_J^H w)/beta is
+  // exactly the reference update, so an elimination event needs no data pass.
+  DArr<double2> y_eff_s, bz;
+  bool data_lag = false;
 };
 
 struct Scratch {
@@ -231,6 +237,8 @@ struct radmm_ctx {
   std::vector<cudaEvent_t> ev_steps;
   std::vector<cudaEvent_t> ev_ends;  // recorded after each round's fusion
   DArr<int> go_flags;                // speculation guards, alternating per round
+  DArr<double2> split_ws;            // split-K partial tiles
+  bool defer_fail_check = false;     // downdates: pivot check folded into the iteration sync
   std::vector<int64_t> iter_launches;
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -261,6 +269,7 @@ namespace {
 
 constexpr size_t kColdotSmemMax = 200 * 1024;
 constexpr int kDefaultCpw = 2;
+constexpr int kDowndateMatvecMax = 8;  // removed columns handled as Hermitian matvecs
 constexpr size_t kColdotBigSmem = 96 * 1024;
 constexpr int kMaxChunk = 2048;  // forward columns per CTA (shared-memory coefficient slab)
 
@@ -349,7 +358,8 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
     S.keep.alloc(N);
     const int nb = (N + kScanBlock - 1) / kScanBlock;
     S.blk_cnt.alloc(nb); S.blk_off.alloc(nb); S.totals.alloc(1);
-    S.x_full.alloc(N); S.x_hat.alloc(N); S.x_hat_new.alloc(N); S.data.alloc(N); S.rhs.alloc(N);
+    S.x_full.alloc(N); S.x_hat.alloc(N); S.x_hat_new.alloc(N); S.data.alloc(N); S.data_new.alloc(N);
+    S.rhs.alloc(N);
   }
 }
 
@@ -365,6 +375,8 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.ld = round_up(rows, 64);
   S.A.alloc((size_t)S.ld * c->N);  // zero padding rows
   S.y_eff.alloc(S.ld);
+  S.y_eff_s.alloc(S.ld);
+  S.bz.alloc(S.ld);
   S.v.alloc(S.ld);
   S.w.alloc(S.ld);
   const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
@@ -489,8 +501,31 @@ void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
       nn = std::max(nn, pk.j[i].n);
     }
     if (mm == 0 || nn == 0) continue;
+    const int tiles = ((nn + kGB - 1) / kGB) * ((mm + kGB - 1) / kGB);
+    int kmax = 0, herm = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      kmax = std::max(kmax, pk.j[i].k);
+      herm |= pk.j[i].herm;
+    }
+    // skinny products (rank-r downdates): split K so the grid fills the GPU
+    int nsplit = 1;
+    // (>= 32 k-steps per split, aim for ~4 CTAs per SM)
+    if (EPI == GEPI_PLAIN && !herm && tiles * (int)nb < 4 * c->sm_count && kmax >= 64 * kGK) {
+      nsplit = std::min(kmax / (32 * kGK), (4 * c->sm_count + tiles * (int)nb - 1) / (tiles * (int)nb));
+      nsplit = std::max(1, nsplit);
+    }
+    if (nsplit > 1) {
+      const size_t need = (size_t)nsplit * nb * (size_t)mm * nn;
+      if (c->split_ws.n < need) c->split_ws.alloc(need, false);
+      dim3 grid((nn + kGB - 1) / kGB, (mm + kGB - 1) / kGB, (unsigned)(nb * nsplit));
+      const int64_t stride = (int64_t)mm * nn;  // uniform per (job, split) slot
+      LAUNCH(c, gemm_kernel<GEPI_SPLIT>, grid, 256, 0, pk, nsplit, c->split_ws.p, stride);
+      dim3 rg((unsigned)(((int64_t)mm * nn + 255) / 256), (unsigned)nb);
+      LAUNCH(c, gemm_split_reduce, rg, 256, 0, pk, nsplit, c->split_ws.p, stride);
+      continue;
+    }
     dim3 grid((nn + kGB - 1) / kGB, (mm + kGB - 1) / kGB, (unsigned)nb);
-    LAUNCH(c, gemm_kernel<EPI>, grid, 256, 0, pk);
+    LAUNCH(c, gemm_kernel<EPI>, grid, 256, 0, pk, 1, (double2*)nullptr, (int64_t)0);
   }
 }
 
@@ -545,6 +580,21 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     n_max = std::max(n_max, targets[i].n);
   }
   CK(cudaMemsetAsync(c->fail_flags.p, 0, sizeof(int) * kMaxBatch, c->stream));
+  CK(cudaFuncSetAttribute(gj_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjSmem));
+  if (n_max <= kGJB) {
+    // every matrix is a single pivot block (the r x r downdate systems):
+    // one in-shared-memory Gauss-Jordan, written back in place
+    Pack<DiagJob> dj;
+    for (size_t i = 0; i < T; ++i) {
+      DiagJob d{};
+      d.M = targets[i].M; d.ld = targets[i].ld; d.n = targets[i].n; d.k0 = 0; d.kb = targets[i].n;
+      d.P = targets[i].M; d.ldp = targets[i].ld;
+      d.fail = c->fail_flags.p + i;
+      dj.j[i] = d;
+    }
+    LAUNCH(c, gj_diag_kernel, dim3((unsigned)T), 1024, kGjSmem, dj);
+    n_max = 0;  // skip the blocked sweep below
+  }
   for (int k0 = 0; k0 < n_max; k0 += kGJB) {
     Pack<DiagJob> dj;
     std::vector<GemmJob> rjobs, ujobs;
@@ -639,6 +689,21 @@ void data_terms(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     jobs.push_back(j);
   }
   coldot<float2, EPI_STORE>(c, jobs, mu, 1.0);
+  for (int q : qs) {  // the data term is exact again: snapshot y_eff, no lag
+    Sensor& S = c->sensors[q];
+    CK(cudaMemcpyAsync(S.y_eff_s.p, S.y_eff.p, sizeof(double2) * S.ld, cudaMemcpyDeviceToDevice, c->stream));
+    S.data_lag = false;
+  }
+}
+
+// Lagged data term for dual sensors after an elimination event: bz = beta (y_eff_s - y_eff).
+void lag_data_terms(radmm_ctx* c, const std::vector<int>& qs, double beta) {
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    LAUNCH(c, scaled_diff_kernel, dim3((unsigned)((S.ld + 255) / 256)), 256, 0, S.bz.p, S.y_eff_s.p, S.y_eff.p,
+           beta, S.ld);
+    S.data_lag = true;
+  }
 }
 
 // Low-rank downdates after screening removed rem_q columns.
@@ -653,11 +718,12 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     const size_t r = S.removed_now;
     const size_t dimr = round_up(r, 64);
     if (S.primal) need += (dimr * dimr + (size_t)round_up(S.n_act, 64) * dimr) * sizeof(double2);
-    else need += (2 * (size_t)S.ld * dimr + dimr * dimr) * sizeof(double2);
+    else need += (3 * (size_t)S.ld * dimr + dimr * dimr) * sizeof(double2);
     need += (64 * 64 + 2 * dimr * 64) * sizeof(double2) + 4096;
   }
   c->scratch.reserve(need);
   std::vector<GemmJob> st1, st2, st3, st4;
+  std::vector<std::vector<ColDotJob>> p_by_col;  // P[:, u] = G a_u jobs, by column u
   std::vector<InvTarget> inv;
   Pack<SubJob> sub;
   int nsub = 0;
@@ -673,9 +739,24 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       const int m = S.rows;
       Pm[t] = c->scratch.take<double2>((size_t)S.ld * r);
       Tm[t] = c->scratch.take<double2>((size_t)S.ld * r);
-      // P = G R
-      st1.push_back(gjob(m, r, m, mref(S.G.p, S.ldg, false),
-                         mref(S.A.p, S.ld, true, false, false, nullptr, S.rem_pix.p), Pm[t], S.ld, 1.0, 0.0));
+      // P = G R: few columns -> r Hermitian matvecs G a_t through the streaming
+      // column-dot kernel (G read once per removed column, all sensors batched);
+      // many columns -> tiled GEMM
+      if (r <= kDowndateMatvecMax) {
+        double2* Rb = c->scratch.take<double2>((size_t)S.ld * r);
+        LAUNCH(c, gather_cols_c128_kernel, dim3((unsigned)((S.ld * r + 255) / 256)), 256, 0, S.A.p, S.ld,
+               S.rem_pix.p, r, Rb);
+        for (int u = 0; u < r; ++u) {
+          ColDotJob j{};
+          j.M = S.G.p; j.ld = S.ldg; j.len = S.rows; j.n_out = S.rows; j.vec = Rb + (size_t)u * S.ld;
+          j.out = Pm[t] + (size_t)u * S.ld; j.scale = 1.0;
+          if ((int)p_by_col.size() <= u) p_by_col.resize(u + 1);
+          p_by_col[u].push_back(j);
+        }
+      } else {
+        st1.push_back(gjob(m, r, m, mref(S.G.p, S.ldg, false),
+                           mref(S.A.p, S.ld, true, false, false, nullptr, S.rem_pix.p), Pm[t], S.ld, 1.0, 0.0));
+      }
       // S = I - mu R^H P
       st2.push_back(gjob(r, r, m, mref(S.A.p, S.ld, true, true, true, nullptr, S.rem_pix.p),
                          mref(Pm[t], S.ld, false), Sm[t], ldr, -mu, 0.0, 1.0));
@@ -717,6 +798,7 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     const int blocks = (int)std::min<int64_t>(2048, (sub_max + 255) / 256);
     LAUNCH(c, gather_sub_kernel, dim3(std::max(1, blocks), nsub), 256, 0, sub);
   }
+  for (const auto& jobs : p_by_col) coldot<double2, EPI_STORE>(c, jobs, mu, 1.0);
   gemm<GEPI_PLAIN>(c, st1);
   gemm<GEPI_PLAIN>(c, st2);
   gj_invert(c, inv, "factorize");
@@ -819,7 +901,8 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       f.rhs_out = S.rhs.p; f.part = S.part.p;
       plan_chunks(c, S, S.n_act, n_dual, f.n_chunks, f.chunk_len);
       fj.push_back(f);
-      rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0});
+      // v = beta z + A_J rhs_s when the data term lags (see Sensor::data_lag)
+      rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, S.data_lag ? S.bz.p : nullptr, S.v.p, 1.0});
       ColDotJob g{};
       g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
       gj.push_back(g);
@@ -897,6 +980,8 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go =
   LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
 
+bool fused_enabled();
+
 // SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386).
 // Returns the notice bytes of this round.
 uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
@@ -911,6 +996,7 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     j.keep = S.keep.p; j.block_counts = S.blk_cnt.p; j.block_offsets = S.blk_off.p; j.totals = S.totals.p;
     j.Jnew = S.Jnew.p; j.keep_pos = S.keep_pos.p; j.rem_pix = S.rem_pix.p; j.rem_pos = S.rem_pos.p;
     j.x_hat = S.x_hat.p; j.x_hat_new = S.x_hat_new.p;
+    j.data = S.data.p; j.data_new = S.data_new.p;
     pk.j[q] = j;
     n_max = std::max(n_max, S.n_act);
   }
@@ -942,6 +1028,7 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     S.v_ready = false;  // the speculative v was formed over the old active set
     std::swap(S.J, S.Jnew);
     std::swap(S.x_hat, S.x_hat_new);
+    std::swap(S.data, S.data_new);
     S.n_act = kept;
     changed.push_back(q);
     notice += notice_size((size_t)removed);
@@ -962,7 +1049,18 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   }
   PhaseScope ps(c, RADMM_PHASE_REFACTOR, rb);
   update_y_eff(c, changed);
-  data_terms(c, changed, h->mu);
+  {
+    // dual sensors that stay dual keep a lagged data term (no full pass);
+    // primal sensors (and the experimental fused sweeps) recompute it
+    std::vector<int> lag, exact;
+    for (int q : changed) {
+      const Sensor& S = c->sensors[q];
+      const bool stays_dual = !S.primal && S.n_act > S.rows;
+      (stays_dual && !fused_enabled() ? lag : exact).push_back(q);
+    }
+    lag_data_terms(c, lag, h->beta);
+    data_terms(c, exact, h->mu);
+  }
   std::vector<int> rebuild, down;
   for (int q : changed) {
     Sensor& S = c->sensors[q];
