@@ -1503,3 +1503,297 @@ __global__ void __launch_bounds__(kS2Threads, 1) fused_sweep2_kernel(const __gri
 }
 
 }  // namespace radmm_dev
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// Fused sweep v3: row-split cluster, TMA-fed shared-memory column ring.
+//
+// A cluster of kS3R CTAs owns a pixel range; CTA `rank` owns rows
+// [rank*sl, (rank+1)*sl) of EVERY sensor's operator (sl = ld / kS3R).  Per
+// pixel tile (kS3P pixels) one elected thread bulk-copies (TMA,
+// cp.async.bulk) the row slices of the tile's active columns of all sensors
+// into one of two shared-memory buffers.  Then:
+//   dots     warp q computes the partial dots slice(A_q(:,j))^H w_q[slice]
+//            for sensor q's columns of the tile (w slices live in smem)
+//   exchange cluster barrier; every CTA sums the kS3R partial dots of each
+//            column from its peers' shared memory (DSMEM, fixed rank order)
+//            -> identical full dots in every CTA
+//   x-update x = (rhs - mu u)/beta for the tile's columns (rank 0 writes)
+//   fusion   FusionCore::round for the tile's pixels, computed redundantly
+//            (identically) by every CTA from the local x values
+//   forward  v_{k+1}[slice] += A(slice, j) rhs_{k+1,j}, from the same smem
+// Each operator byte crosses HBM once per iteration; the TMA of tile t+1
+// overlaps the work on tile t.
+// ---------------------------------------------------------------------------
+constexpr int kS3R = 8;          // CTAs per cluster (row split)
+constexpr int kS3P = 4;          // pixels per tile
+constexpr int kS3Q = 8;          // max sensors (one warp each in the dot phase)
+constexpr int kS3Threads = 256;  // one slice row per thread (sl <= 256)
+constexpr int kS3Cols = kS3P * kS3Q;
+
+struct Sweep3Job {
+  const float2* A;
+  const int* J;
+  int n_act;
+  const double2* w;
+  const double2* data;
+  double2* rhs;
+  double2* x_hat;
+  double2* x_full;
+  double* ring_slot;
+  double2* part;  // [n_clusters][ld]
+};
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ double2 dsmem_load2(const double2* local, unsigned rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  double x, y;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(ra) : "memory");
+  return make_double2(x, y);
+}
+
+struct __align__(16) S3Tile {  // one tile, staged by the producer warp (per buffer)
+  double2 rhs[kS3Cols];   // rhs_k of each column (column order, contiguous per sensor)
+  double2 data[kS3Cols];  // data term of each column
+  double2 xg[kS3P];       // x_G before this round
+  double2 sg[kS3P];       // sigma before this round
+  double2 xf[kS3Q][kS3P]; // x_q before this round (frozen values, ring baseline)
+  int n;                  // columns in the tile
+  int q[kS3Cols];         // sensor of column c
+  int i[kS3Cols];         // active index within J_q
+  int pix[kS3Cols];       // pixel
+  int qstart[kS3Q + 1];   // columns of sensor q: [qstart[q], qstart[q+1])
+  int pq[kS3P][kS3Q];     // column of (pixel p, sensor q), -1 if frozen
+};
+
+__global__ void __launch_bounds__(kS3Threads, 1) fused_sweep3_kernel(const __grid_constant__ Pack<Sweep3Job> jobs,
+                                                                     const __grid_constant__ FusionArgs fa, double mu,
+                                                                     double beta, int64_t ld, int range) {
+  extern __shared__ __align__(128) unsigned char s3_raw[];
+  __shared__ __align__(8) uint64_t full_bar[2];
+  __shared__ S3Tile tiles[2];
+  __shared__ double2 pdot[2][kS3Cols];  // this CTA's partial dots (read by peers)
+  __shared__ double2 xloc[kS3Cols];     // x-update of the tile's columns
+  __shared__ double2 coef[kS3Cols];     // rhs_{k+1} of the tile's columns
+  __shared__ double2 gap_s[kS3P], sig_s[kS3P];
+  const int Q = fa.Q;
+  const unsigned rank = cluster_ctarank();
+  const int cl = blockIdx.x / kS3R;
+  const int sl = (int)(ld / kS3R);  // slice rows (<= 256)
+  const int64_t row0 = (int64_t)rank * sl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p0 = cl * range, p1 = min(fa.N, p0 + range);
+  const int ntiles = p1 > p0 ? (p1 - p0 + kS3P - 1) / kS3P : 0;
+  float2* buf0 = reinterpret_cast<float2*>(s3_raw);                                          // [2][kS3Cols][sl]
+  double2* wsl = reinterpret_cast<double2*>(s3_raw + 2ull * kS3Cols * sl * sizeof(float2));  // [Q][sl]
+  int* tab = reinterpret_cast<int*>(wsl + (size_t)Q * sl);                                   // [Q][ntiles+1]
+  for (int e = tid; e < Q * sl; e += kS3Threads) {
+    const int q = e / sl, r = e % sl;
+    wsl[e] = jobs.j[q].w[row0 + r];
+  }
+  for (int e = tid; e < Q * (ntiles + 1); e += kS3Threads) {
+    const int q = e / (ntiles + 1), t = e % (ntiles + 1);
+    tab[e] = lower_bound_dev(jobs.j[q].J, jobs.j[q].n_act, min(p1, p0 + t * kS3P));
+  }
+  if (tid == 0) {
+    mbar_init(&full_bar[0], 1);
+    mbar_init(&full_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const unsigned slice_bytes = (unsigned)(sl * sizeof(float2));
+  // producer warp: describe tile t and bulk-copy (TMA) its column slices and
+  // every per-tile input into buffer b; completion on full_bar[b]
+  auto issue = [&](int t, int b) {
+    S3Tile& T = tiles[b];
+    const int t0 = p0 + t * kS3P, np = min(p1, t0 + kS3P) - t0;
+    if (lane == 0) {
+      int n = 0;
+      for (int q = 0; q < kS3Q; ++q) {
+        T.qstart[q] = n;
+        if (q < Q) n += tab[q * (ntiles + 1) + t + 1] - tab[q * (ntiles + 1) + t];
+      }
+      T.qstart[kS3Q] = n;
+      T.n = n;
+      unsigned bytes = (unsigned)n * (slice_bytes + 2u * sizeof(double2)) + 2u * np * sizeof(double2) +
+                       (unsigned)Q * np * sizeof(double2);
+      mbar_arrive_expect_tx(&full_bar[b], bytes);
+    }
+    reinterpret_cast<int*>(T.pq)[lane] = -1;  // kS3P * kS3Q == 32
+    __syncwarp();
+    const int n = T.n;
+    float2* dst = buf0 + (size_t)b * kS3Cols * sl;
+    if (lane < n) {
+      int q = 0;
+      while (T.qstart[q + 1] <= lane) ++q;
+      const int i = tab[q * (ntiles + 1) + t] + (lane - T.qstart[q]);
+      const int pix = jobs.j[q].J[i];
+      T.q[lane] = q;
+      T.i[lane] = i;
+      T.pix[lane] = pix;
+      T.pq[pix - t0][q] = lane;
+      tma_bulk_g2s(dst + (size_t)lane * sl, jobs.j[q].A + (int64_t)pix * ld + row0, slice_bytes, &full_bar[b]);
+    }
+    if (lane < Q) {
+      const int q = lane;
+      const int c0 = T.qstart[q], cnt = T.qstart[q + 1] - c0;
+      const int i0 = tab[q * (ntiles + 1) + t];
+      if (cnt > 0) {
+        tma_bulk_g2s(&T.rhs[c0], jobs.j[q].rhs + i0, (unsigned)cnt * sizeof(double2), &full_bar[b]);
+        tma_bulk_g2s(&T.data[c0], jobs.j[q].data + i0, (unsigned)cnt * sizeof(double2), &full_bar[b]);
+      }
+      tma_bulk_g2s(&T.xf[q][0], jobs.j[q].x_full + t0, (unsigned)np * sizeof(double2), &full_bar[b]);
+    } else if (lane == kS3Q) {
+      tma_bulk_g2s(&T.xg[0], fa.xg + t0, (unsigned)np * sizeof(double2), &full_bar[b]);
+    } else if (lane == kS3Q + 1) {
+      tma_bulk_g2s(&T.sg[0], fa.sigma + t0, (unsigned)np * sizeof(double2), &full_bar[b]);
+    }
+  };
+  if (warp == 0) {
+    if (ntiles > 0) issue(0, 0);
+    __syncwarp();
+    if (ntiles > 1) issue(1, 1);
+  }
+  cluster_sync_acqrel();  // peers' pdot buffers exist
+  double acc[kS3Q][2];
+#pragma unroll
+  for (int q = 0; q < kS3Q; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double qn[5] = {0, 0, 0, 0, 0};
+  for (int t = 0; t < ntiles; ++t) {
+    const int b = t & 1;
+    mbar_wait_cluster(&full_bar[b], (t >> 1) & 1);
+    const S3Tile& T = tiles[b];
+    const float2* sb = buf0 + (size_t)b * kS3Cols * sl;
+    const int t0 = p0 + t * kS3P, np = min(p1, t0 + kS3P) - t0;
+    // ---- partial dots: warp q <-> sensor q, up to kS3P columns per warp ----
+    if (warp < Q) {
+      const int c0 = T.qstart[warp], c1 = T.qstart[warp + 1];
+      if (c0 < c1) {
+        double re[kS3P], im[kS3P];
+#pragma unroll
+        for (int u = 0; u < kS3P; ++u) re[u] = im[u] = 0.0;
+        const double2* wq = wsl + (size_t)warp * sl;
+        for (int r = lane; r < sl; r += 32) {
+          const double2 wv = wq[r];
+#pragma unroll
+          for (int u = 0; u < kS3P; ++u)
+            if (c0 + u < c1) {
+              const float2 a = sb[(size_t)(c0 + u) * sl + r];
+              cfma_conj(re[u], im[u], a.x, a.y, wv);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kS3P; ++u) {
+          re[u] = warp_sum(re[u]);
+          im[u] = warp_sum(im[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kS3P; ++u)
+          if (lane == u && c0 + u < c1) pdot[b][c0 + u] = make_double2(re[u], im[u]);
+      }
+    }
+    cluster_sync_acqrel();
+    // ---- full dots (fixed rank order) and the x-update ----
+    if (tid < T.n) {
+      double2 v[kS3R];
+#pragma unroll
+      for (int r = 0; r < kS3R; ++r) v[r] = dsmem_load2(&pdot[b][tid], (unsigned)r);
+      double ur = 0.0, ui = 0.0;
+#pragma unroll
+      for (int r = 0; r < kS3R; ++r) {
+        ur += v[r].x;
+        ui += v[r].y;
+      }
+      const double2 rr = T.rhs[tid];
+      const double2 xh = make_double2(__ddiv_rn(__dsub_rn(rr.x, __dmul_rn(mu, ur)), beta),
+                                      __ddiv_rn(__dsub_rn(rr.y, __dmul_rn(mu, ui)), beta));
+      xloc[tid] = xh;
+      if (rank == 0) {
+        const int q = T.q[tid], p = T.pix[tid];
+        const Sweep3Job& jb = jobs.j[q];
+        jb.ring_slot[p] = c_abs(c_sub(xh, T.xf[q][p - t0]));
+        jb.x_full[p] = xh;
+        jb.x_hat[T.i[tid]] = xh;
+      }
+    }
+    __syncthreads();
+    // ---- fusion for the tile's pixels (identical in every CTA) ----
+    if (tid < np) {
+      const int j = t0 + tid;
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < Q; ++k) {
+        const int c = T.pq[tid][k];
+        s = c_add(s, c >= 0 ? xloc[c] : T.xf[k][tid]);
+      }
+      s = make_double2(__ddiv_rn(s.x, (double)Q), __ddiv_rn(s.y, (double)Q));
+      const double2 xgp = T.xg[tid];
+      const double2 sg = T.sg[tid];
+      const double2 v = make_double2(__dadd_rn(s.x, __ddiv_rn(sg.x, beta)), __dadd_rn(s.y, __ddiv_rn(sg.y, beta)));
+      const double2 xg = soft_threshold1(v, fa.kappa);
+      const double2 eta = c_sub(s, xg);
+      const double2 dx = c_sub(xg, xgp);
+      const double2 sn = make_double2(__dadd_rn(sg.x, __dmul_rn(beta, eta.x)), __dadd_rn(sg.y, __dmul_rn(beta, eta.y)));
+      const double2 gp = c_sub(xg, s);
+      gap_s[tid] = gp;
+      sig_s[tid] = sn;
+      if (rank == 0) {
+        fa.sigma_pre[j] = sg;
+        fa.s[j] = s;
+        fa.xg[j] = xg;
+        fa.sigma[j] = sn;
+        fa.gap[j] = gp;
+        qn[0] += c_norm2(eta);
+        qn[1] += c_norm2(dx);
+        qn[2] += c_norm2(s);
+        qn[3] += c_norm2(xg);
+        qn[4] += c_norm2(sn);
+      }
+    }
+    __syncthreads();
+    // ---- rhs_{k+1} = data + beta gap + beta x - sigma (admm.hpp:114-119) ----
+    if (tid < T.n) {
+      const int p = T.pix[tid] - t0;
+      const double2 d = T.data[tid], g = gap_s[p], xh = xloc[tid], sg = sig_s[p];
+      double2 v;
+      v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+      v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+      coef[tid] = v;
+      if (rank == 0) jobs.j[T.q[tid]].rhs[T.i[tid]] = v;
+    }
+    __syncthreads();
+    // ---- forward accumulate from the same shared-memory slice ----
+    if (tid < sl) {
+#pragma unroll
+      for (int q = 0; q < kS3Q; ++q) {
+        if (q >= Q) break;
+        for (int c = T.qstart[q]; c < T.qstart[q + 1]; ++c) {
+          const float2 a = sb[(size_t)c * sl + tid];
+          cfma(acc[q][0], acc[q][1], a.x, a.y, coef[c]);
+        }
+      }
+    }
+    __syncthreads();  // buffer b (and tiles[b]) free
+    if (warp == 0 && t + 2 < ntiles) issue(t + 2, b);
+  }
+  if (tid < sl) {
+#pragma unroll
+    for (int q = 0; q < kS3Q; ++q) {
+      if (q >= Q) break;
+      jobs.j[q].part[(int64_t)cl * ld + row0 + tid] = make_double2(acc[q][0], acc[q][1]);
+    }
+  }
+  cluster_sync_acqrel();  // peers may still read our pdot
+  fusion_finish(fa, qn);
+}
+
+}  // namespace radmm_dev

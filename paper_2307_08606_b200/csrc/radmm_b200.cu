@@ -1089,17 +1089,17 @@ constexpr int kDefaultSweepTile = 16;
 // RADMM_FUSED: 0 = two-pass local updates (default), 1 = synchronous cluster
 // sweep (v1), 2 = asynchronous warp-specialised sweep (v2).
 int fused_version() {
-  static int v = [] {
-    const char* e = std::getenv("RADMM_FUSED");
-    return e ? std::atoi(e) : 0;  // experimental: see DESIGN.md section 9
-  }();
-  return v;
+  const char* e = std::getenv("RADMM_FUSED");  // read per call: tests switch it
+  return e ? std::atoi(e) : 0;                  // experimental: see DESIGN.md section 9
 }
 
 bool fused_enabled() { return fused_version() != 0; }
 
+bool sweep3_eligible(radmm_ctx* c);
+
 bool fused_eligible(radmm_ctx* c) {
   if (!fused_enabled() || c->world > 1 || c->Q < 1 || c->Q > 8) return false;
+  if (fused_version() == 3 && !sweep3_eligible(c)) return false;
   for (const Sensor& S : c->sensors)
     if (S.primal || S.ld > 4 * 512) return false;
   return true;
@@ -1189,6 +1189,67 @@ void launch_sweep2(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa,
   c->sweep_clusters = clusters;
 }
 
+bool sweep3_eligible(radmm_ctx* c) {
+  if (c->Q > kS3Q) return false;
+  for (const Sensor& S : c->sensors) {
+    if (S.primal || S.ld != c->sensors[0].ld) return false;
+    if (S.ld % kS3R != 0 || S.ld / kS3R > kS3Threads || S.ld / kS3R < 64) return false;
+  }
+  return true;
+}
+
+void launch_sweep3(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa, const radmm_hyperparams* h) {
+  const int64_t ld = c->sensors[0].ld;
+  const int sl = (int)(ld / kS3R);
+  Pack<Sweep3Job> pk;
+  for (int q = 0; q < c->Q; ++q) {
+    const SweepJob& s = sp.j[q];
+    pk.j[q] = Sweep3Job{s.A, s.J, s.n_act, s.w, s.data, s.rhs, s.x_hat, s.x_full, s.ring_slot, s.part};
+  }
+  const size_t base = 2ull * kS3Cols * sl * sizeof(float2) + (size_t)c->Q * sl * sizeof(double2);
+  // per-sensor tile tables: sized for >= 8 clusters, re-checked below
+  const size_t tab_est = sizeof(int) * (size_t)c->Q * ((c->N + 8 * kS3P - 1) / (8 * kS3P) + 2);
+  size_t smem = base + tab_est;
+  CK(cudaFuncSetAttribute(fused_sweep3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kS3R;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kS3Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(kS3R);
+  int clusters = 0;
+  CK(cudaOccupancyMaxActiveClusters(&clusters, (void*)fused_sweep3_kernel, &cfg));
+  clusters = std::max(1, clusters);
+  const int cap = env_int("RADMM_SWEEP_CLUSTERS", 0);
+  if (cap > 0) clusters = std::min(clusters, cap);
+  for (const Sensor& S : c->sensors) clusters = std::min(clusters, S.part_chunks);
+  const int range = (int)round_up((c->N + clusters - 1) / clusters, kS3P);
+  clusters = (c->N + range - 1) / range;
+  const size_t tab = sizeof(int) * (size_t)c->Q * (range / kS3P + 2);
+  if (tab > tab_est) {
+    smem = base + tab;
+    if (smem > 227 * 1024) fail(RADMM_INVALID_ARGUMENT, "fused sweep v3: tile tables exceed shared memory");
+    CK(cudaFuncSetAttribute(fused_sweep3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cfg.dynamicSmemBytes = smem;
+  }
+  cfg.gridDim = dim3((unsigned)(kS3R * clusters));
+  if (c->fpart.n < (size_t)5 * kS3R * clusters) c->fpart.alloc((size_t)5 * kS3R * clusters);
+  FusionArgs a = fa;
+  a.partials = c->fpart.p;
+  if (env_int("RADMM_DEBUG", 0))
+    std::fprintf(stderr, "[radmm] sweep3: clusters=%d grid=%d smem=%zu range=%d sl=%d\n", clusters,
+                 kS3R * clusters, smem, range, sl);
+  CK(cudaLaunchKernelEx(&cfg, fused_sweep3_kernel, pk, a, h->mu, h->beta, ld, range));
+  ++c->launches;
+  c->sweep_clusters = clusters;
+}
+
 FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   FusionArgs a;
   a.contrib = c->contrib.p;
@@ -1261,7 +1322,9 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     PhaseScope ps(c, RADMM_PHASE_SWEEP, a_bytes + 16.0 * c->N * (c->Q + 7));
     const size_t smem = (size_t)ld_max * sizeof(double2) + kSweepTile * (sizeof(double2) + sizeof(int));
     const FusionArgs fa = fusion_args(c, h, k);
-    if (fused_version() == 2) {
+    if (fused_version() == 3) {
+      launch_sweep3(c, sp, fa, h);
+    } else if (fused_version() == 2) {
       if (ld_max <= 256) launch_sweep2<1>(c, sp, fa, h, ld_max);
       else if (ld_max <= 512) launch_sweep2<2>(c, sp, fa, h, ld_max);
       else if (ld_max <= 1024) launch_sweep2<4>(c, sp, fa, h, ld_max);

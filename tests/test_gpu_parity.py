@@ -361,3 +361,20 @@ def test_apply_and_adjoint_match_host():
         lhs, rhs = np.vdot(y, s.apply(q, x)), np.vdot(s.apply_adjoint(q, y), x)
         assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(a128 @ x) * np.linalg.norm(y)
     s.close()
+
+
+@pytest.mark.parametrize("fused", ["1", "2", "3"])
+def test_fused_sweeps_match_oracle(fused, monkeypatch):
+    """The experimental single-kernel sweeps (RADMM_FUSED=1|2|3) reproduce the
+    oracle, including elimination (masks) -- on a shape every variant accepts
+    (Q=4 dual sensors, KM=512, N=1024)."""
+    ops, ys, hyper = _small_c1(nside=32, K=64, M=8, n_targets=6, max_iter=120)
+    hyper = dict(hyper, screening_tol=1e-3)
+    monkeypatch.setenv("RADMM_FUSED", fused)
+    g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    monkeypatch.delenv("RADMM_FUSED")
+    o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
+    bad, near = compare_masks(g, o, 1e-3, 5)
+    assert bad == 0, (bad, near)
+    errs = state_errors(g, o)
+    assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-6, errs
