@@ -49,6 +49,8 @@ void check_cuda(cudaError_t e, const char* what, int line) {
 }
 #define CK(x) check_cuda((x), #x, __LINE__)
 
+int env_int(const char* name, int dflt);
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -154,6 +156,13 @@ struct Sensor {
   DArr<double> ring;
   // cached inverse of the capacitance (dual) or Gram (primal) matrix
   DArr<double2> G, G2;
+  // cached factor of the full active set (depends on A, mu, beta only, not on
+  // y): reused by the next run on this resident problem (frames sharing A)
+  DArr<double2> G0;
+  bool g0_valid = false, g0_primal = false;
+  double g0_mu = 0, g0_beta = 0;
+  int64_t g0_ld = 0;
+  int g0_n = 0;
   int64_t ldg = 0;
   int g_n = 0;
   // forward partials / KM-space vectors
@@ -227,6 +236,7 @@ struct radmm_ctx {
   bool have_result = false;
   int64_t launches = 0;
   int64_t rebuilds = 0, downdates = 0;
+  int64_t factor_cache_hits = 0;
   int W = 5;
   int upd = 0;  // local updates performed in the current run
   // device timing: per-iteration CUDA events (always), per-phase events
@@ -383,6 +393,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.part_chunks = std::max(std::max(1, c->sm_count * c->fwd_per_sm / tiles), (c->N + kMaxChunk - 1) / kMaxChunk) + 1;
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
+  S.g0_valid = false;  // a new operator invalidates the cached factor
   S.has_y = false;
 }
 
@@ -878,7 +889,42 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
     CK(cudaMemsetAsync(v->p, 0, sizeof(double2) * N, c->stream));
   CK(cudaMemsetAsync(c->fcounter.p, 0, sizeof(unsigned), c->stream));
   data_terms(c, all, h->mu);
-  full_rebuild(c, all, h->mu, h->beta);
+  std::vector<int> fresh;
+  for (int q : all) {
+    Sensor& S = c->sensors[q];
+    if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta) {
+      if (S.G.n < (size_t)S.g0_ld * S.g0_n) S.G.alloc((size_t)S.g0_ld * S.g0_n);
+      CK(cudaMemcpyAsync(S.G.p, S.G0.p, sizeof(double2) * (size_t)S.g0_ld * S.g0_n, cudaMemcpyDeviceToDevice,
+                         c->stream));
+      S.primal = S.g0_primal;
+      S.ldg = S.g0_ld;
+      S.g_n = S.g0_n;
+      ++c->factor_cache_hits;
+    } else {
+      fresh.push_back(q);
+    }
+  }
+  full_rebuild(c, fresh, h->mu, h->beta);
+  // keep a copy for the next run when memory allows (always leave >= 4 GB free)
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  for (int q : fresh) {
+    Sensor& S = c->sensors[q];
+    const size_t bytes = sizeof(double2) * (size_t)S.ldg * S.g_n;
+    if (env_int("RADMM_FACTOR_CACHE", 1) == 0 || (S.G0.n < bytes / sizeof(double2) && free_b < bytes + (4ull << 30)))
+      continue;
+    if (S.G0.n < bytes / sizeof(double2)) {
+      S.G0.alloc(bytes / sizeof(double2), false);
+      free_b -= bytes;
+    }
+    CK(cudaMemcpyAsync(S.G0.p, S.G.p, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    S.g0_valid = true;
+    S.g0_primal = S.primal;
+    S.g0_mu = h->mu;
+    S.g0_beta = h->beta;
+    S.g0_ld = S.ldg;
+    S.g0_n = S.g_n;
+  }
 }
 
 // One synchronous Jacobi sweep of local updates (admm.hpp:389-390).

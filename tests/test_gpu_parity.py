@@ -378,3 +378,27 @@ def test_fused_sweeps_match_oracle(fused, monkeypatch):
     assert bad == 0, (bad, near)
     errs = state_errors(g, o)
     assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-6, errs
+
+
+def test_multi_frame_shared_operator_matches_oracle():
+    """BASELINE config 5 at reduced size: frames with fresh targets and noise
+    over the SAME operators, solved one after another on one resident problem
+    (the cached full-set factor is reused after the first frame)."""
+    cfg = scenario.baseline_config("c1", nside=16, K=32, n_targets=5, max_iter=60)
+    ops = [scenario.baseline_operator(cfg, q) for q in range(cfg.Q)]
+    s = api.Solver(cfg.N, cfg.Q)
+    for q, a in enumerate(ops):
+        s.set_operator(q, a)
+    for frame in range(3):
+        cfg.frame = frame
+        per_sensor = scenario.baseline_scene(cfg)
+        ys = scenario.baseline_measurements(cfg, ops, per_sensor)
+        hyper = scenario.baseline_hyper(cfg, scenario.baseline_lambda(cfg, ops, ys))
+        for q, y in enumerate(ys):
+            s.set_measurement(q, y)
+        g = s.run(api.Hyperparams(**hyper), api.Mode.ASADMM, fixed_iterations=True)
+        assert g.rebuilds == (cfg.Q if frame == 0 else 0)  # factor reused from frame 1 on
+        o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
+        errs = state_errors(g, o)
+        assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-8, (frame, errs)
+    s.close()
