@@ -163,10 +163,11 @@ def build_workload(cfg, solver, q_begin: int, q_end: int, dist=None):
 
 
 def algorithmic_bytes_per_iteration(cfg, sizes):
-    """Dual form: 2 passes over the active columns + the KM^2 capacitance
-    inverse (c128) + O(N) vectors."""
+    """Dual form: 2 passes over the active columns + the Hermitian triangle of
+    the KM x KM capacitance inverse (c128, KM(KM+1)/2 entries) + O(N) vectors
+    (SURVEY 8d)."""
     km = cfg.KM
-    return sum(2.0 * km * n * 8 + km * km * 16 for n in sizes) + 12.0 * cfg.N * 16
+    return sum(2.0 * km * n * 8 + km * (km + 1) * 8 for n in sizes) + 12.0 * cfg.N * 16
 
 
 # ---------------------------------------------------------------------------
@@ -379,7 +380,18 @@ def e2e_run(cfg, hyper, ys, to_tolerance=True):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    r = api.run(prob, hyper, api.Mode.ASADMM, fixed_iterations=not to_tolerance)
+    # api.run(prob, hyper, ASADMM), spelled out so each stage can be timed
+    t0 = time.perf_counter()
+    prob.validate()
+    hyper.validate()
+    solver = api.Solver.from_problem(prob)
+    t1 = time.perf_counter()
+    try:
+        r = solver.run(hyper, api.Mode.ASADMM, fixed_iterations=not to_tolerance)
+        t2 = time.perf_counter()
+    finally:
+        solver.close()
+    t3 = time.perf_counter()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -390,7 +402,9 @@ def e2e_run(cfg, hyper, ys, to_tolerance=True):
             "d2h_bytes_per_step": int(d2h),
             "step": f"one api.run call ({'to tolerance' if to_tolerance else 'fixed'}; "
                     f"{r.iterations} iterations, converged={r.converged})",
-            "ms": ms, "setup_ms": r.setup_ms, "solve_ms": r.solve_ms}
+            "ms": ms, "setup_ms": r.setup_ms, "solve_ms": r.solve_ms,
+            "stages_ms": {"context_and_upload": 1e3 * (t1 - t0), "run_and_fetch": 1e3 * (t2 - t1),
+                          "close": 1e3 * (t3 - t2)}}
 
 
 def stress(args):

@@ -848,6 +848,138 @@ __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<
   }
 }
 
+// Large products (Gram / capacitance builds, Gauss-Jordan rank-64 updates):
+// (16 TM) x (16 TN) tiles, TM x TN complex outputs per thread, the next K
+// slice prefetched into registers while the current one is multiplied, shared
+// rows padded by one element so transposed stores are conflict-free.  Every
+// output accumulates over k in the same order with the same FMA sequence as
+// gemm_kernel, so the two are bitwise identical.
+constexpr int kBigTM = 8, kBigTN = 4;
+constexpr int kBigBM = 16 * kBigTM, kBigBN = 16 * kBigTN;
+constexpr size_t kGemmBigSmem = (size_t)2 * kGK * ((kBigBM + 1) + (kBigBN + 1)) * sizeof(double2);
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_big_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  constexpr int TM = kBigTM, TN = kBigTN, BM = kBigBM, BN = kBigBN;
+  constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;  // prefetched elements per thread
+  const GemmJob& jb = jobs.j[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 + BM <= n0) return;  // strictly-upper tiles come from the mirror
+  extern __shared__ double2 gsm[];
+  double2(*As)[kGK][BM + 1] = reinterpret_cast<double2(*)[kGK][BM + 1]>(gsm);
+  double2(*Bs)[kGK][BN + 1] = reinterpret_cast<double2(*)[kGK][BN + 1]>(gsm + 2 * kGK * (BM + 1));
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc_r[TM][TN], acc_i[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc_r[a][b] = acc_i[a][b] = 0.0;
+  const MatRef A = jb.a, B = jb.b;
+  double2 pa[LA], pb[LB];
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (!A.trans) { ii = e % BM; kk = e / BM; } else { kk = e & 7; ii = e >> 3; }
+  };
+  auto b_pos = [&](int e, int& jj, int& kk) {
+    if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e % BN; kk = e / BN; }
+  };
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      const int gi = m0 + ii, gk = kk0 + kk;
+      pa[t] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      const int gj = n0 + jj, gk = kk0 + kk;
+      pb[t] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      As[buf][kk][ii] = pa[t];
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      Bs[buf][kk][jj] = pb[t];
+    }
+  };
+  const int nk = (jb.k + kGK - 1) / kGK;
+  if (nk > 0) {
+    fetch(0);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * kGK);  // in flight during the multiply below
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double2 av[TM], bv[TN];
+#pragma unroll
+      for (int a = 0; a < TM; ++a) av[a] = As[cur][kk][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < TN; ++b) bv[b] = Bs[cur][kk][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) {
+          acc_r[a][b] = fma(av[a].x, bv[b].x, acc_r[a][b]);
+          acc_r[a][b] = fma(-av[a].y, bv[b].y, acc_r[a][b]);
+          acc_i[a][b] = fma(av[a].x, bv[b].y, acc_i[a][b]);
+          acc_i[a][b] = fma(av[a].y, bv[b].x, acc_i[a][b]);
+        }
+    }
+    if (t + 1 < nk) stash(cur ^ 1);  // that buffer's readers finished in the previous iteration
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const int i = m0 + tx + 16 * a;
+    if (i >= jb.m) continue;
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+      const int j = n0 + ty + 16 * b;
+      if (j >= jb.n) continue;
+      double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+      if (EPI == GEPI_PLAIN) {
+        if (jb.herm && i < j) continue;  // written (bit-exactly) as the mirror of (j, i)
+        double2 o = make_double2(jb.alpha * acc_r[a][b], jb.alpha * acc_i[a][b]);
+        if (jb.beta0 != 0.0) {
+          const double2 c0 = *cp;
+          o.x += jb.beta0 * c0.x;
+          o.y += jb.beta0 * c0.y;
+        }
+        if (i == j) {
+          o.x += jb.diag_add;
+          if (jb.herm) o.y = 0.0;
+        }
+        *cp = o;
+        if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+      } else {
+        const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+        if (iK) {
+          *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+        } else {
+          const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+          const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+          *cp = make_double2(c0.x - acc_r[a][b], c0.y - acc_i[a][b]);
+        }
+      }
+    }
+  }
+}
+
 // C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
 __global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
                                   const double2* __restrict__ ws, int64_t ws_stride) {
@@ -1794,6 +1926,362 @@ __global__ void __launch_bounds__(kS3Threads, 1) fused_sweep3_kernel(const __gri
   }
   cluster_sync_acqrel();  // peers may still read our pdot
   fusion_finish(fa, qn);
+}
+
+}  // namespace radmm_dev
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// Hermitian G-apply  w = G v  reading only the lower block triangle of G.
+//
+// G (dual capacitance inverse, complex128, column-major, ld) is split into
+// 64 x 64 tiles; a work item is a strip of up to kHermStrip tiles
+// (I0 .. I0+nt-1) of tile column J, I0 >= J.  Column j of the strip feeds
+//   dot part: w[j] += sum_i conj(G[i, j]) v[i]   (i in the strip, incl. the
+//             diagonal tile: G[j, i] = conj(G[i, j]))
+//   ax part:  w[i] += sum_j G[i, j] v[j]         (tiles strictly below the
+//             diagonal: their upper mirror is never read)
+// Each item writes one dot partial (64 values, slot (J, g)) and one ax
+// partial per off-diagonal tile (slot tri(I, J)); herm_reduce_kernel sums
+// them in a fixed order, so the result is deterministic.  HBM bytes per
+// apply: ~(n^2/2 + 32 n) * 16 instead of n^2 * 16.
+// ---------------------------------------------------------------------------
+constexpr int kHermTile = 64;
+constexpr int kHermStrip = 4;
+
+struct HermJob {
+  const double2* G;
+  int64_t ld;
+  int n;             // matrix order (rows of the sensor)
+  int nb;            // tiles per side
+  int groups;        // strip groups per tile column: ceil(nb / kHermStrip)
+  const double2* v;
+  double2* w;
+  double2* dotp;     // [nb][groups][64]
+  double2* axp;      // [nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J
+};
+
+// item word: q (16) | J (16) | I0 (16) | nt (16)
+__host__ __device__ inline uint64_t herm_item(int q, int J, int I0, int nt) {
+  return (uint64_t)q << 48 | (uint64_t)J << 32 | (uint64_t)I0 << 16 | (uint64_t)nt;
+}
+
+__global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                         const uint64_t* __restrict__ items,
+                                                         const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
+  const uint64_t it = items[blockIdx.x];
+  const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+  const HermJob& jb = P.j[q];
+  __shared__ double2 vJ[kHermTile];
+  __shared__ double2 vI[kHermStrip * kHermTile];
+  __shared__ double2 sax[8][kHermTile];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = jb.n;
+  if (tid < kHermTile) {
+    const int j = J * kHermTile + tid;
+    vJ[tid] = j < n ? jb.v[j] : make_double2(0.0, 0.0);
+  }
+  for (int t = tid; t < nt * kHermTile; t += 256) {
+    const int i = I0 * kHermTile + t;
+    vI[t] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int c0 = warp * 8;  // this warp's 8 columns of the tile column
+  double dr[8], di[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+  const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
+  for (int t = 0; t < nt; ++t) {
+    const int I = I0 + t;
+    const int ib = I * kHermTile;
+    double2 g[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ib + lane + 32 * h, j = J * kHermTile + c0 + k;
+        g[k][h] = (i < n && j < n) ? __ldg(Gc + (int64_t)k * jb.ld + i) : make_double2(0.0, 0.0);
+      }
+    double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double2 vi = vI[t * kHermTile + lane + 32 * h];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        // conj(g) * v_i
+        dr[k] = fma(g[k][h].x, vi.x, dr[k]);
+        dr[k] = fma(g[k][h].y, vi.y, dr[k]);
+        di[k] = fma(g[k][h].x, vi.y, di[k]);
+        di[k] = fma(-g[k][h].y, vi.x, di[k]);
+        // g * v_j
+        const double2 vj = vJ[c0 + k];
+        ar[h] = fma(g[k][h].x, vj.x, ar[h]);
+        ar[h] = fma(-g[k][h].y, vj.y, ar[h]);
+        ai[h] = fma(g[k][h].x, vj.y, ai[h]);
+        ai[h] = fma(g[k][h].y, vj.x, ai[h]);
+      }
+    }
+    if (I != J) {  // strictly-lower tile: its mirror contributes to rows of block I
+#pragma unroll
+      for (int h = 0; h < 2; ++h) sax[warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+      __syncthreads();
+      if (tid < kHermTile) {
+        double2 s = sax[0][tid];
+#pragma unroll
+        for (int w8 = 1; w8 < 8; ++w8) {
+          s.x += sax[w8][tid].x;
+          s.y += sax[w8][tid].y;
+        }
+        jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = s;
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    dr[k] = warp_sum(dr[k]);
+    di[k] = warp_sum(di[k]);
+  }
+  if (lane == 0) {
+    const int g = (I0 - J) / kHermStrip;
+    double2* dp = jb.dotp + ((int64_t)J * jb.groups + g) * kHermTile + c0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
+  }
+}
+
+// w[b*64 + r] = sum_g dotp[b][g][r] + sum_{J < b} axp[tri(b, J)][r]  (fixed order)
+// 256 threads per row block: slice s = tid / 64 sums the partials k = s, s+4, ...
+// of the row's list (4 independent loads in flight), then the 4 slice sums are
+// added in slice order -- deterministic.
+__global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                         const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const HermJob& jb = P.j[blockIdx.y];
+  const int b = blockIdx.x, r = threadIdx.x & 63, sl = threadIdx.x >> 6;
+  __shared__ double2 part[4][kHermTile];
+  if (b >= jb.nb) return;
+  const int ng = (jb.nb - b + kHermStrip - 1) / kHermStrip;
+  const int total = ng + b;  // dot partials, then ax partials J = 0 .. b-1
+  const double2* dbase = jb.dotp + (int64_t)b * jb.groups * kHermTile + r;
+  const double2* abase = jb.axp + (int64_t)b * (b - 1) / 2 * kHermTile + r;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k0 = sl; k0 < total; k0 += 16) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 4 * u;
+      v[u] = k < total ? (k < ng ? dbase[(int64_t)k * kHermTile] : abase[(int64_t)(k - ng) * kHermTile])
+                       : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s.x += v[u].x;
+      s.y += v[u].y;
+    }
+  }
+  part[sl][r] = s;
+  __syncthreads();
+  if (sl == 0) {
+    const int row = b * kHermTile + r;
+    double2 t = part[0][r];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      t.x += part[u][r].x;
+      t.y += part[u][r].y;
+    }
+    if (row < jb.n) jb.w[row] = t;
+  }
+}
+
+// TMA-staged variant: persistent CTAs (one per SM) walk the item list
+// round-robin; warp 8 streams each 64 x 64 tile (64 column segments of
+// <= 1 KB) into a kHermStages-deep shared ring with cp.async.bulk, and the
+// eight compute warps consume it exactly like herm_gapply_kernel.
+constexpr int kHermStages = 3;
+constexpr int kHermTileBytes = kHermTile * kHermTile * 16;
+constexpr size_t kHermTmaSmem = (size_t)kHermStages * kHermTileBytes + 2 * 8 * kHermTile * 16 + 2 * kHermStages * 8;
+
+__device__ __forceinline__ void mbar_wait_cta_acq(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "HW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra HW_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(288, 1) herm_gapply_tma_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                                const uint64_t* __restrict__ items, int n_items,
+                                                                const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  extern __shared__ __align__(128) uint8_t hsm[];
+  double2* ring = reinterpret_cast<double2*>(hsm);
+  double2(*sax)[8][kHermTile] = reinterpret_cast<double2(*)[8][kHermTile]>(hsm + (size_t)kHermStages * kHermTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hsm + (size_t)kHermStages * kHermTileBytes + 2 * 8 * kHermTile * 16);
+  uint64_t* empty = full + kHermStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kHermStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    // producer: the same tile sequence the consumers walk
+    int slot = 0;
+    unsigned phase = 0;
+    int seq = 0;
+    for (int it_i = blockIdx.x; it_i < n_items; it_i += gridDim.x) {
+      const uint64_t it = items[it_i];
+      const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF),
+                nt = (int)(it & 0xFFFF);
+      const HermJob& jb = P.j[q];
+      const int cols = min(kHermTile, jb.n - J * kHermTile);
+      for (int t = 0; t < nt; ++t, ++seq) {
+        const int I = I0 + t;
+        const int rows = min(kHermTile, jb.n - I * kHermTile);
+        if (seq >= kHermStages) mbar_wait_cta_acq(&empty[slot], phase ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(cols * rows * 16));
+        __syncwarp();
+        double2* dst = ring + (size_t)slot * kHermTile * kHermTile;
+        const double2* src = jb.G + (int64_t)(J * kHermTile) * jb.ld + I * kHermTile;
+        for (int c = lane; c < cols; c += 32)
+          tma_bulk_g2s(dst + c * kHermTile, src + (int64_t)c * jb.ld, (unsigned)(rows * 16), &full[slot]);
+        if (++slot == kHermStages) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  // consumers (warps 0..7)
+  int slot = 0;
+  unsigned phase = 0;
+  int par = 0;
+  const int c0 = warp * 8;
+  for (int it_i = blockIdx.x; it_i < n_items; it_i += gridDim.x) {
+    const uint64_t it = items[it_i];
+    const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+    const HermJob& jb = P.j[q];
+    const int n = jb.n;
+    double2 vj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = J * kHermTile + c0 + k;
+      vj[k] = j < n ? jb.v[j] : make_double2(0.0, 0.0);
+    }
+    double dr[8], di[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const int I = I0 + t;
+      const int ib = I * kHermTile;
+      double2 vi[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ib + lane + 32 * h;
+        vi[h] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
+      }
+      mbar_wait_cta_acq(&full[slot], phase);
+      const double2* tile = ring + (size_t)slot * kHermTile * kHermTile;
+      double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = J * kHermTile + c0 + k;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = ib + lane + 32 * h;
+          const double2 g = (i < n && j < n) ? tile[(c0 + k) * kHermTile + lane + 32 * h] : make_double2(0.0, 0.0);
+          dr[k] = fma(g.x, vi[h].x, dr[k]);
+          dr[k] = fma(g.y, vi[h].y, dr[k]);
+          di[k] = fma(g.x, vi[h].y, di[k]);
+          di[k] = fma(-g.y, vi[h].x, di[k]);
+          ar[h] = fma(g.x, vj[k].x, ar[h]);
+          ar[h] = fma(-g.y, vj[k].y, ar[h]);
+          ai[h] = fma(g.x, vj[k].y, ai[h]);
+          ai[h] = fma(g.y, vj[k].x, ai[h]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[slot]);
+      if (++slot == kHermStages) {
+        slot = 0;
+        phase ^= 1;
+      }
+      if (I != J) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sax[par][warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (tid < kHermTile) {
+          double2 s = sax[par][0][tid];
+#pragma unroll
+          for (int w8 = 1; w8 < 8; ++w8) {
+            s.x += sax[par][w8][tid].x;
+            s.y += sax[par][w8][tid].y;
+          }
+          jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = s;
+        }
+        par ^= 1;  // the other buffer is free: its readers passed this barrier
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dr[k] = warp_sum(dr[k]);
+      di[k] = warp_sum(di[k]);
+    }
+    if (lane == 0) {
+      const int g = (I0 - J) / kHermStrip;
+      double2* dp = jb.dotp + ((int64_t)J * jb.groups + g) * kHermTile + c0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
+    }
+  }
+}
+
+// Hermitian projection of a factor in place: G <- (G + G^H) / 2 (the nearest
+// Hermitian matrix; never increases the Frobenius error of an inverse).
+// One 32 x 32 tile pair (I > J) or diagonal tile per CTA, staged through
+// shared memory so both halves are read and written coalesced.
+__global__ void __launch_bounds__(256) herm_symmetrize_kernel(double2* __restrict__ G, int64_t ld, int n) {
+  __shared__ double2 a[32][33], b[32][33];
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;          // tile (I, J): column j, row i
+    a[r][tx] = (i < n && j < n) ? G[i + (int64_t)j * ld] : make_double2(0.0, 0.0);
+    const int i2 = J * 32 + tx, j2 = I * 32 + r;        // tile (J, I)
+    b[r][tx] = (i2 < n && j2 < n) ? G[i2 + (int64_t)j2 * ld] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 m[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = ty + 8 * u;
+    // element (row I*32+tx, col J*32+r) pairs with (row J*32+r, col I*32+tx) = b[tx][r]
+    const double2 x = a[r][tx], y = b[tx][r];
+    m[u] = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+    if (I * 32 + tx == J * 32 + r) m[u].y = 0.0;
+  }
+  __syncthreads();  // everyone has read a and b
+#pragma unroll
+  for (int u = 0; u < 4; ++u) a[ty + 8 * u][tx] = m[u];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;  // tile (I, J), coalesced over tx
+    if (i < n && j < n) G[i + (int64_t)j * ld] = a[r][tx];
+    const int i2 = J * 32 + tx, j2 = I * 32 + r;  // tile (J, I) = conj transpose
+    const double2 v = a[tx][r];
+    if (I != J && i2 < n && j2 < n) G[i2 + (int64_t)j2 * ld] = make_double2(v.x, -v.y);
+  }
 }
 
 }  // namespace radmm_dev

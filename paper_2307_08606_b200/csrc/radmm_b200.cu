@@ -81,17 +81,30 @@ struct DArr {
     return *this;
   }
   ~DArr() { release(); }
+  // Device memory comes from the device's stream-ordered pool (see
+  // configure_pool): freed blocks stay reserved up to a retention threshold,
+  // so the next context on this device allocates without driver calls.
+  // Context streams are non-blocking, so frees wait for the device first.
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, 0);
+    }
     p = nullptr;
     n = 0;
   }
   void alloc(size_t count, bool zero = true) {
     release();
     if (count == 0) return;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    CK(cudaMallocAsync(&p, count * sizeof(T), 0));
+    CK(cudaStreamSynchronize(0));  // usable from any stream from here on
     n = count;
-    if (zero) CK(cudaMemset(p, 0, count * sizeof(T)));
+    if (zero) {
+      // legacy-stream memset: context streams are non-blocking, so finish it
+      // before any of their work can touch the buffer
+      CK(cudaMemset(p, 0, count * sizeof(T)));
+      CK(cudaStreamSynchronize(0));
+    }
   }
   void ensure(size_t count) {
     if (count > n) alloc(count);
@@ -176,6 +189,8 @@ struct Sensor {
   // exactly the reference update, so an elimination event needs no data pass.
   DArr<double2> y_eff_s, bz;
   bool data_lag = false;
+  // Hermitian G-apply partials (dot: nb x groups x 64, ax: nb(nb-1)/2 x 64)
+  DArr<double2> hdot, hax;
 };
 
 struct Scratch {
@@ -248,6 +263,9 @@ struct radmm_ctx {
   std::vector<cudaEvent_t> ev_ends;  // recorded after each round's fusion
   DArr<int> go_flags;                // speculation guards, alternating per round
   DArr<double2> split_ws;            // split-K partial tiles
+  DArr<uint64_t> herm_items;         // Hermitian G-apply work items (largest first)
+  std::vector<int64_t> herm_sig;     // (batch position, order) the items were built for
+  int herm_n_items = 0;
   bool defer_fail_check = false;     // downdates: pivot check folded into the iteration sync
   std::vector<int64_t> iter_launches;
   bool profiling = false;
@@ -335,14 +353,27 @@ void flush_marks(radmm_ctx* c) {
 
 void set_device(radmm_ctx* c) { CK(cudaSetDevice(c->device)); }
 
+// Keep up to RADMM_POOL_KEEP_GB (default 16) of freed device memory reserved
+// in the device's default pool between contexts (0: release at every sync).
+void configure_pool(int device) {
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = (uint64_t)std::max(0, env_int("RADMM_POOL_KEEP_GB", 16)) << 30;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+}
+
 void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   c->device = device;
   CK(cudaSetDevice(device));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
+  configure_pool(device);
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
     fail(RADMM_CUDA, "radmm_b200 requires an sm_100 (Blackwell) GPU; found " + std::string(prop.name));
-  c->sm_count = prop.multiProcessorCount;
+  }
+  CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS>, kFwdThreads, 16 * 1024));
   c->fwd_per_sm = std::max(1, c->fwd_per_sm);
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -383,7 +414,10 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   if (rows < 1) fail(RADMM_INVALID_ARGUMENT, "ForwardOperator: rows must be >= 1");
   S.rows = rows;
   S.ld = round_up(rows, 64);
-  S.A.alloc((size_t)S.ld * c->N);  // zero padding rows
+  if (S.A.n != (size_t)S.ld * c->N) S.A.alloc((size_t)S.ld * c->N, false);
+  if (S.ld > rows)  // zero padding rows (ordered before the upload on the context stream)
+    CK(cudaMemset2DAsync(S.A.p + rows, S.ld * sizeof(float2), 0, (S.ld - rows) * sizeof(float2), c->N,
+                         c->stream));
   S.y_eff.alloc(S.ld);
   S.y_eff_s.alloc(S.ld);
   S.bz.alloc(S.ld);
@@ -461,6 +495,74 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
   }
 }
 
+// ---- Hermitian G-apply (dual form): w = G v from the lower block triangle ----
+bool herm_enabled() { return env_int("RADMM_HERM", 1) != 0; }
+
+// algorithmic bytes of one G-apply: the Hermitian triangle (or the full matrix)
+double gapply_bytes(int n) { return herm_enabled() ? 8.0 * n * (n + 1.0) : 16.0 * n * (double)n; }
+
+void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
+  if (qs.empty()) return;
+  if (!herm_enabled() || qs.size() > (size_t)kMaxBatch) {
+    std::vector<ColDotJob> gj;
+    for (int q : qs) {
+      Sensor& S = c->sensors[q];
+      ColDotJob g{};
+      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
+      gj.push_back(g);
+    }
+    coldot<double2, EPI_STORE>(c, gj, 1.0, 1.0, go);
+    return;
+  }
+  Pack<HermJob> pk;
+  std::vector<int64_t> sig;
+  int nb_max = 0;
+  for (size_t i = 0; i < qs.size(); ++i) {
+    Sensor& S = c->sensors[qs[i]];
+    HermJob h{};
+    h.G = S.G.p; h.ld = S.ldg; h.n = S.rows;
+    h.nb = (S.rows + kHermTile - 1) / kHermTile;
+    h.groups = (h.nb + kHermStrip - 1) / kHermStrip;
+    const size_t nd = (size_t)h.nb * h.groups * kHermTile, na = (size_t)h.nb * (h.nb - 1) / 2 * kHermTile;
+    if (S.hdot.n < nd) S.hdot.alloc(nd, false);
+    if (S.hax.n < std::max<size_t>(na, 1)) S.hax.alloc(std::max<size_t>(na, 1), false);
+    h.v = S.v.p; h.w = S.w.p; h.dotp = S.hdot.p; h.axp = S.hax.p;
+    pk.j[i] = h;
+    nb_max = std::max(nb_max, h.nb);
+    sig.push_back(h.n);
+  }
+  if (sig != c->herm_sig) {
+    std::vector<uint64_t> items;
+    for (int nt = kHermStrip; nt >= 1; --nt)  // largest strips first (tail balance)
+      for (size_t i = 0; i < qs.size(); ++i) {
+        const int nb = pk.j[i].nb;
+        for (int J = 0; J < nb; ++J)
+          for (int I0 = J; I0 < nb; I0 += kHermStrip)
+            if (std::min(kHermStrip, nb - I0) == nt) items.push_back(herm_item((int)i, J, I0, nt));
+      }
+    if (c->herm_items.n < items.size()) {
+      CK(cudaStreamSynchronize(c->stream));  // queued launches may still read the old table
+      c->herm_items.alloc(items.size(), false);
+    }
+    // ordered in the context stream: launches already queued (a speculative
+    // iteration) read the previous table before it is overwritten
+    CK(cudaMemcpyAsync(c->herm_items.p, items.data(), items.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       c->stream));
+    c->herm_n_items = (int)items.size();
+    c->herm_sig = sig;
+  }
+  if (env_int("RADMM_HERM", 1) == 2) {
+    CK(cudaFuncSetAttribute(herm_gapply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kHermTmaSmem));
+    const int grid = std::min(c->herm_n_items, c->sm_count);
+    LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
+           c->herm_n_items, go);
+  } else {
+    LAUNCH(c, herm_gapply_kernel, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
+  }
+  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)qs.size()), 256, 0, pk, go);
+}
+
 // ---- forward (axpy) launches ------------------------------------------------
 template <int MODE>
 void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<ReduceJob>& red, double beta,
@@ -533,6 +635,13 @@ void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
       LAUNCH(c, gemm_kernel<GEPI_SPLIT>, grid, 256, 0, pk, nsplit, c->split_ws.p, stride);
       dim3 rg((unsigned)(((int64_t)mm * nn + 255) / 256), (unsigned)nb);
       LAUNCH(c, gemm_split_reduce, rg, 256, 0, pk, nsplit, c->split_ws.p, stride);
+      continue;
+    }
+    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 0)) {
+      CK(cudaFuncSetAttribute(gemm_big_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kGemmBigSmem));
+      dim3 grid((nn + kBigBN - 1) / kBigBN, (mm + kBigBM - 1) / kBigBM, (unsigned)nb);
+      LAUNCH(c, gemm_big_kernel<EPI>, grid, 256, kGemmBigSmem, pk);
       continue;
     }
     dim3 grid((nn + kGB - 1) / kGB, (mm + kGB - 1) / kGB, (unsigned)nb);
@@ -655,6 +764,18 @@ void ensure_g(Sensor& S, int dim, int64_t ld) {
   if (S.G.n < need) S.G.alloc(need);
 }
 
+// Hermitian projection of the dual factors (see herm_symmetrize_kernel): the
+// lower-triangle G-apply then uses exactly the matrix the full apply would.
+void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
+  if (env_int("RADMM_SYMM", 1) == 0) return;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    if (S.primal || S.g_n <= 0) continue;
+    const int nt = (S.g_n + 31) / 32;
+    LAUNCH(c, herm_symmetrize_kernel, dim3((unsigned)((int64_t)nt * (nt + 1) / 2)), 256, 0, S.G.p, S.ldg, S.g_n);
+  }
+}
+
 // Full rebuild for the listed sensors (batched): data term + factor.
 void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
   if (qs.empty()) return;
@@ -687,6 +808,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
   for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
   c->scratch.reserve(need);
   gj_invert(c, inv, "factorize");
+  symmetrize(c, qs);
 }
 
 // Data term mu A_J^H y_eff for the listed sensors (admm.hpp:177).
@@ -815,6 +937,7 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   gj_invert(c, inv, "factorize");
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
+  symmetrize(c, qs);
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     if (S.primal) {
@@ -933,10 +1056,12 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
   for (Sensor& S : c->sensors) S.v_ready = false;  // partial buffers are reused below
   std::vector<FwdJob> fj;
   std::vector<ReduceJob> rj;
-  std::vector<ColDotJob> gj, aj, pj;
+  std::vector<ColDotJob> aj, pj;
+  std::vector<int> gq;
   Pack<RhsJob> rh;
   int n_rhs = 0, rhs_max = 0;
   int n_dual = 0;
+  double g_bytes = 0;
   for (int q = 0; q < c->Q; ++q) if (!c->sensors[q].primal) ++n_dual;
   for (int q = 0; q < c->Q; ++q) {
     Sensor& S = c->sensors[q];
@@ -949,9 +1074,8 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       fj.push_back(f);
       // v = beta z + A_J rhs_s when the data term lags (see Sensor::data_lag)
       rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, S.data_lag ? S.bz.p : nullptr, S.v.p, 1.0});
-      ColDotJob g{};
-      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
-      gj.push_back(g);
+      gq.push_back(q);
+      g_bytes += gapply_bytes(S.rows);
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = S.n_act; a.cols = S.J.p; a.pix = S.J.p;
       a.vec = S.w.p; a.rhs = S.rhs.p; a.x_hat = S.x_hat.p; a.x_full = S.x_full.p; a.ring_slot = ring_slot;
@@ -966,9 +1090,8 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       pj.push_back(p);
     }
   }
-  double a_bytes = 0, g_bytes = 0, p_bytes = 0;
+  double a_bytes = 0, p_bytes = 0;
   for (const auto& a : aj) a_bytes += 8.0 * a.len * a.n_out;
-  for (const auto& g : gj) g_bytes += 16.0 * g.len * g.n_out;
   for (const auto& p : pj) p_bytes += 16.0 * p.len * p.n_out;
   if (!fj.empty()) {
     {
@@ -977,7 +1100,7 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
     }
     {
       PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
-      coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta, go);
+      gapply(c, gq, go);
     }
     PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
     coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta, go);
@@ -1329,7 +1452,7 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   Pack<ReduceJob> rj_sweep;
   int n_ready = 0;
   int64_t ld_max = 0;
-  std::vector<ColDotJob> gj;
+  std::vector<int> gq;
   Pack<SweepJob> sp;
   double a_bytes = 0, g_bytes = 0, f_bytes = 0;
   for (int q = 0; q < c->Q; ++q) {
@@ -1346,10 +1469,8 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     } else {
       rj_sweep.j[n_ready++] = ReduceJob{S.part.p, c->sweep_clusters, S.ld, S.rows, nullptr, S.v.p, 1.0};
     }
-    ColDotJob g{};
-    g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
-    gj.push_back(g);
-    g_bytes += 16.0 * S.rows * S.rows;
+    gq.push_back(q);
+    g_bytes += gapply_bytes(S.rows);
     a_bytes += 8.0 * S.rows * S.n_act;
     sp.j[q] = SweepJob{S.A.p, S.ld, S.n_act, S.J.p, S.w.p, S.data.p, S.rhs.p, S.x_hat.p, S.x_full.p,
                        S.ring.p + (size_t)slot * c->N, S.part.p};
@@ -1362,7 +1483,7 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   }
   {
     PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
-    coldot<double2, EPI_STORE>(c, gj, h->mu, h->beta);
+    gapply(c, gq);
   }
   {
     PhaseScope ps(c, RADMM_PHASE_SWEEP, a_bytes + 16.0 * c->N * (c->Q + 7));
@@ -1651,9 +1772,12 @@ int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int6
     if (lda < rows) fail(RADMM_INVALID_ARGUMENT, "lda < rows");
     set_device(ctx);
     prepare_operator(ctx, S, rows);
-    CK(cudaMemcpy2DAsync(S.A.p, S.ld * sizeof(float2), a, lda * sizeof(float2), rows * sizeof(float2), ctx->N,
-                         ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                         ctx->stream));
+    const cudaMemcpyKind kind = ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (lda == S.ld && rows == S.ld)  // contiguous: one linear copy
+      CK(cudaMemcpyAsync(S.A.p, a, sizeof(float2) * (size_t)rows * ctx->N, kind, ctx->stream));
+    else
+      CK(cudaMemcpy2DAsync(S.A.p, S.ld * sizeof(float2), a, lda * sizeof(float2), rows * sizeof(float2), ctx->N,
+                           kind, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1863,9 +1987,7 @@ int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
       f.A = S.A.p; f.ld = S.ld; f.n = sc->cols; f.J = S.J.p; f.src = S.rhs.p; f.part = S.part.p;
       plan_chunks(c, S, sc->cols, 1, f.n_chunks, f.chunk_len);
       forward<MODE_GATHER>(c, {f}, {ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0}}, 0.0);
-      ColDotJob g{};
-      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
-      coldot<double2, EPI_STORE>(c, {g}, sc->mu, sc->beta);
+      gapply(c, {0});
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = sc->cols; a.cols = S.J.p; a.pix = S.J.p; a.vec = S.w.p;
       a.rhs = S.rhs.p; a.x_hat = sc->x.p; a.x_full = sc->tmp.p; a.ring_slot = sc->ring.p;

@@ -22,6 +22,8 @@ PHASE_OF = {  # kernel name fragment (mangled or demangled) -> bench phase name
     "coldot_kernelI7double2Li2": "primal",
     "fusion_kernel": "fusion",
     "fused_sweep2_kernel": "sweep",
+    "herm_gapply_tma_kernel": "gapply",
+    "herm_gapply_kernel": "gapply",
     "coldot_kernel<float2, 1": "adjoint",
     "fwd_kernel<0>": "forward",
     "coldot_kernel<double2, 0": "gapply",
