@@ -322,9 +322,10 @@ def ours(args, cfg):
                "scaling": "strong", "vs_baseline": None, "dtype": "c64 operator, fp64 arithmetic",
                "data": "synthetic (seeded BASELINE dechirp operators generated on device)",
                "config": {"workload": f"BASELINE {cfg.name}: Q={cfg.Q} M={cfg.M} K={cfg.K} KM={cfg.KM} "
-                                      f"N={cfg.N} (128x128), {cfg.n_targets} targets, {cfg.snr_db} dB",
+                                      f"N={cfg.N} ({cfg.nside}x{cfg.nside}), {cfg.n_targets} targets, {cfg.snr_db} dB",
                           "global_batch": cfg.Q, "parallelism": f"sensor-sharded x{world}",
-                          "l2": "inputs 2.15 GB >> 126 MB L2 (no flush needed)",
+                          "l2": f"operators {cfg.Q * cfg.KM * cfg.N * 8 / 1e9:.2f} GB >> 126 MB L2 "
+                                "(streamed every iteration; no flush needed)",
                           "hyper": {"mu": cfg.mu, "beta": cfg.beta, "lambda": lam, "eps_rel": cfg.eps_rel,
                                     "eps_abs": cfg.eps_abs, "W": 5, "tol": 1e-5}},
                "gpu_launches": launches, "clocks": clk, "roofline": roofline,

@@ -84,6 +84,7 @@ struct ColDotJob {
   double2* x_hat;      // x-update outputs (compacted)
   double2* x_full;     // x-update scatter target (N)
   double* ring_slot;   // screening ring row for this update (N doubles)
+  int64_t vld;         // rows of vec staged in shared memory (0: ld); < ld for row segments
 };
 
 // Columns per warp (CPW): each vector element fetched from shared memory
@@ -241,9 +242,10 @@ __global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__
   const int i_end = (int)((gw + 1) * n_out / nw);
   if ((int)((int64_t)blockIdx.x * kWarps * n_out / nw) >= n_out) return;  // whole CTA idle
   const int64_t ld = jb.ld;
-  const int64_t half = ld >> 1;
+  const int64_t vld = jb.vld ? jb.vld : ld;
+  const int64_t half = vld >> 1;
   if (SMEM_VEC) {
-    for (int r = threadIdx.x; r < ld; r += blockDim.x)
+    for (int r = threadIdx.x; r < vld; r += blockDim.x)
       sv[ColLoad<T, CPW>::slot(r, half)] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
     __syncthreads();
   }
@@ -2282,6 +2284,31 @@ __global__ void __launch_bounds__(256) herm_symmetrize_kernel(double2* __restric
     const double2 v = a[tx][r];
     if (I != J && i2 < n && j2 < n) G[i2 + (int64_t)j2 * ld] = make_double2(v.x, -v.y);
   }
+}
+
+// Row-segmented adjoint (KM too large for one shared vector per CTA): the
+// segment kernels stored partial dots part[s * stride + i]; sum them in
+// segment order and apply the x-update epilogue (admm.hpp:114-122).
+struct XFinJob {
+  ColDotJob a;
+  const double2* part;
+  int nseg;
+  int64_t stride;
+};
+
+__global__ void __launch_bounds__(256) xdual_finish_kernel(const __grid_constant__ Pack<XFinJob> P, double mu,
+                                                          double beta, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const XFinJob& jb = P.j[blockIdx.y];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= jb.a.n_out) return;
+  double re = 0.0, im = 0.0;
+  for (int sg = 0; sg < jb.nseg; ++sg) {
+    const double2 v = jb.part[(int64_t)sg * jb.stride + i];
+    re += v.x;
+    im += v.y;
+  }
+  coldot_epilogue<EPI_XDUAL>(jb.a, i, re, im, mu, beta);
 }
 
 }  // namespace radmm_dev

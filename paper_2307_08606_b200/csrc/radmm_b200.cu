@@ -191,6 +191,7 @@ struct Sensor {
   bool data_lag = false;
   // Hermitian G-apply partials (dot: nb x groups x 64, ax: nb(nb-1)/2 x 64)
   DArr<double2> hdot, hax;
+  DArr<double2> apart;  // row-segmented adjoint partials (nseg x N)
 };
 
 struct Scratch {
@@ -475,7 +476,7 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
     int n_max = 0;
     for (size_t i = 0; i < nb; ++i) {
       pk.j[i] = jobs[b0 + i];
-      ld_max = std::max(ld_max, pk.j[i].ld);
+      ld_max = std::max(ld_max, pk.j[i].vld ? pk.j[i].vld : pk.j[i].ld);
       n_max = std::max(n_max, pk.j[i].n_out);
     }
     if (n_max == 0) continue;
@@ -637,7 +638,7 @@ void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
       LAUNCH(c, gemm_split_reduce, rg, 256, 0, pk, nsplit, c->split_ws.p, stride);
       continue;
     }
-    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 0)) {
+    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 1)) {
       CK(cudaFuncSetAttribute(gemm_big_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kGemmBigSmem));
       dim3 grid((nn + kBigBN - 1) / kBigBN, (mm + kBigBM - 1) / kBigBM, (unsigned)nb);
@@ -1050,6 +1051,60 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
   }
 }
 
+// Adjoint + x-update.  When KM is so large that one shared copy of w per
+// CTA leaves a single CTA per SM (KM > 6144, BASELINE config 3), the columns
+// are dotted in row segments of kAdjSeg rows (2048: 32 KB of w per CTA, the
+// config-2 occupancy) into partials, then summed in segment order.
+constexpr int kAdjSeg = 2048;
+
+void adjoint(radmm_ctx* c, const std::vector<ColDotJob>& aj, const std::vector<int>& aq, double mu, double beta,
+             const int* go) {
+  std::vector<ColDotJob> whole, segs;
+  std::vector<XFinJob> fin;
+  for (size_t t = 0; t < aj.size(); ++t) {
+    const ColDotJob& a = aj[t];
+    // RADMM_ADJ_SPLIT_ROWS / RADMM_ADJ_SEG override the switch point and the
+    // segment (tests force several segments at oracle-sized problems)
+    const int split_rows = env_int("RADMM_ADJ_SPLIT_ROWS", (int)(kColdotBigSmem / sizeof(double2)) + 1);
+    const int seg = (int)round_up(std::max(64, env_int("RADMM_ADJ_SEG", kAdjSeg)), 64);
+    if (a.len < split_rows) {
+      whole.push_back(a);
+      continue;
+    }
+    Sensor& S = c->sensors[aq[t]];
+    const int nseg = (a.len + seg - 1) / seg;
+    const size_t need = (size_t)nseg * c->N;
+    if (S.apart.n < need) S.apart.alloc(need, false);
+    for (int sg = 0; sg < nseg; ++sg) {
+      ColDotJob j{};
+      j.M = reinterpret_cast<const float2*>(a.M) + (int64_t)sg * seg;
+      j.ld = a.ld;
+      j.len = std::min(seg, a.len - sg * seg);
+      j.vld = seg;
+      j.n_out = a.n_out;
+      j.cols = a.cols;
+      j.vec = a.vec + (int64_t)sg * seg;
+      j.out = S.apart.p + (size_t)sg * c->N;
+      j.scale = 1.0;
+      segs.push_back(j);
+    }
+    fin.push_back(XFinJob{a, S.apart.p, nseg, c->N});
+  }
+  if (!whole.empty()) coldot<float2, EPI_XDUAL>(c, whole, mu, beta, go);
+  if (segs.empty()) return;
+  coldot<float2, EPI_STORE>(c, segs, mu, beta, go);
+  for (size_t b0 = 0; b0 < fin.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, fin.size() - b0);
+    Pack<XFinJob> pk;
+    int n_max = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = fin[b0 + i];
+      n_max = std::max(n_max, pk.j[i].a.n_out);
+    }
+    LAUNCH(c, xdual_finish_kernel, dim3((unsigned)((n_max + 255) / 256), (unsigned)nb), 256, 0, pk, mu, beta, go);
+  }
+}
+
 // One synchronous Jacobi sweep of local updates (admm.hpp:389-390).
 void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nullptr) {
   const int slot = c->upd % c->W;
@@ -1103,7 +1158,7 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       gapply(c, gq, go);
     }
     PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
-    coldot<float2, EPI_XDUAL>(c, aj, h->mu, h->beta, go);
+    adjoint(c, aj, gq, h->mu, h->beta, go);  // gq lists the same dual sensors in the same order
   }
   if (n_rhs) {
     PhaseScope ps(c, RADMM_PHASE_PRIMAL, p_bytes);
@@ -1991,7 +2046,7 @@ int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = sc->cols; a.cols = S.J.p; a.pix = S.J.p; a.vec = S.w.p;
       a.rhs = S.rhs.p; a.x_hat = sc->x.p; a.x_full = sc->tmp.p; a.ring_slot = sc->ring.p;
-      coldot<float2, EPI_XDUAL>(c, {a}, sc->mu, sc->beta);
+      adjoint(c, {a}, {0}, sc->mu, sc->beta, nullptr);
     }
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(x, sc->x.p, sizeof(double2) * sc->cols, cudaMemcpyDeviceToHost));

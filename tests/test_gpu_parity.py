@@ -92,12 +92,17 @@ def test_random_solves_match_inverse(rows, cols):
         assert np.linalg.norm(system @ x - rhs) < 1e-8 * np.linalg.norm(rhs)
 
 
-@pytest.mark.parametrize("herm", ["0", "1", "2"])
+@pytest.mark.parametrize("herm", ["0", "1", "2", "1-split"])
 @pytest.mark.parametrize("rows,cols", [(130, 700), (256, 1024), (64, 65)])
 def test_dual_solves_hermitian_apply(rows, cols, herm, monkeypatch):
     """Dual-form solves (cols > rows) through each G-apply variant (RADMM_HERM:
     0 full-matrix column dots, 1 lower-triangle registers, 2 lower-triangle
-    TMA ring) against the exact inverse; includes the C1 operator shape."""
+    TMA ring; "-split": row-segmented adjoint, 64-row segments) against the
+    exact inverse; includes the C1 operator shape."""
+    if herm.endswith("-split"):
+        herm = herm.split("-")[0]
+        monkeypatch.setenv("RADMM_ADJ_SPLIT_ROWS", "64")
+        monkeypatch.setenv("RADMM_ADJ_SEG", "64")
     monkeypatch.setenv("RADMM_HERM", herm)
     rng = np.random.default_rng(rows + cols)
     if (rows, cols) == (256, 1024):
@@ -316,7 +321,13 @@ def test_device_generator_matches_host():
     s.close()
 
 
-def test_c1_fixed_iterations_parity():
+@pytest.mark.parametrize("adj_split", [False, True])
+def test_c1_fixed_iterations_parity(adj_split, monkeypatch):
+    """adj_split forces the row-segmented adjoint (used for KM > 6144, config 3)
+    with four 64-row segments."""
+    if adj_split:
+        monkeypatch.setenv("RADMM_ADJ_SPLIT_ROWS", "64")
+        monkeypatch.setenv("RADMM_ADJ_SEG", "64")
     cfg = scenario.baseline_config("c1")
     ops, ys, _, hyper = scenario.baseline_problem(cfg)
     g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
