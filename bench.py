@@ -209,7 +209,22 @@ def cpu_sample(cfg, iters: int, sample_sensors: int = 2):
         t_local += t1 - t0
         t_fusion += t2 - t1
     per_iter = (t_local / sample_sensors) * cfg.Q / iters + t_fusion / iters
+    # one more iteration of one sensor on a single BLAS thread (SURVEY 8d asks
+    # for the 1-thread figure next to the all-core one)
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            sensors[0].local_update(fusion.gap, fusion.sigma)
+            t1 = time.perf_counter()
+            fusion.round()
+            t2 = time.perf_counter()
+        one = 1.0 / ((t1 - t0) * cfg.Q + (t2 - t1))
+    except Exception:
+        pass
     return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": int(cores), "kind": "port",
+            "value_1thread": one,
             "sample": (f"fp64 NumPy/SciPy oracle (Woodbury form), {sample_sensors} of {cfg.Q} sensors x {iters} "
                        f"iterations timed, per-sensor local-update time x{cfg.Q} + fusion; "
                        f"setup excluded; {cfg.name} shapes")}

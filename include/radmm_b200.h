@@ -188,6 +188,30 @@ int radmm_apply_operator(radmm_ctx* ctx, int q, const double* x, double* y);
 /* x = A_q^H y (y: rows complex128, x: N complex128), host buffers. */
 int radmm_apply_adjoint(radmm_ctx* ctx, int q, const double* y, double* x);
 
+/* ---- Multi-frame batches (BASELINE config 5) -------------------------------
+ * F independent scenes observed through the same operators (the reference
+ * solves them one after another: one run(problem_f, ...) per frame,
+ * proj/include/radmm/admm.hpp:357-445).  Frame f is a child context that
+ * views this context's operators (no copy) and owns everything that depends
+ * on its measurements.  Setting an operator on the parent drops its frames. */
+/* Measurement of sensor q in frame f (creates frames 0..f on first use). */
+int radmm_set_frame_measurement(radmm_ctx* ctx, int frame, int q, const double* y, int ptr_kind);
+/* Run frames 0..frames-1 in lockstep, frame f with hypers[f]; each frame stops
+ * on its own rule exactly as run() on that frame alone would.  summaries:
+ * frames entries (may be NULL).  Observers are not supported here. */
+int radmm_run_frames(radmm_ctx* ctx, int frames, const radmm_hyperparams* hypers, const radmm_run_options* opts,
+                     radmm_run_summary* summaries);
+/* Borrowed handle of frame f: every radmm_get_* result getter works on it.
+ * Owned by ctx (radmm_ctx_destroy refuses it). */
+int radmm_frame(radmm_ctx* ctx, int frame, radmm_ctx** out);
+
+/* Matched-filter image |sum_q A_q^H y_q| normalised to unit peak, on the
+ * resident operators and measurements (an all-zero result stays all-zero).
+ * Replaces back_projection(operators, measurements)
+ * (proj/include/radmm/forward_model.hpp:201-220).  image: N doubles.
+ * Sharded contexts: collective over all ranks (every rank gets the image). */
+int radmm_back_projection(radmm_ctx* ctx, double* image);
+
 /* ---- device-side measurement ------------------------------------------- */
 /* Phases of one iteration, timed with CUDA events on the context's stream
  * when profiling is enabled; bytes are ALGORITHMIC bytes. */

@@ -105,6 +105,9 @@ SIGNATURES = {
                                                   C.c_double, C.c_double, C.c_double]),
     "radmm_get_operator_c64": (C.c_int, [_VP, C.c_int, _VP]),
     "radmm_run": (C.c_int, [_VP, C.POINTER(Hyper), C.POINTER(Options), C.POINTER(Summary)]),
+    "radmm_set_frame_measurement": (C.c_int, [_VP, C.c_int, C.c_int, _VP, C.c_int]),
+    "radmm_run_frames": (C.c_int, [_VP, C.c_int, C.POINTER(Hyper), C.POINTER(Options), C.POINTER(Summary)]),
+    "radmm_frame": (C.c_int, [_VP, C.c_int, C.POINTER(_VP)]),
     "radmm_get_image": (C.c_int, [_VP, _DP]),
     "radmm_get_vector": (C.c_int, [_VP, C.c_int, _DP]),
     "radmm_get_sensor_image": (C.c_int, [_VP, C.c_int, _DP]),
@@ -120,6 +123,7 @@ SIGNATURES = {
     "radmm_soft_threshold": (C.c_int, [C.c_int, _DP, C.c_int64, C.c_double, _DP]),
     "radmm_apply_operator": (C.c_int, [_VP, C.c_int, _DP, _DP]),
     "radmm_apply_adjoint": (C.c_int, [_VP, C.c_int, _DP, _DP]),
+    "radmm_back_projection": (C.c_int, [_VP, _DP]),
     "radmm_set_profiling": (C.c_int, [_VP, C.c_int]),
     "radmm_get_phase_stats": (C.c_int, [_VP, C.POINTER(PhaseStat)]),
     "radmm_get_iteration_stats": (C.c_int, [_VP, _DP, C.POINTER(C.c_int64), C.c_int]),

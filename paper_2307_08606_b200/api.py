@@ -236,6 +236,9 @@ class Solver:
         return s
 
     def close(self) -> None:
+        if getattr(self, "_borrowed", False):  # a frame handle: owned by its parent
+            self._h = None
+            return
         if getattr(self, "_h", None):
             _lib.lib().radmm_ctx_destroy(self._h)
             self._h = None
@@ -311,6 +314,58 @@ class Solver:
         x = np.empty(self.N, dtype=np.complex128)
         _lib.check(_lib.lib().radmm_apply_adjoint(self._h, q, _dptr(y), _dptr(x)))
         return x
+
+    # ---- multi-frame batches (BASELINE config 5) -------------------------
+    def set_frame_measurement(self, frame: int, q: int, y) -> None:
+        """Measurement of sensor q in frame `frame` (frames share this
+        solver's operators; see radmm_set_frame_measurement)."""
+        y = _c128(y)
+        if self.rows[q] and y.shape[0] != self.rows[q]:
+            raise InvalidArgument(_lib.INVALID_ARGUMENT, "Problem: measurement length mismatch")
+        _lib.check(_lib.lib().radmm_set_frame_measurement(self._h, int(frame), q, y.ctypes.data_as(C.c_void_p),
+                                                          _lib.PTR_HOST))
+
+    def frame(self, f: int) -> "Solver":
+        """Borrowed Solver view of frame f (result getters); owned by self."""
+        h = C.c_void_p()
+        _lib.check(_lib.lib().radmm_frame(self._h, int(f), C.byref(h)))
+        v = Solver(self.N, self.Q, self.device, _ctx=h)
+        v.rows = list(self.rows)
+        v._borrowed = True
+        return v
+
+    def run_frames(self, hypers, mode: Mode = Mode.ASADMM, disable_screening: bool = False,
+                   fixed_iterations: bool = False, fetch: bool = True) -> list:
+        """Solve frames 0..F-1 (F = len(hypers)) in lockstep on the resident
+        operators; frame f behaves exactly like run(problem_f, hypers[f])
+        (admm.hpp:357-445).  Returns one RunResult per frame."""
+        hypers = list(hypers)
+        F = len(hypers)
+        arr = (_lib.Hyper * F)(*[h._c() for h in hypers])
+        summ = (_lib.Summary * F)()
+        opts = _lib.Options(int(mode), int(bool(disable_screening)), int(bool(fixed_iterations)),
+                            _lib.OBSERVER(), None)
+        _lib.check(_lib.lib().radmm_run_frames(self._h, F, arr, C.byref(opts), summ))
+        out = []
+        for f in range(F):
+            sm = summ[f]
+            res = RunResult(converged=bool(sm.converged), screening_stalled=bool(sm.screening_stalled),
+                            iterations=int(sm.iterations), setup_ms=sm.setup_ms, solve_ms=sm.solve_ms,
+                            kernel_launches=int(sm.kernel_launches), rebuilds=int(sm.rebuilds),
+                            downdates=int(sm.downdates))
+            res.report.total_active_solves = int(sm.total_active_solves)
+            res.report.total_bytes = int(sm.total_bytes)
+            if fetch:
+                self.frame(f)._fetch(res)
+            out.append(res)
+        return out
+
+    def back_projection(self) -> np.ndarray:
+        """back_projection (forward_model.hpp:201-220) on the resident operators
+        and measurements: |sum_q A_q^H y_q| normalised to unit peak."""
+        img = np.empty(self.N)
+        _lib.check(_lib.lib().radmm_back_projection(self._h, _dptr(img)))
+        return img
 
     def set_profiling(self, enabled: bool) -> None:
         _lib.check(_lib.lib().radmm_set_profiling(self._h, int(bool(enabled))))
@@ -417,6 +472,21 @@ def run(problem: Problem, hyper: Hyperparams, mode: Mode = Mode.ASADMM, observer
     solver = Solver.from_problem(problem, device)
     try:
         return solver.run(hyper, mode, observer, disable_screening, fixed_iterations)
+    finally:
+        solver.close()
+
+
+def back_projection(operators, measurements, device: int = 0) -> np.ndarray:
+    """back_projection(operators, measurements) (forward_model.hpp:201-220):
+    the matched-filter image |sum_q A_q^H y_q| / peak, computed on the GPU."""
+    ops = [op if isinstance(op, ForwardOperator) else ForwardOperator.from_matrix(op) for op in operators]
+    if not ops or len(ops) != len(measurements):
+        raise InvalidArgument(_lib.INVALID_ARGUMENT, "back_projection: need one measurement per operator")
+    if any(op.cols() != ops[0].cols() for op in ops):
+        raise InvalidArgument(_lib.INVALID_ARGUMENT, "back_projection: operators disagree on pixel count")
+    solver = Solver.from_problem(Problem(ops, list(measurements)), device)
+    try:
+        return solver.back_projection()
     finally:
         solver.close()
 

@@ -982,6 +982,160 @@ __global__ void __launch_bounds__(256, 1) gemm_big_kernel(const __grid_constant_
   }
 }
 
+// fp64 tensor-core (DMMA) variant of the large products.  mma.sync m8n8k4
+// f64 fragments (PTX ISA):  A 8x4 row: a = A[lane/4][lane%4];  B 4x8 col:
+// b = B[lane%4][lane/4];  C 8x8: c[v] = C[lane/4][2 (lane%4) + v].
+// A complex 8x8x4 block is four real MMAs (Cr += Ar Br - Ai Bi,
+// Ci += Ar Bi + Ai Br).  CTA tile 128 x 64, BK = 8, 8 warps as 4 (m) x 2 (n),
+// each warp a 32 x 32 block = 4 x 4 DMMA tiles.  Shared planes (real / imag,
+// k-major) have pitches = 4 (mod 16) doubles: the fragment loads of a half
+// warp hit 16 distinct banks.  Same register-prefetch pipeline and epilogues
+// as gemm_big_kernel; products are exact fp64 (not bitwise equal to the SIMT
+// kernels: the tensor core's accumulation order differs).
+constexpr int kDmBM = 128, kDmBN = 64, kDmPA = 132, kDmPB = 68;
+constexpr size_t kGemmDmmaSmem = (size_t)2 * 2 * kGK * (kDmPA + kDmPB) * sizeof(double);
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  constexpr int BM = kDmBM, BN = kDmBN, PA = kDmPA, PB = kDmPB;
+  constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;
+  const GemmJob& jb = jobs.j[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 + BM <= n0) return;
+  extern __shared__ double dsm[];
+  // [buf][plane][kk][pitch]
+  double* Ash = dsm;                            // 2 x 2 x kGK x PA
+  double* Bsh = dsm + 2 * 2 * kGK * PA;         // 2 x 2 x kGK x PB
+  auto As = [&](int buf, int pl, int kk) { return Ash + ((buf * 2 + pl) * kGK + kk) * PA; };
+  auto Bs = [&](int buf, int pl, int kk) { return Bsh + ((buf * 2 + pl) * kGK + kk) * PB; };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;  // warp block origin in the tile
+  const int fr = lane >> 2, fc = lane & 3;                // fragment row / k
+  double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+  const MatRef A = jb.a, B = jb.b;
+  double2 pa[LA], pb[LB];
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (!A.trans) { ii = e % BM; kk = e / BM; } else { kk = e & 7; ii = e >> 3; }
+  };
+  auto b_pos = [&](int e, int& jj, int& kk) {
+    if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e % BN; kk = e / BN; }
+  };
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      const int gi = m0 + ii, gk = kk0 + kk;
+      pa[t] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      const int gj = n0 + jj, gk = kk0 + kk;
+      pb[t] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      As(buf, 0, kk)[ii] = pa[t].x;
+      As(buf, 1, kk)[ii] = pa[t].y;
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      Bs(buf, 0, kk)[jj] = pb[t].x;
+      Bs(buf, 1, kk)[jj] = pb[t].y;
+    }
+  };
+  const int nk = (jb.k + kGK - 1) / kGK;
+  if (nk > 0) {
+    fetch(0);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * kGK);
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ar[a] = As(cur, 0, k4 + fc)[wm + 8 * a + fr];
+        ai[a] = As(cur, 1, k4 + fc)[wm + 8 * a + fr];
+        nai[a] = -ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        br[b] = Bs(cur, 0, k4 + fc)[wn + 8 * b + fr];
+        bi[b] = Bs(cur, 1, k4 + fc)[wn + 8 * b + fr];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma884(cr[a][b], ar[a], br[b]);
+          dmma884(cr[a][b], nai[a], bi[b]);
+          dmma884(ci[a][b], ar[a], bi[b]);
+          dmma884(ci[a][b], ai[a], br[b]);
+        }
+    }
+    if (t + 1 < nk) stash(cur ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * a + fr, j = n0 + wn + 8 * b + 2 * fc + v;
+        if (i >= jb.m || j >= jb.n) continue;
+        double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+        const double accr = cr[a][b][v], acci = ci[a][b][v];
+        if (EPI == GEPI_PLAIN) {
+          if (jb.herm && i < j) continue;
+          double2 o = make_double2(jb.alpha * accr, jb.alpha * acci);
+          if (jb.beta0 != 0.0) {
+            const double2 c0 = *cp;
+            o.x += jb.beta0 * c0.x;
+            o.y += jb.beta0 * c0.y;
+          }
+          if (i == j) {
+            o.x += jb.diag_add;
+            if (jb.herm) o.y = 0.0;
+          }
+          *cp = o;
+          if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+        } else {
+          const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+          if (iK) {
+            *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+          } else {
+            const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+            const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+            *cp = make_double2(c0.x - accr, c0.y - acci);
+          }
+        }
+      }
+}
+
 // C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
 __global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
                                   const double2* __restrict__ ws, int64_t ws_stride) {
@@ -2309,6 +2463,206 @@ __global__ void __launch_bounds__(256) xdual_finish_kernel(const __grid_constant
     im += v.y;
   }
   coldot_epilogue<EPI_XDUAL>(jb.a, i, re, im, mu, beta);
+}
+
+// back_projection (forward_model.hpp:203-220): |sum_q A_q^H y_q| for every
+// pixel, summing the per-sensor adjoint images in global sensor order.
+__global__ void bp_sum_kernel(const double2* const* __restrict__ imgs, int Q, int N, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = 0; q < Q; ++q) acc = c_add(acc, imgs[q][j]);
+  out[j] = c_abs(acc);
+}
+
+// ---------------------------------------------------------------------------
+// Frame-batched contractions (BASELINE config 5).  F <= 16 frames that share
+// a sensor's operator and full active set turn the three per-iteration
+// matvecs into GEMMs with F right-hand sides, so A_q is streamed ONCE for all
+// frames and the work runs on the fp64 tensor cores (DMMA m8n8k4):
+//   FWD  V_f = A_q RHS_f        (M = rows,   K = pixels; split-K partials)
+//   GAP  W_f = G_q V_f          (M = rows,   K = rows;   split-K partials)
+//   ADJ  X_f = (RHS_f - mu A_q^H W_f) / beta, + history / scatter epilogue
+//        (M = pixels, K = rows)
+// CTA tile 128 x 16 (frames), BK = 8, 8 warps x (16 rows x 16 frames).
+// ---------------------------------------------------------------------------
+constexpr int kFB = 16;            // max frames per batch
+constexpr int kFbBM = 128, kFbPA = 132, kFbPB = 20;
+enum { FB_FWD = 0, FB_GAP = 1, FB_ADJ = 2 };
+
+struct FrameBatchJob {
+  const void* A;        // float2 operator (FWD/ADJ) or double2 factor (GAP)
+  int64_t lda;
+  int m, k;             // GEMM M and K
+  int nf;               // frames in this batch
+  const double2* B[kFB];  // per-frame right-hand side (length k)
+  double2* part;        // FWD/GAP: partials [split][kFB][ldp]
+  int64_t ldp;
+  // ADJ epilogue, per frame
+  const double2* rhs[kFB];
+  double2* x_hat[kFB];
+  double2* x_full[kFB];
+  double* ring[kFB];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) frame_batch_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
+                                                         double mu, double beta) {
+  const FrameBatchJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.x * kFbBM;
+  if (m0 >= jb.m) return;
+  const int split = blockIdx.y;
+  const int nk_all = (jb.k + kGK - 1) / kGK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per, t1 = min(nk_all, t0 + per);
+  __shared__ double As[2][2][kGK][kFbPA];
+  __shared__ double Bs[2][2][kGK][kFbPB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp * 16, fr = lane >> 2, fc = lane & 3;
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+  double2 pa[4], pb = make_double2(0.0, 0.0);
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + t * 256;
+      int ii, kk;
+      if (MODE == FB_ADJ) { kk = e & 7; ii = e >> 3; } else { ii = e & 127; kk = e >> 7; }
+      const int gi = m0 + ii, gk = kk0 + kk;
+      double2 v = make_double2(0.0, 0.0);
+      if (gi < jb.m && gk < jb.k) {
+        if (MODE == FB_GAP) {
+          v = reinterpret_cast<const double2*>(jb.A)[gi + (int64_t)gk * jb.lda];
+        } else if (MODE == FB_FWD) {
+          const float2 x = reinterpret_cast<const float2*>(jb.A)[gi + (int64_t)gk * jb.lda];
+          v = make_double2((double)x.x, (double)x.y);
+        } else {  // conj(A[gk, gi])
+          const float2 x = reinterpret_cast<const float2*>(jb.A)[gk + (int64_t)gi * jb.lda];
+          v = make_double2((double)x.x, -(double)x.y);
+        }
+      }
+      pa[t] = v;
+    }
+    if (tid < kGK * kFB) {
+      const int kk = tid & 7, f = tid >> 3, gk = kk0 + kk;
+      pb = (f < jb.nf && gk < jb.k) ? jb.B[f][gk] : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + t * 256;
+      int ii, kk;
+      if (MODE == FB_ADJ) { kk = e & 7; ii = e >> 3; } else { ii = e & 127; kk = e >> 7; }
+      As[buf][0][kk][ii] = pa[t].x;
+      As[buf][1][kk][ii] = pa[t].y;
+    }
+    if (tid < kGK * kFB) {
+      const int kk = tid & 7, f = tid >> 3;
+      Bs[buf][0][kk][f] = pb.x;
+      Bs[buf][1][kk][f] = pb.y;
+    }
+  };
+  if (t0 < t1) {
+    fetch(t0 * kGK);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = t0; t < t1; ++t) {
+    const int cur = (t - t0) & 1;
+    if (t + 1 < t1) fetch((t + 1) * kGK);
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      double ar[2], ai[2], nai[2], br[2], bi[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        ar[a] = As[cur][0][k4 + fc][wm + 8 * a + fr];
+        ai[a] = As[cur][1][k4 + fc][wm + 8 * a + fr];
+        nai[a] = -ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        br[b] = Bs[cur][0][k4 + fc][8 * b + fr];
+        bi[b] = Bs[cur][1][k4 + fc][8 * b + fr];
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          dmma884(cr[a][b], ar[a], br[b]);
+          dmma884(cr[a][b], nai[a], bi[b]);
+          dmma884(ci[a][b], ar[a], bi[b]);
+          dmma884(ci[a][b], ai[a], br[b]);
+        }
+    }
+    if (t + 1 < t1) stash(cur ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * a + fr, f = 8 * b + 2 * fc + v;
+        if (i >= jb.m || f >= jb.nf) continue;
+        if (MODE != FB_ADJ) {
+          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cr[a][b][v], ci[a][b][v]);
+        } else {
+          // x = (rhs - mu A^H w) / beta  (Woodbury form of solver_core.hpp:47-51), admm.hpp:120-123
+          const double2 r = jb.rhs[f][i];
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cr[a][b][v])), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, ci[a][b][v])), beta));
+          const double2 old = jb.x_full[f][i];
+          jb.ring[f][i] = c_abs(c_sub(xh, old));
+          jb.x_full[f][i] = xh;
+          jb.x_hat[f][i] = xh;
+        }
+      }
+}
+
+// out_f[i] = sum_s part[s][f][i] (fixed split order) for every frame of a job
+struct FrameReduceJob {
+  const double2* part;
+  int64_t ldp;
+  int m, nf, nsplit;
+  double2* out[kFB];
+};
+
+__global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
+  const FrameReduceJob& jb = jobs[blockIdx.z];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, f = blockIdx.y;
+  if (i >= jb.m || f >= jb.nf) return;
+  double2 s = make_double2(0.0, 0.0);
+  for (int sp = 0; sp < jb.nsplit; ++sp) {
+    const double2 v = jb.part[((int64_t)sp * kFB + f) * jb.ldp + i];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  jb.out[f][i] = s;
+}
+
+// rhs_f[j] = data_f[j] + beta gap_f[j] + beta x_hat_f[j] - sigma_f[j] for the
+// full active set (admm.hpp:114-119), every (sensor, frame) of the batch.
+struct FrameRhsJob {
+  int n;
+  const double2* data;
+  const double2* x_hat;
+  const double2* gap;
+  const double2* sigma;
+  double2* rhs;
+};
+
+__global__ void frame_rhs_kernel(const FrameRhsJob* __restrict__ jobs, double beta) {
+  const FrameRhsJob& jb = jobs[blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jb.n) return;
+  const double2 d = jb.data[j], g = jb.gap[j], x = jb.x_hat[j], sg = jb.sigma[j];
+  jb.rhs[j] = make_double2(__dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, x.x)), sg.x),
+                           __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, x.y)), sg.y));
 }
 
 }  // namespace radmm_dev

@@ -72,13 +72,20 @@ template <typename T>
 struct DArr {
   T* p = nullptr;
   size_t n = 0;
+  bool own = true;  // false: a view of memory owned elsewhere (frame contexts share operators)
   DArr() = default;
   DArr(const DArr&) = delete;
   DArr& operator=(const DArr&) = delete;
-  DArr(DArr&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DArr(DArr&& o) noexcept : p(o.p), n(o.n), own(o.own) { o.p = nullptr; o.n = 0; o.own = true; }
   DArr& operator=(DArr&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; own = o.own; o.p = nullptr; o.n = 0; o.own = true; }
     return *this;
+  }
+  void view(T* ptr, size_t count) {
+    release();
+    p = ptr;
+    n = count;
+    own = false;
   }
   ~DArr() { release(); }
   // Device memory comes from the device's stream-ordered pool (see
@@ -86,12 +93,13 @@ struct DArr {
   // so the next context on this device allocates without driver calls.
   // Context streams are non-blocking, so frees wait for the device first.
   void release() {
-    if (p) {
+    if (p && own) {
       cudaDeviceSynchronize();
       cudaFreeAsync(p, 0);
     }
     p = nullptr;
     n = 0;
+    own = true;
   }
   void alloc(size_t count, bool zero = true) {
     release();
@@ -278,9 +286,20 @@ struct radmm_ctx {
   double prof_bytes[RADMM_PHASE_COUNT] = {};
   int64_t prof_launches[RADMM_PHASE_COUNT] = {};
   int64_t prof_calls[RADMM_PHASE_COUNT] = {};
+  // Multi-frame batches (BASELINE config 5): one child context per frame,
+  // sharing this context's operators (views) and stream.
+  std::vector<std::unique_ptr<radmm_ctx>> frames;
+  radmm_ctx* parent = nullptr;
+  bool own_stream = true;
+  // frame-batched contractions: job tables + split-K partials (parent only)
+  DArr<FrameBatchJob> fb_jobs;
+  DArr<FrameReduceJob> fb_red;
+  DArr<FrameRhsJob> fb_rhs;
+  DArr<double2> fb_part;
 
   ~radmm_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    frames.clear();  // children use this context's stream and operators
     if (ev_it0) cudaEventDestroy(ev_it0);
     if (ev_it1) cudaEventDestroy(ev_it1);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
@@ -290,7 +309,7 @@ struct radmm_ctx {
     if (fs_host) cudaFreeHost(fs_host);
     if (h_totals) cudaFreeHost(h_totals);
     if (h_flags) cudaFreeHost(h_flags);
-    if (stream) cudaStreamDestroy(stream);
+    if (stream && own_stream) cudaStreamDestroy(stream);
   }
 };
 
@@ -413,6 +432,11 @@ Sensor& sensor_at(radmm_ctx* c, int q) {
 
 void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   if (rows < 1) fail(RADMM_INVALID_ARGUMENT, "ForwardOperator: rows must be >= 1");
+  if (c->parent) fail(RADMM_INVALID_ARGUMENT, "frame contexts share their parent's operators");
+  if (!c->frames.empty()) {  // frame contexts view the old operators
+    CK(cudaStreamSynchronize(c->stream));
+    c->frames.clear();
+  }
   S.rows = rows;
   S.ld = round_up(rows, 64);
   if (S.A.n != (size_t)S.ld * c->N) S.A.alloc((size_t)S.ld * c->N, false);
@@ -638,7 +662,14 @@ void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
       LAUNCH(c, gemm_split_reduce, rg, 256, 0, pk, nsplit, c->split_ws.p, stride);
       continue;
     }
-    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 1)) {
+    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 2) == 2) {
+      CK(cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kGemmDmmaSmem));
+      dim3 grid((nn + kDmBN - 1) / kDmBN, (mm + kDmBM - 1) / kDmBM, (unsigned)nb);
+      LAUNCH(c, gemm_dmma_kernel<EPI>, grid, 256, kGemmDmmaSmem, pk);
+      continue;
+    }
+    if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 2)) {
       CK(cudaFuncSetAttribute(gemm_big_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)kGemmBigSmem));
       dim3 grid((nn + kBigBN - 1) / kBigBN, (mm + kBigBM - 1) / kBigBM, (unsigned)nb);
@@ -1034,6 +1065,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
   CK(cudaMemGetInfo(&free_b, &total_b));
   for (int q : fresh) {
     Sensor& S = c->sensors[q];
+    if (!S.G0.own) S.G0.release();  // never write through a view of another context's factor
     const size_t bytes = sizeof(double2) * (size_t)S.ldg * S.g_n;
     if (env_int("RADMM_FACTOR_CACHE", 1) == 0 || (S.G0.n < bytes / sizeof(double2) && free_b < bytes + (4ull << 30)))
       continue;
@@ -1576,7 +1608,56 @@ void build_contrib(radmm_ctx* c) {
     }
   }
   if (c->contrib.n != ptrs.size()) c->contrib.alloc(ptrs.size());
-  CK(cudaMemcpy(c->contrib.p, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(c->contrib.p, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice, c->stream));
+}
+
+// Record one round (admm.hpp:397-420): residuals, per-sensor active sizes
+// (after this round's screening), bytes_sent, active_fraction, stall flag.
+void record_round(radmm_ctx* c, int k, const FusionScalars& f, uint64_t notice, radmm_run_summary& sm,
+                  std::vector<int32_t>& sizes, std::vector<double>& meta_all,
+                  std::chrono::steady_clock::time_point t1) {
+  radmm_iteration_record rec{};
+  rec.iteration = k;
+  rec.pri_res = f.pri_res;
+  rec.dual_res = f.dual_res;
+  rec.eps_pri = f.eps_pri;
+  rec.eps_dual = f.eps_dual;
+  uint64_t bytes = notice;
+  bool stalled_any = false;
+  if (c->world <= 1) {
+    for (int q = 0; q < c->Q; ++q) {
+      sizes[q] = c->sensors[q].n_act;
+      stalled_any = stalled_any || c->sensors[q].stalled;
+    }
+  } else {
+    const int stride = 2 * c->q_max_local + 1;
+    meta_all.resize((size_t)stride * c->world);
+    CK(cudaMemcpy(meta_all.data(), c->size_recv.p, sizeof(double) * meta_all.size(), cudaMemcpyDeviceToHost));
+    bytes = 0;
+    for (int r = 0; r < c->world; ++r) {
+      const int begin = (int)((int64_t)r * c->Q_total / c->world);
+      const int end = (int)((int64_t)(r + 1) * c->Q_total / c->world);
+      for (int g = begin; g < end; ++g) {
+        sizes[g] = (int32_t)meta_all[(size_t)r * stride + 2 * (g - begin)];
+        stalled_any = stalled_any || meta_all[(size_t)r * stride + 2 * (g - begin) + 1] != 0.0;
+      }
+      bytes += (uint64_t)meta_all[(size_t)r * stride + 2 * c->q_max_local];
+    }
+  }
+  int max_active = 0;
+  for (int g = 0; g < c->Q_total; ++g) {
+    const size_t cb = contribution_size((size_t)sizes[g]);
+    bytes += cb;
+    max_active = std::max(max_active, sizes[g]);
+    sm.total_active_solves += (uint64_t)sizes[g];
+    c->active_log.push_back(sizes[g]);
+  }
+  rec.bytes_sent = bytes;
+  rec.active_fraction = (double)max_active / c->N;
+  rec.ms_elapsed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+  sm.total_bytes += bytes;
+  c->records.push_back(rec);
+  sm.screening_stalled = stalled_any ? 1 : 0;
 }
 
 void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o, radmm_run_summary* out) {
@@ -1616,20 +1697,30 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   if (o && o->observer) { hx.resize(2 * (size_t)c->N); hs.resize(2 * (size_t)c->N); hsig.resize(2 * (size_t)c->N); }
   bool staged_trigger = false;
   FusionScalars f{};
-  // step boundaries: ev_steps[k-1] is recorded when iteration k starts, so
-  // elapsed(ev_steps[k-1], ev_steps[k]) is the device-clock wall time of
-  // iteration k including the host round trip before iteration k+1.
-  while (c->ev_steps.size() < (size_t)h->max_iter + 1) {
+  // step boundaries: STEP(k-1) is recorded when iteration k starts, so
+  // elapsed(STEP(k-1), STEP(k)) is the device-clock wall time of iteration k
+  // including the host round trip before iteration k+1.  Both live in small
+  // rings (creating an event per possible iteration cost ~0.1 s per run);
+  // iteration k's time is read one iteration later, when both are complete.
+  constexpr int kEvRing = 4;
+  while (c->ev_steps.size() < (size_t)kEvRing) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     c->ev_steps.push_back(e);
   }
   c->iter_busy_ms.clear();
-  while (c->ev_ends.size() < (size_t)h->max_iter + 1) {
+  while (c->ev_ends.size() < (size_t)kEvRing) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
     c->ev_ends.push_back(e);
   }
+  auto STEP = [&](int i) { return c->ev_steps[i % kEvRing]; };
+  auto END = [&](int i) { return c->ev_ends[i % kEvRing]; };
+  auto step_time = [&](int it) {  // iteration it (>= 1): STEP(it-1) .. STEP(it), both complete
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, STEP(it - 1), STEP(it)));
+    c->iter_ms.push_back(ms);
+  };
   // Device-guarded speculation: while iteration k runs, iteration k+1 is
   // already enqueued; its kernels run only if fusion_k set go[(k+1)&1] (not
   // converged, and no screening staged).  Otherwise they exit at entry and
@@ -1648,7 +1739,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       exchange(c, (double)notice);
       run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, screen_next_possible());
     }
-    CK(cudaEventRecord(c->ev_ends[kk], c->stream));
+    CK(cudaEventRecord(END(kk), c->stream));
   };
   bool k_launched = false;   // iteration k already enqueued (speculatively)
   int64_t l_k = 0;           // launch counter when iteration k was enqueued
@@ -1656,7 +1747,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   for (int k = 1; k <= h->max_iter; ++k) {
     if (!k_launched) {
       l_k = c->launches;
-      CK(cudaEventRecord(c->ev_steps[k - 1], c->stream));
+      CK(cudaEventRecord(STEP(k - 1), c->stream));
       notice_k = 0;
       if (asadmm && !disable && staged_trigger) notice_k = screen_all(c, h, k);
       issue(k, nullptr, notice_k);
@@ -1668,10 +1759,11 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     int upd_before_next = c->upd;
     if (spec_next) {
       l_k = c->launches;
-      CK(cudaEventRecord(c->ev_steps[k], c->stream));
+      CK(cudaEventRecord(STEP(k), c->stream));
       issue(k + 1, c->go_flags.p + ((k + 1) & 1), 0);
     }
-    CK(cudaEventSynchronize(c->ev_ends[k]));
+    CK(cudaEventSynchronize(END(k)));
+    if (k >= 2) step_time(k - 1);  // STEP(k-1) precedes iteration k's kernels: complete
     c->iter_launches.push_back(l_end - l0);
     flush_marks(c);
     f = c->fs_host[k & 1];
@@ -1687,48 +1779,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
         notice_k = 0;
       }
     }
-    radmm_iteration_record rec{};
-    rec.iteration = k;
-    rec.pri_res = f.pri_res;
-    rec.dual_res = f.dual_res;
-    rec.eps_pri = f.eps_pri;
-    rec.eps_dual = f.eps_dual;
-    uint64_t bytes = notice;
-    bool stalled_any = false;
-    if (c->world <= 1) {
-      for (int q = 0; q < c->Q; ++q) {
-        sizes[q] = c->sensors[q].n_act;
-        stalled_any = stalled_any || c->sensors[q].stalled;
-      }
-    } else {
-      const int stride = 2 * c->q_max_local + 1;
-      meta_all.resize((size_t)stride * c->world);
-      CK(cudaMemcpy(meta_all.data(), c->size_recv.p, sizeof(double) * meta_all.size(), cudaMemcpyDeviceToHost));
-      bytes = 0;
-      for (int r = 0; r < c->world; ++r) {
-        const int begin = (int)((int64_t)r * c->Q_total / c->world);
-        const int end = (int)((int64_t)(r + 1) * c->Q_total / c->world);
-        for (int g = begin; g < end; ++g) {
-          sizes[g] = (int32_t)meta_all[(size_t)r * stride + 2 * (g - begin)];
-          stalled_any = stalled_any || meta_all[(size_t)r * stride + 2 * (g - begin) + 1] != 0.0;
-        }
-        bytes += (uint64_t)meta_all[(size_t)r * stride + 2 * c->q_max_local];
-      }
-    }
-    int max_active = 0;
-    for (int g = 0; g < c->Q_total; ++g) {
-      const size_t cb = contribution_size((size_t)sizes[g]);
-      bytes += cb;
-      max_active = std::max(max_active, sizes[g]);
-      sm.total_active_solves += (uint64_t)sizes[g];
-      c->active_log.push_back(sizes[g]);
-    }
-    rec.bytes_sent = bytes;
-    rec.active_fraction = (double)max_active / c->N;
-    rec.ms_elapsed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
-    sm.total_bytes += bytes;
-    c->records.push_back(rec);
-    sm.screening_stalled = stalled_any ? 1 : 0;
+    record_round(c, k, f, notice, sm, sizes, meta_all, t1);
     if (o && o->observer) {
       CK(cudaMemcpy(hx.data(), c->xg.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(hs.data(), c->s.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
@@ -1744,13 +1795,9 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     staged_trigger = f.trigger != 0;
   }
   if (fixed) sm.converged = f.converged;
-  CK(cudaEventRecord(c->ev_steps[sm.iterations], c->stream));
+  CK(cudaEventRecord(STEP(sm.iterations), c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (int k = 0; k < sm.iterations; ++k) {
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, c->ev_steps[k], c->ev_steps[k + 1]));
-    c->iter_ms.push_back(ms);
-  }
+  if (sm.iterations >= 1) step_time(sm.iterations);
   const auto t2 = std::chrono::steady_clock::now();
   sm.solve_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
   sm.kernel_launches = c->launches;
@@ -1759,6 +1806,302 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   c->summary = sm;
   c->have_result = true;
   if (out) *out = sm;
+}
+
+// ---- multi-frame batches (BASELINE config 5) ---------------------------------
+// Frame f of a context is a child context that views the parent's operators
+// (no copy) and uses the parent's stream; everything that depends on the
+// frame's measurements (y, active sets, factor, ADMM state, records) is its
+// own.  run_frames drives all frames in lockstep; each frame follows the
+// reference loop (admm.hpp:357-445) to its own stopping rule, exactly as a
+// run of that frame alone would.
+radmm_ctx* frame_ctx(radmm_ctx* p, int f) {
+  if (!p) fail(RADMM_INVALID_ARGUMENT, "null context");
+  if (p->parent) fail(RADMM_INVALID_ARGUMENT, "frame contexts cannot hold frames");
+  if (p->world > 1) fail(RADMM_INVALID_ARGUMENT, "multi-frame batches need an unsharded context");
+  if (f < 0 || f >= 4096) fail(RADMM_INVALID_ARGUMENT, "frame index out of range");
+  while ((int)p->frames.size() <= f) {
+    for (int q = 0; q < p->Q; ++q)
+      if (!p->sensors[q].has_op)
+        fail(RADMM_INVALID_ARGUMENT, "Problem: sensor " + std::to_string(q) + " has no operator");
+    auto ch = std::make_unique<radmm_ctx>();
+    init_ctx(ch.get(), p->device, p->N, p->Q);
+    CK(cudaStreamDestroy(ch->stream));
+    ch->stream = p->stream;
+    ch->own_stream = false;
+    ch->parent = p;
+    ch->Q_total = p->Q_total;
+    ch->q_begin = 0;
+    ch->q_max_local = p->Q;
+    for (int q = 0; q < p->Q; ++q) {
+      Sensor& S = ch->sensors[q];
+      Sensor& P = p->sensors[q];
+      S.rows = P.rows;
+      S.ld = P.ld;
+      S.A.view(P.A.p, P.A.n);
+      S.y_eff.alloc(S.ld);
+      S.y_eff_s.alloc(S.ld);
+      S.bz.alloc(S.ld);
+      S.v.alloc(S.ld);
+      S.w.alloc(S.ld);
+      S.part_chunks = P.part_chunks;
+      S.part.alloc((size_t)S.part_chunks * S.ld, false);
+      S.has_op = true;
+    }
+    p->frames.push_back(std::move(ch));
+  }
+  return p->frames[f].get();
+}
+
+// Point frame f's factor cache at a full-set factor computed elsewhere (the
+// parent's, or frame 0's): the frame's begin_run then copies it instead of
+// refactorising (the factor depends on A, mu, beta only).
+void share_factor(radmm_ctx* dst, const radmm_ctx* src, double mu, double beta) {
+  for (int q = 0; q < dst->Q; ++q) {
+    Sensor& D = dst->sensors[q];
+    const Sensor& S = src->sensors[q];
+    if (!S.g0_valid || S.g0_mu != mu || S.g0_beta != beta) continue;
+    if (D.g0_valid && D.g0_mu == mu && D.g0_beta == beta) continue;
+    D.G0.view(S.G0.p, S.G0.n);
+    D.g0_valid = true;
+    D.g0_primal = S.g0_primal;
+    D.g0_mu = mu;
+    D.g0_beta = beta;
+    D.g0_ld = S.g0_ld;
+    D.g0_n = S.g0_n;
+  }
+}
+
+// A frame rides the batched contractions while it has never eliminated a
+// pixel in this run: full active set (J = identity), dual form, and the
+// factor still the shared full-set one (no downdate or rebuild can have
+// happened without an elimination).
+bool frame_attached(const radmm_ctx* c) {
+  for (const Sensor& S : c->sensors)
+    if (S.n_act != c->N || S.primal || S.data_lag) return false;
+  return true;
+}
+
+int split_for(const radmm_ctx* p, int tiles) {
+  const int want = (3 * p->sm_count + tiles - 1) / std::max(1, tiles);
+  return std::max(1, std::min(16, want));
+}
+
+// One synchronous Jacobi sweep (admm.hpp:389-390) for up to kFB attached
+// frames: rhs, V = A RHS, W = G V, X = (RHS - mu A^H W)/beta with the
+// history / scatter epilogue -- every operator column read once for all
+// frames.  fs: frame contexts (same mu, beta; identical factors).
+void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double mu, double beta) {
+  const int Q = p->Q, nf = (int)fs.size();
+  const int N = p->N;
+  if (nf < 1 || nf > kFB) fail(RADMM_INVALID_ARGUMENT, "frame batch size");
+  int64_t ld_max = 0;
+  int rows_max = 0;
+  for (const Sensor& S : p->sensors) {
+    ld_max = std::max(ld_max, S.ld);
+    rows_max = std::max(rows_max, S.rows);
+  }
+  const int mt_rows = (rows_max + kFbBM - 1) / kFbBM;
+  const int sp_fwd = split_for(p, mt_rows * Q);
+  const int sp_gap = split_for(p, mt_rows * Q);
+  const int sp_max = std::max(sp_fwd, sp_gap);
+  const size_t part_per = (size_t)sp_max * kFB * ld_max;
+  if (p->fb_part.n < part_per * Q) p->fb_part.alloc(part_per * Q, false);
+  if (p->fb_jobs.n < (size_t)Q) p->fb_jobs.alloc(Q, false);
+  if (p->fb_red.n < (size_t)Q) p->fb_red.alloc(Q, false);
+  if (p->fb_rhs.n < (size_t)Q * kFB) p->fb_rhs.alloc((size_t)Q * kFB, false);
+  // rhs for every (sensor, frame)
+  std::vector<FrameRhsJob> rj((size_t)Q * nf);
+  for (int q = 0; q < Q; ++q)
+    for (int f = 0; f < nf; ++f) {
+      Sensor& S = fs[f]->sensors[q];
+      rj[(size_t)q * nf + f] = FrameRhsJob{N, S.data.p, S.x_hat.p, fs[f]->gap.p, fs[f]->sigma.p, S.rhs.p};
+    }
+  CK(cudaMemcpyAsync(p->fb_rhs.p, rj.data(), sizeof(FrameRhsJob) * rj.size(), cudaMemcpyHostToDevice, p->stream));
+  LAUNCH(p, frame_rhs_kernel, dim3((unsigned)((N + 255) / 256), (unsigned)(Q * nf)), 256, 0, p->fb_rhs.p, beta);
+  std::vector<FrameBatchJob> jobs(Q);
+  std::vector<FrameReduceJob> red(Q);
+  auto run_pass = [&](int mode, int nsplit) {
+    CK(cudaMemcpyAsync(p->fb_jobs.p, jobs.data(), sizeof(FrameBatchJob) * Q, cudaMemcpyHostToDevice, p->stream));
+    int mmax = 0;
+    for (const auto& j : jobs) mmax = std::max(mmax, j.m);
+    const dim3 grid((unsigned)((mmax + kFbBM - 1) / kFbBM), (unsigned)nsplit, (unsigned)Q);
+    if (mode == FB_FWD) LAUNCH(p, frame_batch_kernel<FB_FWD>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
+    else if (mode == FB_GAP) LAUNCH(p, frame_batch_kernel<FB_GAP>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
+    else LAUNCH(p, frame_batch_kernel<FB_ADJ>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
+    if (mode == FB_ADJ) return;
+    CK(cudaMemcpyAsync(p->fb_red.p, red.data(), sizeof(FrameReduceJob) * Q, cudaMemcpyHostToDevice, p->stream));
+    LAUNCH(p, frame_reduce_kernel, dim3((unsigned)((mmax + 255) / 256), (unsigned)nf, (unsigned)Q), 256, 0,
+           p->fb_red.p);
+  };
+  // V = A RHS
+  for (int q = 0; q < Q; ++q) {
+    const Sensor& P = p->sensors[q];
+    FrameBatchJob j{};
+    j.A = P.A.p; j.lda = P.ld; j.m = P.rows; j.k = N; j.nf = nf;
+    j.part = p->fb_part.p + (size_t)q * part_per; j.ldp = ld_max;
+    FrameReduceJob r{};
+    r.part = j.part; r.ldp = ld_max; r.m = P.rows; r.nf = nf; r.nsplit = sp_fwd;
+    for (int f = 0; f < nf; ++f) {
+      j.B[f] = fs[f]->sensors[q].rhs.p;
+      r.out[f] = fs[f]->sensors[q].v.p;
+    }
+    jobs[q] = j;
+    red[q] = r;
+  }
+  {
+    PhaseScope ps(p, RADMM_PHASE_FORWARD, 8.0 * ld_max * N * Q);
+    run_pass(FB_FWD, sp_fwd);
+  }
+  // W = G V on the shared factor
+  for (int q = 0; q < Q; ++q) {
+    const Sensor& H = fs[0]->sensors[q];
+    FrameBatchJob& j = jobs[q];
+    j.A = H.G.p; j.lda = H.ldg; j.m = H.rows; j.k = H.rows;
+    FrameReduceJob& r = red[q];
+    r.nsplit = sp_gap;
+    for (int f = 0; f < nf; ++f) {
+      j.B[f] = fs[f]->sensors[q].v.p;
+      r.out[f] = fs[f]->sensors[q].w.p;
+    }
+  }
+  {
+    PhaseScope ps(p, RADMM_PHASE_GAPPLY, 16.0 * ld_max * ld_max * Q);
+    run_pass(FB_GAP, sp_gap);
+  }
+  // X = (RHS - mu A^H W) / beta + epilogue
+  for (int q = 0; q < Q; ++q) {
+    const Sensor& P = p->sensors[q];
+    FrameBatchJob& j = jobs[q];
+    j.A = P.A.p; j.lda = P.ld; j.m = N; j.k = P.rows;
+    for (int f = 0; f < nf; ++f) {
+      Sensor& S = fs[f]->sensors[q];
+      j.B[f] = S.w.p;
+      j.rhs[f] = S.rhs.p;
+      j.x_hat[f] = S.x_hat.p;
+      j.x_full[f] = S.x_full.p;
+      j.ring[f] = S.ring.p + (size_t)(fs[f]->upd % fs[f]->W) * N;
+    }
+  }
+  {
+    PhaseScope ps(p, RADMM_PHASE_ADJOINT, 8.0 * ld_max * N * Q);
+    run_pass(FB_ADJ, 1);
+  }
+  for (radmm_ctx* c : fs) {
+    ++c->upd;
+    for (Sensor& S : c->sensors) S.v_ready = false;
+  }
+}
+
+void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_run_options* o,
+                radmm_run_summary* outs) {
+  if (F < 1 || !hs) fail(RADMM_INVALID_ARGUMENT, "run_frames: need at least one frame");
+  if (o && o->observer) fail(RADMM_INVALID_ARGUMENT, "run_frames: observers are not supported");
+  for (int f = 0; f < F; ++f) validate_hyper(&hs[f]);
+  set_device(p);
+  const bool asadmm = o && o->mode == RADMM_MODE_ASADMM;
+  const bool disable = o && o->disable_screening;
+  const bool fixed = o && o->fixed_iterations;
+  // frame-batched contractions (RADMM_FRAME_BATCH=0: per-frame kernels only)
+  const bool batched = env_int("RADMM_FRAME_BATCH", 1) != 0;
+  std::vector<radmm_ctx*> ch(F);
+  for (int f = 0; f < F; ++f) {
+    ch[f] = frame_ctx(p, f);
+    for (int q = 0; q < p->Q; ++q)
+      if (!ch[f]->sensors[q].has_y)
+        fail(RADMM_INVALID_ARGUMENT, "run_frames: frame " + std::to_string(f) + " sensor " + std::to_string(q) +
+                                         " has no measurement");
+  }
+  std::vector<radmm_run_summary> sm(F);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int f = 0; f < F; ++f) {
+    radmm_ctx* c = ch[f];
+    c->records.clear();
+    c->active_log.clear();
+    c->removal_log.clear();
+    c->have_result = false;
+    c->launches = 0;
+    c->rebuilds = c->downdates = 0;
+    c->iter_ms.clear();
+    c->iter_launches.clear();
+    c->marks.clear();
+    c->ev_used = 0;
+    share_factor(c, p, hs[f].mu, hs[f].beta);
+    if (f > 0) share_factor(c, ch[0], hs[f].mu, hs[f].beta);
+    build_contrib(c);
+    begin_run(c, &hs[f]);
+  }
+  CK(cudaStreamSynchronize(p->stream));
+  const auto t1 = std::chrono::steady_clock::now();
+  const double setup_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  int max_iter = 0;
+  for (int f = 0; f < F; ++f) max_iter = std::max(max_iter, hs[f].max_iter);
+  std::vector<char> done(F, 0), staged(F, 0);
+  std::vector<uint64_t> notice(F, 0);
+  std::vector<FusionScalars> last(F);
+  std::vector<int32_t> sizes(p->Q_total);
+  std::vector<double> meta_all;
+  std::vector<int> live;
+  for (int k = 1; k <= max_iter; ++k) {
+    live.clear();
+    for (int f = 0; f < F; ++f)
+      if (!done[f] && k <= hs[f].max_iter) live.push_back(f);
+    if (live.empty()) break;
+    for (int f : live) notice[f] = (asadmm && !disable && staged[f]) ? screen_all(ch[f], &hs[f], k) : 0;
+    // attached frames with equal (mu, beta) share the batched contractions
+    std::vector<int> single;
+    std::vector<std::vector<int>> groups;
+    for (int f : live) {
+      if (!batched || !frame_attached(ch[f])) {
+        single.push_back(f);
+        continue;
+      }
+      bool placed = false;
+      for (auto& g : groups)
+        if ((int)g.size() < kFB && hs[g[0]].mu == hs[f].mu && hs[g[0]].beta == hs[f].beta) {
+          g.push_back(f);
+          placed = true;
+          break;
+        }
+      if (!placed) groups.push_back({f});
+    }
+    for (auto& g : groups) {
+      if (g.size() == 1) {
+        single.push_back(g[0]);
+        continue;
+      }
+      std::vector<radmm_ctx*> fc;
+      for (int f : g) fc.push_back(ch[f]);
+      frame_batch_updates(p, fc, hs[g[0]].mu, hs[g[0]].beta);
+    }
+    for (int f : single) local_updates(ch[f], &hs[f]);
+    for (int f : live) run_fusion(ch[f], &hs[f], k, nullptr, nullptr, fixed ? 0 : 1, 0);
+    CK(cudaStreamSynchronize(p->stream));
+    const auto now = std::chrono::steady_clock::now();
+    for (int f : live) {
+      const FusionScalars fs = ch[f]->fs_host[k & 1];
+      record_round(ch[f], k, fs, notice[f], sm[f], sizes, meta_all, t1);
+      sm[f].iterations = k;
+      last[f] = fs;
+      staged[f] = fs.trigger != 0;
+      if ((fs.converged && !fixed) || k == hs[f].max_iter) {
+        if (fs.converged && !fixed) sm[f].converged = 1;
+        done[f] = 1;
+        sm[f].solve_ms = std::chrono::duration<double, std::milli>(now - t1).count();
+      }
+    }
+  }
+  for (int f = 0; f < F; ++f) {
+    radmm_ctx* c = ch[f];
+    if (fixed) sm[f].converged = last[f].converged;
+    sm[f].setup_ms = setup_ms;
+    sm[f].kernel_launches = c->launches;
+    sm[f].rebuilds = c->rebuilds;
+    sm[f].downdates = c->downdates;
+    c->summary = sm[f];
+    c->have_result = true;
+    if (outs) outs[f] = sm[f];
+  }
 }
 
 void copy_out(radmm_ctx* c, const void* dev, void* host, size_t bytes) {
@@ -1817,7 +2160,10 @@ int radmm_ctx_create(int device, int n_pixels, int n_sensors, radmm_ctx** out) {
 }
 
 int radmm_ctx_destroy(radmm_ctx* ctx) {
-  return guarded([&] { delete ctx; });
+  return guarded([&] {
+    if (ctx && ctx->parent) fail(RADMM_INVALID_ARGUMENT, "frame contexts are owned by their parent context");
+    delete ctx;
+  });
 }
 
 int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int64_t lda, int ptr_kind) {
@@ -1861,6 +2207,30 @@ int radmm_set_operator_c128(radmm_ctx* ctx, int q, int rows, const double* a, in
   });
 }
 
+int radmm_set_frame_measurement(radmm_ctx* ctx, int frame, int q, const double* y, int ptr_kind) {
+  return guarded([&] {
+    radmm_ctx* fc = frame_ctx(ctx, frame);
+    const int st = radmm_set_measurement(fc, q, y, ptr_kind);
+    if (st != RADMM_OK) fail(st, g_last_error);
+  });
+}
+
+int radmm_run_frames(radmm_ctx* ctx, int frames, const radmm_hyperparams* hypers, const radmm_run_options* opts,
+                     radmm_run_summary* summaries) {
+  return guarded([&] {
+    if (!ctx) fail(RADMM_INVALID_ARGUMENT, "null context");
+    run_frames(ctx, frames, hypers, opts, summaries);
+  });
+}
+
+int radmm_frame(radmm_ctx* ctx, int frame, radmm_ctx** out) {
+  return guarded([&] {
+    if (!ctx || !out) fail(RADMM_INVALID_ARGUMENT, "null argument");
+    if (frame < 0 || frame >= (int)ctx->frames.size()) fail(RADMM_INVALID_ARGUMENT, "frame index out of range");
+    *out = ctx->frames[frame].get();
+  });
+}
+
 int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind) {
   return guarded([&] {
     Sensor& S = sensor_at(ctx, q);
@@ -1868,8 +2238,10 @@ int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind) 
     if (!y) fail(RADMM_INVALID_ARGUMENT, "null measurement");
     set_device(ctx);
     S.y.alloc(S.ld);
-    CK(cudaMemcpy(S.y.p, y, sizeof(double2) * S.rows,
-                  ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(S.y.p, y, sizeof(double2) * S.rows,
+                       ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // the caller may reuse y on return
     S.has_y = true;
   });
 }
@@ -1884,10 +2256,10 @@ int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const d
     const int N = ctx->N;
     DArr<double> dpix, dtx, drx, dphi;
     dpix.alloc(3 * (size_t)N, false); dtx.alloc(3, false); drx.alloc(3 * (size_t)M, false); dphi.alloc(N, false);
-    CK(cudaMemcpy(dpix.p, pix, sizeof(double) * 3 * N, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dtx.p, tx, sizeof(double) * 3, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(drx.p, rx, sizeof(double) * 3 * M, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dphi.p, phi, sizeof(double) * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dpix.p, pix, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(dtx.p, tx, sizeof(double) * 3, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(drx.p, rx, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(dphi.p, phi, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
     const int64_t total = (int64_t)M * K * N;
     const double pi = 3.141592653589793238462643383279502884;
     LAUNCH(ctx, dechirp_kernel, dim3((unsigned)((total + 255) / 256)), 256, 0, S.A.p, S.ld, M, K, N, dpix.p, dtx.p,
@@ -2032,7 +2404,7 @@ int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
     radmm_ctx* c = sc->ctx;
     set_device(c);
     Sensor& S = c->sensors[0];
-    CK(cudaMemcpy(S.rhs.p, rhs, sizeof(double2) * sc->cols, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(S.rhs.p, rhs, sizeof(double2) * sc->cols, cudaMemcpyHostToDevice, c->stream));
     if (S.primal) {
       ColDotJob j{};
       j.M = S.G.p; j.ld = S.ldg; j.len = sc->cols; j.n_out = sc->cols; j.vec = S.rhs.p; j.out = sc->x.p; j.scale = 1.0;
@@ -2083,7 +2455,7 @@ int radmm_apply_operator(radmm_ctx* ctx, int q, const double* x, double* y) {
     DArr<int> idx;
     dx.alloc(N, false);
     idx.alloc(N, false);
-    CK(cudaMemcpy(dx.p, x, sizeof(double2) * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dx.p, x, sizeof(double2) * N, cudaMemcpyHostToDevice, ctx->stream));
     LAUNCH(ctx, iota_kernel, dim3((N + 255) / 256), 256, 0, idx.p, N);
     FwdJob f{};
     f.A = S.A.p; f.ld = S.ld; f.n = N; f.J = idx.p; f.src = dx.p; f.part = S.part.p;
@@ -2105,13 +2477,66 @@ int radmm_apply_adjoint(radmm_ctx* ctx, int q, const double* y, double* x) {
     dy.alloc(S.ld);
     dx.alloc(N, false);
     idx.alloc(N, false);
-    CK(cudaMemcpy(dy.p, y, sizeof(double2) * S.rows, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dy.p, y, sizeof(double2) * S.rows, cudaMemcpyHostToDevice, ctx->stream));
     LAUNCH(ctx, iota_kernel, dim3((N + 255) / 256), 256, 0, idx.p, N);
     ColDotJob j{};
     j.M = S.A.p; j.ld = S.ld; j.len = S.rows; j.n_out = N; j.cols = idx.p; j.vec = dy.p; j.out = dx.p; j.scale = 1.0;
     coldot<float2, EPI_STORE>(ctx, {j}, 1.0, 1.0);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(x, dx.p, sizeof(double2) * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+int radmm_back_projection(radmm_ctx* ctx, double* image) {
+  return guarded([&] {
+    if (!ctx || !image) fail(RADMM_INVALID_ARGUMENT, "back_projection: null argument");
+    for (const Sensor& S : ctx->sensors)
+      if (!S.has_op || !S.has_y) fail(RADMM_INVALID_ARGUMENT, "back_projection: need one measurement per operator");
+    set_device(ctx);
+    radmm_ctx* c = ctx;
+    const size_t N = c->N;
+    // per-sensor adjoint images A_q^H y_q: into the exchange send buffer when
+    // sharded (then all-gathered), else into a local Q x N buffer
+    DArr<double2> local;
+    double2* dst = c->world > 1 ? c->send_buf.p : nullptr;
+    if (!dst) {
+      local.alloc((size_t)c->Q * N, false);
+      dst = local.p;
+    }
+    std::vector<ColDotJob> jobs;
+    for (int q = 0; q < c->Q; ++q) {
+      Sensor& S = c->sensors[q];
+      ColDotJob j{};
+      j.M = S.A.p; j.ld = S.ld; j.len = S.rows; j.n_out = (int)N; j.vec = S.y.p; j.out = dst + (size_t)q * N;
+      j.scale = 1.0;
+      jobs.push_back(j);
+    }
+    coldot<float2, EPI_STORE>(c, jobs, 1.0, 1.0);
+    std::vector<const double2*> ptrs(c->Q_total);
+    if (c->world > 1) {
+      g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble,
+                                    c->comm, c->stream), "ncclAllGather(back_projection)");
+      for (int g = 0; g < c->Q_total; ++g) {
+        int r = 0;
+        while (r + 1 < c->world && (int64_t)(r + 1) * c->Q_total / c->world <= g) ++r;
+        const int begin = (int)((int64_t)r * c->Q_total / c->world);
+        ptrs[g] = c->gathered.p + ((size_t)r * c->q_max_local + (g - begin)) * N;
+      }
+    } else {
+      for (int q = 0; q < c->Q; ++q) ptrs[q] = dst + (size_t)q * N;
+    }
+    DArr<const double2*> dptrs;
+    dptrs.alloc(ptrs.size(), false);
+    CK(cudaMemcpyAsync(dptrs.p, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice, c->stream));
+    DArr<double> mag;
+    mag.alloc(N, false);
+    LAUNCH(c, bp_sum_kernel, dim3((unsigned)((N + 255) / 256)), 256, 0, dptrs.p, c->Q_total, (int)N, mag.p);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(image, mag.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    double peak = 0.0;
+    for (size_t j = 0; j < N; ++j) peak = std::max(peak, image[j]);
+    if (peak > 0.0)
+      for (size_t j = 0; j < N; ++j) image[j] /= peak;  // an all-zero result stays all-zero
   });
 }
 

@@ -19,7 +19,7 @@ import pytest
 from oracle import admm_ref
 from paper_2307_08606_b200 import api, scenario
 
-from ._parity import compare_masks, gpu_run, oracle_run, quantize, rel, state_errors
+from ._parity import compare_masks, gpu_masks, gpu_run, oracle_run, quantize, rel, state_errors
 
 pytestmark = pytest.mark.gpu
 
@@ -275,6 +275,22 @@ def test_desk_parity(desk):
     assert abs(api.nmse_db(g.image, truth) - (-13.70)) < 0.01
 
 
+def test_back_projection_desk(desk):
+    """back_projection on the GPU (forward_model.hpp:201-220) against the host
+    restatement on the same complex64 operators: the desk's published BP NMSE
+    is -5.92 dB (proj/test_output.txt:21)."""
+    ops, ys, truth = desk
+    img = api.back_projection(ops, ys)
+    ref = scenario.back_projection([a.astype(np.complex128) for a in ops], ys)
+    assert rel(img, ref) < 1e-12
+    assert img.max() == 1.0
+    assert abs(api.nmse_db(img, truth) - (-5.92)) < 0.01
+    zero = api.back_projection(ops, [np.zeros_like(y) for y in ys])
+    assert not zero.any()  # an all-zero result stays all-zero
+    with pytest.raises(api.InvalidArgument):
+        api.back_projection(ops, ys[:-1])
+
+
 def test_clean_desk_screening_parity():
     sc = scenario.desk_scenario()
     sc.snr_db = math.inf
@@ -437,4 +453,110 @@ def test_multi_frame_shared_operator_matches_oracle():
         o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
         errs = state_errors(g, o)
         assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-8, (frame, errs)
+    s.close()
+
+
+def test_mask_replay_event_paths():
+    """Mask replay: the GPU runs free; the oracle adopts the GPU's
+    active set at every screening step (oracle/admm_ref.py forced_masks) and
+    the iterates are compared at EVERY iteration -- sigma and the residual
+    records -- so a divergence is localised to the step it appears.  The
+    oracle's own decisions are reported: wherever they differ from the
+    replayed ones, the pixel's zeta must sit within round-off of tol."""
+    tol = 1e-3
+    ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=120)
+    hyper = dict(hyper, screening_tol=tol)
+    g_sig = []
+    g = gpu_run(ops, ys, hyper, True, fixed_iterations=True,
+                observer=lambda v: g_sig.append(v.sigma.copy()))
+    gm = gpu_masks(g, len(ops))
+    active = [np.arange(ops[0].shape[1]) for _ in ops]
+
+    def forced(k, q):
+        rem = gm.get((k, q))
+        if rem is not None and rem.size:
+            active[q] = np.setdiff1d(active[q], rem)
+        return active[q]
+
+    o_sig = []
+    o = oracle_run(ops, ys, hyper, True, fixed_iterations=True, forced_masks=forced,
+                   observer=lambda k, f, s: o_sig.append(f.sigma.copy()))
+    assert g.downdates + g.rebuilds > len(ops)
+    assert len(g_sig) == len(o_sig) == g.iterations
+    worst = max(rel(a, b) for a, b in zip(g_sig, o_sig))
+    for rg, ro in zip(g.report.iterations, o.records):
+        assert rg.active_sizes == ro.active_sizes
+        assert abs(rg.pri_res - ro.pri_res) <= 1e-6 * max(ro.pri_res, 1e-300)
+    own_diff = sum(len(set(e.own_removed.tolist()) ^ set(e.removed.tolist())) for e in o.events)
+    print(f"mask replay: worst per-iteration sigma rel {worst:.2e}; own-decision differences {own_diff}")
+    assert worst < 1e-6
+    bad, _ = compare_masks(g, o, tol, 5)  # replayed decisions == oracle's own, up to round-off
+    assert bad == 0
+
+
+# ---- multi-frame batches (BASELINE config 5) ---------------------------------------
+def _frames_problem(n_frames, **kw):
+    cfg = scenario.baseline_config("c1", **kw)
+    ops = [scenario.baseline_operator(cfg, q) for q in range(cfg.Q)]
+    frames = []
+    for f in range(n_frames):
+        cfg.frame = f
+        per = scenario.baseline_scene(cfg)
+        ys = scenario.baseline_measurements(cfg, ops, per)
+        frames.append((ys, scenario.baseline_hyper(cfg, scenario.baseline_lambda(cfg, ops, ys))))
+    return cfg, ops, frames
+
+
+@pytest.mark.parametrize("batched", [False, True])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_frames_match_separate_runs(fixed, batched, monkeypatch):
+    """run_frames (frames in lockstep on shared operators) against a separate
+    run per frame.  Per-frame kernels (RADMM_FRAME_BATCH=0): every state
+    vector, record and removal log bitwise equal, including frames that stop
+    at different iterations.  Batched contractions (frames that still share
+    the full active set go through one DMMA GEMM per operator): same
+    iterations and masks, states within 1e-9 (fp64 accumulation order)."""
+    monkeypatch.setenv("RADMM_FRAME_BATCH", "1" if batched else "0")
+    cfg, ops, frames = _frames_problem(3, max_iter=150 if fixed else 400)
+    s = api.Solver(cfg.N, cfg.Q)
+    for q in range(cfg.Q):
+        s.set_operator(q, ops[q])
+    for f, (ys, _) in enumerate(frames):
+        for q in range(cfg.Q):
+            s.set_frame_measurement(f, q, ys[q])
+    hypers = [api.Hyperparams(**h) for _, h in frames]
+    batch = s.run_frames(hypers, api.Mode.ASADMM, fixed_iterations=fixed)
+    iters = set()
+    for f, (ys, h) in enumerate(frames):
+        one = gpu_run(ops, ys, h, True, fixed_iterations=fixed)
+        b = batch[f]
+        iters.add(b.iterations)
+        assert b.iterations == one.iterations and b.converged == one.converged
+        if batched:
+            errs = state_errors(b, one)
+            assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-9, errs
+            assert [r.active_sizes for r in b.report.iterations] == [r.active_sizes for r in one.report.iterations]
+            continue
+        for k in ("x_global", "s", "sigma", "image"):
+            assert np.array_equal(getattr(b, k), getattr(one, k)), (f, k)
+        for xa, xb in zip(b.sensor_images, one.sensor_images):
+            assert np.array_equal(xa, xb)
+        assert [r.pri_res for r in b.report.iterations] == [r.pri_res for r in one.report.iterations]
+        assert [r.active_sizes for r in b.report.iterations] == [r.active_sizes for r in one.report.iterations]
+        assert np.array_equal(np.asarray(b.removal_log), np.asarray(one.removal_log))
+    if fixed:
+        assert sum(len(x.removal_log) for x in batch) > 0  # elimination happened
+    s.close()
+
+
+def test_frames_reject_bad_use():
+    cfg, ops, frames = _frames_problem(1)
+    s = api.Solver(cfg.N, cfg.Q)
+    with pytest.raises(api.InvalidArgument):  # operators first
+        s.set_frame_measurement(0, 0, frames[0][0][0])
+    for q in range(cfg.Q):
+        s.set_operator(q, ops[q])
+    s.set_frame_measurement(0, 0, frames[0][0][0])
+    with pytest.raises(api.InvalidArgument):  # sensor 1 of frame 0 has no measurement
+        s.run_frames([api.Hyperparams(**frames[0][1])])
     s.close()
