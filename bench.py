@@ -467,9 +467,16 @@ def stress(args):
 
 def frames(args):
     """BASELINE config 5 (multi-frame): the config-2 operators shared by F
-    seeded scenes (fresh targets + noise per frame), solved one after another
-    on one resident problem, each to the time-to-tolerance rule.  The operator
-    stays in HBM and the full-set factor is computed once (frame 0) and reused.
+    seeded scenes (fresh targets + noise per frame), each solved to the
+    time-to-tolerance rule.  Two ways on one resident problem:
+      sequential -- one run per frame (the reference's way); the full-set
+                    factor is computed once (frame 0) and reused;
+      batched    -- run_frames: all frames in lockstep; frames that still
+                    share the full active set go through frame-batched DMMA
+                    contractions (each operator column read once per
+                    iteration for all frames).
+    Reports frames/s of both (host wall clock around the solve calls,
+    operators already resident) and the per-frame agreement between them.
     One auxiliary JSON line."""
     import __graft_entry__
     from paper_2307_08606_b200 import api, scenario
@@ -481,32 +488,81 @@ def frames(args):
     for q in range(cfg.Q):
         s.generate_dechirp_operator(q, cfg.M, cfg.K, pix, tx[q], rx[q], scenario.baseline_phases(cfg, q),
                                     cfg.fc, cfg.bw, cfg.pulse)
-    per_frame = []
-    for f in range(args.frames):
+    F = args.frames
+    ys_all, hypers = [], []
+    for f in range(F):
         cfg.frame = f
         xs = scenario.baseline_scene(cfg)
         seed = cfg.seed if f == 0 else mix_seed(cfg.seed, 10000 + f)
         lam = 0.0
+        ys = []
         for q in range(cfg.Q):
             y = s.apply(q, xs[q].astype(np.complex128))
             sig = math.sqrt(float(np.vdot(y, y).real) / (cfg.KM * 10.0 ** (cfg.snr_db / 10.0)))
             y = y + sig * ComplexGaussian(mix_seed(seed, q + 1)).draw(cfg.KM)
-            s.set_measurement(q, y)
+            ys.append(y)
             lam = max(lam, float(np.abs(s.apply_adjoint(q, y)).max()))
-        h = api.Hyperparams(mu=cfg.mu, lambda_=cfg.lambda_frac * lam, beta=cfg.beta, eps_abs=cfg.eps_abs,
-                            eps_rel=cfg.eps_rel, max_iter=args.ttt_max_iter)
-        t, _ = time_to_tolerance(s, h, args.ttt_max_iter)
-        per_frame.append(t)
+        ys_all.append(ys)
+        hypers.append(api.Hyperparams(mu=cfg.mu, lambda_=cfg.lambda_frac * lam, beta=cfg.beta,
+                                      eps_abs=cfg.eps_abs, eps_rel=cfg.eps_rel, max_iter=args.ttt_max_iter))
+    # the time-to-tolerance rule per frame: eps_abs from that frame's pri_res(1)
+    for f in range(F):
+        for q in range(cfg.Q):
+            s.set_frame_measurement(f, q, ys_all[f][q])
+    first = s.run_frames([api.Hyperparams(**{**h.__dict__, "max_iter": 1}) for h in hypers], fetch=True)
+    hyp = [api.Hyperparams(**{**h.__dict__, "eps_abs": 1e-5 * r.report.iterations[0].pri_res / math.sqrt(cfg.N)})
+           for h, r in zip(hypers, first)]
+    # both timed paths start from a cached full-set factor (an untimed
+    # 1-iteration run caches the parent's; the frames already hold theirs)
+    for q in range(cfg.Q):
+        s.set_measurement(q, ys_all[0][q])
+    s.run(api.Hyperparams(**{**hyp[0].__dict__, "max_iter": 1}), api.Mode.ASADMM, fetch=False)
+    # sequential: one run per frame on the resident problem
+    seq = []
+    t0 = time.perf_counter()
+    for f in range(F):
+        for q in range(cfg.Q):
+            s.set_measurement(q, ys_all[f][q])
+        seq.append(s.run(hyp[f], api.Mode.ASADMM, fetch=False))
+    t_seq = time.perf_counter() - t0
+    # batched
+    t0 = time.perf_counter()
+    bat = s.run_frames(hyp, api.Mode.ASADMM, fetch=False)
+    t_bat = time.perf_counter() - t0
+    # agreement at a FIXED iteration count (to-tolerance runs stop at
+    # slightly different iterations, which dominates any end-state diff):
+    # batched vs sequential, next to two sequential paths that differ only in
+    # fp64 summation order (full vs lower-triangle G-apply) -- the spread the
+    # degenerate objective gives any change of rounding.
+    kfix = 200
+    hfix = [api.Hyperparams(**{**h.__dict__, "max_iter": kfix}) for h in hyp[:2]]
+    bfix = s.run_frames(hfix, api.Mode.ASADMM, fixed_iterations=True, fetch=True)
+    sfix, sfix0 = [], []
+    for f in range(2):
+        for q in range(cfg.Q):
+            s.set_measurement(q, ys_all[f][q])
+        sfix.append(s.run(hfix[f], api.Mode.ASADMM, fixed_iterations=True, fetch=True))
+        os.environ["RADMM_HERM"] = "0"
+        sfix0.append(s.run(hfix[f], api.Mode.ASADMM, fixed_iterations=True, fetch=True))
+        os.environ.pop("RADMM_HERM")
     s.close()
-    tot_s = sum(t["time_to_tolerance_s"] for t in per_frame)
-    iters = sum(t["iterations"] for t in per_frame)
-    print(json.dumps({"config": "c5", "frames": args.frames, "frames_per_s": args.frames / tot_s,
-                      "total_s_device": tot_s, "iterations_total": iters, "iterations_per_s": iters / tot_s,
-                      "setup_s_per_frame": [round(t["setup_s"], 4) for t in per_frame],
-                      "iterations_per_frame": [t["iterations"] for t in per_frame],
-                      "converged": all(t["converged"] for t in per_frame),
-                      "note": "frames solved sequentially on one resident problem; full-set factor cached "
-                              "after frame 0; time per frame = setup (data term + factor copy) + iterations"}),
+    cat = lambda r: np.concatenate(r.sensor_images)  # noqa: E731
+    agree = [api.relative_l2_diff(cat(a), cat(b)) for a, b in zip(bfix, sfix)]
+    spread = [api.relative_l2_diff(cat(a), cat(b)) for a, b in zip(sfix0, sfix)]
+    iters_seq = [r.iterations for r in seq]
+    iters_bat = [r.iterations for r in bat]
+    print(json.dumps({"config": "c5", "frames": F,
+                      "frames_per_s_sequential": F / t_seq, "frames_per_s_batched": F / t_bat,
+                      "speedup_batched": t_seq / t_bat,
+                      "wall_s_sequential": t_seq, "wall_s_batched": t_bat,
+                      "iterations_per_frame_sequential": iters_seq, "iterations_per_frame_batched": iters_bat,
+                      "frame_iterations_per_s_batched": sum(iters_bat) / t_bat,
+                      f"sensor_images_rel_diff_at_{kfix}_iterations": {"batched_vs_sequential": max(agree),
+                                                                      "summation_order_spread": max(spread)},
+                      "converged": all(r.converged for r in bat) and all(r.converged for r in seq),
+                      "note": "operators resident; full-set factor computed once and shared; time-to-tolerance "
+                              "rule per frame (eps_abs = 1e-5 pri_res(1)/sqrt(N)); wall clock around the solve "
+                              "calls; batched = run_frames with frame-batched DMMA contractions"}),
           flush=True)
 
 

@@ -507,13 +507,11 @@ __device__ __forceinline__ void fusion_pixel(const FusionArgs& a, int j, Contrib
 // Block-reduce the five partial sums, publish them, and let the last block of
 // the grid reduce all blocks in fixed order and evaluate the stopping rule
 // (admm.hpp:244-256).  Deterministic for a fixed grid.
-__device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5]) {
+__device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5], int nblocks, int bid) {
   __shared__ double red[5][32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = (blockDim.x + 31) >> 5;
-  const int nblocks = gridDim.x * gridDim.y * gridDim.z;
-  const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
 #pragma unroll
   for (int t = 0; t < 5; ++t) {
     const double w = warp_sum(q[t]);
@@ -563,12 +561,29 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
   }
 }
 
+// whole grid = one fusion round
+__device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5]) {
+  fusion_finish(a, q, gridDim.x * gridDim.y * gridDim.z,
+                blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+}
+
 __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
   if (a.go && __ldg(a.go) == 0) return;  // cancelled speculative iteration
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double q[5] = {0, 0, 0, 0, 0};
   if (j < a.N) fusion_pixel(a, j, [&](int k) { return a.contrib[k][j]; }, q);
   fusion_finish(a, q);
+}
+
+// One fusion round per frame of a multi-frame batch (blockIdx.y = frame);
+// each frame reduces over its own row of blocks with its own counter.
+__global__ void __launch_bounds__(kFusionThreads) fusion_frames_kernel(const __grid_constant__ Pack<FusionArgs> P) {
+  const FusionArgs& a = P.j[blockIdx.y];
+  if (a.go && __ldg(a.go) == 0) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double q[5] = {0, 0, 0, 0, 0};
+  if (j < a.N) fusion_pixel(a, j, [&](int k) { return a.contrib[k][j]; }, q);
+  fusion_finish(a, q, gridDim.x, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -2505,32 +2520,40 @@ struct FrameBatchJob {
   double* ring[kFB];
 };
 
+constexpr int kFbBK = 16;  // K per shared stage (4 DMMA k-steps per barrier)
+constexpr size_t kFbSmem = (size_t)2 * 2 * kFbBK * (kFbPA + kFbPB) * sizeof(double);
+
 template <int MODE>
-__global__ void __launch_bounds__(256) frame_batch_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
-                                                         double mu, double beta) {
+__global__ void __launch_bounds__(256, 2) frame_batch_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
+                                                            double mu, double beta) {
+  constexpr int BK = kFbBK, LA = kFbBM * BK / 256;
   const FrameBatchJob& jb = jobs[blockIdx.z];
   const int m0 = blockIdx.x * kFbBM;
   if (m0 >= jb.m) return;
   const int split = blockIdx.y;
-  const int nk_all = (jb.k + kGK - 1) / kGK;
+  const int nk_all = (jb.k + BK - 1) / BK;
   const int per = (nk_all + nsplit - 1) / nsplit;
   const int t0 = split * per, t1 = min(nk_all, t0 + per);
-  __shared__ double As[2][2][kGK][kFbPA];
-  __shared__ double Bs[2][2][kGK][kFbPB];
+  extern __shared__ double fsm[];
+  double(*As)[2][BK][kFbPA] = reinterpret_cast<double(*)[2][BK][kFbPA]>(fsm);
+  double(*Bs)[2][BK][kFbPB] = reinterpret_cast<double(*)[2][BK][kFbPB]>(fsm + 2 * 2 * BK * kFbPA);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp * 16, fr = lane >> 2, fc = lane & 3;
+  const int nb = jb.nf > 8 ? 2 : 1;  // 8-frame DMMA column blocks actually used
   double cr[2][2][2], ci[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
-  double2 pa[4], pb = make_double2(0.0, 0.0);
+  double2 pa[LA], pb = make_double2(0.0, 0.0);
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (MODE == FB_ADJ) { kk = e & (BK - 1); ii = e / BK; } else { ii = e & (kFbBM - 1); kk = e / kFbBM; }
+  };
   auto fetch = [&](int kk0) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int e = tid + t * 256;
+    for (int t = 0; t < LA; ++t) {
       int ii, kk;
-      if (MODE == FB_ADJ) { kk = e & 7; ii = e >> 3; } else { ii = e & 127; kk = e >> 7; }
+      a_pos(tid + t * 256, ii, kk);
       const int gi = m0 + ii, gk = kk0 + kk;
       double2 v = make_double2(0.0, 0.0);
       if (gi < jb.m && gk < jb.k) {
@@ -2546,36 +2569,33 @@ __global__ void __launch_bounds__(256) frame_batch_kernel(const FrameBatchJob* _
       }
       pa[t] = v;
     }
-    if (tid < kGK * kFB) {
-      const int kk = tid & 7, f = tid >> 3, gk = kk0 + kk;
+    {  // B: BK x 16 frames, one element per thread
+      const int kk = tid & (BK - 1), f = tid / BK, gk = kk0 + kk;
       pb = (f < jb.nf && gk < jb.k) ? jb.B[f][gk] : make_double2(0.0, 0.0);
     }
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int e = tid + t * 256;
+    for (int t = 0; t < LA; ++t) {
       int ii, kk;
-      if (MODE == FB_ADJ) { kk = e & 7; ii = e >> 3; } else { ii = e & 127; kk = e >> 7; }
+      a_pos(tid + t * 256, ii, kk);
       As[buf][0][kk][ii] = pa[t].x;
       As[buf][1][kk][ii] = pa[t].y;
     }
-    if (tid < kGK * kFB) {
-      const int kk = tid & 7, f = tid >> 3;
-      Bs[buf][0][kk][f] = pb.x;
-      Bs[buf][1][kk][f] = pb.y;
-    }
+    const int kk = tid & (BK - 1), f = tid / BK;
+    Bs[buf][0][kk][f] = pb.x;
+    Bs[buf][1][kk][f] = pb.y;
   };
   if (t0 < t1) {
-    fetch(t0 * kGK);
+    fetch(t0 * BK);
     stash(0);
   }
   __syncthreads();
   for (int t = t0; t < t1; ++t) {
     const int cur = (t - t0) & 1;
-    if (t + 1 < t1) fetch((t + 1) * kGK);
+    if (t + 1 < t1) fetch((t + 1) * BK);  // a whole stage ahead of its use
 #pragma unroll
-    for (int k4 = 0; k4 < kGK; k4 += 4) {
+    for (int k4 = 0; k4 < BK; k4 += 4) {
       double ar[2], ai[2], nai[2], br[2], bi[2];
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
@@ -2592,10 +2612,12 @@ __global__ void __launch_bounds__(256) frame_batch_kernel(const FrameBatchJob* _
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-          dmma884(cr[a][b], ar[a], br[b]);
-          dmma884(cr[a][b], nai[a], bi[b]);
-          dmma884(ci[a][b], ar[a], bi[b]);
-          dmma884(ci[a][b], ai[a], br[b]);
+          if (b < nb) {
+            dmma884(cr[a][b], ar[a], br[b]);
+            dmma884(cr[a][b], nai[a], bi[b]);
+            dmma884(ci[a][b], ar[a], bi[b]);
+            dmma884(ci[a][b], ai[a], br[b]);
+          }
         }
     }
     if (t + 1 < t1) stash(cur ^ 1);
@@ -2616,6 +2638,152 @@ __global__ void __launch_bounds__(256) frame_batch_kernel(const FrameBatchJob* _
           const double2 r = jb.rhs[f][i];
           const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cr[a][b][v])), beta),
                                           __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, ci[a][b][v])), beta));
+          const double2 old = jb.x_full[f][i];
+          jb.ring[f][i] = c_abs(c_sub(xh, old));
+          jb.x_full[f][i] = xh;
+          jb.x_hat[f][i] = xh;
+        }
+      }
+}
+
+// Operator passes (FWD, ADJ) of the frame batch as a kFbStages-deep cp.async
+// pipeline: raw complex64 operator tiles and complex128 frame vectors go
+// global -> shared without registers (zero-filled outside the matrix), and
+// are converted to fp64 (conjugated for ADJ) when the DMMA fragments are
+// loaded.  FWD tiles are k-major ([kk][row], 128 contiguous complex64 per
+// kk); ADJ tiles are pixel-major ([pixel][kk], each pixel's 16 rows are one
+// 128-B run), so every 16-B chunk lands contiguously.  Pitches keep the
+// fragment loads of each half warp on distinct banks.
+constexpr int kFbStages = 4;
+constexpr int kFbPF = 132;  // FWD: float2 per kk row (128 + 4)
+constexpr int kFbPX = 20;   // ADJ: float2 per pixel row (16 + 4)
+constexpr int kFbPV = 20;   // frame vectors: double2 per frame row (16 + 4)
+constexpr size_t kFbStageA = (size_t)kFbBK * kFbPF * 8 > (size_t)kFbBM * kFbPX * 8 ? (size_t)kFbBK * kFbPF * 8
+                                                                                     : (size_t)kFbBM * kFbPX * 8;
+constexpr size_t kFbStageB = (size_t)kFB * kFbPV * 16;
+constexpr size_t kFb2Smem = kFbStages * (kFbStageA + kFbStageB) + kFB * 8;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
+                                                             double mu, double beta) {
+  constexpr int BK = kFbBK, S = kFbStages;
+  const FrameBatchJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.x * kFbBM;
+  if (m0 >= jb.m) return;
+  const int split = blockIdx.y;
+  const int nk_all = (jb.k + BK - 1) / BK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per, t1 = min(nk_all, t0 + per);
+  const int nt = max(0, t1 - t0);
+  extern __shared__ __align__(16) uint8_t fsm2[];
+  uint8_t* sA = fsm2;
+  uint8_t* sB = fsm2 + S * kFbStageA;
+  const double2** Bp = reinterpret_cast<const double2**>(fsm2 + S * (kFbStageA + kFbStageB));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kFB) Bp[tid] = tid < jb.nf ? jb.B[tid] : nullptr;
+  __syncthreads();
+  const int wm = warp * 16, fr = lane >> 2, fc = lane & 3;
+  const int nb = jb.nf > 8 ? 2 : 1;
+  const int m = jb.m, kdim = jb.k, nf = jb.nf;
+  const int64_t lda = jb.lda;
+  const float2* A = reinterpret_cast<const float2*>(jb.A);
+  auto issue = [&](int t, int slot) {  // stage t (absolute) -> shared slot
+    const int k0 = t * BK;
+    float2* a = reinterpret_cast<float2*>(sA + slot * kFbStageA);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 1024 16-B chunks of A
+      const int c = tid + 256 * u;
+      if (MODE == FB_FWD) {  // chunk: rows 2*(c & 63) .. +1 of column kk = c >> 6
+        const int kk = c >> 6, ii = 2 * (c & 63);
+        const int gi = m0 + ii, gk = k0 + kk;
+        // rows [m, lda) are the operator's zeroed padding: readable, and zero
+        const bool ok = gi < lda && gk < kdim;
+        cp_async16(a + kk * kFbPF + ii, ok ? A + gi + (int64_t)gk * lda : A, ok);
+      } else {  // ADJ chunk: rows 2*(c & 7) .. +1 of pixel ii = c >> 3
+        const int ii = c >> 3, kk = 2 * (c & 7);
+        const int gi = m0 + ii, gk = k0 + kk;
+        const bool ok = gi < m && gk < kdim;
+        cp_async16(a + ii * kFbPX + kk, ok ? A + gk + (int64_t)gi * lda : A, ok);
+      }
+    }
+    {  // B: 16 frames x 16 k (double2), one chunk per thread
+      double2* b = reinterpret_cast<double2*>(sB + slot * kFbStageB);
+      const int f = tid >> 4, kk = tid & 15, gk = k0 + kk;
+      const bool ok = f < nf && gk < kdim;
+      cp_async16(b + f * kFbPV + kk, ok ? Bp[f] + gk : reinterpret_cast<const double2*>(A), ok);
+    }
+  };
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < S - 1; ++s0) {
+    if (s0 < nt) issue(t0 + s0, s0);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nt; ++t) {
+    cp_async_wait<S - 2>();
+    __syncthreads();  // stage t landed for everyone; slot (t-1) % S is free
+    if (t + S - 1 < nt) issue(t0 + t + S - 1, (t + S - 1) % S);
+    cp_async_commit();
+    const int slot = t % S;
+    const float2* a = reinterpret_cast<const float2*>(sA + slot * kFbStageA);
+    const double2* b = reinterpret_cast<const double2*>(sB + slot * kFbStageB);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[2], ai[2], nai[2], br[2], bi[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int row = wm + 8 * q + fr, kk = k4 + fc;
+        const float2 x = MODE == FB_FWD ? a[kk * kFbPF + row] : a[row * kFbPX + kk];
+        ar[q] = (double)x.x;
+        ai[q] = MODE == FB_FWD ? (double)x.y : -(double)x.y;
+        nai[q] = -ai[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 y = b[(8 * q + fr) * kFbPV + k4 + fc];
+        br[q] = y.x;
+        bi[q] = y.y;
+      }
+#pragma unroll
+      for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < 2; ++qb)
+          if (qb < nb) {
+            dmma884(cr[qa][qb], ar[qa], br[qb]);
+            dmma884(cr[qa][qb], nai[qa], bi[qb]);
+            dmma884(ci[qa][qb], ar[qa], bi[qb]);
+            dmma884(ci[qa][qb], ai[qa], br[qb]);
+          }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < 2; ++qb)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * qa + fr, f = 8 * qb + 2 * fc + v;
+        if (i >= m || f >= nf) continue;
+        if (MODE == FB_FWD) {
+          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cr[qa][qb][v], ci[qa][qb][v]);
+        } else {
+          const double2 r = jb.rhs[f][i];
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cr[qa][qb][v])), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, ci[qa][qb][v])), beta));
           const double2 old = jb.x_full[f][i];
           jb.ring[f][i] = c_abs(c_sub(xh, old));
           jb.x_full[f][i] = xh;

