@@ -228,7 +228,7 @@ __device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, doub
 // THREADS = 256 normally; 1024 when the shared vector is so large (KM = 8192:
 // 128 KB) that only one CTA fits per SM, to keep enough loads in flight.
 template <typename T, int EPI, bool SMEM_VEC, int CPW, int THREADS>
-__global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? 5 : 1) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
                                                          const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ double2 sv[];
@@ -2789,6 +2789,140 @@ __global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJo
           jb.x_full[f][i] = xh;
           jb.x_hat[f][i] = xh;
         }
+      }
+}
+
+// Dual capacitance C = beta I + mu A_J A_J^H (the Woodbury system of
+// solver_core.hpp:39-40) on the fp64 tensor cores: 4-stage cp.async pipeline
+// of the complex64 columns A(:, J_k) (both operands come from the same
+// columns: rows i of the tile and rows j of its mirror), DMMA m8n8k4 f64.
+// Lower 128 x 64 tiles only; the upper triangle is written as the exact
+// conjugate mirror and the diagonal is exactly real, as the SIMT path does.
+// The active-column indices of stage t+S-1 are fetched into registers one
+// iteration ahead so the gathered addresses never stall the pipeline.
+struct GramJob {
+  const float2* A;
+  int64_t lda;
+  const int* J;  // active columns (n entries)
+  int n;         // K
+  int m;         // rows (matrix order)
+  double2* C;
+  int64_t ldc;
+};
+constexpr int kGrBM = 128, kGrBN = 64, kGrPA = 132, kGrPB = 68;
+constexpr size_t kGrStage = (size_t)kFbBK * (kGrPA + kGrPB) * 8;
+constexpr size_t kGramSmem = kFbStages * kGrStage;
+
+__global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __restrict__ jobs, double mu, double beta) {
+  constexpr int BK = kFbBK, S = kFbStages;
+  const GramJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.y * kGrBM, n0 = blockIdx.x * kGrBN;
+  const int m = jb.m;
+  if (m0 >= m || n0 >= m || m0 + kGrBM <= n0) return;  // outside, or strictly upper
+  extern __shared__ __align__(16) uint8_t gsm2[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32, fr = lane >> 2, fc = lane & 3;
+  const int64_t lda = jb.lda;
+  const float2* A = jb.A;
+  const int* J = jb.J;
+  const int nk = (jb.n + BK - 1) / BK;
+  // chunk c of the A tile: rows 2*(c & 63) of column kk = c >> 6 (4 per thread);
+  // B tile: rows 2*(c & 31) of column kk = c >> 5 (2 per thread)
+  int ja[4], jbn[2];
+  auto load_j = [&](int t) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int gk = t * BK + ((tid + 256 * u) >> 6);
+      ja[u] = gk < jb.n ? (J ? __ldg(J + gk) : gk) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int gk = t * BK + ((tid + 256 * u) >> 5);
+      jbn[u] = gk < jb.n ? (J ? __ldg(J + gk) : gk) : -1;
+    }
+  };
+  auto issue = [&](int slot) {
+    float2* a = reinterpret_cast<float2*>(gsm2 + slot * kGrStage);
+    float2* b = a + BK * kGrPA;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = tid + 256 * u, kk = c >> 6, ii = 2 * (c & 63);
+      const int gi = m0 + ii;
+      const bool ok = ja[u] >= 0 && gi < lda;
+      cp_async16(a + kk * kGrPA + ii, ok ? A + gi + (int64_t)ja[u] * lda : A, ok);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + 256 * u, kk = c >> 5, jj = 2 * (c & 31);
+      const int gj = n0 + jj;
+      const bool ok = jbn[u] >= 0 && gj < lda;
+      cp_async16(b + kk * kGrPB + jj, ok ? A + gj + (int64_t)jbn[u] * lda : A, ok);
+    }
+  };
+  double cr[4][4][2], ci[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < S - 1; ++s0) {
+    if (s0 < nk) {
+      load_j(s0);
+      issue(s0);
+    }
+    cp_async_commit();
+  }
+  if (S - 1 < nk) load_j(S - 1);
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (t + S - 1 < nk) {
+      issue((t + S - 1) % S);                   // indices fetched last iteration
+      if (t + S < nk) load_j(t + S);            // in flight during this stage's math
+    }
+    cp_async_commit();
+    const float2* a = reinterpret_cast<const float2*>(gsm2 + (t % S) * kGrStage);
+    const float2* b = a + BK * kGrPA;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 x = a[(k4 + fc) * kGrPA + wm + 8 * q + fr];
+        ar[q] = (double)x.x;
+        ai[q] = (double)x.y;
+        nai[q] = -ai[q];
+        const float2 y = b[(k4 + fc) * kGrPB + wn + 8 * q + fr];  // B = conj(A(j, k))
+        br[q] = (double)y.x;
+        bi[q] = -(double)y.y;
+      }
+#pragma unroll
+      for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < 4; ++qb) {
+          dmma884(cr[qa][qb], ar[qa], br[qb]);
+          dmma884(cr[qa][qb], nai[qa], bi[qb]);
+          dmma884(ci[qa][qb], ar[qa], bi[qb]);
+          dmma884(ci[qa][qb], ai[qa], br[qb]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < 4; ++qb)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * qa + fr, j = n0 + wn + 8 * qb + 2 * fc + v;
+        if (i >= m || j >= m || i < j) continue;
+        double2 o = make_double2(mu * cr[qa][qb][v], mu * ci[qa][qb][v]);
+        if (i == j) {
+          o.x += beta;
+          o.y = 0.0;  // exact real diagonal of a Hermitian matrix
+        }
+        jb.C[i + (int64_t)j * jb.ldc] = o;
+        if (i != j) jb.C[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
       }
 }
 

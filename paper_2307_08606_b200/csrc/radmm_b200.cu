@@ -296,6 +296,7 @@ struct radmm_ctx {
   DArr<FrameReduceJob> fb_red;
   DArr<FrameRhsJob> fb_rhs;
   DArr<double2> fb_part;
+  DArr<GramJob> gram_jobs;
 
   ~radmm_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -812,6 +813,7 @@ void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
 void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
   if (qs.empty()) return;
   std::vector<GemmJob> jobs;
+  std::vector<GramJob> grams;
   std::vector<InvTarget> inv;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
@@ -826,14 +828,29 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
       // Gram mu A_J^H A_J + beta I (solver_core.hpp:39-40)
       jobs.push_back(gjob(dim, dim, S.rows, mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p),
                           mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
+      jobs.back().herm = 1;  // Hermitian: lower tiles + mirror
+    } else if (env_int("RADMM_GRAM", 1)) {
+      // capacitance beta I + mu A_J A_J^H on the fp64 tensor cores
+      grams.push_back(GramJob{S.A.p, S.ld, S.J.p, S.n_act, S.rows, S.G.p, ldg});
     } else {
       // capacitance beta I + mu A_J A_J^H (Woodbury form of the same system)
       jobs.push_back(gjob(dim, dim, S.n_act, mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p),
                           mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
+      jobs.back().herm = 1;
     }
-    jobs.back().herm = 1;  // Gram / capacitance are Hermitian: lower tiles + mirror
     inv.push_back({S.G.p, ldg, dim});
     ++c->rebuilds;
+  }
+  if (!grams.empty()) {
+    if (c->gram_jobs.n < grams.size()) c->gram_jobs.alloc(grams.size(), false);
+    CK(cudaMemcpyAsync(c->gram_jobs.p, grams.data(), sizeof(GramJob) * grams.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    int mmax = 0;
+    for (const auto& g : grams) mmax = std::max(mmax, g.m);
+    CK(cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
+    LAUNCH(c, gram_dmma_kernel, dim3((unsigned)((mmax + kGrBN - 1) / kGrBN), (unsigned)((mmax + kGrBM - 1) / kGrBM),
+                                     (unsigned)grams.size()),
+           256, kGramSmem, c->gram_jobs.p, mu, beta);
   }
   gemm<GEPI_PLAIN>(c, jobs);
   size_t need = 0;
