@@ -228,7 +228,7 @@ __device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, doub
 // THREADS = 256 normally; 1024 when the shared vector is so large (KM = 8192:
 // 128 KB) that only one CTA fits per SM, to keep enough loads in flight.
 template <typename T, int EPI, bool SMEM_VEC, int CPW, int THREADS>
-__global__ void __launch_bounds__(THREADS, THREADS == 256 ? 5 : 1) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
+__global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
                                                          const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ double2 sv[];
