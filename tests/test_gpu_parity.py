@@ -566,3 +566,118 @@ def test_frames_reject_bad_use():
     with pytest.raises(api.InvalidArgument):  # sensor 1 of frame 0 has no measurement
         s.run_frames([api.Hyperparams(**frames[0][1])])
     s.close()
+
+
+# ---- ragged shapes and full-size properties ------------------------------------------
+def _ragged_problem(seed=3, n=700, rows=(130, 256, 65, 200), n_targets=6):
+    rng = np.random.default_rng(seed)
+    ops = [(rng.normal(size=(r, n)) + 1j * rng.normal(size=(r, n))).astype(np.complex64) / np.sqrt(r) for r in rows]
+    x = np.zeros(n)
+    x[rng.choice(n, n_targets, replace=False)] = rng.uniform(0.5, 1.0, n_targets)
+    ys = [a.astype(np.complex128) @ x + 0.01 * (rng.normal(size=a.shape[0]) + 1j * rng.normal(size=a.shape[0]))
+          for a in ops]
+    return ops, ys
+
+
+@pytest.mark.parametrize("variant", ["default", "full_gapply", "adj_segments", "simt_gram"])
+def test_ragged_dual_sensors_match_oracle(variant, monkeypatch):
+    """Ragged sensors (KM = 130/256/65/200, N = 700: no shape a multiple of the
+    64 / 128 tiles) in the dual form with elimination, through every kernel
+    variant's padding paths, against the oracle at every step."""
+    env = {"full_gapply": {"RADMM_HERM": "0"}, "adj_segments": {"RADMM_ADJ_SPLIT_ROWS": "64", "RADMM_ADJ_SEG": "64"},
+           "simt_gram": {"RADMM_GRAM": "0", "RADMM_GEMM_BIG": "0"}}.get(variant, {})
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ops, ys = _ragged_problem()
+    hyper = dict(mu=1.0, lambda_=0.05, beta=1.0, eps_abs=1e-6, eps_rel=1e-4, screening_tol=2e-3, max_iter=120)
+    g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
+    assert g.downdates + g.rebuilds > len(ops)  # elimination events happened
+    bad, near = compare_masks(g, o, hyper["screening_tol"], 5)
+    assert bad == 0, (bad, near)
+    errs = state_errors(g, o)
+    assert max(errs[k] for k in ("sensor_images", "sigma", "s")) < 1e-6, errs
+
+
+def test_ragged_frames_batched_match_separate(monkeypatch):
+    """Frame-batched contractions on ragged sensors (padding in every tile)."""
+    ops, ys0 = _ragged_problem()
+    frames = [ys0, _ragged_problem(seed=4)[1]]
+    rng = np.random.default_rng(11)
+    frames.append([y + 0.05 * (rng.normal(size=y.shape) + 1j * rng.normal(size=y.shape)) for y in ys0])
+    hyper = dict(mu=1.0, lambda_=0.05, beta=1.0, eps_abs=1e-6, eps_rel=1e-4, max_iter=40)
+    s = api.Solver(ops[0].shape[1], len(ops))
+    for q, a in enumerate(ops):
+        s.set_operator(q, a)
+    for f, ys in enumerate(frames):
+        for q in range(len(ops)):
+            s.set_frame_measurement(f, q, ys[q])
+    res = s.run_frames([api.Hyperparams(**hyper)] * len(frames), api.Mode.SADMM, fixed_iterations=True)
+    for f, ys in enumerate(frames):
+        one = gpu_run(ops, ys, hyper, False, fixed_iterations=True)
+        errs = state_errors(res[f], one)
+        assert errs["sensor_images"] < 1e-9 and errs["sigma"] < 1e-9, errs
+    s.close()
+
+
+@pytest.fixture(scope="module")
+def c2_solver():
+    cfg = scenario.baseline_config("c2")
+    s = api.Solver(cfg.N, cfg.Q)
+    pix, tx, rx = scenario.baseline_geometry(cfg)
+    for q in range(cfg.Q):
+        s.generate_dechirp_operator(q, cfg.M, cfg.K, pix, tx[q], rx[q], scenario.baseline_phases(cfg, q),
+                                    cfg.fc, cfg.bw, cfg.pulse)
+    xs = scenario.baseline_scene(cfg)
+    ys = []
+    for q in range(cfg.Q):
+        y = s.apply(q, xs[q].astype(np.complex128))
+        ys.append(y)
+        s.set_measurement(q, y)
+    yield cfg, s, ys
+    s.close()
+
+
+def test_c2_full_size_disabled_screening_is_sadmm(c2_solver):
+    """Size-independent property at BASELINE config 2's full size: ASADMM with
+    screening disabled is SADMM, bitwise (test_admm.cpp:266-288)."""
+    cfg, s, _ = c2_solver
+    h = api.Hyperparams(mu=1.0, lambda_=100.0, beta=1.0, eps_abs=1e-12, eps_rel=1e-5, max_iter=12)
+    a = s.run(h, api.Mode.ASADMM, disable_screening=True, fixed_iterations=True)
+    b = s.run(h, api.Mode.SADMM, fixed_iterations=True)
+    for k in ("x_global", "s", "sigma"):
+        assert np.array_equal(getattr(a, k), getattr(b, k))
+    assert all(np.array_equal(x, y) for x, y in zip(a.sensor_images, b.sensor_images))
+
+
+def test_c2_full_size_woodbury_solve_residual(c2_solver):
+    """At full size (KM = 2048, N = 16384) the cached Woodbury solve satisfies
+    the reference's system (mu A^H A + beta I) x = rhs (solver_core.hpp:39-51)
+    to 1e-9, checked with the GPU operator products."""
+    cfg, s, _ = c2_solver
+    a = s.get_operator(0)
+    cache = api.factorize(a.astype(np.complex128), 1.0, 1.0)
+    rng = np.random.default_rng(2)
+    rhs = rng.normal(size=cfg.N) + 1j * rng.normal(size=cfg.N)
+    x = cache.solve(rhs)
+    resid = s.apply_adjoint(0, s.apply(0, x)) + x - rhs
+    assert np.linalg.norm(resid) < 1e-9 * np.linalg.norm(rhs)
+
+
+def test_c2_full_size_batched_frames_agree(c2_solver):
+    """Two frames at full size through the frame-batched tensor-core
+    contractions vs separate runs: 10 iterations within fp64 round-off."""
+    cfg, s, ys = c2_solver
+    rng = np.random.default_rng(5)
+    frames = [ys, [y + 1e-3 * (rng.normal(size=y.shape) + 1j * rng.normal(size=y.shape)) for y in ys]]
+    for f, yf in enumerate(frames):
+        for q in range(cfg.Q):
+            s.set_frame_measurement(f, q, yf[q])
+    h = api.Hyperparams(mu=1.0, lambda_=100.0, beta=1.0, eps_abs=1e-12, eps_rel=1e-5, max_iter=10)
+    res = s.run_frames([h, h], api.Mode.ASADMM, fixed_iterations=True)
+    for f, yf in enumerate(frames):
+        for q in range(cfg.Q):
+            s.set_measurement(q, yf[q])
+        one = s.run(h, api.Mode.ASADMM, fixed_iterations=True)
+        errs = state_errors(res[f], one)
+        assert errs["sensor_images"] < 1e-9 and errs["sigma"] < 1e-7, errs

@@ -24,12 +24,16 @@ PHASE_OF = {  # kernel name fragment (mangled or demangled) -> bench phase name
     "fused_sweep2_kernel": "sweep",
     "herm_gapply_tma_kernel": "gapply",
     "herm_gapply_kernel": "gapply",
+    "herm_reduce_kernel": "gapply_reduce",
+    "gram_dmma_kernel": "gram",
+    "frame_batch2_kernelILi0": "frames_forward",
+    "frame_batch2_kernelILi2": "frames_adjoint",
     "coldot_kernel<float2, 1": "adjoint",
     "fwd_kernel<0>": "forward",
     "coldot_kernel<double2, 0": "gapply",
     "coldot_kernel<double2, 2": "primal",
 }
-METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+METRICS = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
@@ -99,6 +103,12 @@ def main():
         per = collections.defaultdict(list)
         for rep in a.rep:
             for d in capture_rows(rep):
+                try:  # a launch cut off by -c has no metric values
+                    if float(d.get("dram__bytes_read.sum", "").replace(",", "")) != \
+                            float(d.get("dram__bytes_read.sum", "").replace(",", "")):
+                        continue  # nan
+                except ValueError:
+                    continue
                 for frag, phase in PHASE_OF.items():
                     if frag in d["name"]:
                         per[phase].append(d)
@@ -120,6 +130,7 @@ def main():
                    f"regs {ds[0].get('launch__registers_per_thread')}; grid {ds[0].get('launch__grid_size')} x "
                    f"{ds[0].get('launch__block_size')}",
                    f"- fp64 pipe {ds[0].get('sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active')}%; "
+                   f"tensor pipe {ds[0].get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active')}%; "
                    f"smem ld bank conflicts {ds[0].get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum')};"
                    f" L2 hit {ds[0].get('lts__t_sector_hit_rate.pct')}%",
                    f"- top stalls: {ds[0]['stalls']}", ""]
