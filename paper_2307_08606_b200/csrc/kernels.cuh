@@ -2147,7 +2147,7 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
   const HermJob& jb = P.j[q];
   __shared__ double2 vJ[kHermTile];
   __shared__ double2 vI[kHermStrip * kHermTile];
-  __shared__ double2 sax[8][kHermTile];
+  __shared__ double2 sax[2][8][kHermTile];  // double-buffered: one barrier per tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = jb.n;
   if (tid < kHermTile) {
@@ -2158,16 +2158,11 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
     const int i = I0 * kHermTile + t;
     vI[t] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
   }
-  __syncthreads();
   const int c0 = warp * 8;  // this warp's 8 columns of the tile column
-  double dr[8], di[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
   const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
-  for (int t = 0; t < nt; ++t) {
-    const int I = I0 + t;
+  double2 g[8][2];
+  auto load_tile = [&](int I) {
     const int ib = I * kHermTile;
-    double2 g[8][2];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -2175,6 +2170,15 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
         const int i = ib + lane + 32 * h, j = J * kHermTile + c0 + k;
         g[k][h] = (i < n && j < n) ? __ldg(Gc + (int64_t)k * jb.ld + i) : make_double2(0.0, 0.0);
       }
+  };
+  load_tile(I0);
+  __syncthreads();
+  double dr[8], di[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+  int par = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int I = I0 + t;
     double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -2194,20 +2198,21 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
         ai[h] = fma(g[k][h].y, vj.x, ai[h]);
       }
     }
+    if (t + 1 < nt) load_tile(I + 1);  // in flight across the reduction below
     if (I != J) {  // strictly-lower tile: its mirror contributes to rows of block I
 #pragma unroll
-      for (int h = 0; h < 2; ++h) sax[warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+      for (int h = 0; h < 2; ++h) sax[par][warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
       __syncthreads();
       if (tid < kHermTile) {
-        double2 s = sax[0][tid];
+        double2 sum = sax[par][0][tid];
 #pragma unroll
         for (int w8 = 1; w8 < 8; ++w8) {
-          s.x += sax[w8][tid].x;
-          s.y += sax[w8][tid].y;
+          sum.x += sax[par][w8][tid].x;
+          sum.y += sax[par][w8][tid].y;
         }
-        jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = s;
+        jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = sum;
       }
-      __syncthreads();
+      par ^= 1;  // the other buffer's readers are past this barrier
     }
   }
 #pragma unroll
@@ -2216,8 +2221,8 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
     di[k] = warp_sum(di[k]);
   }
   if (lane == 0) {
-    const int g = (I0 - J) / kHermStrip;
-    double2* dp = jb.dotp + ((int64_t)J * jb.groups + g) * kHermTile + c0;
+    const int gi = (I0 - J) / kHermStrip;
+    double2* dp = jb.dotp + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
   }

