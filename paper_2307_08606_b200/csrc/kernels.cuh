@@ -529,11 +529,21 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < 5) {
-    double acc = 0;
-    for (int b = 0; b < nblocks; ++b) acc += ((volatile double*)a.partials)[b * 5 + threadIdx.x];
-    red[threadIdx.x][0] = acc;
+  // all threads stage the block partials into shared memory in parallel, then
+  // threads 0..4 add them in block order (the same order, bitwise, as a
+  // sequential walk -- without its ~nblocks dependent L2 round trips)
+  __shared__ double stage[5 * 64];
+  double acc = 0.0;
+  for (int b0 = 0; b0 < nblocks; b0 += 64) {
+    const int nb = min(64, nblocks - b0);
+    for (int e = threadIdx.x; e < 5 * nb; e += blockDim.x)
+      stage[e] = ((volatile double*)a.partials)[b0 * 5 + e];
+    __syncthreads();
+    if (threadIdx.x < 5)
+      for (int b = 0; b < nb; ++b) acc += stage[b * 5 + threadIdx.x];
+    __syncthreads();
   }
+  if (threadIdx.x < 5) red[threadIdx.x][0] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     FusionScalars f;
