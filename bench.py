@@ -331,8 +331,8 @@ def ours(args, cfg):
     # One step = one api.run() solve to tolerance (the call a user makes):
     # H2D of the operators + setup + every iteration + D2H of every result.
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = e2e_run(cfg, ttt_hyper or hyper, ys, to_tolerance=ttt_hyper is not None)
+    if not args.no_e2e:
+        e2e = e2e_run(cfg, ttt_hyper or hyper, ys, to_tolerance=ttt_hyper is not None, q0=q0, q1=q1, dist=dist)
 
     # ---- CPU baseline ------------------------------------------------------
     cpu = None
@@ -381,48 +381,71 @@ def time_to_tolerance(solver, hyper, max_iter):
              "active_sizes_end": last.active_sizes}, h2)
 
 
-def e2e_run(cfg, hyper, ys, to_tolerance=True):
-    """The public call a user makes (api.run on host numpy arrays), with the
-    operators in pinned host memory: H2D of A + y, initial factorization,
-    the iterations (to tolerance) and D2H of every RunResult field, timed with
-    CUDA events around the call."""
+def e2e_run(cfg, hyper, ys, to_tolerance=True, q0=0, q1=None, dist=None):
+    """The public call a user makes, with the operators in pinned host memory:
+    api.run(problem, hyper, ASADMM) on one GPU, run_distributed (every rank
+    passes the Problem and uploads its own sensors, runtime.hpp:768-775)
+    under torchrun.  H2D of A + y, initial factorization, the iterations (to
+    tolerance) and D2H of every RunResult field are inside the timed region
+    (CUDA events; max over ranks; bytes summed over ranks)."""
     import torch
-    from paper_2307_08606_b200 import api, scenario
-    pinned = torch.empty((cfg.Q, cfg.N, cfg.KM), dtype=torch.complex64, pin_memory=True)
-    gen = api.Solver(cfg.N, cfg.Q)
+    from paper_2307_08606_b200 import api, scenario, distributed as D
+    q1 = cfg.Q if q1 is None else q1
+    nloc = q1 - q0
+    world = dist.get_world_size() if dist is not None else 1
+    pinned = torch.empty((nloc, cfg.N, cfg.KM), dtype=torch.complex64, pin_memory=True)
+    gen = api.Solver(cfg.N, nloc, torch.cuda.current_device())
     pix, tx, rx = scenario.baseline_geometry(cfg)
-    for q in range(cfg.Q):
-        gen.generate_dechirp_operator(q, cfg.M, cfg.K, pix, tx[q], rx[q], scenario.baseline_phases(cfg, q),
+    for q in range(q0, q1):
+        gen.generate_dechirp_operator(q - q0, cfg.M, cfg.K, pix, tx[q], rx[q], scenario.baseline_phases(cfg, q),
                                       cfg.fc, cfg.bw, cfg.pulse)
-        pinned[q].numpy()[:] = gen.get_operator(q).T
+        pinned[q - q0].numpy()[:] = gen.get_operator(q - q0).T
     gen.close()
-    ops = [api.ForwardOperator.from_matrix(pinned[q].numpy().T) for q in range(cfg.Q)]  # F-contiguous views
-    prob = api.Problem(ops, ys)
+    # sensors owned by other ranks: shape-only placeholders (never uploaded here)
+    hole = np.broadcast_to(np.zeros((1, 1), dtype=np.complex64), (cfg.KM, cfg.N))
+    ops = [api.ForwardOperator.from_matrix(pinned[q - q0].numpy().T if q0 <= q < q1 else hole)
+           for q in range(cfg.Q)]  # F-contiguous views of the pinned buffers
+    ys_all = [ys[q - q0] if q0 <= q < q1 else np.zeros(cfg.KM, dtype=np.complex128) for q in range(cfg.Q)]
+    prob = api.Problem(ops, ys_all)
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    # api.run(prob, hyper, ASADMM), spelled out so each stage can be timed
     t0 = time.perf_counter()
-    prob.validate()
-    hyper.validate()
-    solver = api.Solver.from_problem(prob)
-    t1 = time.perf_counter()
-    try:
-        r = solver.run(hyper, api.Mode.ASADMM, fixed_iterations=not to_tolerance)
+    if world == 1:  # api.run(prob, hyper, ASADMM), spelled out so each stage can be timed
+        prob.validate()
+        hyper.validate()
+        solver = api.Solver.from_problem(prob)
+        t1 = time.perf_counter()
+        try:
+            r = solver.run(hyper, api.Mode.ASADMM, fixed_iterations=not to_tolerance)
+            t2 = time.perf_counter()
+        finally:
+            solver.close()
+    else:
+        t1 = t0
+        r = D.run_distributed(prob, hyper, api.Mode.ASADMM, fixed_iterations=not to_tolerance)
         t2 = time.perf_counter()
-    finally:
-        solver.close()
     t3 = time.perf_counter()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    h2d = sum(a.matrix().nbytes for a in ops) + sum(np.asarray(y).nbytes for y in ys)
+    h2d = sum(ops[q].matrix().nbytes for q in range(q0, q1)) + sum(np.asarray(y).nbytes for y in ys)
     d2h = (r.image.nbytes + 4 * r.x_global.nbytes + sum(x.nbytes for x in r.sensor_images)
            + sum(a.nbytes for a in r.active_sets))
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        b = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        h2d, d2h = int(b[0].item()), int(b[1].item())
     return {"value": r.iterations / (ms / 1000.0), "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
-            "step": f"one api.run call ({'to tolerance' if to_tolerance else 'fixed'}; "
-                    f"{r.iterations} iterations, converged={r.converged})",
+            "step": f"one {'api.run' if world == 1 else 'run_distributed'} call "
+                    f"({'to tolerance' if to_tolerance else 'fixed'}; {r.iterations} iterations, "
+                    f"converged={r.converged})",
             "ms": ms, "setup_ms": r.setup_ms, "solve_ms": r.solve_ms,
             "stages_ms": {"context_and_upload": 1e3 * (t1 - t0), "run_and_fetch": 1e3 * (t2 - t1),
                           "close": 1e3 * (t3 - t2)}}
