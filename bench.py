@@ -307,7 +307,7 @@ def ours(args, cfg):
     phases = solver.phase_stats()
     solver.set_profiling(False)
     peak, peak_kind = measured_peaks()
-    kern = max(("forward", "adjoint", "gapply", "primal"), key=lambda p: phases[p]["ms"])
+    kern = max(("forward", "adjoint", "gapply", "primal", "sweep"), key=lambda p: phases[p]["ms"])
     ph = phases[kern]
     per_launch_ms = ph["ms"] / max(1, ph["calls"])
     per_launch_bytes = ph["bytes"] / max(1, ph["calls"])

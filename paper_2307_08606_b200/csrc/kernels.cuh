@@ -2737,11 +2737,16 @@ __global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJo
       cp_async16(b + f * kFbPV + kk, ok ? Bp[f] + gk : reinterpret_cast<const double2*>(A), ok);
     }
   };
-  double cr[2][2][2], ci[2][2][2];
+  // 3M (Karatsuba) complex products: P1 = sum Ar Br, P2 = sum Ai Bi,
+  // P3 = sum (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2 (3 DMMAs per
+  // complex 8x8x4 block instead of 4)
+  double p1[2][2][2], p2[2][2][2], p3[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
 #pragma unroll
   for (int s0 = 0; s0 < S - 1; ++s0) {
     if (s0 < nt) issue(t0 + s0, s0);
@@ -2757,30 +2762,30 @@ __global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJo
     const double2* b = reinterpret_cast<const double2*>(sB + slot * kFbStageB);
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
-      double ar[2], ai[2], nai[2], br[2], bi[2];
+      double ar[2], ai[2], as[2], br[2], bi[2], bs[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int row = wm + 8 * q + fr, kk = k4 + fc;
         const float2 x = MODE == FB_FWD ? a[kk * kFbPF + row] : a[row * kFbPX + kk];
         ar[q] = (double)x.x;
         ai[q] = MODE == FB_FWD ? (double)x.y : -(double)x.y;
-        nai[q] = -ai[q];
+        as[q] = ar[q] + ai[q];
       }
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const double2 y = b[(8 * q + fr) * kFbPV + k4 + fc];
         br[q] = y.x;
         bi[q] = y.y;
+        bs[q] = y.x + y.y;
       }
 #pragma unroll
       for (int qa = 0; qa < 2; ++qa)
 #pragma unroll
         for (int qb = 0; qb < 2; ++qb)
           if (qb < nb) {
-            dmma884(cr[qa][qb], ar[qa], br[qb]);
-            dmma884(cr[qa][qb], nai[qa], bi[qb]);
-            dmma884(ci[qa][qb], ar[qa], bi[qb]);
-            dmma884(ci[qa][qb], ai[qa], br[qb]);
+            dmma884(p1[qa][qb], ar[qa], br[qb]);
+            dmma884(p2[qa][qb], ai[qa], bi[qb]);
+            dmma884(p3[qa][qb], as[qa], bs[qb]);
           }
     }
   }
@@ -2793,12 +2798,14 @@ __global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJo
       for (int v = 0; v < 2; ++v) {
         const int i = m0 + wm + 8 * qa + fr, f = 8 * qb + 2 * fc + v;
         if (i >= m || f >= nf) continue;
+        const double cre = p1[qa][qb][v] - p2[qa][qb][v];
+        const double cim = p3[qa][qb][v] - p1[qa][qb][v] - p2[qa][qb][v];
         if (MODE == FB_FWD) {
-          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cr[qa][qb][v], ci[qa][qb][v]);
+          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cre, cim);
         } else {
           const double2 r = jb.rhs[f][i];
-          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cr[qa][qb][v])), beta),
-                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, ci[qa][qb][v])), beta));
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cre)), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, cim)), beta));
           const double2 old = jb.x_full[f][i];
           jb.ring[f][i] = c_abs(c_sub(xh, old));
           jb.x_full[f][i] = xh;
@@ -2980,6 +2987,488 @@ __global__ void frame_rhs_kernel(const FrameRhsJob* __restrict__ jobs, double be
   const double2 d = jb.data[j], g = jb.gap[j], x = jb.x_hat[j], sg = jb.sigma[j];
   jb.rhs[j] = make_double2(__dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, x.x)), sg.x),
                            __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, x.y)), sg.y));
+}
+
+// ---------------------------------------------------------------------------
+// Fused single-pass sweep v4 (RADMM_FUSED=4): every operator column is read
+// ONCE per iteration.  Cooperative persistent grid: CTA (c, q) owns sensor q's
+// 4-pixel tiles of pixel chunk c (the Q CTAs of a chunk run concurrently).
+// Shared memory: w_q (the capacitance-inverse apply, KM complex128) and a
+// 3-slot ring of A tiles (4 columns x KM complex64, bulk-copied).  Step b:
+//   dots(b): x_q = (rhs_q - mu A_q^H w_q) / beta for the tile, + the x-update
+//            epilogue (history, scatter) -- admm.hpp:114-123;
+//   publish: the Q-th sensor to finish tile b (global arrival counter) runs
+//            FusionCore::round for its 4 pixels (admm.hpp:236-258), writes the
+//            tile's norm partials and releases the tile flag;
+//   fwd(b-1): once tile b-1's flag is up, rhs_{k+1} = data + beta gap +
+//            beta x_hat - sigma (admm.hpp:114-119) and v += A(:, tile) rhs from
+//            the tile still in shared memory (register accumulators);
+//   refill:  tile b+2 into tile b-1's slot.
+// The last CTA reduces the tile norm partials in tile order (deterministic)
+// and evaluates the stopping rule.  Requires the full active set (J = id).
+// ---------------------------------------------------------------------------
+constexpr int kS4P = 4;          // pixels per tile
+constexpr int kS4Slots = 3;
+constexpr int kS4Threads = 256;
+
+struct Sweep4Job {
+  const float2* A;
+  const double2* w;
+  const double2* data;
+  double2* rhs;
+  double2* x_hat;
+  double2* x_full;
+  double* ring_slot;
+  double2* part;  // [chunk][ld]
+};
+
+struct Sweep4Ctl {
+  unsigned* tile_cnt;    // arrivals per tile (monotonic)
+  unsigned* tile_flag;   // = seq when the tile's fusion is done
+  double* tile_norms;    // 5 per tile
+  unsigned* done;        // CTAs finished (reset by the last one)
+  unsigned seq;
+  int tiles_per_chunk;
+  double2* xg_out;       // v5: new x_G / sigma (the inputs fa.xg / fa.sigma stay untouched)
+  double2* sigma_out;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kS4Threads, 1) fused_sweep4_kernel(const __grid_constant__ Pack<Sweep4Job> P,
+                                                                     const __grid_constant__ FusionArgs fa,
+                                                                     const __grid_constant__ Sweep4Ctl ctl,
+                                                                     double mu, double beta, int64_t ld) {
+  if (fa.go && __ldg(fa.go) == 0) return;  // cancelled speculative iteration
+  extern __shared__ __align__(128) uint8_t s4[];
+  const int q = blockIdx.y, chunk = blockIdx.x;
+  const Sweep4Job& jb = P.j[q];
+  const int Q = fa.Q, N = fa.N;
+  double2* sw = reinterpret_cast<double2*>(s4);                             // ld
+  float2* ring = reinterpret_cast<float2*>(s4 + (size_t)ld * sizeof(double2));  // slots x P x ld
+  uint64_t* full = reinterpret_cast<uint64_t*>(s4 + (size_t)ld * 16 + (size_t)kS4Slots * kS4P * ld * 8);
+  __shared__ double dots[kS4P][2][2];
+  __shared__ double2 rhs4[kS4P];
+  __shared__ double qn[kS4P][5];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = (N + kS4P - 1) / kS4P;
+  const int t0 = chunk * ctl.tiles_per_chunk, t1 = min(ntiles, t0 + ctl.tiles_per_chunk);
+  const unsigned tile_bytes = (unsigned)(kS4P * ld * sizeof(float2));
+  if (tid == 0) {
+    for (int i = 0; i < kS4Slots; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int r = tid; r < ld; r += kS4Threads) sw[r] = jb.w[r];
+  __syncthreads();
+  auto issue = [&](int b) {  // tile b -> its slot (thread 0)
+    const int slot = (b - t0) % kS4Slots;
+    mbar_arrive_expect_tx(&full[slot], tile_bytes);
+    for (int p = 0; p < kS4P; ++p)
+      tma_bulk_g2s(ring + ((size_t)slot * kS4P + p) * ld, jb.A + (int64_t)(b * kS4P + p) * ld,
+                   (unsigned)(ld * sizeof(float2)), &full[slot]);
+  };
+  if (tid == 0)
+    for (int b = t0; b < min(t1, t0 + kS4Slots - 1); ++b) issue(b);
+  double2 vacc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) vacc[i] = make_double2(0.0, 0.0);
+  const int rows_per_half = (int)(ld / 2);
+  auto forward_tile = [&](int b) {  // v += A(:, tile b) rhs_{k+1}(tile b), once the tile's fusion is done
+    if (tid == 0)
+      while (ld_acquire_u32(ctl.tile_flag + b) != ctl.seq) {
+      }
+    __syncwarp();
+    __syncthreads();
+    if (tid < kS4P) {
+      const int j = b * kS4P + tid;
+      double2 r = make_double2(0.0, 0.0);
+      if (j < N) {
+        // gap / sigma were just written by another CTA: read through L2 (L1 is not coherent)
+        const double2 d = jb.data[j], g = __ldcg(fa.gap + j), xh = jb.x_hat[j], sg = __ldcg(fa.sigma + j);
+        r.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
+        r.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
+        jb.rhs[j] = r;
+      }
+      rhs4[tid] = r;
+    }
+    __syncthreads();
+    const int slot = (b - t0) % kS4Slots;
+#pragma unroll
+    for (int p = 0; p < kS4P; ++p) {
+      const float2* col = ring + ((size_t)slot * kS4P + p) * ld;
+      const double2 r = rhs4[p];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = tid + kS4Threads * i;
+        if (row < ld) {
+          const float2 a = col[row];
+          vacc[i].x = fma((double)a.x, r.x, fma(-(double)a.y, r.y, vacc[i].x));
+          vacc[i].y = fma((double)a.x, r.y, fma((double)a.y, r.x, vacc[i].y));
+        }
+      }
+    }
+    __syncthreads();  // the slot is free again
+  };
+  for (int b = t0; b < t1; ++b) {
+    const int slot = (b - t0) % kS4Slots;
+    const unsigned par = (unsigned)(((b - t0) / kS4Slots) & 1);
+    mbar_wait_cta_acq(&full[slot], par);
+    {  // dots: warp (pixel p = warp & 3, row half h = warp >> 2)
+      const int p = warp & 3, h = warp >> 2;
+      const float2* col = ring + ((size_t)slot * kS4P + p) * ld + (size_t)h * rows_per_half;
+      const double2* wv = sw + (size_t)h * rows_per_half;
+      double re = 0.0, im = 0.0;
+      for (int r = lane; r < rows_per_half; r += 32) {
+        const float2 a = col[r];
+        const double2 v = wv[r];
+        cfma_conj(re, im, (double)a.x, (double)a.y, v);
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) {
+        dots[p][h][0] = re;
+        dots[p][h][1] = im;
+      }
+    }
+    __syncthreads();
+    if (tid < kS4P) {  // x-update epilogue (admm.hpp:120-123) for pixel j = b*4 + tid
+      const int j = b * kS4P + tid;
+      if (j < N) {
+        const double re = dots[tid][0][0] + dots[tid][1][0], im = dots[tid][0][1] + dots[tid][1][1];
+        const double2 r = jb.rhs[j];
+        const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, re)), beta),
+                                        __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, im)), beta));
+        const double2 old = jb.x_full[j];
+        jb.ring_slot[j] = c_abs(c_sub(xh, old));
+        jb.x_full[j] = xh;
+        jb.x_hat[j] = xh;
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    {  // publish; the Q-th arrival runs the tile's fusion round
+      __shared__ bool last;
+      if (tid == 0) last = (atomicAdd(ctl.tile_cnt + b, 1u) % (unsigned)Q) == (unsigned)(Q - 1);
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        if (tid < kS4P) {
+          double qv[5] = {0, 0, 0, 0, 0};
+          const int j = b * kS4P + tid;
+          if (j < N)
+            // other CTAs' x_q: through L2 (L1 may hold a stale line from a neighbouring tile)
+            fusion_pixel(fa, j, [&](int k) { return __ldcg(fa.contrib[k] + j); }, qv);
+          for (int t = 0; t < 5; ++t) qn[tid][t] = qv[t];
+        }
+        __syncthreads();
+        if (tid < 5) {
+          double a = 0.0;
+          for (int p = 0; p < kS4P; ++p) a += qn[p][tid];  // fixed pixel order
+          ctl.tile_norms[(size_t)b * 5 + tid] = a;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release_u32(ctl.tile_flag + b, ctl.seq);
+      }
+    }
+    if (b > t0) forward_tile(b - 1);
+    if (tid == 0 && b + kS4Slots - 1 < t1) issue(b + kS4Slots - 1);
+  }
+  if (t1 > t0) forward_tile(t1 - 1);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = tid + kS4Threads * i;
+    if (row < ld) jb.part[(size_t)chunk * ld + row] = vacc[i];
+  }
+  // grid-wide: the last CTA reduces the tile norms in tile order and
+  // evaluates the stopping rule (admm.hpp:244-256)
+  __threadfence();
+  __shared__ bool lastcta;
+  __syncthreads();
+  if (tid == 0) lastcta = atomicAdd(ctl.done, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!lastcta) return;
+  __threadfence();
+  __shared__ double red5[5][kS4Threads / 32];
+  double acc[5] = {0, 0, 0, 0, 0};
+  // each thread sums a contiguous block of tiles (in order), then blocks in order
+  const int per = (ntiles + kS4Threads - 1) / kS4Threads;
+  const int b0 = tid * per, b1 = min(ntiles, b0 + per);
+  for (int b = b0; b < b1; ++b)
+    for (int t = 0; t < 5; ++t) acc[t] += ((volatile const double*)ctl.tile_norms)[(size_t)b * 5 + t];
+  double* blocksum = reinterpret_cast<double*>(ring);  // the tile ring is free now: 5 x threads
+  for (int t = 0; t < 5; ++t) blocksum[t * kS4Threads + tid] = acc[t];
+  __syncthreads();
+  if (tid < 5) {
+    double a = 0.0;
+    for (int i = 0; i < kS4Threads; ++i) a += blocksum[tid * kS4Threads + i];
+    red5[tid][0] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    FusionScalars f;
+    for (int t = 0; t < 5; ++t) f.sq[t] = red5[t][0];
+    f.pri_res = sqrt(f.sq[0]);
+    f.dual_res = fa.beta * sqrt(f.sq[1]);
+    f.eps_pri = fa.root_n_eps_abs + fa.eps_rel * fmax(sqrt(f.sq[2]), sqrt(f.sq[3]));
+    f.eps_dual = fa.root_n_eps_abs + fa.eps_rel * sqrt(f.sq[4]);
+    f.trigger = f.pri_res <= f.eps_pri;
+    f.converged = fa.has_prev && f.trigger && f.dual_res <= f.eps_dual;
+    if (fa.go_next) *fa.go_next = !((fa.stop_on_converge && f.converged) || (fa.screen_next_possible && f.trigger));
+    f.iteration = fa.iteration;
+    f.pad = 0;
+    *fa.out_dev = f;
+    if (fa.out_host) {
+      volatile FusionScalars* hp = fa.out_host;
+      hp->pri_res = f.pri_res; hp->dual_res = f.dual_res; hp->eps_pri = f.eps_pri; hp->eps_dual = f.eps_dual;
+      for (int t = 0; t < 5; ++t) hp->sq[t] = f.sq[t];
+      hp->trigger = f.trigger; hp->converged = f.converged;
+      __threadfence_system();
+      hp->iteration = f.iteration;
+    }
+    *ctl.done = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused single-pass sweep v5 (RADMM_FUSED=5): v4's data flow with the
+// cross-SM latency chain taken off the streaming path (warp specialisation):
+//   warp 0       producer: bulk-copies tile b into a 3-slot ring;
+//   warps 1-8    dots + x-update epilogue for tile b, free the slot at once,
+//                then publish (red.release on the tile's arrival counter);
+//   warp 9       (sensor-0 CTA of each chunk) fusion: waits for all Q
+//                arrivals of tile b, runs FusionCore::round for its 4 pixels,
+//                writes the tile's norm partials, releases the tile flag;
+//   warps 10-17  forward: wait for the flag of tile b, form rhs_{k+1} and add
+//                A(:, tile) rhs into register accumulators, re-reading the
+//                tile's columns from L2.
+// The dot warps stay at most kS5Lag tiles ahead of the forward warps, which
+// bounds the L2 footprint of the re-read (~kS5Lag x 64 KB per CTA).
+// ---------------------------------------------------------------------------
+constexpr int kS5Slots = 3;
+constexpr int kS5Lag = 3;
+constexpr int kS5DotWarps = 4;   // one per pixel of the tile, all rows
+constexpr int kS5FwdWarps = 16;  // 4 rows per thread (KM <= 2048)
+constexpr int kS5Threads = (1 + kS5DotWarps + kS5FwdWarps) * 32;
+constexpr int kS5FwdRows = 4;
+
+__global__ void __launch_bounds__(kS5Threads, 1) fused_sweep5_kernel(const __grid_constant__ Pack<Sweep4Job> P,
+                                                                     const __grid_constant__ FusionArgs fa,
+                                                                     const __grid_constant__ Sweep4Ctl ctl,
+                                                                     double mu, double beta, int64_t ld) {
+  if (fa.go && __ldg(fa.go) == 0) return;
+  extern __shared__ __align__(128) uint8_t s5[];
+  const int q = blockIdx.y, chunk = blockIdx.x;
+  const Sweep4Job& jb = P.j[q];
+  const int Q = fa.Q, N = fa.N;
+  double2* sw = reinterpret_cast<double2*>(s5);
+  float2* ring = reinterpret_cast<float2*>(s5 + (size_t)ld * sizeof(double2));
+  uint64_t* full = reinterpret_cast<uint64_t*>(s5 + (size_t)ld * 16 + (size_t)kS5Slots * kS4P * ld * 8);
+  uint64_t* empty = full + kS5Slots;
+  __shared__ double2 rhs4[2][kS4P];
+  __shared__ volatile int fwd_done;  // last tile whose forward finished (t0 - 1 initially)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = N / kS4P;
+  const int t0 = chunk * ctl.tiles_per_chunk, t1 = min(ntiles, t0 + ctl.tiles_per_chunk);
+  const unsigned tile_bytes = (unsigned)(kS4P * ld * sizeof(float2));
+  // arrivals per tile after this launch: one per (sensor, tile)
+  const unsigned target = ctl.seq * (unsigned)Q;
+  if (tid == 0) {
+    for (int i = 0; i < kS5Slots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kS5DotWarps);
+    }
+    fwd_done = t0 - 1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int r = tid; r < ld; r += kS5Threads) sw[r] = jb.w[r];
+  __syncthreads();
+  if (warp == 0) {
+    // ---- producer --------------------------------------------------------
+    if (lane == 0) {
+      for (int b = t0; b < t1; ++b) {
+        const int u = b - t0, slot = u % kS5Slots;
+        if (u >= kS5Slots) mbar_wait_cta_acq(&empty[slot], (unsigned)(((u / kS5Slots) - 1) & 1));
+        mbar_arrive_expect_tx(&full[slot], tile_bytes);
+        for (int p = 0; p < kS4P; ++p)
+          tma_bulk_g2s(ring + ((size_t)slot * kS4P + p) * ld, jb.A + (int64_t)(b * kS4P + p) * ld,
+                       (unsigned)(ld * sizeof(float2)), &full[slot]);
+      }
+    }
+    __syncwarp();
+  } else if (warp <= kS5DotWarps) {
+    // ---- dots + x-update + publish (warp = pixel of the tile) ---------------
+    const int p = warp - 1;
+    for (int b = t0; b < t1; ++b) {
+      const int u = b - t0, slot = u % kS5Slots;
+      while (b - fwd_done > kS5Lag) __nanosleep(64);  // bound the L2 re-read distance
+      const int j = b * kS4P + p;
+      double2 r_in = make_double2(0.0, 0.0), old = make_double2(0.0, 0.0);
+      if (lane == 0) {  // epilogue inputs, fetched before the tile lands
+        r_in = jb.rhs[j];
+        old = jb.x_full[j];
+      }
+      mbar_wait_cta_acq(&full[slot], (unsigned)((u / kS5Slots) & 1));
+      const float2* col = ring + ((size_t)slot * kS4P + p) * ld;
+      double re = 0.0, im = 0.0;
+      for (int r = lane; r < ld; r += 32) {
+        const float2 a = col[r];
+        cfma_conj(re, im, (double)a.x, (double)a.y, sw[r]);
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_local(&empty[slot]);  // slot consumed
+        const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r_in.x, __dmul_rn(mu, re)), beta),
+                                        __ddiv_rn(__dsub_rn(r_in.y, __dmul_rn(mu, im)), beta));
+        jb.ring_slot[j] = c_abs(c_sub(xh, old));
+        jb.x_full[j] = xh;
+        jb.x_hat[j] = xh;
+      }
+      // one arrival per (sensor, tile) once all 4 pixels are written: each
+      // writer fences, the dot warps meet, and warp 1 publishes (release)
+      if (lane == 0) __threadfence();
+      __syncwarp();
+      asm volatile("bar.sync 1, %0;" ::"n"(kS5DotWarps * 32) : "memory");
+      if (p == 0 && lane == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctl.tile_cnt + b) : "memory");
+      __syncwarp();
+    }
+  } else {
+    // ---- forward: v += A(:, tile) rhs_{k+1}; next tile's columns prefetched --
+    const int ft = tid - (kS5DotWarps + 1) * 32;  // 0 .. 16 * 32 - 1
+    constexpr int FT = kS5FwdWarps * 32;
+    double2 vacc[kS5FwdRows];
+#pragma unroll
+    for (int i = 0; i < kS5FwdRows; ++i) vacc[i] = make_double2(0.0, 0.0);
+    float2 a[kS4P][kS5FwdRows];
+    auto load = [&](int b) {  // A does not depend on the fusion: fetched ahead of the flag
+#pragma unroll
+      for (int pp = 0; pp < kS4P; ++pp)
+#pragma unroll
+        for (int i = 0; i < kS5FwdRows; ++i) {
+          const int row = ft + FT * i;
+          a[pp][i] = row < ld ? __ldcg(jb.A + (int64_t)(b * kS4P + pp) * ld + row) : make_float2(0.f, 0.f);
+        }
+    };
+    if (t0 < t1) load(t0);
+    for (int b = t0; b < t1; ++b) {
+      const int par = (b - t0) & 1;
+      if (ft == 0)  // all Q sensors have published tile b
+        while (ld_acquire_u32(ctl.tile_cnt + b) < target) {
+        }
+      __syncwarp();
+      asm volatile("bar.sync 2, %0;" ::"n"(FT) : "memory");
+      if (ft < kS4P) {
+        // FusionCore::round for pixel j (admm.hpp:236-258), computed identically
+        // in every sensor's CTA from the previous round's x_G / sigma (never
+        // overwritten in this launch); sensor 0's CTA stores the new state.
+        const int j = b * kS4P + ft;
+        double2 sm = make_double2(0.0, 0.0);
+        for (int k = 0; k < Q; ++k) sm = c_add(sm, __ldcg(fa.contrib[k] + j));  // fixed sensor order
+        sm = make_double2(__ddiv_rn(sm.x, (double)Q), __ddiv_rn(sm.y, (double)Q));
+        const double2 xgp = fa.xg[j];
+        const double2 sg = fa.sigma[j];
+        const double2 vv = make_double2(__dadd_rn(sm.x, __ddiv_rn(sg.x, fa.beta)), __dadd_rn(sm.y, __ddiv_rn(sg.y, fa.beta)));
+        const double2 xg = soft_threshold1(vv, fa.kappa);
+        const double2 eta = c_sub(sm, xg);
+        const double2 dx = c_sub(xg, xgp);
+        const double2 sn = make_double2(__dadd_rn(sg.x, __dmul_rn(fa.beta, eta.x)), __dadd_rn(sg.y, __dmul_rn(fa.beta, eta.y)));
+        const double2 gp = c_sub(xg, sm);
+        if (q == 0) {
+          fa.sigma_pre[j] = sg;
+          fa.s[j] = sm;
+          ctl.xg_out[j] = xg;
+          ctl.sigma_out[j] = sn;
+          fa.gap[j] = gp;
+          double qv[5] = {c_norm2(eta), c_norm2(dx), c_norm2(sm), c_norm2(xg), c_norm2(sn)};
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {  // fixed pixel order: (p0 + p1) + (p2 + p3)
+            double a2 = qv[t] + __shfl_down_sync(0xFu, qv[t], 1);
+            a2 = a2 + __shfl_down_sync(0xFu, a2, 2);
+            if (ft == 0) ctl.tile_norms[(size_t)b * 5 + t] = a2;
+          }
+        }
+        // rhs_{k+1} = data + beta gap + beta x_hat - sigma (admm.hpp:114-119)
+        const double2 d = jb.data[j], xh = __ldcg(jb.x_hat + j);
+        double2 r;
+        r.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, gp.x)), __dmul_rn(beta, xh.x)), sn.x);
+        r.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, gp.y)), __dmul_rn(beta, xh.y)), sn.y);
+        jb.rhs[j] = r;
+        rhs4[par][ft] = r;
+      }
+      __syncwarp();
+      asm volatile("bar.sync 2, %0;" ::"n"(FT) : "memory");
+#pragma unroll
+      for (int pp = 0; pp < kS4P; ++pp) {
+        const double2 r = rhs4[par][pp];
+#pragma unroll
+        for (int i = 0; i < kS5FwdRows; ++i) {
+          vacc[i].x = fma((double)a[pp][i].x, r.x, fma(-(double)a[pp][i].y, r.y, vacc[i].x));
+          vacc[i].y = fma((double)a[pp][i].x, r.y, fma((double)a[pp][i].y, r.x, vacc[i].y));
+        }
+      }
+      if (b + 1 < t1) load(b + 1);  // in flight during the next flag wait
+      if (ft == 0) fwd_done = b;
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < kS5FwdRows; ++i) {
+      const int row = ft + FT * i;
+      if (row < ld) jb.part[(size_t)chunk * ld + row] = vacc[i];
+    }
+  }
+  // ---- grid-wide: stopping rule by the last CTA ------------------------------
+  __syncthreads();
+  __threadfence();
+  __shared__ bool lastcta;
+  if (tid == 0) lastcta = atomicAdd(ctl.done, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!lastcta) return;
+  __threadfence();
+  double acc[5] = {0, 0, 0, 0, 0};
+  const int per = (ntiles + kS5Threads - 1) / kS5Threads;
+  const int b0 = tid * per, b1 = min(ntiles, b0 + per);
+  for (int b = b0; b < b1; ++b)
+    for (int t = 0; t < 5; ++t) acc[t] += ((volatile const double*)ctl.tile_norms)[(size_t)b * 5 + t];
+  double* blocksum = reinterpret_cast<double*>(ring);
+  for (int t = 0; t < 5; ++t) blocksum[t * kS5Threads + tid] = acc[t];
+  __syncthreads();
+  if (tid == 0) {
+    FusionScalars f;
+    for (int t = 0; t < 5; ++t) {
+      double a = 0.0;
+      for (int i = 0; i < kS5Threads; ++i) a += blocksum[t * kS5Threads + i];
+      f.sq[t] = a;
+    }
+    f.pri_res = sqrt(f.sq[0]);
+    f.dual_res = fa.beta * sqrt(f.sq[1]);
+    f.eps_pri = fa.root_n_eps_abs + fa.eps_rel * fmax(sqrt(f.sq[2]), sqrt(f.sq[3]));
+    f.eps_dual = fa.root_n_eps_abs + fa.eps_rel * sqrt(f.sq[4]);
+    f.trigger = f.pri_res <= f.eps_pri;
+    f.converged = fa.has_prev && f.trigger && f.dual_res <= f.eps_dual;
+    if (fa.go_next) *fa.go_next = !((fa.stop_on_converge && f.converged) || (fa.screen_next_possible && f.trigger));
+    f.iteration = fa.iteration;
+    f.pad = 0;
+    *fa.out_dev = f;
+    if (fa.out_host) {
+      volatile FusionScalars* hp = fa.out_host;
+      hp->pri_res = f.pri_res; hp->dual_res = f.dual_res; hp->eps_pri = f.eps_pri; hp->eps_dual = f.eps_dual;
+      for (int t = 0; t < 5; ++t) hp->sq[t] = f.sq[t];
+      hp->trigger = f.trigger; hp->converged = f.converged;
+      __threadfence_system();
+      hp->iteration = f.iteration;
+    }
+    *ctl.done = 0u;
+  }
 }
 
 }  // namespace radmm_dev

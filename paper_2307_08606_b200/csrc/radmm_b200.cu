@@ -297,6 +297,11 @@ struct radmm_ctx {
   DArr<FrameRhsJob> fb_rhs;
   DArr<double2> fb_part;
   DArr<GramJob> gram_jobs;
+  // fused sweep v4 control (tile arrival counters / flags / norm partials)
+  DArr<unsigned> s4_cnt, s4_flag, s4_done;
+  DArr<double> s4_norms;
+  unsigned s4_seq = 0;
+  DArr<double2> xg_alt, sigma_alt;  // v5 writes the new x_G / sigma here, then they swap
 
   ~radmm_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -1370,7 +1375,15 @@ bool fused_enabled() { return fused_version() != 0; }
 
 bool sweep3_eligible(radmm_ctx* c);
 
+bool sweep4_eligible(radmm_ctx* c) {
+  if (c->N % kS4P != 0 || c->sm_count / c->Q < 1) return false;
+  for (const Sensor& S : c->sensors)
+    if (S.n_act != c->N || S.primal || S.ld != c->sensors[0].ld || S.ld > 2048) return false;
+  return true;
+}
+
 bool fused_eligible(radmm_ctx* c) {
+  if (fused_version() == 4 || fused_version() == 5) return c->world <= 1 && sweep4_eligible(c);
   if (!fused_enabled() || c->world > 1 || c->Q < 1 || c->Q > 8) return false;
   if (fused_version() == 3 && !sweep3_eligible(c)) return false;
   for (const Sensor& S : c->sensors)
@@ -1469,6 +1482,56 @@ bool sweep3_eligible(radmm_ctx* c) {
     if (S.ld % kS3R != 0 || S.ld / kS3R > kS3Threads || S.ld / kS3R < 64) return false;
   }
   return true;
+}
+
+void launch_sweep4(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa, const radmm_hyperparams* h) {
+  const int64_t ld = c->sensors[0].ld;
+  const int ntiles = c->N / kS4P;
+  int chunks = std::max(1, c->sm_count / c->Q);
+  for (const Sensor& S : c->sensors) chunks = std::min(chunks, S.part_chunks);
+  const int tpc = (ntiles + chunks - 1) / chunks;
+  chunks = (ntiles + tpc - 1) / tpc;
+  if (c->s4_cnt.n < (size_t)ntiles) {
+    c->s4_cnt.alloc(ntiles);
+    c->s4_flag.alloc(ntiles);
+    c->s4_norms.alloc((size_t)5 * ntiles, false);
+  }
+  if (c->s4_done.n < 1) c->s4_done.alloc(1);
+  Pack<Sweep4Job> pk;
+  for (int q = 0; q < c->Q; ++q) {
+    const SweepJob& j = sp.j[q];
+    pk.j[q] = Sweep4Job{j.A, j.w, j.data, j.rhs, j.x_hat, j.x_full, j.ring_slot, j.part};
+  }
+  const bool v5 = fused_version() == 5;
+  if (v5 && c->xg_alt.n < (size_t)c->N) {
+    c->xg_alt.alloc(c->N);
+    c->sigma_alt.alloc(c->N);
+  }
+  Sweep4Ctl ctl{c->s4_cnt.p, c->s4_flag.p, c->s4_norms.p, c->s4_done.p, ++c->s4_seq, tpc,
+                v5 ? c->xg_alt.p : nullptr, v5 ? c->sigma_alt.p : nullptr};
+  const size_t smem = (size_t)ld * sizeof(double2) + (size_t)kS4Slots * kS4P * ld * sizeof(float2) +
+                      kS4Slots * sizeof(uint64_t);
+  CK(cudaFuncSetAttribute(fused_sweep4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  double mu = h->mu, beta = h->beta;
+  int64_t ldv = ld;
+  void* args[] = {(void*)&pk, (void*)&fa, (void*)&ctl, (void*)&mu, (void*)&beta, (void*)&ldv};
+  if (env_int("RADMM_DEBUG", 0))
+    std::fprintf(stderr, "[radmm] sweep4: chunks=%d tiles/chunk=%d grid=%dx%d smem=%zu\n", chunks, tpc, chunks,
+                 c->Q, smem);
+  if (fused_version() == 5) {
+    const size_t smem5 = (size_t)ld * sizeof(double2) + (size_t)kS5Slots * kS4P * ld * sizeof(float2) +
+                         2 * kS5Slots * sizeof(uint64_t);
+    CK(cudaFuncSetAttribute(fused_sweep5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    CK(cudaLaunchCooperativeKernel((void*)fused_sweep5_kernel, dim3((unsigned)chunks, (unsigned)c->Q),
+                                   dim3(kS5Threads), args, smem5, c->stream));
+    std::swap(c->xg, c->xg_alt);  // the round's new x_G / sigma
+    std::swap(c->sigma, c->sigma_alt);
+  } else {
+    CK(cudaLaunchCooperativeKernel((void*)fused_sweep4_kernel, dim3((unsigned)chunks, (unsigned)c->Q),
+                                   dim3(kS4Threads), args, smem, c->stream));
+  }
+  ++c->launches;
+  c->sweep_clusters = chunks;
 }
 
 void launch_sweep3(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa, const radmm_hyperparams* h) {
@@ -1593,7 +1656,9 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     PhaseScope ps(c, RADMM_PHASE_SWEEP, a_bytes + 16.0 * c->N * (c->Q + 7));
     const size_t smem = (size_t)ld_max * sizeof(double2) + kSweepTile * (sizeof(double2) + sizeof(int));
     const FusionArgs fa = fusion_args(c, h, k);
-    if (fused_version() == 3) {
+    if (fused_version() == 4 || fused_version() == 5) {
+      launch_sweep4(c, sp, fa, h);
+    } else if (fused_version() == 3) {
       launch_sweep3(c, sp, fa, h);
     } else if (fused_version() == 2) {
       if (ld_max <= 256) launch_sweep2<1>(c, sp, fa, h, ld_max);

@@ -415,7 +415,7 @@ def test_apply_and_adjoint_match_host():
     s.close()
 
 
-@pytest.mark.parametrize("fused", ["1", "2", "3"])
+@pytest.mark.parametrize("fused", ["1", "2", "3", "4", "5"])
 def test_fused_sweeps_match_oracle(fused, monkeypatch):
     """The experimental single-kernel sweeps (RADMM_FUSED=1|2|3) reproduce the
     oracle, including elimination (masks) -- on a shape every variant accepts
