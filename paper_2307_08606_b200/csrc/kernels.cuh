@@ -1043,11 +1043,14 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;  // warp block origin in the tile
   const int fr = lane >> 2, fc = lane & 3;                // fragment row / k
-  double cr[4][4][2], ci[4][4][2];
+  // 3M complex products: Re = P1 - P2, Im = P3 - P1 - P2 (see frame_batch2_kernel)
+  double p1[4][4][2], p2[4][4][2], p3[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
   const MatRef A = jb.a, B = jb.b;
   double2 pa[LA], pb[LB];
   auto a_pos = [&](int e, int& ii, int& kk) {
@@ -1099,26 +1102,26 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
     if (t + 1 < nk) fetch((t + 1) * kGK);
 #pragma unroll
     for (int k4 = 0; k4 < kGK; k4 += 4) {
-      double ar[4], ai[4], nai[4], br[4], bi[4];
+      double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         ar[a] = As(cur, 0, k4 + fc)[wm + 8 * a + fr];
         ai[a] = As(cur, 1, k4 + fc)[wm + 8 * a + fr];
-        nai[a] = -ai[a];
+        as[a] = ar[a] + ai[a];
       }
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         br[b] = Bs(cur, 0, k4 + fc)[wn + 8 * b + fr];
         bi[b] = Bs(cur, 1, k4 + fc)[wn + 8 * b + fr];
+        bs[b] = br[b] + bi[b];
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          dmma884(cr[a][b], ar[a], br[b]);
-          dmma884(cr[a][b], nai[a], bi[b]);
-          dmma884(ci[a][b], ar[a], bi[b]);
-          dmma884(ci[a][b], ai[a], br[b]);
+          dmma884(p1[a][b], ar[a], br[b]);
+          dmma884(p2[a][b], ai[a], bi[b]);
+          dmma884(p3[a][b], as[a], bs[b]);
         }
     }
     if (t + 1 < nk) stash(cur ^ 1);
@@ -1133,7 +1136,7 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
         const int i = m0 + wm + 8 * a + fr, j = n0 + wn + 8 * b + 2 * fc + v;
         if (i >= jb.m || j >= jb.n) continue;
         double2* cp = jb.c + i + (int64_t)j * jb.ldc;
-        const double accr = cr[a][b][v], acci = ci[a][b][v];
+        const double accr = p1[a][b][v] - p2[a][b][v], acci = p3[a][b][v] - p1[a][b][v] - p2[a][b][v];
         if (EPI == GEPI_PLAIN) {
           if (jb.herm && i < j) continue;
           double2 o = make_double2(jb.alpha * accr, jb.alpha * acci);
@@ -2881,11 +2884,15 @@ __global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __rest
       cp_async16(b + kk * kGrPB + jj, ok ? A + gj + (int64_t)jbn[u] * lda : A, ok);
     }
   };
-  double cr[4][4][2], ci[4][4][2];
+  // 3M complex products (see frame_batch2_kernel): P1 = sum ar br, P2 = sum ai bi,
+  // P3 = sum (ar + ai)(br + bi); Re = P1 - P2, Im = P3 - P1 - P2
+  double p1[4][4][2], p2[4][4][2], p3[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
 #pragma unroll
   for (int s0 = 0; s0 < S - 1; ++s0) {
     if (s0 < nk) {
@@ -2907,25 +2914,25 @@ __global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __rest
     const float2* b = a + BK * kGrPA;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
-      double ar[4], ai[4], nai[4], br[4], bi[4];
+      double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float2 x = a[(k4 + fc) * kGrPA + wm + 8 * q + fr];
         ar[q] = (double)x.x;
         ai[q] = (double)x.y;
-        nai[q] = -ai[q];
+        as[q] = ar[q] + ai[q];
         const float2 y = b[(k4 + fc) * kGrPB + wn + 8 * q + fr];  // B = conj(A(j, k))
         br[q] = (double)y.x;
         bi[q] = -(double)y.y;
+        bs[q] = br[q] + bi[q];
       }
 #pragma unroll
       for (int qa = 0; qa < 4; ++qa)
 #pragma unroll
         for (int qb = 0; qb < 4; ++qb) {
-          dmma884(cr[qa][qb], ar[qa], br[qb]);
-          dmma884(cr[qa][qb], nai[qa], bi[qb]);
-          dmma884(ci[qa][qb], ar[qa], bi[qb]);
-          dmma884(ci[qa][qb], ai[qa], br[qb]);
+          dmma884(p1[qa][qb], ar[qa], br[qb]);
+          dmma884(p2[qa][qb], ai[qa], bi[qb]);
+          dmma884(p3[qa][qb], as[qa], bs[qb]);
         }
     }
   }
@@ -2938,7 +2945,9 @@ __global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __rest
       for (int v = 0; v < 2; ++v) {
         const int i = m0 + wm + 8 * qa + fr, j = n0 + wn + 8 * qb + 2 * fc + v;
         if (i >= m || j >= m || i < j) continue;
-        double2 o = make_double2(mu * cr[qa][qb][v], mu * ci[qa][qb][v]);
+        const double cre = p1[qa][qb][v] - p2[qa][qb][v];
+        const double cim = p3[qa][qb][v] - p1[qa][qb][v] - p2[qa][qb][v];
+        double2 o = make_double2(mu * cre, mu * cim);
         if (i == j) {
           o.x += beta;
           o.y = 0.0;  // exact real diagonal of a Hermitian matrix
