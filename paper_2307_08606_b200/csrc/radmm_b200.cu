@@ -276,6 +276,12 @@ struct radmm_ctx {
   std::vector<int64_t> herm_sig;     // (batch position, order) the items were built for
   int herm_n_items = 0;
   bool defer_fail_check = false;     // downdates: pivot check folded into the iteration sync
+  int pending_fail = 0;              // deferred pivot flags waiting in h_flags
+  // removal log kept on the device during a run (one D2H at the end)
+  DArr<int> dlog;
+  struct LogSeg { int k, q, count; int64_t off; };
+  std::vector<LogSeg> log_segs;
+  int64_t log_used = 0;
   std::vector<int64_t> iter_launches;
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -787,10 +793,22 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     gemm<GEPI_GJ>(c, ujobs);
   }
   CK(cudaMemcpyAsync(c->h_flags, c->fail_flags.p, sizeof(int) * T, cudaMemcpyDeviceToHost, c->stream));
+  sc.off = base_off;
+  if (c->defer_fail_check) {  // checked after the iteration's own sync (check_deferred)
+    c->pending_fail = (int)T;
+    return;
+  }
   CK(cudaStreamSynchronize(c->stream));
   for (size_t i = 0; i < T; ++i)
     if (c->h_flags[i]) fail(RADMM_NUMERICAL, std::string(what) + ": Cholesky failed");
-  sc.off = base_off;
+}
+
+// Deferred pivot check of the last downdate (the stream has been synchronised).
+void check_deferred(radmm_ctx* c) {
+  const int t = c->pending_fail;
+  c->pending_fail = 0;
+  for (int i = 0; i < t; ++i)
+    if (c->h_flags[i]) fail(RADMM_NUMERICAL, "factorize: Cholesky failed");
 }
 
 // ---------------------------------------------------------------------------
@@ -929,7 +947,7 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       // P = G R: few columns -> r Hermitian matvecs G a_t through the streaming
       // column-dot kernel (G read once per removed column, all sensors batched);
       // many columns -> tiled GEMM
-      if (r <= kDowndateMatvecMax) {
+      if (r <= env_int("RADMM_DD_MATVEC", kDowndateMatvecMax)) {
         double2* Rb = c->scratch.take<double2>((size_t)S.ld * r);
         LAUNCH(c, gather_cols_c128_kernel, dim3((unsigned)((S.ld * r + 255) / 256)), 256, 0, S.A.p, S.ld,
                S.rem_pix.p, r, Rb);
@@ -950,9 +968,12 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       inv.push_back({Sm[t], ldr, r});
       // T = P Sinv
       st3.push_back(gjob(m, r, r, mref(Pm[t], S.ld, false), mref(Sm[t], ldr, false), Tm[t], S.ld, 1.0, 0.0));
-      // G += mu T P^H
+      // G += mu T P^H: a Hermitian rank-r update, applied to the lower tiles
+      // with an exact conjugate mirror -- G stays exactly Hermitian (no
+      // projection pass needed after a downdate)
       st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
                          S.ldg, mu, 1.0));
+      st4.back().herm = 1;
     } else {
       const int nn = S.n_act;  // kept
       const int64_t ld_new = round_up(nn, 32);
@@ -988,10 +1009,11 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   for (const auto& jobs : p_by_col) coldot<double2, EPI_STORE>(c, jobs, mu, 1.0);
   gemm<GEPI_PLAIN>(c, st1);
   gemm<GEPI_PLAIN>(c, st2);
+  c->defer_fail_check = true;  // the r x r pivots are checked after the iteration's sync
   gj_invert(c, inv, "factorize");
+  c->defer_fail_check = false;
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
-  symmetrize(c, qs);
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     if (S.primal) {
@@ -1082,6 +1104,17 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
     }
   }
   full_rebuild(c, fresh, h->mu, h->beta);
+  // size the event-path scratch once (a 64-column downdate on every sensor)
+  // so elimination rounds never stop to grow it
+  {
+    size_t need = 0;
+    for (const Sensor& S : c->sensors) {
+      const size_t dimr = 64, n64 = (size_t)round_up(std::max<int64_t>(S.n_act, S.rows), 64);
+      need += (3 * (size_t)S.ld * dimr + dimr * dimr + n64 * dimr) * sizeof(double2);
+      need += (64 * 64 + 2 * dimr * 64) * sizeof(double2) + 4096;
+    }
+    c->scratch.reserve(need);
+  }
   // keep a copy for the next run when memory allows (always leave >= 4 GB free)
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1292,7 +1325,6 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   CK(cudaStreamSynchronize(c->stream));
   uint64_t notice = 0;
   std::vector<int> changed;
-  std::vector<int> pix;
   for (int q = 0; q < c->Q; ++q) {
     Sensor& S = c->sensors[q];
     const int kept = c->h_totals[q];
@@ -1310,13 +1342,20 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     S.n_act = kept;
     changed.push_back(q);
     notice += notice_size((size_t)removed);
-    pix.resize(removed);
-    CK(cudaMemcpy(pix.data(), S.rem_pix.p, sizeof(int) * removed, cudaMemcpyDeviceToHost));
-    for (int p : pix) {
-      c->removal_log.push_back(k);
-      c->removal_log.push_back(c->q_begin + q);
-      c->removal_log.push_back(p);
+    // the removed pixel list stays on the device until the run ends
+    if (c->dlog.n < (size_t)(c->log_used + removed)) {
+      const size_t cap = std::max<size_t>((size_t)c->Q * c->N, (size_t)(c->log_used + removed));
+      DArr<int> grown;
+      grown.alloc(cap, false);
+      if (c->log_used)
+        CK(cudaMemcpyAsync(grown.p, c->dlog.p, sizeof(int) * c->log_used, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      c->dlog = std::move(grown);
     }
+    CK(cudaMemcpyAsync(c->dlog.p + c->log_used, S.rem_pix.p, sizeof(int) * removed, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    c->log_segs.push_back({k, c->q_begin + q, removed, c->log_used});
+    c->log_used += removed;
   }
   if (changed.empty()) return notice;
   // rebuild() (admm.hpp:171-179): frozen echo, data term, factor
@@ -1742,6 +1781,24 @@ void record_round(radmm_ctx* c, int k, const FusionScalars& f, uint64_t notice, 
   sm.screening_stalled = stalled_any ? 1 : 0;
 }
 
+// Removal log: one D2H of the device log at the end of a run, expanded into
+// (iteration, sensor, pixel) triples.
+void finish_removal_log(radmm_ctx* c) {
+  if (c->log_used) {
+    std::vector<int> pix((size_t)c->log_used);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(pix.data(), c->dlog.p, sizeof(int) * pix.size(), cudaMemcpyDeviceToHost));
+    for (const auto& sg : c->log_segs)
+      for (int i = 0; i < sg.count; ++i) {
+        c->removal_log.push_back(sg.k);
+        c->removal_log.push_back(sg.q);
+        c->removal_log.push_back(pix[(size_t)sg.off + i]);
+      }
+  }
+  c->log_segs.clear();
+  c->log_used = 0;
+}
+
 void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o, radmm_run_summary* out) {
   validate_hyper(h);
   set_device(c);
@@ -1751,6 +1808,9 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   c->records.clear();
   c->active_log.clear();
   c->removal_log.clear();
+  c->log_segs.clear();
+  c->log_used = 0;
+  c->pending_fail = 0;
   c->have_result = false;
   c->launches = 0;
   c->rebuilds = c->downdates = 0;
@@ -1845,6 +1905,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       issue(k + 1, c->go_flags.p + ((k + 1) & 1), 0);
     }
     CK(cudaEventSynchronize(END(k)));
+    check_deferred(c);             // pivots of a downdate issued before iteration k
     if (k >= 2) step_time(k - 1);  // STEP(k-1) precedes iteration k's kernels: complete
     c->iter_launches.push_back(l_end - l0);
     flush_marks(c);
@@ -1879,6 +1940,8 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   if (fixed) sm.converged = f.converged;
   CK(cudaEventRecord(STEP(sm.iterations), c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  check_deferred(c);
+  finish_removal_log(c);
   if (sm.iterations >= 1) step_time(sm.iterations);
   const auto t2 = std::chrono::steady_clock::now();
   sm.solve_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -2126,6 +2189,9 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
     c->records.clear();
     c->active_log.clear();
     c->removal_log.clear();
+    c->log_segs.clear();
+    c->log_used = 0;
+    c->pending_fail = 0;
     c->have_result = false;
     c->launches = 0;
     c->rebuilds = c->downdates = 0;
@@ -2198,6 +2264,7 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
       for (size_t i = 0; i < nb; ++i) ++ch[live[b0 + i]]->launches;
     }
     CK(cudaStreamSynchronize(p->stream));
+    for (int f : live) check_deferred(ch[f]);
     flush_marks(p);  // batched-pass phase events (profiling mode) live on the parent
     const auto now = std::chrono::steady_clock::now();
     for (int f : live) {
@@ -2215,6 +2282,7 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
   }
   for (int f = 0; f < F; ++f) {
     radmm_ctx* c = ch[f];
+    finish_removal_log(c);
     if (fixed) sm[f].converged = last[f].converged;
     sm[f].setup_ms = setup_ms;
     sm[f].kernel_launches = c->launches;
