@@ -522,7 +522,7 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
       continue;
     }
     const int cpw = coldot_cpw() ? coldot_cpw() : kDefaultCpw;
-    if (smem > kColdotBigSmem) {  // one CTA per SM: go wide
+    if (smem > (size_t)env_int("RADMM_COLDOT_WIDE_BYTES", (int)kColdotBigSmem)) {  // one CTA per SM: go wide
       coldot_launch<T, EPI, true, 2, 1024>(c, pk, nb, n_max, smem, mu, beta, go);
       continue;
     }
