@@ -1,0 +1,872 @@
+// kernels_batched.cuh: Hermitian G-apply and projection, back-projection, frame-batched DMMA contractions, tensor-core Gram
+// Part of kernels.cuh (see that file's header); included in order from there.
+#pragma once
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// Hermitian G-apply  w = G v  reading only the lower block triangle of G.
+//
+// G (dual capacitance inverse, complex128, column-major, ld) is split into
+// 64 x 64 tiles; a work item is a strip of up to kHermStrip tiles
+// (I0 .. I0+nt-1) of tile column J, I0 >= J.  Column j of the strip feeds
+//   dot part: w[j] += sum_i conj(G[i, j]) v[i]   (i in the strip, incl. the
+//             diagonal tile: G[j, i] = conj(G[i, j]))
+//   ax part:  w[i] += sum_j G[i, j] v[j]         (tiles strictly below the
+//             diagonal: their upper mirror is never read)
+// Each item writes one dot partial (64 values, slot (J, g)) and one ax
+// partial per off-diagonal tile (slot tri(I, J)); herm_reduce_kernel sums
+// them in a fixed order, so the result is deterministic.  HBM bytes per
+// apply: ~(n^2/2 + 32 n) * 16 instead of n^2 * 16.
+// ---------------------------------------------------------------------------
+constexpr int kHermTile = 64;
+constexpr int kHermStrip = 4;
+
+struct HermJob {
+  const double2* G;
+  int64_t ld;
+  int n;             // matrix order (rows of the sensor)
+  int nb;            // tiles per side
+  int groups;        // strip groups per tile column: ceil(nb / kHermStrip)
+  const double2* v;
+  double2* w;
+  double2* dotp;     // [nb][groups][64]
+  double2* axp;      // [nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J
+};
+
+// item word: q (16) | J (16) | I0 (16) | nt (16)
+__host__ __device__ inline uint64_t herm_item(int q, int J, int I0, int nt) {
+  return (uint64_t)q << 48 | (uint64_t)J << 32 | (uint64_t)I0 << 16 | (uint64_t)nt;
+}
+
+__global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                         const uint64_t* __restrict__ items,
+                                                         const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
+  const uint64_t it = items[blockIdx.x];
+  const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+  const HermJob& jb = P.j[q];
+  __shared__ double2 vJ[kHermTile];
+  __shared__ double2 vI[kHermStrip * kHermTile];
+  __shared__ double2 sax[2][8][kHermTile];  // double-buffered: one barrier per tile
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = jb.n;
+  if (tid < kHermTile) {
+    const int j = J * kHermTile + tid;
+    vJ[tid] = j < n ? jb.v[j] : make_double2(0.0, 0.0);
+  }
+  for (int t = tid; t < nt * kHermTile; t += 256) {
+    const int i = I0 * kHermTile + t;
+    vI[t] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
+  }
+  const int c0 = warp * 8;  // this warp's 8 columns of the tile column
+  const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
+  double2 g[8][2];
+  auto load_tile = [&](int I) {
+    const int ib = I * kHermTile;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ib + lane + 32 * h, j = J * kHermTile + c0 + k;
+        g[k][h] = (i < n && j < n) ? __ldg(Gc + (int64_t)k * jb.ld + i) : make_double2(0.0, 0.0);
+      }
+  };
+  load_tile(I0);
+  __syncthreads();
+  double dr[8], di[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+  int par = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int I = I0 + t;
+    double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double2 vi = vI[t * kHermTile + lane + 32 * h];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        // conj(g) * v_i
+        dr[k] = fma(g[k][h].x, vi.x, dr[k]);
+        dr[k] = fma(g[k][h].y, vi.y, dr[k]);
+        di[k] = fma(g[k][h].x, vi.y, di[k]);
+        di[k] = fma(-g[k][h].y, vi.x, di[k]);
+        // g * v_j
+        const double2 vj = vJ[c0 + k];
+        ar[h] = fma(g[k][h].x, vj.x, ar[h]);
+        ar[h] = fma(-g[k][h].y, vj.y, ar[h]);
+        ai[h] = fma(g[k][h].x, vj.y, ai[h]);
+        ai[h] = fma(g[k][h].y, vj.x, ai[h]);
+      }
+    }
+    if (t + 1 < nt) load_tile(I + 1);  // in flight across the reduction below
+    if (I != J) {  // strictly-lower tile: its mirror contributes to rows of block I
+#pragma unroll
+      for (int h = 0; h < 2; ++h) sax[par][warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+      __syncthreads();
+      if (tid < kHermTile) {
+        double2 sum = sax[par][0][tid];
+#pragma unroll
+        for (int w8 = 1; w8 < 8; ++w8) {
+          sum.x += sax[par][w8][tid].x;
+          sum.y += sax[par][w8][tid].y;
+        }
+        jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = sum;
+      }
+      par ^= 1;  // the other buffer's readers are past this barrier
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    dr[k] = warp_sum(dr[k]);
+    di[k] = warp_sum(di[k]);
+  }
+  if (lane == 0) {
+    const int gi = (I0 - J) / kHermStrip;
+    double2* dp = jb.dotp + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
+  }
+}
+
+// w[b*64 + r] = sum_g dotp[b][g][r] + sum_{J < b} axp[tri(b, J)][r]  (fixed order)
+// 256 threads per row block: slice s = tid / 64 sums the partials k = s, s+4, ...
+// of the row's list (4 independent loads in flight), then the 4 slice sums are
+// added in slice order -- deterministic.
+__global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                         const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const HermJob& jb = P.j[blockIdx.y];
+  const int b = blockIdx.x, r = threadIdx.x & 63, sl = threadIdx.x >> 6;
+  __shared__ double2 part[4][kHermTile];
+  if (b >= jb.nb) return;
+  const int ng = (jb.nb - b + kHermStrip - 1) / kHermStrip;
+  const int total = ng + b;  // dot partials, then ax partials J = 0 .. b-1
+  const double2* dbase = jb.dotp + (int64_t)b * jb.groups * kHermTile + r;
+  const double2* abase = jb.axp + (int64_t)b * (b - 1) / 2 * kHermTile + r;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k0 = sl; k0 < total; k0 += 16) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 4 * u;
+      v[u] = k < total ? (k < ng ? dbase[(int64_t)k * kHermTile] : abase[(int64_t)(k - ng) * kHermTile])
+                       : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s.x += v[u].x;
+      s.y += v[u].y;
+    }
+  }
+  part[sl][r] = s;
+  __syncthreads();
+  if (sl == 0) {
+    const int row = b * kHermTile + r;
+    double2 t = part[0][r];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      t.x += part[u][r].x;
+      t.y += part[u][r].y;
+    }
+    if (row < jb.n) jb.w[row] = t;
+  }
+}
+
+// TMA-staged variant: persistent CTAs (one per SM) walk the item list
+// round-robin; warp 8 streams each 64 x 64 tile (64 column segments of
+// <= 1 KB) into a kHermStages-deep shared ring with cp.async.bulk, and the
+// eight compute warps consume it exactly like herm_gapply_kernel.
+constexpr int kHermStages = 3;
+constexpr int kHermTileBytes = kHermTile * kHermTile * 16;
+constexpr size_t kHermTmaSmem = (size_t)kHermStages * kHermTileBytes + 2 * 8 * kHermTile * 16 + 2 * kHermStages * 8;
+
+
+__global__ void __launch_bounds__(288, 1) herm_gapply_tma_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                                const uint64_t* __restrict__ items, int n_items,
+                                                                const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  extern __shared__ __align__(128) uint8_t hsm[];
+  double2* ring = reinterpret_cast<double2*>(hsm);
+  double2(*sax)[8][kHermTile] = reinterpret_cast<double2(*)[8][kHermTile]>(hsm + (size_t)kHermStages * kHermTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hsm + (size_t)kHermStages * kHermTileBytes + 2 * 8 * kHermTile * 16);
+  uint64_t* empty = full + kHermStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kHermStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    // producer: the same tile sequence the consumers walk
+    int slot = 0;
+    unsigned phase = 0;
+    int seq = 0;
+    for (int it_i = blockIdx.x; it_i < n_items; it_i += gridDim.x) {
+      const uint64_t it = items[it_i];
+      const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF),
+                nt = (int)(it & 0xFFFF);
+      const HermJob& jb = P.j[q];
+      const int cols = min(kHermTile, jb.n - J * kHermTile);
+      for (int t = 0; t < nt; ++t, ++seq) {
+        const int I = I0 + t;
+        const int rows = min(kHermTile, jb.n - I * kHermTile);
+        if (seq >= kHermStages) mbar_wait_cta_acq(&empty[slot], phase ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(cols * rows * 16));
+        __syncwarp();
+        double2* dst = ring + (size_t)slot * kHermTile * kHermTile;
+        const double2* src = jb.G + (int64_t)(J * kHermTile) * jb.ld + I * kHermTile;
+        for (int c = lane; c < cols; c += 32)
+          tma_bulk_g2s(dst + c * kHermTile, src + (int64_t)c * jb.ld, (unsigned)(rows * 16), &full[slot]);
+        if (++slot == kHermStages) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  // consumers (warps 0..7)
+  int slot = 0;
+  unsigned phase = 0;
+  int par = 0;
+  const int c0 = warp * 8;
+  for (int it_i = blockIdx.x; it_i < n_items; it_i += gridDim.x) {
+    const uint64_t it = items[it_i];
+    const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+    const HermJob& jb = P.j[q];
+    const int n = jb.n;
+    double2 vj[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = J * kHermTile + c0 + k;
+      vj[k] = j < n ? jb.v[j] : make_double2(0.0, 0.0);
+    }
+    double dr[8], di[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const int I = I0 + t;
+      const int ib = I * kHermTile;
+      double2 vi[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ib + lane + 32 * h;
+        vi[h] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
+      }
+      mbar_wait_cta_acq(&full[slot], phase);
+      const double2* tile = ring + (size_t)slot * kHermTile * kHermTile;
+      double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = J * kHermTile + c0 + k;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = ib + lane + 32 * h;
+          const double2 g = (i < n && j < n) ? tile[(c0 + k) * kHermTile + lane + 32 * h] : make_double2(0.0, 0.0);
+          dr[k] = fma(g.x, vi[h].x, dr[k]);
+          dr[k] = fma(g.y, vi[h].y, dr[k]);
+          di[k] = fma(g.x, vi[h].y, di[k]);
+          di[k] = fma(-g.y, vi[h].x, di[k]);
+          ar[h] = fma(g.x, vj[k].x, ar[h]);
+          ar[h] = fma(-g.y, vj[k].y, ar[h]);
+          ai[h] = fma(g.x, vj[k].y, ai[h]);
+          ai[h] = fma(g.y, vj[k].x, ai[h]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[slot]);
+      if (++slot == kHermStages) {
+        slot = 0;
+        phase ^= 1;
+      }
+      if (I != J) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sax[par][warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (tid < kHermTile) {
+          double2 s = sax[par][0][tid];
+#pragma unroll
+          for (int w8 = 1; w8 < 8; ++w8) {
+            s.x += sax[par][w8][tid].x;
+            s.y += sax[par][w8][tid].y;
+          }
+          jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = s;
+        }
+        par ^= 1;  // the other buffer is free: its readers passed this barrier
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dr[k] = warp_sum(dr[k]);
+      di[k] = warp_sum(di[k]);
+    }
+    if (lane == 0) {
+      const int g = (I0 - J) / kHermStrip;
+      double2* dp = jb.dotp + ((int64_t)J * jb.groups + g) * kHermTile + c0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
+    }
+  }
+}
+
+// Hermitian projection of a factor in place: G <- (G + G^H) / 2 (the nearest
+// Hermitian matrix; never increases the Frobenius error of an inverse).
+// One 32 x 32 tile pair (I > J) or diagonal tile per CTA, staged through
+// shared memory so both halves are read and written coalesced.
+__global__ void __launch_bounds__(256) herm_symmetrize_kernel(double2* __restrict__ G, int64_t ld, int n) {
+  __shared__ double2 a[32][33], b[32][33];
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;          // tile (I, J): column j, row i
+    a[r][tx] = (i < n && j < n) ? G[i + (int64_t)j * ld] : make_double2(0.0, 0.0);
+    const int i2 = J * 32 + tx, j2 = I * 32 + r;        // tile (J, I)
+    b[r][tx] = (i2 < n && j2 < n) ? G[i2 + (int64_t)j2 * ld] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 m[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = ty + 8 * u;
+    // element (row I*32+tx, col J*32+r) pairs with (row J*32+r, col I*32+tx) = b[tx][r]
+    const double2 x = a[r][tx], y = b[tx][r];
+    m[u] = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+    if (I * 32 + tx == J * 32 + r) m[u].y = 0.0;
+  }
+  __syncthreads();  // everyone has read a and b
+#pragma unroll
+  for (int u = 0; u < 4; ++u) a[ty + 8 * u][tx] = m[u];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;  // tile (I, J), coalesced over tx
+    if (i < n && j < n) G[i + (int64_t)j * ld] = a[r][tx];
+    const int i2 = J * 32 + tx, j2 = I * 32 + r;  // tile (J, I) = conj transpose
+    const double2 v = a[tx][r];
+    if (I != J && i2 < n && j2 < n) G[i2 + (int64_t)j2 * ld] = make_double2(v.x, -v.y);
+  }
+}
+
+// Row-segmented adjoint (KM too large for one shared vector per CTA): the
+// segment kernels stored partial dots part[s * stride + i]; sum them in
+// segment order and apply the x-update epilogue (admm.hpp:114-122).
+struct XFinJob {
+  ColDotJob a;
+  const double2* part;
+  int nseg;
+  int64_t stride;
+};
+
+__global__ void __launch_bounds__(256) xdual_finish_kernel(const __grid_constant__ Pack<XFinJob> P, double mu,
+                                                          double beta, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const XFinJob& jb = P.j[blockIdx.y];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= jb.a.n_out) return;
+  double re = 0.0, im = 0.0;
+  for (int sg = 0; sg < jb.nseg; ++sg) {
+    const double2 v = jb.part[(int64_t)sg * jb.stride + i];
+    re += v.x;
+    im += v.y;
+  }
+  coldot_epilogue<EPI_XDUAL>(jb.a, i, re, im, mu, beta);
+}
+
+// back_projection (forward_model.hpp:203-220): |sum_q A_q^H y_q| for every
+// pixel, summing the per-sensor adjoint images in global sensor order.
+__global__ void bp_sum_kernel(const double2* const* __restrict__ imgs, int Q, int N, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = 0; q < Q; ++q) acc = c_add(acc, imgs[q][j]);
+  out[j] = c_abs(acc);
+}
+
+// ---------------------------------------------------------------------------
+// Frame-batched contractions (BASELINE config 5).  F <= 16 frames that share
+// a sensor's operator and full active set turn the three per-iteration
+// matvecs into GEMMs with F right-hand sides, so A_q is streamed ONCE for all
+// frames and the work runs on the fp64 tensor cores (DMMA m8n8k4):
+//   FWD  V_f = A_q RHS_f        (M = rows,   K = pixels; split-K partials)
+//   GAP  W_f = G_q V_f          (M = rows,   K = rows;   split-K partials)
+//   ADJ  X_f = (RHS_f - mu A_q^H W_f) / beta, + history / scatter epilogue
+//        (M = pixels, K = rows)
+// CTA tile 128 x 16 (frames), BK = 8, 8 warps x (16 rows x 16 frames).
+// ---------------------------------------------------------------------------
+constexpr int kFB = 16;            // max frames per batch
+constexpr int kFbBM = 128, kFbPA = 132, kFbPB = 20;
+enum { FB_FWD = 0, FB_GAP = 1, FB_ADJ = 2 };
+
+struct FrameBatchJob {
+  const void* A;        // float2 operator (FWD/ADJ) or double2 factor (GAP)
+  int64_t lda;
+  int m, k;             // GEMM M and K
+  int nf;               // frames in this batch
+  const double2* B[kFB];  // per-frame right-hand side (length k)
+  double2* part;        // FWD/GAP: partials [split][kFB][ldp]
+  int64_t ldp;
+  // ADJ epilogue, per frame
+  const double2* rhs[kFB];
+  double2* x_hat[kFB];
+  double2* x_full[kFB];
+  double* ring[kFB];
+};
+
+constexpr int kFbBK = 16;  // K per shared stage (4 DMMA k-steps per barrier)
+constexpr size_t kFbSmem = (size_t)2 * 2 * kFbBK * (kFbPA + kFbPB) * sizeof(double);
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) frame_batch_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
+                                                            double mu, double beta) {
+  constexpr int BK = kFbBK, LA = kFbBM * BK / 256;
+  const FrameBatchJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.x * kFbBM;
+  if (m0 >= jb.m) return;
+  const int split = blockIdx.y;
+  const int nk_all = (jb.k + BK - 1) / BK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per, t1 = min(nk_all, t0 + per);
+  extern __shared__ double fsm[];
+  double(*As)[2][BK][kFbPA] = reinterpret_cast<double(*)[2][BK][kFbPA]>(fsm);
+  double(*Bs)[2][BK][kFbPB] = reinterpret_cast<double(*)[2][BK][kFbPB]>(fsm + 2 * 2 * BK * kFbPA);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp * 16, fr = lane >> 2, fc = lane & 3;
+  const int nb = jb.nf > 8 ? 2 : 1;  // 8-frame DMMA column blocks actually used
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+  double2 pa[LA], pb = make_double2(0.0, 0.0);
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (MODE == FB_ADJ) { kk = e & (BK - 1); ii = e / BK; } else { ii = e & (kFbBM - 1); kk = e / kFbBM; }
+  };
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      const int gi = m0 + ii, gk = kk0 + kk;
+      double2 v = make_double2(0.0, 0.0);
+      if (gi < jb.m && gk < jb.k) {
+        if (MODE == FB_GAP) {
+          v = reinterpret_cast<const double2*>(jb.A)[gi + (int64_t)gk * jb.lda];
+        } else if (MODE == FB_FWD) {
+          const float2 x = reinterpret_cast<const float2*>(jb.A)[gi + (int64_t)gk * jb.lda];
+          v = make_double2((double)x.x, (double)x.y);
+        } else {  // conj(A[gk, gi])
+          const float2 x = reinterpret_cast<const float2*>(jb.A)[gk + (int64_t)gi * jb.lda];
+          v = make_double2((double)x.x, -(double)x.y);
+        }
+      }
+      pa[t] = v;
+    }
+    {  // B: BK x 16 frames, one element per thread
+      const int kk = tid & (BK - 1), f = tid / BK, gk = kk0 + kk;
+      pb = (f < jb.nf && gk < jb.k) ? jb.B[f][gk] : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      As[buf][0][kk][ii] = pa[t].x;
+      As[buf][1][kk][ii] = pa[t].y;
+    }
+    const int kk = tid & (BK - 1), f = tid / BK;
+    Bs[buf][0][kk][f] = pb.x;
+    Bs[buf][1][kk][f] = pb.y;
+  };
+  if (t0 < t1) {
+    fetch(t0 * BK);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = t0; t < t1; ++t) {
+    const int cur = (t - t0) & 1;
+    if (t + 1 < t1) fetch((t + 1) * BK);  // a whole stage ahead of its use
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[2], ai[2], nai[2], br[2], bi[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        ar[a] = As[cur][0][k4 + fc][wm + 8 * a + fr];
+        ai[a] = As[cur][1][k4 + fc][wm + 8 * a + fr];
+        nai[a] = -ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        br[b] = Bs[cur][0][k4 + fc][8 * b + fr];
+        bi[b] = Bs[cur][1][k4 + fc][8 * b + fr];
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          if (b < nb) {
+            dmma884(cr[a][b], ar[a], br[b]);
+            dmma884(cr[a][b], nai[a], bi[b]);
+            dmma884(ci[a][b], ar[a], bi[b]);
+            dmma884(ci[a][b], ai[a], br[b]);
+          }
+        }
+    }
+    if (t + 1 < t1) stash(cur ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * a + fr, f = 8 * b + 2 * fc + v;
+        if (i >= jb.m || f >= jb.nf) continue;
+        if (MODE != FB_ADJ) {
+          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cr[a][b][v], ci[a][b][v]);
+        } else {
+          // x = (rhs - mu A^H w) / beta  (Woodbury form of solver_core.hpp:47-51), admm.hpp:120-123
+          const double2 r = jb.rhs[f][i];
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cr[a][b][v])), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, ci[a][b][v])), beta));
+          const double2 old = jb.x_full[f][i];
+          jb.ring[f][i] = c_abs(c_sub(xh, old));
+          jb.x_full[f][i] = xh;
+          jb.x_hat[f][i] = xh;
+        }
+      }
+}
+
+// Operator passes (FWD, ADJ) of the frame batch as a kFbStages-deep cp.async
+// pipeline: raw complex64 operator tiles and complex128 frame vectors go
+// global -> shared without registers (zero-filled outside the matrix), and
+// are converted to fp64 (conjugated for ADJ) when the DMMA fragments are
+// loaded.  FWD tiles are k-major ([kk][row], 128 contiguous complex64 per
+// kk); ADJ tiles are pixel-major ([pixel][kk], each pixel's 16 rows are one
+// 128-B run), so every 16-B chunk lands contiguously.  Pitches keep the
+// fragment loads of each half warp on distinct banks.
+constexpr int kFbStages = 4;
+constexpr int kFbPF = 132;  // FWD: float2 per kk row (128 + 4)
+constexpr int kFbPX = 20;   // ADJ: float2 per pixel row (16 + 4)
+constexpr int kFbPV = 20;   // frame vectors: double2 per frame row (16 + 4)
+constexpr size_t kFbStageA = (size_t)kFbBK * kFbPF * 8 > (size_t)kFbBM * kFbPX * 8 ? (size_t)kFbBK * kFbPF * 8
+                                                                                     : (size_t)kFbBM * kFbPX * 8;
+constexpr size_t kFbStageB = (size_t)kFB * kFbPV * 16;
+constexpr size_t kFb2Smem = kFbStages * (kFbStageA + kFbStageB) + kFB * 8;
+
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
+                                                             double mu, double beta) {
+  constexpr int BK = kFbBK, S = kFbStages;
+  const FrameBatchJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.x * kFbBM;
+  if (m0 >= jb.m) return;
+  const int split = blockIdx.y;
+  const int nk_all = (jb.k + BK - 1) / BK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per, t1 = min(nk_all, t0 + per);
+  const int nt = max(0, t1 - t0);
+  extern __shared__ __align__(16) uint8_t fsm2[];
+  uint8_t* sA = fsm2;
+  uint8_t* sB = fsm2 + S * kFbStageA;
+  const double2** Bp = reinterpret_cast<const double2**>(fsm2 + S * (kFbStageA + kFbStageB));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kFB) Bp[tid] = tid < jb.nf ? jb.B[tid] : nullptr;
+  __syncthreads();
+  const int wm = warp * 16, fr = lane >> 2, fc = lane & 3;
+  const int nb = jb.nf > 8 ? 2 : 1;
+  const int m = jb.m, kdim = jb.k, nf = jb.nf;
+  const int64_t lda = jb.lda;
+  const float2* A = reinterpret_cast<const float2*>(jb.A);
+  auto issue = [&](int t, int slot) {  // stage t (absolute) -> shared slot
+    const int k0 = t * BK;
+    float2* a = reinterpret_cast<float2*>(sA + slot * kFbStageA);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 1024 16-B chunks of A
+      const int c = tid + 256 * u;
+      if (MODE == FB_FWD) {  // chunk: rows 2*(c & 63) .. +1 of column kk = c >> 6
+        const int kk = c >> 6, ii = 2 * (c & 63);
+        const int gi = m0 + ii, gk = k0 + kk;
+        // rows [m, lda) are the operator's zeroed padding: readable, and zero
+        const bool ok = gi < lda && gk < kdim;
+        cp_async16(a + kk * kFbPF + ii, ok ? A + gi + (int64_t)gk * lda : A, ok);
+      } else {  // ADJ chunk: rows 2*(c & 7) .. +1 of pixel ii = c >> 3
+        const int ii = c >> 3, kk = 2 * (c & 7);
+        const int gi = m0 + ii, gk = k0 + kk;
+        const bool ok = gi < m && gk < kdim;
+        cp_async16(a + ii * kFbPX + kk, ok ? A + gk + (int64_t)gi * lda : A, ok);
+      }
+    }
+    {  // B: 16 frames x 16 k (double2), one chunk per thread
+      double2* b = reinterpret_cast<double2*>(sB + slot * kFbStageB);
+      const int f = tid >> 4, kk = tid & 15, gk = k0 + kk;
+      const bool ok = f < nf && gk < kdim;
+      cp_async16(b + f * kFbPV + kk, ok ? Bp[f] + gk : reinterpret_cast<const double2*>(A), ok);
+    }
+  };
+  // 3M (Karatsuba) complex products: P1 = sum Ar Br, P2 = sum Ai Bi,
+  // P3 = sum (Ar + Ai)(Br + Bi); Re = P1 - P2, Im = P3 - P1 - P2 (3 DMMAs per
+  // complex 8x8x4 block instead of 4)
+  double p1[2][2][2], p2[2][2][2], p3[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < S - 1; ++s0) {
+    if (s0 < nt) issue(t0 + s0, s0);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nt; ++t) {
+    cp_async_wait<S - 2>();
+    __syncthreads();  // stage t landed for everyone; slot (t-1) % S is free
+    if (t + S - 1 < nt) issue(t0 + t + S - 1, (t + S - 1) % S);
+    cp_async_commit();
+    const int slot = t % S;
+    const float2* a = reinterpret_cast<const float2*>(sA + slot * kFbStageA);
+    const double2* b = reinterpret_cast<const double2*>(sB + slot * kFbStageB);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[2], ai[2], as[2], br[2], bi[2], bs[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int row = wm + 8 * q + fr, kk = k4 + fc;
+        const float2 x = MODE == FB_FWD ? a[kk * kFbPF + row] : a[row * kFbPX + kk];
+        ar[q] = (double)x.x;
+        ai[q] = MODE == FB_FWD ? (double)x.y : -(double)x.y;
+        as[q] = ar[q] + ai[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double2 y = b[(8 * q + fr) * kFbPV + k4 + fc];
+        br[q] = y.x;
+        bi[q] = y.y;
+        bs[q] = y.x + y.y;
+      }
+#pragma unroll
+      for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < 2; ++qb)
+          if (qb < nb) {
+            dmma884(p1[qa][qb], ar[qa], br[qb]);
+            dmma884(p2[qa][qb], ai[qa], bi[qb]);
+            dmma884(p3[qa][qb], as[qa], bs[qb]);
+          }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < 2; ++qb)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * qa + fr, f = 8 * qb + 2 * fc + v;
+        if (i >= m || f >= nf) continue;
+        const double cre = p1[qa][qb][v] - p2[qa][qb][v];
+        const double cim = p3[qa][qb][v] - p1[qa][qb][v] - p2[qa][qb][v];
+        if (MODE == FB_FWD) {
+          jb.part[((int64_t)split * kFB + f) * jb.ldp + i] = make_double2(cre, cim);
+        } else {
+          const double2 r = jb.rhs[f][i];
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(r.x, __dmul_rn(mu, cre)), beta),
+                                          __ddiv_rn(__dsub_rn(r.y, __dmul_rn(mu, cim)), beta));
+          const double2 old = jb.x_full[f][i];
+          jb.ring[f][i] = c_abs(c_sub(xh, old));
+          jb.x_full[f][i] = xh;
+          jb.x_hat[f][i] = xh;
+        }
+      }
+}
+
+// Dual capacitance C = beta I + mu A_J A_J^H (the Woodbury system of
+// solver_core.hpp:39-40) on the fp64 tensor cores: 4-stage cp.async pipeline
+// of the complex64 columns A(:, J_k) (both operands come from the same
+// columns: rows i of the tile and rows j of its mirror), DMMA m8n8k4 f64.
+// Lower 128 x 64 tiles only; the upper triangle is written as the exact
+// conjugate mirror and the diagonal is exactly real, as the SIMT path does.
+// The active-column indices of stage t+S-1 are fetched into registers one
+// iteration ahead so the gathered addresses never stall the pipeline.
+struct GramJob {
+  const float2* A;
+  int64_t lda;
+  const int* J;  // active columns (n entries)
+  int n;         // K
+  int m;         // rows (matrix order)
+  double2* C;
+  int64_t ldc;
+};
+constexpr int kGrBM = 128, kGrBN = 64, kGrPA = 132, kGrPB = 68;
+constexpr size_t kGrStage = (size_t)kFbBK * (kGrPA + kGrPB) * 8;
+constexpr size_t kGramSmem = kFbStages * kGrStage;
+
+__global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __restrict__ jobs, double mu, double beta) {
+  constexpr int BK = kFbBK, S = kFbStages;
+  const GramJob& jb = jobs[blockIdx.z];
+  const int m0 = blockIdx.y * kGrBM, n0 = blockIdx.x * kGrBN;
+  const int m = jb.m;
+  if (m0 >= m || n0 >= m || m0 + kGrBM <= n0) return;  // outside, or strictly upper
+  extern __shared__ __align__(16) uint8_t gsm2[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32, fr = lane >> 2, fc = lane & 3;
+  const int64_t lda = jb.lda;
+  const float2* A = jb.A;
+  const int* J = jb.J;
+  const int nk = (jb.n + BK - 1) / BK;
+  // chunk c of the A tile: rows 2*(c & 63) of column kk = c >> 6 (4 per thread);
+  // B tile: rows 2*(c & 31) of column kk = c >> 5 (2 per thread)
+  int ja[4], jbn[2];
+  auto load_j = [&](int t) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int gk = t * BK + ((tid + 256 * u) >> 6);
+      ja[u] = gk < jb.n ? (J ? __ldg(J + gk) : gk) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int gk = t * BK + ((tid + 256 * u) >> 5);
+      jbn[u] = gk < jb.n ? (J ? __ldg(J + gk) : gk) : -1;
+    }
+  };
+  auto issue = [&](int slot) {
+    float2* a = reinterpret_cast<float2*>(gsm2 + slot * kGrStage);
+    float2* b = a + BK * kGrPA;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = tid + 256 * u, kk = c >> 6, ii = 2 * (c & 63);
+      const int gi = m0 + ii;
+      const bool ok = ja[u] >= 0 && gi < lda;
+      cp_async16(a + kk * kGrPA + ii, ok ? A + gi + (int64_t)ja[u] * lda : A, ok);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = tid + 256 * u, kk = c >> 5, jj = 2 * (c & 31);
+      const int gj = n0 + jj;
+      const bool ok = jbn[u] >= 0 && gj < lda;
+      cp_async16(b + kk * kGrPB + jj, ok ? A + gj + (int64_t)jbn[u] * lda : A, ok);
+    }
+  };
+  // 3M complex products (see frame_batch2_kernel): P1 = sum ar br, P2 = sum ai bi,
+  // P3 = sum (ar + ai)(br + bi); Re = P1 - P2, Im = P3 - P1 - P2
+  double p1[4][4][2], p2[4][4][2], p3[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < S - 1; ++s0) {
+    if (s0 < nk) {
+      load_j(s0);
+      issue(s0);
+    }
+    cp_async_commit();
+  }
+  if (S - 1 < nk) load_j(S - 1);
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (t + S - 1 < nk) {
+      issue((t + S - 1) % S);                   // indices fetched last iteration
+      if (t + S < nk) load_j(t + S);            // in flight during this stage's math
+    }
+    cp_async_commit();
+    const float2* a = reinterpret_cast<const float2*>(gsm2 + (t % S) * kGrStage);
+    const float2* b = a + BK * kGrPA;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 x = a[(k4 + fc) * kGrPA + wm + 8 * q + fr];
+        ar[q] = (double)x.x;
+        ai[q] = (double)x.y;
+        as[q] = ar[q] + ai[q];
+        const float2 y = b[(k4 + fc) * kGrPB + wn + 8 * q + fr];  // B = conj(A(j, k))
+        br[q] = (double)y.x;
+        bi[q] = -(double)y.y;
+        bs[q] = br[q] + bi[q];
+      }
+#pragma unroll
+      for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < 4; ++qb) {
+          dmma884(p1[qa][qb], ar[qa], br[qb]);
+          dmma884(p2[qa][qb], ai[qa], bi[qb]);
+          dmma884(p3[qa][qb], as[qa], bs[qb]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < 4; ++qb)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * qa + fr, j = n0 + wn + 8 * qb + 2 * fc + v;
+        if (i >= m || j >= m || i < j) continue;
+        const double cre = p1[qa][qb][v] - p2[qa][qb][v];
+        const double cim = p3[qa][qb][v] - p1[qa][qb][v] - p2[qa][qb][v];
+        double2 o = make_double2(mu * cre, mu * cim);
+        if (i == j) {
+          o.x += beta;
+          o.y = 0.0;  // exact real diagonal of a Hermitian matrix
+        }
+        jb.C[i + (int64_t)j * jb.ldc] = o;
+        if (i != j) jb.C[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+      }
+}
+
+// out_f[i] = sum_s part[s][f][i] (fixed split order) for every frame of a job
+struct FrameReduceJob {
+  const double2* part;
+  int64_t ldp;
+  int m, nf, nsplit;
+  double2* out[kFB];
+};
+
+__global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
+  const FrameReduceJob& jb = jobs[blockIdx.z];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, f = blockIdx.y;
+  if (i >= jb.m || f >= jb.nf) return;
+  double2 s = make_double2(0.0, 0.0);
+  for (int sp = 0; sp < jb.nsplit; ++sp) {
+    const double2 v = jb.part[((int64_t)sp * kFB + f) * jb.ldp + i];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  jb.out[f][i] = s;
+}
+
+// rhs_f[j] = data_f[j] + beta gap_f[j] + beta x_hat_f[j] - sigma_f[j] for the
+// full active set (admm.hpp:114-119), every (sensor, frame) of the batch.
+struct FrameRhsJob {
+  int n;
+  const double2* data;
+  const double2* x_hat;
+  const double2* gap;
+  const double2* sigma;
+  double2* rhs;
+};
+
+__global__ void frame_rhs_kernel(const FrameRhsJob* __restrict__ jobs, double beta) {
+  const FrameRhsJob& jb = jobs[blockIdx.y];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jb.n) return;
+  const double2 d = jb.data[j], g = jb.gap[j], x = jb.x_hat[j], sg = jb.sigma[j];
+  jb.rhs[j] = make_double2(__dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, x.x)), sg.x),
+                           __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, x.y)), sg.y));
+}
+
+}  // namespace radmm_dev

@@ -1,0 +1,675 @@
+// kernels_dense.cuh: fp64 complex GEMMs (SIMT and DMMA), Gauss-Jordan inverse, small utility kernels
+// Part of kernels.cuh (see that file's header); included in order from there.
+#pragma once
+
+namespace radmm_dev {
+
+// ---------------------------------------------------------------------------
+// fp64 complex GEMM, SIMT tiles (64 x 64 x 8, 256 threads, 4 x 4 per thread):
+//   C = alpha * op(A) op(B) + beta0 * C  (+ diag) with gathered operands.
+// op(M)(i, k): (r, c) = trans ? (k, i) : (i, k); r = ridx ? ridx[r] : r;
+// c = cidx ? cidx[c] : c; value M[r + c*ld] (complex64 promoted or
+// complex128), conjugated if conj.  Drives the factor builds and
+// downdates of LocalSolveCache (solver_core.hpp:34-45) and the
+// Gauss-Jordan inverse.
+// ---------------------------------------------------------------------------
+struct MatRef {
+  const void* p;
+  int64_t ld;
+  const int* ridx;
+  const int* cidx;
+  int c64;
+  int trans;
+  int conj;
+};
+
+enum { GEPI_PLAIN = 0, GEPI_GJ = 1, GEPI_SPLIT = 2 };
+
+struct GemmJob {
+  int m, n, k;
+  MatRef a, b;
+  double2* c;
+  int64_t ldc;
+  double alpha, beta0;
+  double diag_add;  // C[i,i] += diag_add
+  int k0, kb;       // GEPI_GJ: pivot block rows/cols [k0, k0+kb); b = R' (kb x n)
+  int herm;         // result is Hermitian: compute tiles with m0 >= n0, mirror conj
+};
+
+__device__ __forceinline__ double2 mat_load(const MatRef& m, int i, int k) {
+  int r = m.trans ? k : i;
+  int c = m.trans ? i : k;
+  if (m.ridx) r = m.ridx[r];
+  if (m.cidx) c = m.cidx[c];
+  double2 v;
+  if (m.c64) {
+    const float2 f = reinterpret_cast<const float2*>(m.p)[r + (int64_t)c * m.ld];
+    v = make_double2((double)f.x, (double)f.y);
+  } else {
+    v = reinterpret_cast<const double2*>(m.p)[r + (int64_t)c * m.ld];
+  }
+  if (m.conj) v.y = -v.y;
+  return v;
+}
+
+constexpr int kGB = 64, kGK = 8;
+constexpr int kGjSmem = (64 * 65 + 128) * 16;
+
+// GEPI_SPLIT: split-K for skinny products (the rank-r downdates, r << KM):
+// blockIdx.z = job * nsplit + split; each split accumulates its K range and
+// stores the raw partial tile to ws[split][m][n]; gemm_split_reduce applies
+// alpha / beta0 / diag in fixed split order.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
+                                                   double2* __restrict__ ws, int64_t ws_stride) {
+  const int split = blockIdx.z % nsplit;
+  const GemmJob& jb = jobs.j[blockIdx.z / nsplit];
+  const int m0 = blockIdx.y * kGB, n0 = blockIdx.x * kGB;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 < n0) return;  // upper tiles come from the mirror
+  __shared__ double2 As[2][kGK][kGB];
+  __shared__ double2 Bs[2][kGK][kGB];
+  const int tid = threadIdx.x;
+  // thread (tx, ty) owns rows m0 + tx + 16a and columns n0 + ty + 16b: a warp
+  // covers 16 consecutive rows of 2 columns, so the column-major epilogue
+  // (the rank-r updates are read-modify-write bound) is coalesced.
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc_r[4][4], acc_i[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc_r[a][b] = acc_i[a][b] = 0.0;
+
+  const MatRef A = jb.a, B = jb.b;
+  auto load_tile = [&](int buf, int kk0) {
+    // A tile: kGB (i) x kGK (k)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int e = tid + t * 256;
+      int ii, kk;
+      if (!A.trans) { ii = e & 63; kk = e >> 6; } else { kk = e & 7; ii = e >> 3; }
+      const int gi = m0 + ii, gk = kk0 + kk;
+      As[buf][kk][ii] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+    // B tile: kGK (k) x kGB (j)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int e = tid + t * 256;
+      int kk, jj;
+      if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e & 63; kk = e >> 6; }
+      const int gj = n0 + jj, gk = kk0 + kk;
+      Bs[buf][kk][jj] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+
+  const int nk_all = (jb.k + kGK - 1) / kGK;
+  const int per = (nk_all + nsplit - 1) / nsplit;
+  const int t0 = split * per;
+  const int nk = max(0, min(nk_all, t0 + per) - t0);
+  if (nk > 0) load_tile(0, t0 * kGK);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) load_tile(cur ^ 1, (t0 + t + 1) * kGK);
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[cur][kk][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[cur][kk][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          acc_r[a][b] = fma(av[a].x, bv[b].x, acc_r[a][b]);
+          acc_r[a][b] = fma(-av[a].y, bv[b].y, acc_r[a][b]);
+          acc_i[a][b] = fma(av[a].x, bv[b].y, acc_i[a][b]);
+          acc_i[a][b] = fma(av[a].y, bv[b].x, acc_i[a][b]);
+        }
+    }
+    __syncthreads();
+  }
+  // read the C tile first (all 16 loads in flight) when it is accumulated into
+  double2 cold[4][4];
+  if (EPI == GEPI_PLAIN && jb.beta0 != 0.0) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = m0 + tx + 16 * a, j = n0 + ty + 16 * b;
+        cold[a][b] = (i < jb.m && j < jb.n) ? jb.c[i + (int64_t)j * jb.ldc] : make_double2(0.0, 0.0);
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = m0 + tx + 16 * a;
+    if (i >= jb.m) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = n0 + ty + 16 * b;
+      if (j >= jb.n) continue;
+      double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+      if (EPI == GEPI_SPLIT) {
+        ws[(int64_t)blockIdx.z * ws_stride + (int64_t)j * jb.m + i] = make_double2(acc_r[a][b], acc_i[a][b]);
+      } else if (EPI == GEPI_PLAIN) {
+        double2 o = make_double2(jb.alpha * acc_r[a][b], jb.alpha * acc_i[a][b]);
+        if (jb.beta0 != 0.0) {
+          o.x += jb.beta0 * cold[a][b].x;
+          o.y += jb.beta0 * cold[a][b].y;
+        }
+        if (i == j) {
+          o.x += jb.diag_add;
+          if (jb.herm) o.y = 0.0;  // exact real diagonal of a Hermitian matrix
+        }
+        if (jb.herm && i < j) continue;  // written (bit-exactly) as the mirror of (j, i)
+        *cp = o;
+        if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+      } else {
+        // Gauss-Jordan sweep of pivot block K = [k0, k0+kb):
+        //   i in K:      M[i,j] = R'[i-k0, j]
+        //   i not in K:  M[i,j] = (j in K ? 0 : M[i,j]) - (F R')[i,j]
+        const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+        if (iK) {
+          *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+        } else {
+          const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+          const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+          *cp = make_double2(c0.x - acc_r[a][b], c0.y - acc_i[a][b]);
+        }
+      }
+    }
+  }
+}
+
+// Large products (Gram / capacitance builds, Gauss-Jordan rank-64 updates):
+// (16 TM) x (16 TN) tiles, TM x TN complex outputs per thread, the next K
+// slice prefetched into registers while the current one is multiplied, shared
+// rows padded by one element so transposed stores are conflict-free.  Every
+// output accumulates over k in the same order with the same FMA sequence as
+// gemm_kernel, so the two are bitwise identical.
+constexpr int kBigTM = 8, kBigTN = 4;
+constexpr int kBigBM = 16 * kBigTM, kBigBN = 16 * kBigTN;
+constexpr size_t kGemmBigSmem = (size_t)2 * kGK * ((kBigBM + 1) + (kBigBN + 1)) * sizeof(double2);
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_big_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  constexpr int TM = kBigTM, TN = kBigTN, BM = kBigBM, BN = kBigBN;
+  constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;  // prefetched elements per thread
+  const GemmJob& jb = jobs.j[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 + BM <= n0) return;  // strictly-upper tiles come from the mirror
+  extern __shared__ double2 gsm[];
+  double2(*As)[kGK][BM + 1] = reinterpret_cast<double2(*)[kGK][BM + 1]>(gsm);
+  double2(*Bs)[kGK][BN + 1] = reinterpret_cast<double2(*)[kGK][BN + 1]>(gsm + 2 * kGK * (BM + 1));
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc_r[TM][TN], acc_i[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc_r[a][b] = acc_i[a][b] = 0.0;
+  const MatRef A = jb.a, B = jb.b;
+  double2 pa[LA], pb[LB];
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (!A.trans) { ii = e % BM; kk = e / BM; } else { kk = e & 7; ii = e >> 3; }
+  };
+  auto b_pos = [&](int e, int& jj, int& kk) {
+    if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e % BN; kk = e / BN; }
+  };
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      const int gi = m0 + ii, gk = kk0 + kk;
+      pa[t] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      const int gj = n0 + jj, gk = kk0 + kk;
+      pb[t] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      As[buf][kk][ii] = pa[t];
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      Bs[buf][kk][jj] = pb[t];
+    }
+  };
+  const int nk = (jb.k + kGK - 1) / kGK;
+  if (nk > 0) {
+    fetch(0);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * kGK);  // in flight during the multiply below
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      double2 av[TM], bv[TN];
+#pragma unroll
+      for (int a = 0; a < TM; ++a) av[a] = As[cur][kk][tx + 16 * a];
+#pragma unroll
+      for (int b = 0; b < TN; ++b) bv[b] = Bs[cur][kk][ty + 16 * b];
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) {
+          acc_r[a][b] = fma(av[a].x, bv[b].x, acc_r[a][b]);
+          acc_r[a][b] = fma(-av[a].y, bv[b].y, acc_r[a][b]);
+          acc_i[a][b] = fma(av[a].x, bv[b].y, acc_i[a][b]);
+          acc_i[a][b] = fma(av[a].y, bv[b].x, acc_i[a][b]);
+        }
+    }
+    if (t + 1 < nk) stash(cur ^ 1);  // that buffer's readers finished in the previous iteration
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const int i = m0 + tx + 16 * a;
+    if (i >= jb.m) continue;
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+      const int j = n0 + ty + 16 * b;
+      if (j >= jb.n) continue;
+      double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+      if (EPI == GEPI_PLAIN) {
+        if (jb.herm && i < j) continue;  // written (bit-exactly) as the mirror of (j, i)
+        double2 o = make_double2(jb.alpha * acc_r[a][b], jb.alpha * acc_i[a][b]);
+        if (jb.beta0 != 0.0) {
+          const double2 c0 = *cp;
+          o.x += jb.beta0 * c0.x;
+          o.y += jb.beta0 * c0.y;
+        }
+        if (i == j) {
+          o.x += jb.diag_add;
+          if (jb.herm) o.y = 0.0;
+        }
+        *cp = o;
+        if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+      } else {
+        const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+        if (iK) {
+          *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+        } else {
+          const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+          const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+          *cp = make_double2(c0.x - acc_r[a][b], c0.y - acc_i[a][b]);
+        }
+      }
+    }
+  }
+}
+
+// fp64 tensor-core (DMMA) variant of the large products.  mma.sync m8n8k4
+// f64 fragments (PTX ISA):  A 8x4 row: a = A[lane/4][lane%4];  B 4x8 col:
+// b = B[lane%4][lane/4];  C 8x8: c[v] = C[lane/4][2 (lane%4) + v].
+// A complex 8x8x4 block is four real MMAs (Cr += Ar Br - Ai Bi,
+// Ci += Ar Bi + Ai Br).  CTA tile 128 x 64, BK = 8, 8 warps as 4 (m) x 2 (n),
+// each warp a 32 x 32 block = 4 x 4 DMMA tiles.  Shared planes (real / imag,
+// k-major) have pitches = 4 (mod 16) doubles: the fragment loads of a half
+// warp hit 16 distinct banks.  Same register-prefetch pipeline and epilogues
+// as gemm_big_kernel; products are exact fp64 (not bitwise equal to the SIMT
+// kernels: the tensor core's accumulation order differs).
+constexpr int kDmBM = 128, kDmBN = 64, kDmPA = 132, kDmPB = 68;
+constexpr size_t kGemmDmmaSmem = (size_t)2 * 2 * kGK * (kDmPA + kDmPB) * sizeof(double);
+
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  constexpr int BM = kDmBM, BN = kDmBN, PA = kDmPA, PB = kDmPB;
+  constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;
+  const GemmJob& jb = jobs.j[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= jb.m || n0 >= jb.n) return;
+  if (EPI == GEPI_PLAIN && jb.herm && m0 + BM <= n0) return;
+  extern __shared__ double dsm[];
+  // [buf][plane][kk][pitch]
+  double* Ash = dsm;                            // 2 x 2 x kGK x PA
+  double* Bsh = dsm + 2 * 2 * kGK * PA;         // 2 x 2 x kGK x PB
+  auto As = [&](int buf, int pl, int kk) { return Ash + ((buf * 2 + pl) * kGK + kk) * PA; };
+  auto Bs = [&](int buf, int pl, int kk) { return Bsh + ((buf * 2 + pl) * kGK + kk) * PB; };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;  // warp block origin in the tile
+  const int fr = lane >> 2, fc = lane & 3;                // fragment row / k
+  // 3M complex products: Re = P1 - P2, Im = P3 - P1 - P2 (see frame_batch2_kernel)
+  double p1[4][4][2], p2[4][4][2], p3[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
+  const MatRef A = jb.a, B = jb.b;
+  double2 pa[LA], pb[LB];
+  auto a_pos = [&](int e, int& ii, int& kk) {
+    if (!A.trans) { ii = e % BM; kk = e / BM; } else { kk = e & 7; ii = e >> 3; }
+  };
+  auto b_pos = [&](int e, int& jj, int& kk) {
+    if (!B.trans) { kk = e & 7; jj = e >> 3; } else { jj = e % BN; kk = e / BN; }
+  };
+  auto fetch = [&](int kk0) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      const int gi = m0 + ii, gk = kk0 + kk;
+      pa[t] = (gi < jb.m && gk < jb.k) ? mat_load(A, gi, gk) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      const int gj = n0 + jj, gk = kk0 + kk;
+      pb[t] = (gj < jb.n && gk < jb.k) ? mat_load(B, gk, gj) : make_double2(0.0, 0.0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < LA; ++t) {
+      int ii, kk;
+      a_pos(tid + t * 256, ii, kk);
+      As(buf, 0, kk)[ii] = pa[t].x;
+      As(buf, 1, kk)[ii] = pa[t].y;
+    }
+#pragma unroll
+    for (int t = 0; t < LB; ++t) {
+      int jj, kk;
+      b_pos(tid + t * 256, jj, kk);
+      Bs(buf, 0, kk)[jj] = pb[t].x;
+      Bs(buf, 1, kk)[jj] = pb[t].y;
+    }
+  };
+  const int nk = (jb.k + kGK - 1) / kGK;
+  if (nk > 0) {
+    fetch(0);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * kGK);
+#pragma unroll
+    for (int k4 = 0; k4 < kGK; k4 += 4) {
+      double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ar[a] = As(cur, 0, k4 + fc)[wm + 8 * a + fr];
+        ai[a] = As(cur, 1, k4 + fc)[wm + 8 * a + fr];
+        as[a] = ar[a] + ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        br[b] = Bs(cur, 0, k4 + fc)[wn + 8 * b + fr];
+        bi[b] = Bs(cur, 1, k4 + fc)[wn + 8 * b + fr];
+        bs[b] = br[b] + bi[b];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma884(p1[a][b], ar[a], br[b]);
+          dmma884(p2[a][b], ai[a], bi[b]);
+          dmma884(p3[a][b], as[a], bs[b]);
+        }
+    }
+    if (t + 1 < nk) stash(cur ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = m0 + wm + 8 * a + fr, j = n0 + wn + 8 * b + 2 * fc + v;
+        if (i >= jb.m || j >= jb.n) continue;
+        double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+        const double accr = p1[a][b][v] - p2[a][b][v], acci = p3[a][b][v] - p1[a][b][v] - p2[a][b][v];
+        if (EPI == GEPI_PLAIN) {
+          if (jb.herm && i < j) continue;
+          double2 o = make_double2(jb.alpha * accr, jb.alpha * acci);
+          if (jb.beta0 != 0.0) {
+            const double2 c0 = *cp;
+            o.x += jb.beta0 * c0.x;
+            o.y += jb.beta0 * c0.y;
+          }
+          if (i == j) {
+            o.x += jb.diag_add;
+            if (jb.herm) o.y = 0.0;
+          }
+          *cp = o;
+          if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+        } else {
+          const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
+          if (iK) {
+            *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+          } else {
+            const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
+            const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
+            *cp = make_double2(c0.x - accr, c0.y - acci);
+          }
+        }
+      }
+}
+
+// C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
+__global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
+                                  const double2* __restrict__ ws, int64_t ws_stride) {
+  const GemmJob& jb = jobs.j[blockIdx.y];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)jb.m * jb.n) return;
+  const int i = (int)(e % jb.m), j = (int)(e / jb.m);
+  double sr = 0.0, si = 0.0;
+  for (int s = 0; s < nsplit; ++s) {
+    const double2 v = ws[(int64_t)(blockIdx.y * nsplit + s) * ws_stride + (int64_t)j * jb.m + i];
+    sr += v.x;
+    si += v.y;
+  }
+  double2* cp = jb.c + i + (int64_t)j * jb.ldc;
+  double2 o = make_double2(jb.alpha * sr, jb.alpha * si);
+  if (jb.beta0 != 0.0) {
+    const double2 c0 = *cp;
+    o.x += jb.beta0 * c0.x;
+    o.y += jb.beta0 * c0.y;
+  }
+  if (i == j) o.x += jb.diag_add;
+  *cp = o;
+}
+
+// In-place Gauss-Jordan inverse of one kb x kb HPD pivot block (kb <= 64)
+// in shared memory: writes P = inv(M_KK) to P (ld = ldp) and raises *fail
+// if a pivot is not a positive finite real (the Cholesky-failure analogue of
+// solver_core.hpp:42-43).
+struct DiagJob {
+  const double2* M;
+  int64_t ld;
+  int n;          // matrix order
+  int k0, kb;     // pivot block
+  double2* P;     // kb x kb, ld = ldp
+  int64_t ldp;
+  double2* F;     // copy of M[:, K] (n x kb), ld = ldf
+  int64_t ldf;
+  double2* R;     // row panel R' (kb x n), ld = ldr
+  int64_t ldr;
+  int* fail;
+};
+
+__global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.x];
+  if (jb.k0 >= jb.n) return;
+  extern __shared__ double2 gj_smem[];
+  double2 (*S)[65] = reinterpret_cast<double2 (*)[65]>(gj_smem);
+  double2* prow = gj_smem + 64 * 65;
+  double2* pcol = prow + 64;
+  const int kb = jb.kb;
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e % kb, c = e / kb;
+    S[r][c] = jb.M[(jb.k0 + r) + (int64_t)(jb.k0 + c) * jb.ld];
+  }
+  __syncthreads();
+  for (int p = 0; p < kb; ++p) {
+    const double2 piv = S[p][p];
+    if (threadIdx.x == 0 && !(piv.x > 0.0 && isfinite(piv.x) && isfinite(piv.y))) atomicExch(jb.fail, 1);
+    const double den = piv.x * piv.x + piv.y * piv.y;
+    const double2 ip = make_double2(piv.x / den, -piv.y / den);
+    if (threadIdx.x < kb) {
+      const int c = threadIdx.x;
+      const double2 v = S[p][c];
+      prow[c] = (c == p) ? ip : make_double2(v.x * ip.x - v.y * ip.y, v.x * ip.y + v.y * ip.x);
+      pcol[c] = S[c][p];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+      const int r = e % kb, c = e / kb;
+      if (r == p) {
+        S[r][c] = prow[c];
+      } else {
+        const double2 f = pcol[r];
+        const double2 pr = prow[c];
+        const double2 base = (c == p) ? make_double2(0.0, 0.0) : S[r][c];
+        S[r][c] = make_double2(base.x - (f.x * pr.x - f.y * pr.y), base.y - (f.x * pr.y + f.y * pr.x));
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e % kb, c = e / kb;
+    jb.P[r + (int64_t)c * jb.ldp] = S[r][c];
+  }
+}
+
+// F = M[:, K] (pivot column panel), grid-stride over n*kb per job.
+__global__ void gj_panel_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.y];
+  if (jb.k0 >= jb.n) return;
+  const int64_t total = (int64_t)jb.n * jb.kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % jb.n), c = (int)(e / jb.n);
+    jb.F[r + (int64_t)c * jb.ldf] = jb.M[r + (int64_t)(jb.k0 + c) * jb.ld];
+  }
+}
+
+// R'[:, K] = P (overwrite the pivot columns of the row panel).
+__global__ void gj_fix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  const DiagJob& jb = jobs.j[blockIdx.x];
+  if (jb.k0 >= jb.n) return;
+  for (int e = threadIdx.x; e < jb.kb * jb.kb; e += blockDim.x) {
+    const int r = e % jb.kb, c = e / jb.kb;
+    jb.R[r + (int64_t)(jb.k0 + c) * jb.ldr] = jb.P[r + (int64_t)c * jb.ldp];
+  }
+}
+
+// out[i + j*ldo] = M[ridx[i] + cidx[j]*ld] (submatrix gather, grid-stride)
+struct SubJob {
+  const double2* M;
+  int64_t ld;
+  const int* ridx;
+  const int* cidx;
+  int m, n;
+  double2* out;
+  int64_t ldo;
+};
+
+__global__ void gather_sub_kernel(const __grid_constant__ Pack<SubJob> jobs) {
+  const SubJob& jb = jobs.j[blockIdx.y];
+  const int64_t total = (int64_t)jb.m * jb.n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % jb.m), j = (int)(e / jb.m);
+    jb.out[i + (int64_t)j * jb.ldo] = jb.M[jb.ridx[i] + (int64_t)jb.cidx[j] * jb.ld];
+  }
+}
+
+// Utility kernels -----------------------------------------------------------
+__global__ void c128_to_c64_kernel(const double2* __restrict__ src, int64_t lds, float2* __restrict__ dst,
+                                   int64_t ldd, int rows, int cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)rows * cols) return;
+  const int r = (int)(e % rows);
+  const int64_t c = e / rows;
+  const double2 v = src[r + c * lds];
+  dst[r + c * ldd] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+}
+
+__global__ void soft_threshold_kernel(const double2* __restrict__ v, int64_t n, double kappa, double2* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = soft_threshold1(v[i], kappa);
+}
+
+__global__ void abs_kernel(const double2* __restrict__ v, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = c_abs(v[i]);
+}
+
+// out = beta * (a - b): the accumulated frozen echo z = y_eff_s - y_eff,
+// scaled, that is folded into v when the stored data term lags (see
+// local_updates in radmm_b200.cu).
+__global__ void scaled_diff_kernel(double2* __restrict__ out, const double2* __restrict__ a,
+                                   const double2* __restrict__ b, double beta, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double2(beta * (a[i].x - b[i].x), beta * (a[i].y - b[i].y));
+}
+
+// Rb[:, t] = A[:, rem_pix[t]] promoted to complex128 (zero-padded to ld).
+__global__ void gather_cols_c128_kernel(const float2* __restrict__ A, int64_t ld, const int* __restrict__ pix,
+                                        int r, double2* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ld * r) return;
+  const int t = (int)(e / ld);
+  const int64_t row = e % ld;
+  const float2 v = A[row + (int64_t)pix[t] * ld];
+  out[e] = make_double2((double)v.x, (double)v.y);
+}
+
+__global__ void iota_kernel(int* __restrict__ J, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) J[i] = i;
+}
+
+// Gather x_full[J] -> x_hat (and zero a vector) etc.
+__global__ void gather_kernel(const double2* __restrict__ src, const int* __restrict__ idx, int n, double2* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+// BASELINE dechirped-LFM operator generator (mirrors scenario.baseline_operator
+// operation by operation, no FMA contraction).
+__global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K, int N,
+                               const double* __restrict__ pix, const double* __restrict__ tx,
+                               const double* __restrict__ rx, const double* __restrict__ phi,
+                               double alpha, double fc, double t_step, double c_light, double two_pi) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = M * K;
+  if (e >= (int64_t)rows * N) return;
+  const int r = (int)(e % rows);
+  const int n = (int)(e / rows);
+  const int m = r / K, k = r % K;
+  const double px = pix[3 * n], py = pix[3 * n + 1], pz = pix[3 * n + 2];
+  double dx = __dsub_rn(tx[0], px), dy = __dsub_rn(tx[1], py), dz = __dsub_rn(tx[2], pz);
+  const double dtx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  dx = __dsub_rn(rx[3 * m], px); dy = __dsub_rn(rx[3 * m + 1], py); dz = __dsub_rn(rx[3 * m + 2], pz);
+  const double drx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  const double tau = __ddiv_rn(__dadd_rn(dtx, drx), c_light);
+  const double tk = __dmul_rn((double)k, t_step);
+  double cyc = __dadd_rn(__dmul_rn(__dmul_rn(alpha, tau), tk), __dmul_rn(fc, tau));
+  cyc = __dsub_rn(cyc, floor(cyc));
+  const double ang = __dadd_rn(__dmul_rn(two_pi, cyc), phi[n]);
+  double s, c;
+  sincos(ang, &s, &c);
+  A[r + (int64_t)n * ld] = make_float2(__double2float_rn(c), __double2float_rn(s));
+}
+
+}  // namespace radmm_dev
