@@ -474,12 +474,21 @@ def stress(args):
                          "kernels and sizes the event scratch)"}
         s.run(h, api.Mode.ASADMM, fixed_iterations=True, fetch=False)  # warm-up, untimed
         for mode in (api.Mode.SADMM, api.Mode.ASADMM):
-            s.set_profiling(True)
+            # timed run as a user runs it (speculation on), then a profiling run
+            # of the same solve for the per-phase split (phase events serialise)
+            s.set_profiling(False)
             r = s.run(h, mode, fixed_iterations=True)
-            ph = s.phase_stats()
             ms, _ = s.iteration_stats(r.iterations)
+            s.set_profiling(True)
+            s.run(h, mode, fixed_iterations=True, fetch=False)
+            ph = s.phase_stats()
+            s.set_profiling(False)
             trig = next((rec.iteration for rec in r.report.iterations if rec.pri_res <= rec.eps_pri), None)
             sizes = [rec.active_sizes for rec in r.report.iterations]
+            ev = [k for k in range(1, len(sizes)) if sizes[k] != sizes[k - 1]]  # 0-based iterations with an event
+            quiet = [k for k in range(len(sizes)) if k not in set(ev)]
+            ev_ms = float(np.mean([ms[k] for k in ev])) if ev else None
+            quiet_ms = float(np.mean([ms[k] for k in quiet])) if quiet else None
             pick = sorted({1, trig or 1, iters // 4, iters // 2, iters})
             out[api.mode_name(mode)] = {
                 "iterations_per_s": r.iterations / (float(np.sum(ms)) / 1e3),
@@ -487,7 +496,9 @@ def stress(args):
                 "first_trigger_iteration": trig, "rebuilds": r.rebuilds, "downdates": r.downdates,
                 "active_sizes": {str(k): sizes[k - 1] for k in pick},
                 "total_active_solves": r.report.total_active_solves,
+                "event_iterations": len(ev), "ms_per_event_iteration": ev_ms, "ms_per_quiet_iteration": quiet_ms,
                 "compaction_ms_total": ph["screen"]["ms"], "refactor_ms_total": ph["refactor"]["ms"],
+                "phase_ms_note": "compaction/refactor totals from a second, profiled run of the same solve",
                 "screen_calls": ph["screen"]["calls"], "refactor_calls": ph["refactor"]["calls"]}
         s.close()
         a, p = out["asadmm"], out["sadmm"]

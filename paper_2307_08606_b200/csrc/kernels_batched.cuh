@@ -28,10 +28,13 @@ struct HermJob {
   int n;             // matrix order (rows of the sensor)
   int nb;            // tiles per side
   int groups;        // strip groups per tile column: ceil(nb / kHermStrip)
-  const double2* v;
+  const double2* v;  // right-hand side 0 (nullptr: the job sits this launch out)
   double2* w;
-  double2* dotp;     // [nb][groups][64]
-  double2* axp;      // [nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J
+  const double2* v1; // right-hand side 1 (NR = 2 launches; nullptr: none)
+  double2* w1;
+  double2* dotp;     // [NR][nb][groups][64], column stride dstride
+  double2* axp;      // [NR][nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J, column stride astride
+  int64_t dstride, astride;
 };
 
 // item word: q (16) | J (16) | I0 (16) | nt (16)
@@ -39,6 +42,10 @@ __host__ __device__ inline uint64_t herm_item(int q, int J, int I0, int nt) {
   return (uint64_t)q << 48 | (uint64_t)J << 32 | (uint64_t)I0 << 16 | (uint64_t)nt;
 }
 
+// NR right-hand sides per pass of G: NR = 1 is the iteration's w = G v; NR = 2
+// also forms a lazy-downdate column P[:, u] = G a_u from the same tile reads
+// (see lazy_* below).  A missing second column (v1 == nullptr) is zero.
+template <int NR>
 __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant__ Pack<HermJob> P,
                                                          const uint64_t* __restrict__ items,
                                                          const int* __restrict__ go) {
@@ -46,18 +53,24 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
   const uint64_t it = items[blockIdx.x];
   const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
   const HermJob& jb = P.j[q];
-  __shared__ double2 vJ[kHermTile];
-  __shared__ double2 vI[kHermStrip * kHermTile];
-  __shared__ double2 sax[2][8][kHermTile];  // double-buffered: one barrier per tile
+  if (!jb.v) return;
+  __shared__ double2 vJ[NR][kHermTile];
+  __shared__ double2 vI[NR][kHermStrip * kHermTile];
+  __shared__ double2 sax[2][NR][8][kHermTile];  // double-buffered: one barrier per tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = jb.n;
-  if (tid < kHermTile) {
-    const int j = J * kHermTile + tid;
-    vJ[tid] = j < n ? jb.v[j] : make_double2(0.0, 0.0);
-  }
-  for (int t = tid; t < nt * kHermTile; t += 256) {
-    const int i = I0 * kHermTile + t;
-    vI[t] = i < n ? jb.v[i] : make_double2(0.0, 0.0);
+  const double2* vs[2] = {jb.v, jb.v1};
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+    const double2* vc = vs[c];
+    if (tid < kHermTile) {
+      const int j = J * kHermTile + tid;
+      vJ[c][tid] = (vc && j < n) ? vc[j] : make_double2(0.0, 0.0);
+    }
+    for (int t = tid; t < nt * kHermTile; t += 256) {
+      const int i = I0 * kHermTile + t;
+      vI[c][t] = (vc && i < n) ? vc[i] : make_double2(0.0, 0.0);
+    }
   }
   const int c0 = warp * 8;  // this warp's 8 columns of the tile column
   const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
@@ -74,76 +87,94 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
   };
   load_tile(I0);
   __syncthreads();
-  double dr[8], di[8];
+  double dr[NR][8], di[NR][8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) dr[k] = di[k] = 0.0;
+  for (int c = 0; c < NR; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dr[c][k] = di[c][k] = 0.0;
   int par = 0;
   for (int t = 0; t < nt; ++t) {
     const int I = I0 + t;
-    double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+    double ar[NR][2], ai[NR][2];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) ar[c][0] = ar[c][1] = ai[c][0] = ai[c][1] = 0.0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const double2 vi = vI[t * kHermTile + lane + 32 * h];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        // conj(g) * v_i
-        dr[k] = fma(g[k][h].x, vi.x, dr[k]);
-        dr[k] = fma(g[k][h].y, vi.y, dr[k]);
-        di[k] = fma(g[k][h].x, vi.y, di[k]);
-        di[k] = fma(-g[k][h].y, vi.x, di[k]);
-        // g * v_j
-        const double2 vj = vJ[c0 + k];
-        ar[h] = fma(g[k][h].x, vj.x, ar[h]);
-        ar[h] = fma(-g[k][h].y, vj.y, ar[h]);
-        ai[h] = fma(g[k][h].x, vj.y, ai[h]);
-        ai[h] = fma(g[k][h].y, vj.x, ai[h]);
+      for (int c = 0; c < NR; ++c) {
+        const double2 vi = vI[c][t * kHermTile + lane + 32 * h];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          // conj(g) * v_i
+          dr[c][k] = fma(g[k][h].x, vi.x, dr[c][k]);
+          dr[c][k] = fma(g[k][h].y, vi.y, dr[c][k]);
+          di[c][k] = fma(g[k][h].x, vi.y, di[c][k]);
+          di[c][k] = fma(-g[k][h].y, vi.x, di[c][k]);
+          // g * v_j
+          const double2 vj = vJ[c][c0 + k];
+          ar[c][h] = fma(g[k][h].x, vj.x, ar[c][h]);
+          ar[c][h] = fma(-g[k][h].y, vj.y, ar[c][h]);
+          ai[c][h] = fma(g[k][h].x, vj.y, ai[c][h]);
+          ai[c][h] = fma(g[k][h].y, vj.x, ai[c][h]);
+        }
       }
     }
     if (t + 1 < nt) load_tile(I + 1);  // in flight across the reduction below
     if (I != J) {  // strictly-lower tile: its mirror contributes to rows of block I
 #pragma unroll
-      for (int h = 0; h < 2; ++h) sax[par][warp][lane + 32 * h] = make_double2(ar[h], ai[h]);
+      for (int c = 0; c < NR; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sax[par][c][warp][lane + 32 * h] = make_double2(ar[c][h], ai[c][h]);
       __syncthreads();
-      if (tid < kHermTile) {
-        double2 sum = sax[par][0][tid];
+      if (tid < NR * kHermTile) {
+        const int c = tid / kHermTile, r = tid % kHermTile;
+        double2 sum = sax[par][c][0][r];
 #pragma unroll
         for (int w8 = 1; w8 < 8; ++w8) {
-          sum.x += sax[par][w8][tid].x;
-          sum.y += sax[par][w8][tid].y;
+          sum.x += sax[par][c][w8][r].x;
+          sum.y += sax[par][c][w8][r].y;
         }
-        jb.axp[((int64_t)I * (I - 1) / 2 + J) * kHermTile + tid] = sum;
+        jb.axp[c * jb.astride + ((int64_t)I * (I - 1) / 2 + J) * kHermTile + r] = sum;
       }
       par ^= 1;  // the other buffer's readers are past this barrier
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    dr[k] = warp_sum(dr[k]);
-    di[k] = warp_sum(di[k]);
-  }
+  for (int c = 0; c < NR; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dr[c][k] = warp_sum(dr[c][k]);
+      di[c][k] = warp_sum(di[c][k]);
+    }
   if (lane == 0) {
     const int gi = (I0 - J) / kHermStrip;
-    double2* dp = jb.dotp + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[k], di[k]);
+    for (int c = 0; c < NR; ++c) {
+      double2* dp = jb.dotp + c * jb.dstride + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[c][k], di[c][k]);
+    }
   }
 }
 
 // w[b*64 + r] = sum_g dotp[b][g][r] + sum_{J < b} axp[tri(b, J)][r]  (fixed order)
 // 256 threads per row block: slice s = tid / 64 sums the partials k = s, s+4, ...
 // of the row's list (4 independent loads in flight), then the 4 slice sums are
-// added in slice order -- deterministic.
+// added in slice order -- deterministic.  blockIdx.z = right-hand side.
 __global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
                                                          const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;
   const HermJob& jb = P.j[blockIdx.y];
+  const int c = blockIdx.z;
+  double2* const out = c == 0 ? jb.w : jb.w1;
+  if (!jb.v || !out || (c == 1 && !jb.v1)) return;
   const int b = blockIdx.x, r = threadIdx.x & 63, sl = threadIdx.x >> 6;
   __shared__ double2 part[4][kHermTile];
   if (b >= jb.nb) return;
   const int ng = (jb.nb - b + kHermStrip - 1) / kHermStrip;
   const int total = ng + b;  // dot partials, then ax partials J = 0 .. b-1
-  const double2* dbase = jb.dotp + (int64_t)b * jb.groups * kHermTile + r;
-  const double2* abase = jb.axp + (int64_t)b * (b - 1) / 2 * kHermTile + r;
+  const double2* dbase = jb.dotp + c * jb.dstride + (int64_t)b * jb.groups * kHermTile + r;
+  const double2* abase = jb.axp + c * jb.astride + (int64_t)b * (b - 1) / 2 * kHermTile + r;
   double2 s = make_double2(0.0, 0.0);
   for (int k0 = sl; k0 < total; k0 += 16) {
     double2 v[4];
@@ -169,7 +200,257 @@ __global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant_
       t.x += part[u][r].x;
       t.y += part[u][r].y;
     }
-    if (row < jb.n) jb.w[row] = t;
+    if (row < jb.n) out[row] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Lazy Woodbury downdates (dual form).  After columns D (pixels pix[0..d)) are
+// eliminated, the capacitance becomes C_D = C - mu A_D A_D^H; with the factor
+// G = C^{-1} of the base set kept unchanged,
+//   C_D^{-1} v = u + mu P Sinv (A_D^H u),   u = G v,  P = G A_D,
+//   Sinv = (I - mu A_D^H P)^{-1}  (d x d),
+// so an elimination event appends columns to P (one pass of G, shared with
+// the iteration's own G-apply) instead of rewriting G.
+//   lazy_dot_kernel:   t = A_D^H u            grid (d, jobs)
+//   lazy_axpy_kernel:  w = u + mu P (Sinv t)  grid (row blocks, jobs)
+// ---------------------------------------------------------------------------
+constexpr int kLazyMax = 64;  // accumulated columns before they are folded into G
+
+struct LazyJob {
+  const float2* A;      // operator (complex64, column-major, ld)
+  int64_t ld;
+  int rows;
+  const int* pix;       // D: eliminated pixels (operator columns)
+  int d;
+  const double2* P;     // ld x d
+  const double2* Sinv;  // d x d, leading dimension lds
+  int64_t lds;
+  double2* w;           // in: u = G v; out: C_D^{-1} v
+  double2* t;           // d (scratch)
+};
+
+__global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ Pack<LazyJob> P, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const LazyJob& jb = P.j[blockIdx.y];
+  const int j = blockIdx.x;
+  if (j >= jb.d) return;
+  const float2* a = jb.A + (int64_t)jb.pix[j] * jb.ld;
+  double re = 0.0, im = 0.0;
+  for (int i = threadIdx.x; i < jb.rows; i += 256) {
+    const float2 x = a[i];
+    const double2 u = jb.w[i];
+    // conj(a) * u
+    re = fma((double)x.x, u.x, re);
+    re = fma((double)x.y, u.y, re);
+    im = fma((double)x.x, u.y, im);
+    im = fma(-(double)x.y, u.x, im);
+  }
+  __shared__ double sr[8], si[8];
+  re = warp_sum(re);
+  im = warp_sum(im);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sr[warp] = re; si[warp] = im; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a0 = sr[0], b0 = si[0];
+    for (int k = 1; k < 8; ++k) { a0 += sr[k]; b0 += si[k]; }
+    jb.t[j] = make_double2(a0, b0);
+  }
+}
+
+__global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ Pack<LazyJob> P, double mu,
+                                                        const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;
+  const LazyJob& jb = P.j[blockIdx.y];
+  if (jb.d <= 0 || (int64_t)blockIdx.x * 256 >= jb.rows) return;
+  __shared__ double2 sv[kLazyMax];
+  // s = mu Sinv t: four threads per row of Sinv, fixed-order shuffle combine
+  {
+    const int j = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    double re = 0.0, im = 0.0;
+    if (j < jb.d)
+      for (int k = sub; k < jb.d; k += 4) {
+        const double2 m = jb.Sinv[j + (int64_t)k * jb.lds], x = jb.t[k];
+        re = fma(m.x, x.x, re);
+        re = fma(-m.y, x.y, re);
+        im = fma(m.x, x.y, im);
+        im = fma(m.y, x.x, im);
+      }
+    re += __shfl_xor_sync(0xffffffffu, re, 1);
+    im += __shfl_xor_sync(0xffffffffu, im, 1);
+    re += __shfl_xor_sync(0xffffffffu, re, 2);
+    im += __shfl_xor_sync(0xffffffffu, im, 2);
+    if (sub == 0 && j < jb.d) sv[j] = make_double2(mu * re, mu * im);
+  }
+  __syncthreads();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= jb.rows) return;
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < jb.d; ++k) {
+    const double2 p = jb.P[i + (int64_t)k * jb.ld], x = sv[k];
+    re = fma(p.x, x.x, re);
+    re = fma(-p.y, x.y, re);
+    im = fma(p.x, x.y, im);
+    im = fma(p.y, x.x, im);
+  }
+  const double2 u = jb.w[i];
+  jb.w[i] = make_double2(u.x + re, u.y + im);
+}
+
+// Bordered update of Sinv when r <= kBorderMax columns join D (d0 -> d0 + r):
+//   S' = [[S11, S12], [S12^H, S22]],  S12 = -mu A_old^H P_new,
+//   S22 = I - mu A_new^H P_new,  S11^{-1} = Sinv (known)
+//   W = Sinv S12,  Z = S22 - S12^H W (Schur complement, HPD),  X = W Z^{-1}
+//   S'^{-1} = [[Sinv + X W^H, -X], [-X^H, Z^{-1}]]
+// lazy_border_dots_kernel forms B = A_D^H P_new (grid (d0 + r, jobs)), then
+// lazy_border_inv_kernel (one CTA per job) does the O(d^2 r) rest; a
+// non-positive pivot of Z sets *fail (the reference's "Cholesky failed").
+constexpr int kBorderMax = 16;
+
+struct BorderJob {
+  const float2* A;
+  int64_t ld;
+  int rows;
+  const int* pix;      // D (d0 + r pixels)
+  int d0, r;
+  const double2* P;    // ld x (d0 + r)
+  double2* B;          // (d0 + r) x kBorderMax scratch: B[j][u] = a_j^H P[:, d0 + u]
+  double2* Sinv;       // kLazyMax x kLazyMax (column-major)
+  int* fail;
+};
+
+__global__ void __launch_bounds__(256) lazy_border_dots_kernel(const __grid_constant__ Pack<BorderJob> P) {
+  const BorderJob& jb = P.j[blockIdx.y];
+  const int j = blockIdx.x;
+  if (j >= jb.d0 + jb.r) return;
+  const float2* a = jb.A + (int64_t)jb.pix[j] * jb.ld;
+  double re[kBorderMax], im[kBorderMax];
+#pragma unroll
+  for (int u = 0; u < kBorderMax; ++u) re[u] = im[u] = 0.0;
+  for (int i = threadIdx.x; i < jb.rows; i += 256) {
+    const float2 x = a[i];
+    const double xr = x.x, xi = x.y;
+#pragma unroll
+    for (int u = 0; u < kBorderMax; ++u) {
+      if (u >= jb.r) break;
+      const double2 p = jb.P[(int64_t)(jb.d0 + u) * jb.ld + i];
+      re[u] = fma(xr, p.x, re[u]);
+      re[u] = fma(xi, p.y, re[u]);
+      im[u] = fma(xr, p.y, im[u]);
+      im[u] = fma(-xi, p.x, im[u]);
+    }
+  }
+  __shared__ double sr[8][kBorderMax], si[8][kBorderMax];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < kBorderMax; ++u) {
+    if (u >= jb.r) break;
+    const double a0 = warp_sum(re[u]), b0 = warp_sum(im[u]);
+    if (lane == 0) { sr[warp][u] = a0; si[warp][u] = b0; }
+  }
+  __syncthreads();
+  if (threadIdx.x < jb.r) {
+    const int u = threadIdx.x;
+    double a0 = sr[0][u], b0 = si[0][u];
+    for (int w = 1; w < 8; ++w) { a0 += sr[w][u]; b0 += si[w][u]; }
+    jb.B[(int64_t)j * kBorderMax + u] = make_double2(a0, b0);
+  }
+}
+
+constexpr size_t kBorderSmem = (size_t)(kLazyMax * kLazyMax + 3 * kLazyMax * kBorderMax + kBorderMax * kBorderMax) * 16;
+
+__global__ void __launch_bounds__(256) lazy_border_inv_kernel(const __grid_constant__ Pack<BorderJob> P, double mu) {
+  const BorderJob& jb = P.j[blockIdx.x];
+  extern __shared__ __align__(16) double2 bsm[];
+  double2* S = bsm;                                   // Sinv_old  d0 x d0 (ld kLazyMax)
+  double2* S12 = S + kLazyMax * kLazyMax;             // d0 x r   (ld kLazyMax)
+  double2* W = S12 + kLazyMax * kBorderMax;           // d0 x r
+  double2* X = W + kLazyMax * kBorderMax;             // d0 x r
+  double2* Z = X + kLazyMax * kBorderMax;             // r x r    (ld kBorderMax)
+  __shared__ int bad;
+  const int d0 = jb.d0, r = jb.r, tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < d0 * d0; e += 256) {
+    const int i = e % d0, k = e / d0;
+    S[i + k * kLazyMax] = jb.Sinv[i + (int64_t)k * kLazyMax];
+  }
+  for (int e = tid; e < d0 * r; e += 256) {
+    const int i = e % d0, u = e / d0;
+    const double2 b = jb.B[(int64_t)i * kBorderMax + u];
+    S12[i + u * kLazyMax] = make_double2(-mu * b.x, -mu * b.y);
+  }
+  for (int e = tid; e < r * r; e += 256) {
+    const int v = e % r, u = e / r;
+    const double2 b = jb.B[(int64_t)(d0 + v) * kBorderMax + u];
+    Z[v + u * kBorderMax] = make_double2((v == u ? 1.0 : 0.0) - mu * b.x, -mu * b.y);
+  }
+  __syncthreads();
+  // W = Sinv_old S12
+  for (int e = tid; e < d0 * r; e += 256) {
+    const int i = e % d0, u = e / d0;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < d0; ++k) acc = c_fma(S[i + k * kLazyMax], S12[k + u * kLazyMax], acc);
+    W[i + u * kLazyMax] = acc;
+  }
+  __syncthreads();
+  // Z -= S12^H W
+  for (int e = tid; e < r * r; e += 256) {
+    const int v = e % r, u = e / r;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < d0; ++i) acc = c_fma(c_conj(S12[i + v * kLazyMax]), W[i + u * kLazyMax], acc);
+    Z[v + u * kBorderMax] = c_sub(Z[v + u * kBorderMax], acc);
+  }
+  __syncthreads();
+  // Z <- Z^{-1}: Gauss-Jordan without pivoting (Z is HPD)
+  for (int k = 0; k < r; ++k) {
+    const double2 pk = Z[k + k * kBorderMax];
+    if (!(pk.x > 0.0)) {
+      if (tid == 0) bad = 1;
+    }
+    __syncthreads();
+    if (bad) break;
+    const double2 inv = make_double2(1.0 / pk.x, 0.0);  // HPD: real positive pivot
+    // row k of the rest / column k: standard in-place GJ step
+    const int i = tid % kBorderMax, j = tid / kBorderMax;  // 256 threads cover 16 x 16
+    double2 v = make_double2(0.0, 0.0);
+    if (i < r && j < r) {
+      const double2 zik = Z[i + k * kBorderMax], zkj = Z[k + j * kBorderMax], zij = Z[i + j * kBorderMax];
+      if (i == k && j == k) v = inv;
+      else if (i == k) v = c_mul(zkj, inv);
+      else if (j == k) v = c_mul(make_double2(-zik.x, -zik.y), inv);
+      else v = c_sub(zij, c_mul(c_mul(zik, inv), zkj));
+    }
+    __syncthreads();
+    if (i < r && j < r) Z[i + j * kBorderMax] = v;
+    __syncthreads();
+  }
+  if (tid == 0) *jb.fail = bad;
+  if (bad) return;
+  // X = W Zinv
+  for (int e = tid; e < d0 * r; e += 256) {
+    const int i = e % d0, u = e / d0;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int v = 0; v < r; ++v) acc = c_fma(W[i + v * kLazyMax], Z[v + u * kBorderMax], acc);
+    X[i + u * kLazyMax] = acc;
+  }
+  __syncthreads();
+  // S'^{-1}
+  for (int e = tid; e < d0 * d0; e += 256) {
+    const int i = e % d0, k = e / d0;
+    double2 acc = S[i + k * kLazyMax];
+    for (int u = 0; u < r; ++u) acc = c_fma(X[i + u * kLazyMax], c_conj(W[k + u * kLazyMax]), acc);
+    jb.Sinv[i + (int64_t)k * kLazyMax] = acc;
+  }
+  for (int e = tid; e < d0 * r; e += 256) {
+    const int i = e % d0, u = e / d0;
+    const double2 x = X[i + u * kLazyMax];
+    jb.Sinv[i + (int64_t)(d0 + u) * kLazyMax] = make_double2(-x.x, -x.y);
+    jb.Sinv[(d0 + u) + (int64_t)i * kLazyMax] = make_double2(-x.x, x.y);
+  }
+  for (int e = tid; e < r * r; e += 256) {
+    const int v = e % r, u = e / r;
+    jb.Sinv[(d0 + v) + (int64_t)(d0 + u) * kLazyMax] = Z[v + u * kBorderMax];
   }
 }
 

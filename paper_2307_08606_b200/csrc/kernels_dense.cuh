@@ -634,6 +634,46 @@ __global__ void gather_cols_c128_kernel(const float2* __restrict__ A, int64_t ld
   out[e] = make_double2((double)v.x, (double)v.y);
 }
 
+// Per-sensor bookkeeping of one elimination event, all sensors in one launch
+// (blockIdx.y = sensor); every part is optional (null pointer = skip):
+//   log_dst[t] = lz_pix_dst[t] = rem_pix[t]            (removal log, lazy D list)
+//   lz_R[:, t] = A[:, rem_pix[t]] as complex128         (columns for P = G A_D)
+//   bz = beta (y_eff_s - y_eff)                         (lagged data term)
+struct EventJob {
+  const int* rem_pix;
+  int r;
+  int* log_dst;
+  int* lz_pix_dst;
+  const float2* A;
+  int64_t ld;
+  double2* lz_R;
+  double2* bz;
+  const double2* y_eff_s;
+  const double2* y_eff;
+  double beta;
+};
+
+__global__ void event_prep_kernel(const __grid_constant__ Pack<EventJob> P) {
+  const EventJob& jb = P.j[blockIdx.y];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t t = t0; t < jb.r; t += stride) {
+    const int p = jb.rem_pix[t];
+    if (jb.log_dst) jb.log_dst[t] = p;
+    if (jb.lz_pix_dst) jb.lz_pix_dst[t] = p;
+  }
+  if (jb.lz_R)
+    for (int64_t e = t0; e < jb.ld * jb.r; e += stride) {
+      const int u = (int)(e / jb.ld);
+      const int64_t row = e % jb.ld;
+      const float2 v = jb.A[row + (int64_t)jb.rem_pix[u] * jb.ld];
+      jb.lz_R[e] = make_double2((double)v.x, (double)v.y);
+    }
+  if (jb.bz)
+    for (int64_t i = t0; i < jb.ld; i += stride)
+      jb.bz[i] = make_double2(jb.beta * (jb.y_eff_s[i].x - jb.y_eff[i].x), jb.beta * (jb.y_eff_s[i].y - jb.y_eff[i].y));
+}
+
 __global__ void iota_kernel(int* __restrict__ J, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) J[i] = i;

@@ -16,6 +16,14 @@ struct Pack {
 
 __device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 c_conj(double2 a) { return make_double2(a.x, -a.y); }
+// a * b + c
+__device__ __forceinline__ double2 c_fma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
 __device__ __forceinline__ double2 c_scale(double2 a, double s) {
   return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s));
 }
@@ -450,6 +458,9 @@ struct FusionArgs {
   int* go_next;
   int stop_on_converge;     // !fixed_iterations
   int screen_next_possible; // ASADMM, screening enabled, history full after this round
+  // device-guarded screening: set when the next round screens (trigger staged,
+  // not stopping); the screening kernels enqueued behind this round read it
+  int* screen_go;
 };
 
 constexpr int kFusionThreads = 256;
@@ -541,6 +552,8 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
     f.converged = a.has_prev && f.trigger && f.dual_res <= f.eps_dual;
     if (a.go_next)
       *a.go_next = !((a.stop_on_converge && f.converged) || (a.screen_next_possible && f.trigger));
+    if (a.screen_go)
+      *a.screen_go = a.screen_next_possible && f.trigger && !(a.stop_on_converge && f.converged);
     f.iteration = a.iteration;
     f.pad = 0;
     *a.out_dev = f;
@@ -609,7 +622,15 @@ struct ScreenJob {
   double2* data_new;
 };
 
-__global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int W, double tol) {
+// Screening kernels run unconditionally (go, sgo == nullptr) or behind a
+// fusion round, guarded by its go flag and the screen flag it wrote.
+__device__ __forceinline__ bool screen_off(const int* go, const int* sgo) {
+  return (go && __ldg(go) == 0) || (sgo && __ldg(sgo) == 0);
+}
+
+__global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int W, double tol,
+                                                                const int* __restrict__ go, const int* __restrict__ sgo) {
+  if (screen_off(go, sgo)) return;
   const ScreenJob& jb = jobs.j[blockIdx.y];
   __shared__ int wc[kScanBlock / 32];
   const int i = blockIdx.x * kScanBlock + threadIdx.x;
@@ -636,19 +657,41 @@ __global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_c
   }
 }
 
-__global__ void screen_scan_kernel(const __grid_constant__ Pack<ScreenJob> jobs) {
-  const ScreenJob& jb = jobs.j[blockIdx.x];
-  if (threadIdx.x != 0) return;
-  const int nb = (jb.n + kScanBlock - 1) / kScanBlock;
-  int s = 0;
-  for (int b = 0; b < nb; ++b) {
-    jb.block_offsets[b] = s;
-    s += jb.block_counts[b];
+// One block: warp q scans sensor q's block counts; the kept counts go to the
+// mapped host array (the host reads them after the round's event, no copy).
+// If no active set changes (nothing removed; a would-be-empty set stalls and
+// stays), the already-enqueued next round may run: *go_next = 1.
+__global__ void __launch_bounds__(256) screen_scan_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int nq,
+                                                          const int* __restrict__ go, const int* __restrict__ sgo,
+                                                          int* totals_host, int* go_next) {
+  if (screen_off(go, sgo)) return;
+  __shared__ int changed;
+  if (threadIdx.x == 0) changed = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < nq; q += 8) {
+    if (lane != 0) continue;
+    const ScreenJob& jb = jobs.j[q];
+    const int nb = (jb.n + kScanBlock - 1) / kScanBlock;
+    int s = 0;
+    for (int b = 0; b < nb; ++b) {
+      jb.block_offsets[b] = s;
+      s += jb.block_counts[b];
+    }
+    jb.totals[0] = s;
+    if (totals_host) ((volatile int*)totals_host)[q] = s;
+    if (s != jb.n && s != 0) atomicOr(&changed, 1);
   }
-  jb.totals[0] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (go_next && !changed) *go_next = 1;
+  }
 }
 
-__global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid_constant__ Pack<ScreenJob> jobs) {
+__global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid_constant__ Pack<ScreenJob> jobs,
+                                                                  const int* __restrict__ go, const int* __restrict__ sgo) {
+  if (screen_off(go, sgo)) return;
   const ScreenJob& jb = jobs.j[blockIdx.y];
   __shared__ int woff[kScanBlock / 32];
   if ((int)blockIdx.x * kScanBlock >= jb.n) return;

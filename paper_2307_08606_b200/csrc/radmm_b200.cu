@@ -200,7 +200,18 @@ struct Sensor {
   // Hermitian G-apply partials (dot: nb x groups x 64, ax: nb(nb-1)/2 x 64)
   DArr<double2> hdot, hax;
   DArr<double2> apart;  // row-segmented adjoint partials (nseg x N)
+  // Lazy Woodbury downdates (dual form, see lazy_dot_kernel): G stays the
+  // factor of the base active set; the eliminated columns D accumulate in
+  // P = G A_D (ld x kLazyMax) with Sinv = (I - mu A_D^H P)^{-1}, and are
+  // folded into G only when kLazyMax is reached.
+  int lz_d = 0;    // |D|
+  int lz_new = 0;  // 1: P[:, d-1] = G a is formed by the next G-apply (second right-hand side)
+  int lz_r = 0;    // columns added by the last event (bordered Sinv update pending)
+  DArr<double2> lz_P, lz_R, lz_S, lz_t, lz_B;
+  DArr<int> lz_pix;
 };
+
+constexpr int kFlagCap = 4 * kMaxBatch;  // pinned pivot-flag slots
 
 struct Scratch {
   DArr<char> buf;
@@ -244,8 +255,9 @@ struct radmm_ctx {
   FusionScalars* fs_host = nullptr;
   FusionScalars* fs_host_dev = nullptr;
   DArr<const double2*> contrib;
-  int* h_totals = nullptr;   // pinned, per local sensor
-  int* h_flags = nullptr;    // pinned, kMaxBatch
+  int* h_totals = nullptr;   // mapped pinned, 3 slots x local sensors (kept counts; see enqueue_screen)
+  int* d_totals = nullptr;   // device alias of h_totals
+  int* h_flags = nullptr;    // pinned, kFlagCap (deferred pivot flags accumulate)
   Scratch scratch;
   DArr<int> fail_flags;
   // sharded exchange
@@ -271,6 +283,8 @@ struct radmm_ctx {
   std::vector<cudaEvent_t> ev_steps;
   std::vector<cudaEvent_t> ev_ends;  // recorded after each round's fusion
   DArr<int> go_flags;                // speculation guards, alternating per round
+  DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
+  bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
   DArr<uint64_t> herm_items;         // Hermitian G-apply work items (largest first)
   std::vector<int64_t> herm_sig;     // (batch position, order) the items were built for
@@ -421,9 +435,11 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   CK(cudaHostAlloc(&c->fs_host, 2 * sizeof(FusionScalars), cudaHostAllocMapped));
   std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
   c->go_flags.alloc(2);
+  c->sgo_flags.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
-  CK(cudaHostAlloc(&c->h_totals, sizeof(int) * std::max(1, q_local), cudaHostAllocDefault));
-  CK(cudaHostAlloc(&c->h_flags, sizeof(int) * kMaxBatch, cudaHostAllocDefault));
+  CK(cudaHostAlloc(&c->h_totals, sizeof(int) * 3 * std::max(1, q_local), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer((void**)&c->d_totals, c->h_totals, 0));
+  CK(cudaHostAlloc(&c->h_flags, sizeof(int) * kFlagCap, cudaHostAllocDefault));
   c->fail_flags.alloc(kMaxBatch);
   for (int q = 0; q < q_local; ++q) {
     Sensor& S = c->sensors[q];
@@ -538,20 +554,9 @@ bool herm_enabled() { return env_int("RADMM_HERM", 1) != 0; }
 // algorithmic bytes of one G-apply: the Hermitian triangle (or the full matrix)
 double gapply_bytes(int n) { return herm_enabled() ? 8.0 * n * (n + 1.0) : 16.0 * n * (double)n; }
 
-void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
-  if (qs.empty()) return;
-  if (!herm_enabled() || qs.size() > (size_t)kMaxBatch) {
-    std::vector<ColDotJob> gj;
-    for (int q : qs) {
-      Sensor& S = c->sensors[q];
-      ColDotJob g{};
-      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
-      gj.push_back(g);
-    }
-    coldot<double2, EPI_STORE>(c, gj, 1.0, 1.0, go);
-    return;
-  }
-  Pack<HermJob> pk;
+// Job table for the listed (dual) sensors: v = S.v -> w = S.w, plus the work
+// item list, rebuilt only when the batch signature changes.
+int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
   std::vector<int64_t> sig;
   int nb_max = 0;
   for (size_t i = 0; i < qs.size(); ++i) {
@@ -560,10 +565,12 @@ void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
     h.G = S.G.p; h.ld = S.ldg; h.n = S.rows;
     h.nb = (S.rows + kHermTile - 1) / kHermTile;
     h.groups = (h.nb + kHermStrip - 1) / kHermStrip;
-    const size_t nd = (size_t)h.nb * h.groups * kHermTile, na = (size_t)h.nb * (h.nb - 1) / 2 * kHermTile;
-    if (S.hdot.n < nd) S.hdot.alloc(nd, false);
-    if (S.hax.n < std::max<size_t>(na, 1)) S.hax.alloc(std::max<size_t>(na, 1), false);
+    const size_t nd = (size_t)h.nb * h.groups * kHermTile,
+                 na = std::max<size_t>((size_t)h.nb * (h.nb - 1) / 2 * kHermTile, 1);
+    if (S.hdot.n < 2 * nd) S.hdot.alloc(2 * nd, false);  // two right-hand sides
+    if (S.hax.n < 2 * na) S.hax.alloc(2 * na, false);
     h.v = S.v.p; h.w = S.w.p; h.dotp = S.hdot.p; h.axp = S.hax.p;
+    h.dstride = (int64_t)nd; h.astride = (int64_t)na;
     pk.j[i] = h;
     nb_max = std::max(nb_max, h.nb);
     sig.push_back(h.n);
@@ -588,16 +595,53 @@ void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
     c->herm_n_items = (int)items.size();
     c->herm_sig = sig;
   }
-  if (env_int("RADMM_HERM", 1) == 2) {
+  return nb_max;
+}
+
+// nr = 2 when some job carries a second right-hand side (v1 -> w1).
+void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go) {
+  if (nr == 1 && env_int("RADMM_HERM", 1) == 2) {
     CK(cudaFuncSetAttribute(herm_gapply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kHermTmaSmem));
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
+  } else if (nr == 1) {
+    LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   } else {
-    LAUNCH(c, herm_gapply_kernel, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
+    LAUNCH(c, herm_gapply_kernel<2>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
-  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)qs.size()), 256, 0, pk, go);
+  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), 256, 0, pk, go);
+}
+
+void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
+  if (qs.empty()) return;
+  if (!herm_enabled() || qs.size() > (size_t)kMaxBatch) {
+    std::vector<ColDotJob> gj;
+    for (int q : qs) {
+      Sensor& S = c->sensors[q];
+      ColDotJob g{};
+      g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
+      gj.push_back(g);
+      if (S.lz_new) {  // pending lazy-downdate column P[:, d-1] = G a
+        g.vec = S.lz_R.p; g.out = S.lz_P.p + (size_t)(S.lz_d - 1) * S.ld;
+        gj.push_back(g);
+      }
+    }
+    coldot<double2, EPI_STORE>(c, gj, 1.0, 1.0, go);
+    return;
+  }
+  Pack<HermJob> pk;
+  const int nb_max = herm_pack(c, qs, pk);
+  int nr = 1;
+  for (size_t i = 0; i < qs.size(); ++i) {
+    Sensor& S = c->sensors[qs[i]];
+    if (!S.lz_new) continue;
+    pk.j[i].v1 = S.lz_R.p;
+    pk.j[i].w1 = S.lz_P.p + (size_t)(S.lz_d - 1) * S.ld;
+    nr = 2;
+  }
+  herm_launch(c, pk, qs.size(), nb_max, nr, go);
 }
 
 // ---- forward (axpy) launches ------------------------------------------------
@@ -718,6 +762,8 @@ struct InvTarget {
 
 constexpr int kGJB = 64;
 
+void check_deferred(radmm_ctx* c);
+
 // Inverts every target in place; raises RADMM_NUMERICAL if a pivot fails.
 void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* what) {
   if (targets.empty()) return;
@@ -792,15 +838,21 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     LAUNCH(c, gj_fix_kernel, dim3((unsigned)T), 256, 0, dj);
     gemm<GEPI_GJ>(c, ujobs);
   }
-  CK(cudaMemcpyAsync(c->h_flags, c->fail_flags.p, sizeof(int) * T, cudaMemcpyDeviceToHost, c->stream));
+  // flags land after any still-unchecked deferred ones
+  if (c->pending_fail + T > (size_t)kFlagCap) {
+    CK(cudaStreamSynchronize(c->stream));
+    check_deferred(c);
+  }
+  const int off = c->pending_fail;
+  CK(cudaMemcpyAsync(c->h_flags + off, c->fail_flags.p, sizeof(int) * T, cudaMemcpyDeviceToHost, c->stream));
   sc.off = base_off;
   if (c->defer_fail_check) {  // checked after the iteration's own sync (check_deferred)
-    c->pending_fail = (int)T;
+    c->pending_fail = off + (int)T;
     return;
   }
   CK(cudaStreamSynchronize(c->stream));
   for (size_t i = 0; i < T; ++i)
-    if (c->h_flags[i]) fail(RADMM_NUMERICAL, std::string(what) + ": Cholesky failed");
+    if (c->h_flags[off + i]) fail(RADMM_NUMERICAL, std::string(what) + ": Cholesky failed");
 }
 
 // Deferred pivot check of the last downdate (the stream has been synchronised).
@@ -841,6 +893,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     S.primal = S.n_act <= S.rows;
+    S.lz_d = S.lz_new = 0;  // a fresh factor of the current set
     const int dim = S.primal ? S.n_act : S.rows;
     const int64_t ldg = S.primal ? round_up(dim, 32) : S.ld;
     ensure_g(S, dim, ldg);
@@ -901,21 +954,200 @@ void data_terms(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   }
 }
 
-// Lagged data term for dual sensors after an elimination event: bz = beta (y_eff_s - y_eff).
-void lag_data_terms(radmm_ctx* c, const std::vector<int>& qs, double beta) {
+// One batched bookkeeping launch per event (see event_prep_kernel).
+void event_prep(radmm_ctx* c, const std::vector<EventJob>& jobs) {
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<EventJob> pk;
+    int64_t work = 1;
+    for (size_t i = 0; i < nb; ++i) {
+      const EventJob& j = jobs[b0 + i];
+      pk.j[i] = j;
+      work = std::max<int64_t>(work, std::max<int64_t>(j.r, (j.lz_R ? j.ld * j.r : 0) + (j.bz ? j.ld : 0)));
+    }
+    const unsigned blocks = (unsigned)std::min<int64_t>(1024, (work + 255) / 256);
+    LAUNCH(c, event_prep_kernel, dim3(blocks, (unsigned)nb), 256, 0, pk);
+  }
+}
+
+// ---- lazy Woodbury downdates (dual form) ------------------------------------
+bool fused_enabled();
+bool lazy_enabled() { return env_int("RADMM_LAZY", 1) != 0 && !fused_enabled(); }
+// RADMM_LAZY_MAX (<= kLazyMax) lowers the fold point (tests force folds)
+int lazy_max() { return std::min(kLazyMax, std::max(1, env_int("RADMM_LAZY_MAX", kLazyMax))); }
+
+void lazy_reserve(Sensor& S) {
+  if (S.lz_P.n < (size_t)S.ld * kLazyMax) {
+    S.lz_P.alloc((size_t)S.ld * kLazyMax, false);
+    S.lz_R.alloc((size_t)S.ld * kLazyMax, false);
+    S.lz_S.alloc((size_t)kLazyMax * kLazyMax, false);
+    S.lz_t.alloc(kLazyMax, false);
+    S.lz_pix.alloc(kLazyMax, false);
+    S.lz_B.alloc((size_t)kLazyMax * kBorderMax, false);
+  }
+}
+
+// Sinv <- (I - mu A_D^H P)^{-1} for the listed sensors, whose last lz_r
+// columns of P were just formed: bordered update (lazy_border_*_kernel), two
+// launches for all sensors.  Pivots are checked at the iteration's sync, like
+// the eager path's.
+void lazy_finish(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  if (qs.empty()) return;
+  if (qs.size() > (size_t)kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
+  Pack<BorderJob> pk;
+  int dmax = 0;
+  for (size_t i = 0; i < qs.size(); ++i) {
+    Sensor& S = c->sensors[qs[i]];
+    pk.j[i] = BorderJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d - S.lz_r, S.lz_r, S.lz_P.p, S.lz_B.p, S.lz_S.p,
+                        c->fail_flags.p + i};
+    dmax = std::max(dmax, S.lz_d);
+  }
+  const unsigned nb = (unsigned)qs.size();
+  LAUNCH(c, lazy_border_dots_kernel, dim3((unsigned)dmax, nb), 256, 0, pk);
+  CK(cudaFuncSetAttribute(lazy_border_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBorderSmem));
+  LAUNCH(c, lazy_border_inv_kernel, dim3(nb), 256, kBorderSmem, pk, mu);
+  if (c->pending_fail + (int)nb > kFlagCap) {
+    CK(cudaStreamSynchronize(c->stream));
+    check_deferred(c);
+  }
+  CK(cudaMemcpyAsync(c->h_flags + c->pending_fail, c->fail_flags.p, sizeof(int) * nb, cudaMemcpyDeviceToHost,
+                     c->stream));
+  c->pending_fail += (int)nb;
+}
+
+// Fold the accumulated columns into G: G <- G + mu P Sinv P^H (Hermitian,
+// lower tiles + exact mirror), D <- {}.
+void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  if (qs.empty()) return;
+  size_t need = 0;
+  for (int q : qs) need += (size_t)c->sensors[q].ld * kLazyMax * sizeof(double2) + 1024;
+  c->scratch.reserve(need);
+  std::vector<GemmJob> st3, st4;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
-    LAUNCH(c, scaled_diff_kernel, dim3((unsigned)((S.ld + 255) / 256)), 256, 0, S.bz.p, S.y_eff_s.p, S.y_eff.p,
-           beta, S.ld);
-    S.data_lag = true;
+    const int m = S.rows, d = S.lz_d;
+    double2* T = c->scratch.take<double2>((size_t)S.ld * kLazyMax);
+    st3.push_back(gjob(m, d, d, mref(S.lz_P.p, S.ld, false), mref(S.lz_S.p, kLazyMax, false), T, S.ld, 1.0, 0.0));
+    st4.push_back(gjob(m, m, d, mref(T, S.ld, false), mref(S.lz_P.p, S.ld, false, true, true), S.G.p, S.ldg, mu,
+                       1.0));
+    st4.back().herm = 1;
+    S.lz_d = 0;
+    S.lz_new = 0;
   }
+  gemm<GEPI_PLAIN>(c, st3);
+  gemm<GEPI_PLAIN>(c, st4);
+}
+
+// Append this event's removed columns to D.  A single column rides the next
+// iteration's G-apply as a second right-hand side (no extra pass over G);
+// more columns are formed now, two per pass of G's lower triangle.
+void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  if (qs.empty()) return;
+  std::vector<int> now;
+  int passes = 0;
+  std::vector<EventJob> ej;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    const int r = S.removed_now;
+    lazy_reserve(S);
+    EventJob e{};
+    e.rem_pix = S.rem_pix.p; e.r = r; e.lz_pix_dst = S.lz_pix.p + S.lz_d; e.A = S.A.p; e.ld = S.ld; e.lz_R = S.lz_R.p;
+    ej.push_back(e);
+    S.lz_d += r;
+    S.lz_r = r;
+    if (r == 1 && herm_enabled()) {
+      S.lz_new = 1;
+    } else {
+      now.push_back(q);
+      passes = std::max(passes, (r + 1) / 2);
+    }
+    ++c->downdates;
+  }
+  event_prep(c, ej);
+  if (now.empty()) return;
+  std::vector<int> dual;  // the iteration's G-apply batch (same item table)
+  for (int q = 0; q < c->Q; ++q)
+    if (!c->sensors[q].primal) dual.push_back(q);
+  if (!herm_enabled() || dual.size() > (size_t)kMaxBatch) {
+    std::vector<ColDotJob> gj;
+    for (int q : now) {
+      Sensor& S = c->sensors[q];
+      const int r = S.removed_now, d0 = S.lz_d - r;
+      for (int u = 0; u < r; ++u) {
+        ColDotJob g{};
+        g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.scale = 1.0;
+        g.vec = S.lz_R.p + (size_t)u * S.ld; g.out = S.lz_P.p + (size_t)(d0 + u) * S.ld;
+        gj.push_back(g);
+      }
+    }
+    coldot<double2, EPI_STORE>(c, gj, 1.0, 1.0);
+  } else {
+    Pack<HermJob> pk;
+    const int nb_max = herm_pack(c, dual, pk);
+    for (int p = 0; p < passes; ++p) {
+      for (size_t i = 0; i < dual.size(); ++i) {
+        Sensor& S = c->sensors[dual[i]];
+        HermJob& h = pk.j[i];
+        h.v = h.v1 = nullptr;
+        h.w = h.w1 = nullptr;
+        if (std::find(now.begin(), now.end(), dual[i]) == now.end()) continue;
+        const int r = S.removed_now, d0 = S.lz_d - r;
+        for (int t = 0; t < 2; ++t) {
+          const int u = 2 * p + t;
+          if (u >= r) break;
+          (t ? h.v1 : h.v) = S.lz_R.p + (size_t)u * S.ld;
+          (t ? h.w1 : h.w) = S.lz_P.p + (size_t)(d0 + u) * S.ld;
+        }
+      }
+      herm_launch(c, pk, dual.size(), nb_max, 2, nullptr);
+    }
+  }
+  lazy_finish(c, now, mu);
+}
+
+// w <- C_D^{-1} v from u = G v for every listed sensor with accumulated columns.
+void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go) {
+  Pack<LazyJob> pk;
+  int nb = 0, dmax = 0, rmax = 0;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    if (S.primal || S.lz_d == 0) continue;
+    if (nb >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
+    pk.j[nb++] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax, S.w.p, S.lz_t.p};
+    dmax = std::max(dmax, S.lz_d);
+    rmax = std::max(rmax, S.rows);
+  }
+  if (!nb) return;
+  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, go);
+  LAUNCH(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
+}
+
+void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu);
+
+// Downdates after screening removed rem_q columns: dual sensors accumulate
+// them lazily (up to kLazyMax, then fold); primal sensors and large removals
+// take the eager path.
+void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+  if (qs.empty()) return;
+  std::vector<int> lazy, fold, eager;
+  const bool lz = lazy_enabled();
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    const int cap = lazy_max();
+    const bool use_lazy = lz && !S.primal && S.removed_now <= std::min(cap, kBorderMax);
+    if (!S.primal && S.lz_d > 0 && (!use_lazy || S.lz_d + S.removed_now > cap)) fold.push_back(q);
+    (use_lazy ? lazy : eager).push_back(q);
+  }
+  lazy_fold(c, fold, mu);
+  lazy_append(c, lazy, mu);
+  eager_downdate(c, eager, mu);
 }
 
 // Low-rank downdates after screening removed rem_q columns.
 //   dual:   G <- G + mu P (I - mu R^H P)^{-1} P^H,  P = G R   (Woodbury)
 //   primal: Hinv_KK <- Hinv_KK - Hinv_KD inv(Hinv_DD) Hinv_DK (inverse of a
 //           principal submatrix), written compacted into G2 then swapped.
-void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
+void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   if (qs.empty()) return;
   size_t need = 0;
   for (int q : qs) {
@@ -1075,6 +1307,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
     S.stalled = false;
     S.removed_now = 0;
     S.v_ready = false;
+    S.lz_d = S.lz_new = 0;
     LAUNCH(c, iota_kernel, dim3((N + 255) / 256), 256, 0, S.J.p, N);
     CK(cudaMemsetAsync(S.x_full.p, 0, sizeof(double2) * N, c->stream));
     CK(cudaMemsetAsync(S.x_hat.p, 0, sizeof(double2) * N, c->stream));
@@ -1243,6 +1476,14 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
     {
       PhaseScope ps(c, RADMM_PHASE_GAPPLY, g_bytes);
       gapply(c, gq, go);
+      std::vector<int> fin;  // lazy columns the G-apply just formed
+      for (int q : gq)
+        if (c->sensors[q].lz_new) {
+          c->sensors[q].lz_new = 0;
+          fin.push_back(q);
+        }
+      lazy_finish(c, fin, h->mu);
+      lazy_correct(c, gq, h->mu, go);
     }
     PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
     adjoint(c, aj, gq, h->mu, h->beta, go);  // gq lists the same dual sensors in the same order
@@ -1281,22 +1522,28 @@ void exchange(radmm_ctx* c, double notice_bytes) {
 FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k);
 
 void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go = nullptr,
-                int* go_next = nullptr, int stop_on_converge = 1, int screen_next_possible = 0) {
+                int* go_next = nullptr, int stop_on_converge = 1, int screen_next_possible = 0,
+                int* screen_go = nullptr) {
   FusionArgs a = fusion_args(c, h, k);
   a.go = go;
   a.go_next = go_next;
   a.stop_on_converge = stop_on_converge;
   a.screen_next_possible = screen_next_possible;
+  a.screen_go = screen_go;
   PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
   LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
 
 bool fused_enabled();
 
-// SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386).
-// Returns the notice bytes of this round.
-uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
-  if (c->upd < c->W) return 0;  // history shorter than W+1 (admm.hpp:137)
+// SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386),
+// device part: zeta, keep flags, compaction into the *_new buffers and the
+// kept counts (mapped host slot `slot`).  Guarded (go, sgo) when it is
+// enqueued behind a fusion round; go_next lets the next round run when no
+// active set changes.  Returns false if the history is still short.
+bool enqueue_screen(radmm_ctx* c, const radmm_hyperparams* h, int slot, const int* go, const int* sgo,
+                    int* go_next) {
+  if (c->upd < c->W) return false;  // history shorter than W+1 (admm.hpp:137)
   Pack<ScreenJob> pk;
   int n_max = 0;
   if (c->Q > kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors per GPU for screening batch");
@@ -1312,28 +1559,49 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     n_max = std::max(n_max, S.n_act);
   }
   const int nb = (n_max + kScanBlock - 1) / kScanBlock;
-  {
-    double sb = 0;
-    for (int q = 0; q < c->Q; ++q) sb += (double)c->sensors[q].n_act * (8.0 * c->W + 4 + 1 + 4 + 4 + 32);
-    PhaseScope ps(c, RADMM_PHASE_SCREEN, sb);
-    LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol);
-    LAUNCH(c, screen_scan_kernel, dim3(c->Q), 32, 0, pk);
-    LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk);
-  }
-  for (int q = 0; q < c->Q; ++q)
-    CK(cudaMemcpyAsync(c->h_totals + q, c->sensors[q].totals.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  double sb = 0;
+  for (int q = 0; q < c->Q; ++q) sb += (double)c->sensors[q].n_act * (8.0 * c->W + 4 + 1 + 4 + 4 + 32);
+  PhaseScope ps(c, RADMM_PHASE_SCREEN, sb);
+  LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol, go, sgo);
+  LAUNCH(c, screen_scan_kernel, dim3(1), 256, 0, pk, c->Q, go, sgo, c->d_totals + (size_t)slot * c->Q, go_next);
+  LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, go, sgo);
+  return true;
+}
+
+// Host part, after the kept counts of slot `slot` are visible: stall flags,
+// active-set swaps, removal log, then rebuild() (admm.hpp:171-179) as frozen
+// echo + lagged data term + downdates.  Returns the notice bytes of the round.
+uint64_t apply_screen(radmm_ctx* c, const radmm_hyperparams* h, int k, int slot) {
+  const volatile int* tot = c->h_totals + (size_t)slot * c->Q;
   uint64_t notice = 0;
   std::vector<int> changed;
+  int64_t log_need = c->log_used;
   for (int q = 0; q < c->Q; ++q) {
     Sensor& S = c->sensors[q];
-    const int kept = c->h_totals[q];
+    const int kept = tot[q];
     const int removed = S.n_act - kept;
     if (removed == 0) continue;
     if (kept == 0) {  // admm.hpp:148-151
       S.stalled = true;
       continue;
     }
+    log_need += removed;
+  }
+  if (c->dlog.n < (size_t)log_need) {  // the removal log stays on the device until the run ends
+    const size_t cap = std::max<size_t>((size_t)c->Q * c->N, (size_t)log_need);
+    DArr<int> grown;
+    grown.alloc(cap, false);
+    if (c->log_used)
+      CK(cudaMemcpyAsync(grown.p, c->dlog.p, sizeof(int) * c->log_used, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->dlog = std::move(grown);
+  }
+  std::vector<EventJob> ej;
+  for (int q = 0; q < c->Q; ++q) {
+    Sensor& S = c->sensors[q];
+    const int kept = tot[q];
+    const int removed = S.n_act - kept;
+    if (removed == 0 || kept == 0) continue;
     S.removed_now = removed;
     S.v_ready = false;  // the speculative v was formed over the old active set
     std::swap(S.J, S.Jnew);
@@ -1342,23 +1610,13 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
     S.n_act = kept;
     changed.push_back(q);
     notice += notice_size((size_t)removed);
-    // the removed pixel list stays on the device until the run ends
-    if (c->dlog.n < (size_t)(c->log_used + removed)) {
-      const size_t cap = std::max<size_t>((size_t)c->Q * c->N, (size_t)(c->log_used + removed));
-      DArr<int> grown;
-      grown.alloc(cap, false);
-      if (c->log_used)
-        CK(cudaMemcpyAsync(grown.p, c->dlog.p, sizeof(int) * c->log_used, cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      c->dlog = std::move(grown);
-    }
-    CK(cudaMemcpyAsync(c->dlog.p + c->log_used, S.rem_pix.p, sizeof(int) * removed, cudaMemcpyDeviceToDevice,
-                       c->stream));
+    EventJob e{};
+    e.rem_pix = S.rem_pix.p; e.r = removed; e.log_dst = c->dlog.p + c->log_used;
+    ej.push_back(e);
     c->log_segs.push_back({k, c->q_begin + q, removed, c->log_used});
     c->log_used += removed;
   }
   if (changed.empty()) return notice;
-  // rebuild() (admm.hpp:171-179): frozen echo, data term, factor
   double rb = 0;
   for (int q : changed) {
     const Sensor& S = c->sensors[q];
@@ -1366,18 +1624,21 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   }
   PhaseScope ps(c, RADMM_PHASE_REFACTOR, rb);
   update_y_eff(c, changed);
-  {
-    // dual sensors that stay dual keep a lagged data term (no full pass);
-    // primal sensors (and the experimental fused sweeps) recompute it
-    std::vector<int> lag, exact;
-    for (int q : changed) {
-      const Sensor& S = c->sensors[q];
-      const bool stays_dual = !S.primal && S.n_act > S.rows;
-      (stays_dual && !fused_enabled() ? lag : exact).push_back(q);
+  // dual sensors that stay dual keep a lagged data term (no full pass);
+  // primal sensors (and the experimental fused sweeps) recompute it
+  std::vector<int> exact;
+  for (size_t t = 0; t < changed.size(); ++t) {
+    Sensor& S = c->sensors[changed[t]];
+    const bool stays_dual = !S.primal && S.n_act > S.rows;
+    if (stays_dual && !fused_enabled()) {
+      ej[t].bz = S.bz.p; ej[t].y_eff_s = S.y_eff_s.p; ej[t].y_eff = S.y_eff.p; ej[t].ld = S.ld; ej[t].beta = h->beta;
+      S.data_lag = true;
+    } else {
+      exact.push_back(changed[t]);
     }
-    lag_data_terms(c, lag, h->beta);
-    data_terms(c, exact, h->mu);
   }
+  event_prep(c, ej);
+  data_terms(c, exact, h->mu);
   std::vector<int> rebuild, down;
   for (int q : changed) {
     Sensor& S = c->sensors[q];
@@ -1393,6 +1654,20 @@ uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   full_rebuild(c, rebuild, h->mu, h->beta);
   downdate(c, down, h->mu);
   return notice;
+}
+
+// Synchronous screening (observer / sharded / fused / profiling runs).
+uint64_t screen_all(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  if (!enqueue_screen(c, h, 2, nullptr, nullptr, nullptr)) return 0;
+  CK(cudaStreamSynchronize(c->stream));
+  return apply_screen(c, h, k, 2);
+}
+
+// Stall flags of a screening round whose active sets did not change.
+void note_stalls(radmm_ctx* c, int slot) {
+  const volatile int* tot = c->h_totals + (size_t)slot * c->Q;
+  for (int q = 0; q < c->Q; ++q)
+    if (tot[q] == 0 && c->sensors[q].n_act > 0) c->sensors[q].stalled = true;
 }
 
 // ---- single-pass fused sweep (one GPU, all sensors dual, Q <= 8) ------------
@@ -1645,6 +1920,7 @@ FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   a.go_next = nullptr;
   a.stop_on_converge = 1;
   a.screen_next_possible = 0;
+  a.screen_go = nullptr;
   return a;
 }
 
@@ -1872,16 +2148,32 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
                     env_int("RADMM_SPECULATE", 1) != 0;
   auto screen_next_possible = [&]() { return (asadmm && !disable && c->upd >= c->W) ? 1 : 0; };
   // issue one round: local updates (+ exchange) + fusion; go == nullptr = unconditional
+  // With speculation the next round's screening is enqueued right behind this
+  // round's fusion, guarded by the flag the fusion writes; the host then reads
+  // the kept counts at the same sync as the round's scalars (no extra round
+  // trip), and a screening round that changes no active set does not even
+  // cancel the speculative round.
   auto issue = [&](int kk, const int* go, uint64_t notice) {
     int* go_next = spec ? c->go_flags.p + ((kk + 1) & 1) : nullptr;
+    c->pre_screened[kk & 1] = false;
     if (fused_eligible(c)) {
       fused_iteration(c, h, kk);
     } else {
       local_updates(c, h, go);
       exchange(c, (double)notice);
-      run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, screen_next_possible());
+      const int snp = screen_next_possible();
+      int* sgo = (spec && snp) ? c->sgo_flags.p + (kk & 1) : nullptr;
+      run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, snp, sgo);
+      if (sgo) c->pre_screened[kk & 1] = enqueue_screen(c, h, kk & 1, go, sgo, go_next);
     }
     CK(cudaEventRecord(END(kk), c->stream));
+  };
+  // active sets changed by the screening enqueued behind round kk
+  auto pre_changed = [&](int kk) {
+    const volatile int* tot = c->h_totals + (size_t)(kk & 1) * c->Q;
+    for (int q = 0; q < c->Q; ++q)
+      if (tot[q] != 0 && tot[q] != c->sensors[q].n_act) return true;
+    return false;
   };
   bool k_launched = false;   // iteration k already enqueued (speculatively)
   int64_t l_k = 0;           // launch counter when iteration k was enqueued
@@ -1891,7 +2183,8 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       l_k = c->launches;
       CK(cudaEventRecord(STEP(k - 1), c->stream));
       notice_k = 0;
-      if (asadmm && !disable && staged_trigger) notice_k = screen_all(c, h, k);
+      if (asadmm && !disable && staged_trigger)
+        notice_k = c->pre_screened[(k - 1) & 1] ? apply_screen(c, h, k, (k - 1) & 1) : screen_all(c, h, k);
       issue(k, nullptr, notice_k);
     }
     const uint64_t notice = notice_k;
@@ -1912,12 +2205,18 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     f = c->fs_host[k & 1];
     k_launched = false;
     if (spec_next) {
-      const bool cancelled = (!fixed && f.converged) || (f.trigger && asadmm && !disable && upd_before_next >= c->W);
+      const bool screens = f.trigger && asadmm && !disable && upd_before_next >= c->W;
+      // the screening behind round k ran on the device; it cancelled round
+      // k+1 only if an active set changed
+      const bool pre = screens && c->pre_screened[k & 1];
+      const bool cancelled = (!fixed && f.converged) || (screens && (!pre || pre_changed(k)));
       if (cancelled) {
-        CK(cudaStreamSynchronize(c->stream));
+        // the cancelled round's kernels exit at entry; what the host enqueues
+        // next runs after them in stream order
         c->upd = upd_before_next;  // the no-op round consumed no update
         for (Sensor& S : c->sensors) S.v_ready = false;
       } else {
+        if (pre) note_stalls(c, k & 1);
         k_launched = true;
         notice_k = 0;
       }

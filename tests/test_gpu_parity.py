@@ -364,13 +364,25 @@ def _small_c1(**kw):
     return ops, ys, hyper
 
 
+DOWNDATE_VARIANTS = {
+    "lazy": {},                        # default: columns accumulate in P = G A_D, folded at 64
+    "lazy_folds": {"RADMM_LAZY_MAX": "3"},  # fold into G every few events
+    "lazy_full_gapply": {"RADMM_HERM": "0"},  # pending columns through the column-dot G-apply
+    "eager": {"RADMM_LAZY": "0"},      # G rewritten at every event
+}
+
+
+@pytest.mark.parametrize("variant", list(DOWNDATE_VARIANTS))
 @pytest.mark.parametrize("nside,K,tol,iters", [(16, 16, 1e-3, 150), (12, 8, 3e-3, 150), (16, 64, 1e-3, 120)])
-def test_elimination_event_paths_match_oracle(nside, K, tol, iters):
-    """Aggressive screening drives the active sets through low-rank downdates,
-    dual->primal form switches and large-removal rebuilds; masks and states
-    must track the oracle at every step."""
+def test_elimination_event_paths_match_oracle(nside, K, tol, iters, variant, monkeypatch):
+    """Aggressive screening drives the active sets through low-rank downdates
+    (lazy Woodbury columns, folds, eager rewrites), dual->primal form switches
+    and large-removal rebuilds; masks and states must track the oracle at
+    every step."""
     ops, ys, hyper = _small_c1(nside=nside, K=K, n_targets=4, max_iter=iters)
     hyper = dict(hyper, screening_tol=tol)
+    for k, v in DOWNDATE_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     g = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
     o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
     print(f"nside={nside} K={K}: rebuilds={g.rebuilds} downdates={g.downdates} "
