@@ -157,6 +157,154 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
   }
 }
 
+constexpr size_t herm_persist_smem(int nr) {
+  return (size_t)(2 * nr * kHermTile + 2 * nr * kHermStrip * kHermTile + 2 * nr * 8 * kHermTile) * 16;
+}
+
+// Persistent variant: a fixed grid (resident CTAs) walks the item list
+// round-robin; while the last tile of one item is reduced, the first tile of
+// the CTA's next item and that item's vector slices are already loading
+// (registers and a second shared buffer), so items cost no start-up latency.
+// Per-item arithmetic and partial slots are exactly herm_gapply_kernel's.
+template <int NR>
+__global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                                    const uint64_t* __restrict__ items, int n_items,
+                                                                    const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
+  extern __shared__ __align__(16) double2 hps[];  // herm_persist_smem(NR) bytes
+  double2(*vJ)[NR][kHermTile] = reinterpret_cast<double2(*)[NR][kHermTile]>(hps);
+  double2(*vI)[NR][kHermStrip * kHermTile] =
+      reinterpret_cast<double2(*)[NR][kHermStrip * kHermTile]>(hps + 2 * NR * kHermTile);
+  double2(*sax)[NR][8][kHermTile] =
+      reinterpret_cast<double2(*)[NR][8][kHermTile]>(hps + 2 * NR * kHermTile + 2 * NR * kHermStrip * kHermTile);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = warp * 8;
+  // next active item at or after index i (inactive jobs have v == nullptr)
+  auto next_item = [&](int i) {
+    for (; i < n_items; i += gridDim.x) {
+      const uint64_t it = __ldg(items + i);
+      if (P.j[(int)(it >> 48)].v) return i;
+    }
+    return n_items;
+  };
+  auto load_vec = [&](int buf, uint64_t it) {
+    const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+    const HermJob& jb = P.j[q];
+    const double2* vs[2] = {jb.v, jb.v1};
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      const double2* vc = vs[c];
+      if (tid < kHermTile) {
+        const int j = J * kHermTile + tid;
+        vJ[buf][c][tid] = (vc && j < jb.n) ? vc[j] : make_double2(0.0, 0.0);
+      }
+      for (int t = tid; t < nt * kHermTile; t += 256) {
+        const int i = I0 * kHermTile + t;
+        vI[buf][c][t] = (vc && i < jb.n) ? vc[i] : make_double2(0.0, 0.0);
+      }
+    }
+  };
+  double2 g[8][2];
+  auto load_tile = [&](uint64_t it, int I) {
+    const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF);
+    const HermJob& jb = P.j[q];
+    const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
+    const int ib = I * kHermTile;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = ib + lane + 32 * h, j = J * kHermTile + c0 + k;
+        g[k][h] = (i < jb.n && j < jb.n) ? __ldg(Gc + (int64_t)k * jb.ld + i) : make_double2(0.0, 0.0);
+      }
+  };
+  int cur = next_item(blockIdx.x);
+  if (cur >= n_items) return;
+  uint64_t it = __ldg(items + cur);
+  int buf = 0;
+  load_vec(buf, it);
+  load_tile(it, (int)(it >> 16 & 0xFFFF));
+  int par = 0;
+  while (true) {
+    const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
+    const HermJob& jb = P.j[q];
+    const int nxt = next_item(cur + gridDim.x);
+    const uint64_t it_n = nxt < n_items ? __ldg(items + nxt) : 0;
+    __syncthreads();  // vectors of `buf` visible; the other buffer's readers are done
+    if (nxt < n_items) load_vec(buf ^ 1, it_n);
+    double dr[NR][8], di[NR][8];
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dr[c][k] = di[c][k] = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const int I = I0 + t;
+      double ar[NR][2], ai[NR][2];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) ar[c][0] = ar[c][1] = ai[c][0] = ai[c][1] = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double2 vi = vI[buf][c][t * kHermTile + lane + 32 * h];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            dr[c][k] = fma(g[k][h].x, vi.x, dr[c][k]);
+            dr[c][k] = fma(g[k][h].y, vi.y, dr[c][k]);
+            di[c][k] = fma(g[k][h].x, vi.y, di[c][k]);
+            di[c][k] = fma(-g[k][h].y, vi.x, di[c][k]);
+            const double2 vj = vJ[buf][c][c0 + k];
+            ar[c][h] = fma(g[k][h].x, vj.x, ar[c][h]);
+            ar[c][h] = fma(-g[k][h].y, vj.y, ar[c][h]);
+            ai[c][h] = fma(g[k][h].x, vj.y, ai[c][h]);
+            ai[c][h] = fma(g[k][h].y, vj.x, ai[c][h]);
+          }
+        }
+      }
+      if (t + 1 < nt) load_tile(it, I + 1);                       // in flight across the reduction below
+      else if (nxt < n_items) load_tile(it_n, (int)(it_n >> 16 & 0xFFFF));  // the next item's first tile
+      if (I != J) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) sax[par][c][warp][lane + 32 * h] = make_double2(ar[c][h], ai[c][h]);
+        __syncthreads();
+        if (tid < NR * kHermTile) {
+          const int c = tid / kHermTile, r = tid % kHermTile;
+          double2 sum = sax[par][c][0][r];
+#pragma unroll
+          for (int w8 = 1; w8 < 8; ++w8) {
+            sum.x += sax[par][c][w8][r].x;
+            sum.y += sax[par][c][w8][r].y;
+          }
+          jb.axp[c * jb.astride + ((int64_t)I * (I - 1) / 2 + J) * kHermTile + r] = sum;
+        }
+        par ^= 1;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        dr[c][k] = warp_sum(dr[c][k]);
+        di[c][k] = warp_sum(di[c][k]);
+      }
+    if (lane == 0) {
+      const int gi = (I0 - J) / kHermStrip;
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        double2* dp = jb.dotp + c * jb.dstride + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[c][k], di[c][k]);
+      }
+    }
+    if (nxt >= n_items) break;
+    cur = nxt;
+    it = it_n;
+    buf ^= 1;
+  }
+}
+
 // w[b*64 + r] = sum_g dotp[b][g][r] + sum_{J < b} axp[tri(b, J)][r]  (fixed order)
 // 256 threads per row block: slice s = tid / 64 sums the partials k = s, s+4, ...
 // of the row's list (4 independent loads in flight), then the 4 slice sums are

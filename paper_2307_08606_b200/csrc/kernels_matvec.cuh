@@ -276,6 +276,140 @@ __global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__
   }
 }
 
+// Software-pipelined column dot for complex64 operators (the adjoint pass):
+// the same math and summation order as coldot_kernel<float2, EPI, true, 2>,
+// but a warp streams its columns as one continuous sequence -- the loads of
+// the next column pair are issued before the current pair's shuffle
+// reduction and epilogue, and the epilogue's inputs (rhs, pixel, old x) are
+// fetched at the start of the pair -- so no load bubble opens at column
+// boundaries.  Needs a multiple of four 64-row steps (KM % 256 == 0).
+template <int EPI, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) coldot_pipe_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu,
+                                                              double beta, const int* __restrict__ go) {
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
+  constexpr int CPW = 2;
+  extern __shared__ double2 sv[];
+  constexpr int kWarps = THREADS / 32;
+  const ColDotJob& jb = jobs.j[blockIdx.y];
+  const int n_out = jb.n_out;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  const int i_begin = (int)(gw * n_out / nw);
+  const int i_end = (int)((gw + 1) * n_out / nw);
+  if ((int)((int64_t)blockIdx.x * kWarps * n_out / nw) >= n_out) return;  // whole CTA idle
+  const int64_t ld = jb.ld;
+  const int64_t vld = jb.vld ? jb.vld : ld;
+  const int64_t half = vld >> 1;
+  for (int r = threadIdx.x; r < vld; r += blockDim.x)
+    sv[ColLoad<float2, CPW>::slot(r, half)] = (r < jb.len) ? jb.vec[r] : make_double2(0.0, 0.0);
+  __syncthreads();
+  if (i_begin >= i_end) return;
+  const int lane = threadIdx.x & 31;
+  const int steps = (int)((jb.len + 63) / 64);  // multiple of 4 (host-checked)
+  const float2* base = reinterpret_cast<const float2*>(jb.M);
+  const double2* ve = sv + lane;
+  const double2* vo = sv + half + lane;
+  auto colptr = [&](int i) -> const float4* {
+    const int ic = min(i, i_end - 1);
+    const int col = jb.cols ? __ldg(jb.cols + ic) : ic;
+    return reinterpret_cast<const float4*>(base + (int64_t)col * ld) + lane;
+  };
+  const float4* p[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) p[c] = colptr(i_begin + c);
+  // ping-pong register buffers (no register moves of in-flight loads):
+  // buffer A holds steps s, s+1 while B loads s+2, s+3, and vice versa; the
+  // step count is a multiple of 4, so A holds the next pair's first steps
+  // when a pair ends.
+  float4 a0[CPW], a1[CPW], b0[CPW], b1[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    a0[c] = __ldg(p[c]);
+    a1[c] = __ldg(p[c] + 32);
+  }
+  for (int i0 = i_begin; i0 < i_end; i0 += CPW) {
+    const int i1 = i0 + CPW;
+    const float4* pn[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) pn[c] = colptr(i1 + c);
+    // epilogue inputs of this pair (lane c finishes column i0 + c)
+    double2 e_rhs = make_double2(0.0, 0.0), e_old = make_double2(0.0, 0.0);
+    int e_pix = 0;
+    if (EPI == EPI_XDUAL && lane < CPW && i0 + lane < i_end) {
+      e_rhs = jb.rhs[i0 + lane];
+      e_pix = jb.pix[i0 + lane];
+      e_old = jb.x_full[e_pix];
+    }
+    double re[CPW], im[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) re[c] = im[c] = 0.0;
+    const bool more = i1 < i_end;
+#pragma unroll 1
+    for (int s = 0; s < steps; s += 4) {
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {  // B <- steps s+2, s+3 (always inside this pair)
+        b0[c] = __ldg(p[c] + (s + 2) * 32);
+        b1[c] = __ldg(p[c] + (s + 3) * 32);
+      }
+      {
+        const double2 e0 = ve[(s + 0) * 32], o0 = vo[(s + 0) * 32];
+        const double2 e1 = ve[(s + 1) * 32], o1 = vo[(s + 1) * 32];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          cfma_conj(re[c], im[c], a0[c].x, a0[c].y, e0);
+          cfma_conj(re[c], im[c], a0[c].z, a0[c].w, o0);
+          cfma_conj(re[c], im[c], a1[c].x, a1[c].y, e1);
+          cfma_conj(re[c], im[c], a1[c].z, a1[c].w, o1);
+        }
+      }
+      if (s + 4 < steps) {  // A <- steps s+4, s+5, or the next pair's first two
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          a0[c] = __ldg(p[c] + (s + 4) * 32);
+          a1[c] = __ldg(p[c] + (s + 5) * 32);
+        }
+      } else if (more) {
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          a0[c] = __ldg(pn[c]);
+          a1[c] = __ldg(pn[c] + 32);
+        }
+      }
+      {
+        const double2 e0 = ve[(s + 2) * 32], o0 = vo[(s + 2) * 32];
+        const double2 e1 = ve[(s + 3) * 32], o1 = vo[(s + 3) * 32];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+          cfma_conj(re[c], im[c], b0[c].x, b0[c].y, e0);
+          cfma_conj(re[c], im[c], b0[c].z, b0[c].w, o0);
+          cfma_conj(re[c], im[c], b1[c].x, b1[c].y, e1);
+          cfma_conj(re[c], im[c], b1[c].z, b1[c].w, o1);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      re[c] = warp_sum(re[c]);
+      im[c] = warp_sum(im[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+      if (lane == c && i0 + c < i_end) {
+        if (EPI == EPI_XDUAL) {
+          const double2 xh = make_double2(__ddiv_rn(__dsub_rn(e_rhs.x, __dmul_rn(mu, re[c])), beta),
+                                          __ddiv_rn(__dsub_rn(e_rhs.y, __dmul_rn(mu, im[c])), beta));
+          jb.ring_slot[e_pix] = c_abs(c_sub(xh, e_old));  // admm.hpp:143
+          jb.x_full[e_pix] = xh;                          // admm.hpp:121-122
+          jb.x_hat[i0 + c] = xh;                          // admm.hpp:120
+        } else {
+          coldot_epilogue<EPI>(jb, i0 + c, re[c], im[c], mu, beta);
+        }
+      }
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) p[c] = pn[c];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Forward kernel: v = sum_i A[:, J_i] * coef_i over a chunk of active columns
 // (rows in 512-row tiles, 2 complex per thread via float4), with the

@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -509,6 +510,20 @@ void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max
   LAUNCH(c, kern, dim3(gx, (unsigned)nb), THREADS, SMEM ? smem : 0, pk, mu, beta, go);
 }
 
+template <int EPI>
+void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
+                        double beta, const int* go) {
+  const int minb = env_int("RADMM_PIPE_MINB", 2);  // measured: 2 CTAs/SM (128 regs) streams best
+  auto kern = minb >= 4 ? coldot_pipe_kernel<EPI, 256, 4> : minb == 2 ? coldot_pipe_kernel<EPI, 256, 2>
+                                                                       : coldot_pipe_kernel<EPI, 256, 3>;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  int per_sm = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  const int target = c->sm_count * std::max(1, per_sm);
+  const int gx = std::max(1, std::min((n_max + 8 * 2 - 1) / (8 * 2), (int)((target + nb - 1) / nb)));
+  LAUNCH(c, kern, dim3(gx, (unsigned)nb), 256, smem, pk, mu, beta, go);
+}
+
 int coldot_cpw() {
   static int v = [] {
     const char* e = std::getenv("RADMM_CPW");
@@ -542,7 +557,11 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
       coldot_launch<T, EPI, true, 2, 1024>(c, pk, nb, n_max, smem, mu, beta, go);
       continue;
     }
-    if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta, go);
+    bool even = true;  // the pipelined kernel streams 64-row steps in fours
+    for (size_t i = 0; i < nb; ++i) even = even && ((pk.j[i].len + 63) / 64) % 4 == 0;
+    if (std::is_same<T, float2>::value && EPI != EPI_XPRIMAL && cpw == 2 && even && env_int("RADMM_COLDOT_PIPE", 1))
+      coldot_pipe_launch<EPI>(c, pk, nb, n_max, smem, mu, beta, go);
+    else if (cpw == 1) coldot_launch<T, EPI, true, 1>(c, pk, nb, n_max, smem, mu, beta, go);
     else if (cpw == 2) coldot_launch<T, EPI, true, 2>(c, pk, nb, n_max, smem, mu, beta, go);
     else coldot_launch<T, EPI, true, 4>(c, pk, nb, n_max, smem, mu, beta, go);
   }
@@ -606,6 +625,14 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
+  } else if (env_int("RADMM_HERM_PERSIST", 1)) {
+    auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
+    const size_t smem = herm_persist_smem(nr);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
+    LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
   } else if (nr == 1) {
     LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   } else {
