@@ -1138,9 +1138,8 @@ constexpr int kGrBM = 128, kGrBN = 64, kGrPA = 132, kGrPB = 68;
 constexpr size_t kGrStage = (size_t)kFbBK * (kGrPA + kGrPB) * 8;
 constexpr size_t kGramSmem = kFbStages * kGrStage;
 
-__global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __restrict__ jobs, double mu, double beta) {
+__device__ __forceinline__ void gram_dmma_body(const GramJob& jb, double mu, double beta) {
   constexpr int BK = kFbBK, S = kFbStages;
-  const GramJob& jb = jobs[blockIdx.z];
   const int m0 = blockIdx.y * kGrBM, n0 = blockIdx.x * kGrBN;
   const int m = jb.m;
   if (m0 >= m || n0 >= m || m0 + kGrBM <= n0) return;  // outside, or strictly upper
@@ -1255,6 +1254,32 @@ __global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __rest
         jb.C[i + (int64_t)j * jb.ldc] = o;
         if (i != j) jb.C[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
       }
+}
+
+__global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __restrict__ jobs, double mu, double beta) {
+  gram_dmma_body(jobs[blockIdx.z], mu, beta);
+}
+
+// one job passed by value (no job-table upload on the issuing stream)
+__global__ void __launch_bounds__(256, 1) gram_dmma1_kernel(const __grid_constant__ GramJob job, double mu, double beta) {
+  gram_dmma_body(job, mu, beta);
+}
+
+// C <- beta I + mu C for a raw Gram (eager_gram): the same roundings as
+// gram_dmma_kernel applying mu, beta itself (mu * c, then + beta on the
+// diagonal, imaginary diagonal exactly 0).
+__global__ void gram_scale_kernel(double2* __restrict__ C, int64_t ldc, int n, double mu, double beta) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  const int i = (int)(e % n), j = (int)(e / n);
+  double2* p = C + i + (int64_t)j * ldc;
+  const double2 v = *p;
+  double2 o = make_double2(mu * v.x, mu * v.y);
+  if (i == j) {
+    o.x += beta;
+    o.y = 0.0;
+  }
+  *p = o;
 }
 
 // out_f[i] = sum_s part[s][f][i] (fixed split order) for every frame of a job

@@ -205,6 +205,9 @@ struct Sensor {
   // factor of the base active set; the eliminated columns D accumulate in
   // P = G A_D (ld x kLazyMax) with Sinv = (I - mu A_D^H P)^{-1}, and are
   // folded into G only when kLazyMax is reached.
+  // raw full-set Gram A A^H computed right after the operator upload (overlaps
+  // the next sensor's upload); the run's first factorization scales it
+  bool raw_gram = false;
   int lz_d = 0;    // |D|
   int lz_new = 0;  // 1: P[:, d-1] = G a is formed by the next G-apply (second right-hand side)
   int lz_r = 0;    // columns added by the last event (bordered Sinv update pending)
@@ -248,6 +251,9 @@ struct radmm_ctx {
   int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API)
   int sweep_clusters = 0;  // clusters of the last fused sweep (= partial chunks it left)
   cudaStream_t stream = nullptr;
+  cudaStream_t up_stream = nullptr;  // operator uploads (overlap the previous sensor's Gram)
+  cudaEvent_t up_event = nullptr;
+  std::vector<cudaEvent_t> gram_evs;  // per sensor: its eager Gram (a re-upload waits for it)
   std::vector<Sensor> sensors;
   DArr<double2> s, xg, sigma, sigma_pre, gap;
   DArr<double> fpart;
@@ -337,6 +343,10 @@ struct radmm_ctx {
     if (h_totals) cudaFreeHost(h_totals);
     if (h_flags) cudaFreeHost(h_flags);
     if (stream && own_stream) cudaStreamDestroy(stream);
+    if (up_stream) cudaStreamDestroy(up_stream);
+    if (up_event) cudaEventDestroy(up_event);
+    for (cudaEvent_t e : gram_evs)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -482,6 +492,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
   S.g0_valid = false;  // a new operator invalidates the cached factor
+  S.raw_gram = false;
   S.has_y = false;
 }
 
@@ -510,6 +521,19 @@ void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max
   LAUNCH(c, kern, dim3(gx, (unsigned)nb), THREADS, SMEM ? smem : 0, pk, mu, beta, go);
 }
 
+// CTAs per job for a batch of nb jobs on `slots` resident CTA slots: the
+// smallest count whose total fills whole waves (< 3% idle in the last wave),
+// so a large batch (the segmented config-3 adjoint: 64 jobs) has no
+// nearly-empty tail wave.  At most gmax (the columns to go round).
+int wave_grid(int slots, int nb, int gmax) {
+  int best = std::max(1, std::min(gmax, (slots + nb - 1) / nb));
+  for (int gx = 1; gx <= std::min(gmax, 64 * slots); ++gx) {
+    const int64_t total = (int64_t)gx * nb, waves = (total + slots - 1) / slots;
+    if (waves * slots - total <= (waves * slots) * 3 / 100 && total >= slots) return gx;
+  }
+  return best;
+}
+
 template <int EPI>
 void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
                         double beta, const int* go) {
@@ -519,9 +543,9 @@ void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int 
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   int per_sm = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-  const int target = c->sm_count * std::max(1, per_sm);
-  const int gx = std::max(1, std::min((n_max + 8 * 2 - 1) / (8 * 2), (int)((target + nb - 1) / nb)));
-  LAUNCH(c, kern, dim3(gx, (unsigned)nb), 256, smem, pk, mu, beta, go);
+  const int slots = c->sm_count * std::max(1, per_sm);
+  const int gmax = std::max(1, (n_max + 8 * 2 - 1) / (8 * 2));
+  LAUNCH(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
 }
 
 int coldot_cpw() {
@@ -923,15 +947,21 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
     S.lz_d = S.lz_new = 0;  // a fresh factor of the current set
     const int dim = S.primal ? S.n_act : S.rows;
     const int64_t ldg = S.primal ? round_up(dim, 32) : S.ld;
+    const bool raw = S.raw_gram && !S.primal && S.n_act == c->N && S.ldg == ldg;
     ensure_g(S, dim, ldg);
     S.ldg = ldg;
     S.g_n = dim;
-    CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)ldg * dim, c->stream));
+    if (!raw) CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)ldg * dim, c->stream));
     if (S.primal) {
       // Gram mu A_J^H A_J + beta I (solver_core.hpp:39-40)
       jobs.push_back(gjob(dim, dim, S.rows, mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p),
                           mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
       jobs.back().herm = 1;  // Hermitian: lower tiles + mirror
+    } else if (S.raw_gram && S.n_act == c->N && S.ldg == ldg) {
+      // the full-set Gram was formed at upload (eager_gram): scale it in place
+      // (same roundings as forming beta I + mu A A^H directly)
+      LAUNCH(c, gram_scale_kernel, dim3((unsigned)((int64_t)dim * dim + 255) / 256), 256, 0, S.G.p, ldg, dim, mu,
+             beta);
     } else if (env_int("RADMM_GRAM", 1)) {
       // capacitance beta I + mu A_J A_J^H on the fp64 tensor cores
       grams.push_back(GramJob{S.A.p, S.ld, S.J.p, S.n_act, S.rows, S.G.p, ldg});
@@ -942,6 +972,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
       jobs.back().herm = 1;
     }
     inv.push_back({S.G.p, ldg, dim});
+    S.raw_gram = false;  // G now holds (becomes) the factor
     ++c->rebuilds;
   }
   if (!grams.empty()) {
@@ -2682,6 +2713,30 @@ int radmm_ctx_destroy(radmm_ctx* ctx) {
   });
 }
 
+// Eager full-set Gram A A^H (dual sensors) on the context stream, ordered
+// after `ev` (the operator upload): the tensor-core Gram of sensor q runs
+// while sensor q+1 uploads.  The first run scales it (full_rebuild).
+void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
+  if (c->parent || S.rows >= c->N || !env_int("RADMM_EAGER_GRAM", 1) || !env_int("RADMM_GRAM", 1)) return;
+  if (ev) CK(cudaStreamWaitEvent(c->stream, ev, 0));
+  ensure_g(S, S.rows, S.ld);
+  S.ldg = S.ld;
+  S.g_n = S.rows;
+  S.primal = false;
+  CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)S.ld * S.rows, c->stream));
+  // the job travels as a kernel parameter: a pageable job-table upload would
+  // wait for the previous sensor's Gram and serialise the pipeline
+  const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, S.G.p, S.ld};
+  CK(cudaFuncSetAttribute(gram_dmma1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
+  LAUNCH(c, gram_dmma1_kernel,
+         dim3((unsigned)((S.rows + kGrBN - 1) / kGrBN), (unsigned)((S.rows + kGrBM - 1) / kGrBM), 1u), 256,
+         kGramSmem, g, 1.0, 0.0);
+  S.raw_gram = true;
+  if (c->gram_evs.size() < (size_t)c->Q) c->gram_evs.resize(c->Q, nullptr);
+  if (!c->gram_evs[q]) CK(cudaEventCreateWithFlags(&c->gram_evs[q], cudaEventDisableTiming));
+  CK(cudaEventRecord(c->gram_evs[q], c->stream));
+}
+
 int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int64_t lda, int ptr_kind) {
   return guarded([&] {
     Sensor& S = sensor_at(ctx, q);
@@ -2690,12 +2745,26 @@ int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int6
     set_device(ctx);
     prepare_operator(ctx, S, rows);
     const cudaMemcpyKind kind = ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // host operators upload on their own stream (the data rows; the padding
+    // rows are zeroed on the context stream), so the previous sensor's eager
+    // Gram keeps running; the call returns once the host buffer is consumed
+    const bool host = ptr_kind != RADMM_PTR_DEVICE && !ctx->parent;
+    if (host && !ctx->up_stream) {
+      CK(cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->up_event, cudaEventDisableTiming));
+    }
+    cudaStream_t st = host ? ctx->up_stream : ctx->stream;
+    if (host && (size_t)q < ctx->gram_evs.size() && ctx->gram_evs[q])  // a queued Gram may still read A_q
+      CK(cudaStreamWaitEvent(st, ctx->gram_evs[q], 0));
     if (lda == S.ld && rows == S.ld)  // contiguous: one linear copy
-      CK(cudaMemcpyAsync(S.A.p, a, sizeof(float2) * (size_t)rows * ctx->N, kind, ctx->stream));
+      CK(cudaMemcpyAsync(S.A.p, a, sizeof(float2) * (size_t)rows * ctx->N, kind, st));
     else
       CK(cudaMemcpy2DAsync(S.A.p, S.ld * sizeof(float2), a, lda * sizeof(float2), rows * sizeof(float2), ctx->N,
-                           kind, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+                           kind, st));
+    if (host) CK(cudaEventRecord(ctx->up_event, st));
+    eager_gram(ctx, S, q, host ? ctx->up_event : nullptr);
+    if (host) CK(cudaStreamSynchronize(st));
+    else CK(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -2754,10 +2823,19 @@ int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind) 
     if (!y) fail(RADMM_INVALID_ARGUMENT, "null measurement");
     set_device(ctx);
     S.y.alloc(S.ld);
-    CK(cudaMemcpyAsync(S.y.p, y, sizeof(double2) * S.rows,
-                       ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));  // the caller may reuse y on return
+    if (ptr_kind != RADMM_PTR_DEVICE && ctx->up_stream) {
+      // on the upload stream (a queued eager Gram keeps running); the context
+      // stream is ordered after it by an event
+      CK(cudaMemcpyAsync(S.y.p, y, sizeof(double2) * S.rows, cudaMemcpyHostToDevice, ctx->up_stream));
+      CK(cudaEventRecord(ctx->up_event, ctx->up_stream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->up_event, 0));
+      CK(cudaStreamSynchronize(ctx->up_stream));  // the caller may reuse y on return
+    } else {
+      CK(cudaMemcpyAsync(S.y.p, y, sizeof(double2) * S.rows,
+                         ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));  // the caller may reuse y on return
+    }
     S.has_y = true;
   });
 }

@@ -396,6 +396,20 @@ def test_elimination_event_paths_match_oracle(nside, K, tol, iters, variant, mon
     assert max(errs[k] for k in ("sensor_images", "sigma")) < 1e-6, errs
 
 
+def test_eager_upload_gram_is_bitwise_identical(monkeypatch):
+    """The full-set Gram formed right after each operator upload (overlapping
+    the next sensor's upload) and scaled at run time gives the same factor,
+    bit for bit, as forming beta I + mu A A^H at run time."""
+    ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=60)
+    hyper = dict(hyper, screening_tol=1e-3)
+    eager = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    monkeypatch.setenv("RADMM_EAGER_GRAM", "0")
+    late = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    for a, b in zip(eager.sensor_images, late.sensor_images):
+        assert np.array_equal(a, b)
+    assert np.array_equal(eager.sigma, late.sigma)
+
+
 def test_sharded_context_world1_equals_plain():
     from paper_2307_08606_b200 import distributed as D
     ops, ys, hyper = _small_c1(nside=16, K=16, max_iter=40)
