@@ -429,21 +429,43 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
     if (t + 1 < nk) stash(cur ^ 1);
     __syncthreads();
   }
+  // Epilogue, one 8-row block (a) at a time: its 8 C / R' inputs are loaded
+  // first (independent loads in flight together), then combined and stored.
+  // Interleaving each read with the previous element's store would serialise
+  // them (the compiler cannot move a load above a possibly aliasing store):
+  // 32 dependent round trips per thread on the read-modify-write updates.
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 4; ++a) {
+    const int i = m0 + wm + 8 * a + fr;
+    double2 cin[4][2];
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int i = m0 + wm + 8 * a + fr, j = n0 + wn + 8 * b + 2 * fc + v;
+        const int j = n0 + wn + 8 * b + 2 * fc + v;
+        cin[b][v] = make_double2(0.0, 0.0);
+        if (i >= jb.m || j >= jb.n) continue;
+        if (EPI == GEPI_PLAIN) {
+          if (jb.beta0 != 0.0 && !(jb.herm && i < j)) cin[b][v] = jb.c[i + (int64_t)j * jb.ldc];
+        } else if (i >= jb.k0 && i < jb.k0 + jb.kb) {
+          cin[b][v] = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
+        } else if (!(j >= jb.k0 && j < jb.k0 + jb.kb)) {
+          cin[b][v] = jb.c[i + (int64_t)j * jb.ldc];
+        }
+      }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = n0 + wn + 8 * b + 2 * fc + v;
         if (i >= jb.m || j >= jb.n) continue;
         double2* cp = jb.c + i + (int64_t)j * jb.ldc;
         const double accr = p1[a][b][v] - p2[a][b][v], acci = p3[a][b][v] - p1[a][b][v] - p2[a][b][v];
+        const double2 c0 = cin[b][v];
         if (EPI == GEPI_PLAIN) {
           if (jb.herm && i < j) continue;
           double2 o = make_double2(jb.alpha * accr, jb.alpha * acci);
           if (jb.beta0 != 0.0) {
-            const double2 c0 = *cp;
             o.x += jb.beta0 * c0.x;
             o.y += jb.beta0 * c0.y;
           }
@@ -453,17 +475,15 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
           }
           *cp = o;
           if (jb.herm && i != j) jb.c[j + (int64_t)i * jb.ldc] = make_double2(o.x, -o.y);
+        } else if (i >= jb.k0 && i < jb.k0 + jb.kb) {
+          //   i in K:      M[i,j] = R'[i-k0, j]
+          *cp = c0;
         } else {
-          const bool iK = i >= jb.k0 && i < jb.k0 + jb.kb;
-          if (iK) {
-            *cp = reinterpret_cast<const double2*>(jb.b.p)[(i - jb.k0) + (int64_t)j * jb.b.ld];
-          } else {
-            const bool jK = j >= jb.k0 && j < jb.k0 + jb.kb;
-            const double2 c0 = jK ? make_double2(0.0, 0.0) : *cp;
-            *cp = make_double2(c0.x - accr, c0.y - acci);
-          }
+          //   i not in K:  M[i,j] = (j in K ? 0 : M[i,j]) - (F R')[i,j]
+          *cp = make_double2(c0.x - accr, c0.y - acci);
         }
       }
+  }
 }
 
 // C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.

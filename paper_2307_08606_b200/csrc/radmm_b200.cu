@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include <chrono>
 #include <cmath>
@@ -183,6 +184,11 @@ struct Sensor {
   DArr<double2> G0;
   bool g0_valid = false, g0_primal = false;
   double g0_mu = 0, g0_beta = 0;
+  // G itself still holds the full-set factor of (base_mu, base_beta) (no
+  // downdate, fold or rebuild since): the next run reuses it in place, and G0
+  // is written only just before G is first modified (snapshot_base)
+  bool g_is_base = false;
+  double base_mu = 0, base_beta = 0;
   int64_t g0_ld = 0;
   int g0_n = 0;
   int64_t ldg = 0;
@@ -239,6 +245,35 @@ struct Scratch {
 
 }  // namespace
 
+// Process-wide free list of mapped pinned host blocks (size classes of
+// powers of two from 64 KB).  Never returned to the driver.
+size_t pinned_class(size_t bytes) {
+  size_t c = 64 << 10;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+std::mutex g_pinned_mu;
+std::vector<std::pair<size_t, char*>> g_pinned_free;
+char* pinned_get(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    for (size_t i = 0; i < g_pinned_free.size(); ++i)
+      if (g_pinned_free[i].first == bytes) {
+        char* p = g_pinned_free[i].second;
+        g_pinned_free.erase(g_pinned_free.begin() + i);
+        return p;
+      }
+  }
+  char* p = nullptr;
+  CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  return p;
+}
+void pinned_put(char* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back({bytes, p});
+}
+
 struct radmm_ctx {
   int device = 0;
   int N = 0;
@@ -262,6 +297,8 @@ struct radmm_ctx {
   FusionScalars* fs_host = nullptr;
   FusionScalars* fs_host_dev = nullptr;
   DArr<const double2*> contrib;
+  char* pinned_block = nullptr;  // mapped pinned block holding fs_host, h_totals, h_flags (pinned_get)
+  size_t pinned_bytes = 0;
   int* h_totals = nullptr;   // mapped pinned, 3 slots x local sensors (kept counts; see enqueue_screen)
   int* d_totals = nullptr;   // device alias of h_totals
   int* h_flags = nullptr;    // pinned, kFlagCap (deferred pivot flags accumulate)
@@ -331,6 +368,14 @@ struct radmm_ctx {
   DArr<double2> xg_alt, sigma_alt;  // v5 writes the new x_G / sigma here, then they swap
 
   ~radmm_ctx() {
+    const bool tr = std::getenv("RADMM_TRACE_DESTROY") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!tr) return;
+      const auto n = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[radmm ~ctx] %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+      t = n;
+    };
     if (device >= 0) cudaSetDevice(device);
     frames.clear();  // children use this context's stream and operators
     if (ev_it0) cudaEventDestroy(ev_it0);
@@ -338,15 +383,22 @@ struct radmm_ctx {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_steps) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_ends) cudaEventDestroy(e);
+    mark("events");
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
-    if (fs_host) cudaFreeHost(fs_host);
-    if (h_totals) cudaFreeHost(h_totals);
-    if (h_flags) cudaFreeHost(h_flags);
+    pinned_put(pinned_block, pinned_bytes);  // fs_host / h_totals / h_flags live in it
+    mark("host");
     if (stream && own_stream) cudaStreamDestroy(stream);
     if (up_stream) cudaStreamDestroy(up_stream);
     if (up_event) cudaEventDestroy(up_event);
     for (cudaEvent_t e : gram_evs)
       if (e) cudaEventDestroy(e);
+    mark("streams");
+    scratch.buf.release();
+    mark("scratch");
+    for (DArr<double2>* v : {&s, &xg, &sigma, &sigma_pre, &gap, &send_buf, &gathered, &split_ws, &fb_part, &xg_alt,
+                             &sigma_alt})
+      v->release();
+    mark("vectors");
   }
 };
 
@@ -443,14 +495,22 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   c->fpart.alloc((size_t)fblocks * 5);
   c->fcounter.alloc(1);
   c->fs_dev.alloc(1);
-  CK(cudaHostAlloc(&c->fs_host, 2 * sizeof(FusionScalars), cudaHostAllocMapped));
+  // one mapped pinned block for the host-visible scalars, from a process-wide
+  // free list: cudaFreeHost can stall for hundreds of ms, so blocks are reused
+  // across contexts instead of freed
+  const size_t off_tot = round_up(2 * sizeof(FusionScalars), 256);
+  const size_t off_flags = off_tot + round_up(sizeof(int) * 3 * std::max(1, q_local), 256);
+  c->pinned_bytes = pinned_class(off_flags + sizeof(int) * kFlagCap);
+  c->pinned_block = pinned_get(c->pinned_bytes);
+  std::memset(c->pinned_block, 0, c->pinned_bytes);
+  c->fs_host = reinterpret_cast<FusionScalars*>(c->pinned_block);
   std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
   c->go_flags.alloc(2);
   c->sgo_flags.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
-  CK(cudaHostAlloc(&c->h_totals, sizeof(int) * 3 * std::max(1, q_local), cudaHostAllocMapped));
+  c->h_totals = reinterpret_cast<int*>(c->pinned_block + off_tot);
   CK(cudaHostGetDevicePointer((void**)&c->d_totals, c->h_totals, 0));
-  CK(cudaHostAlloc(&c->h_flags, sizeof(int) * kFlagCap, cudaHostAllocDefault));
+  c->h_flags = reinterpret_cast<int*>(c->pinned_block + off_flags);
   c->fail_flags.alloc(kMaxBatch);
   for (int q = 0; q < q_local; ++q) {
     Sensor& S = c->sensors[q];
@@ -492,6 +552,7 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
   S.g0_valid = false;  // a new operator invalidates the cached factor
+  S.g_is_base = false;
   S.raw_gram = false;
   S.has_y = false;
 }
@@ -1181,6 +1242,7 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
 }
 
 void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu);
+void snapshot_base(radmm_ctx* c, Sensor& S, bool modify);
 
 // Downdates after screening removed rem_q columns: dual sensors accumulate
 // them lazily (up to kLazyMax, then fold); primal sensors and large removals
@@ -1196,6 +1258,8 @@ void downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     if (!S.primal && S.lz_d > 0 && (!use_lazy || S.lz_d + S.removed_now > cap)) fold.push_back(q);
     (use_lazy ? lazy : eager).push_back(q);
   }
+  for (int q : fold) snapshot_base(c, c->sensors[q], true);
+  for (int q : eager) snapshot_base(c, c->sensors[q], true);
   lazy_fold(c, fold, mu);
   lazy_append(c, lazy, mu);
   eager_downdate(c, eager, mu);
@@ -1382,19 +1446,30 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
   std::vector<int> fresh;
   for (int q : all) {
     Sensor& S = c->sensors[q];
-    if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta) {
+    if (S.g_is_base && S.base_mu == h->mu && S.base_beta == h->beta) {
+      ++c->factor_cache_hits;  // G is untouched since its full-set factorization
+    } else if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta) {
       if (S.G.n < (size_t)S.g0_ld * S.g0_n) S.G.alloc((size_t)S.g0_ld * S.g0_n);
       CK(cudaMemcpyAsync(S.G.p, S.G0.p, sizeof(double2) * (size_t)S.g0_ld * S.g0_n, cudaMemcpyDeviceToDevice,
                          c->stream));
       S.primal = S.g0_primal;
       S.ldg = S.g0_ld;
       S.g_n = S.g0_n;
+      S.g_is_base = true;
+      S.base_mu = h->mu;
+      S.base_beta = h->beta;
       ++c->factor_cache_hits;
     } else {
       fresh.push_back(q);
     }
   }
   full_rebuild(c, fresh, h->mu, h->beta);
+  for (int q : fresh) {
+    Sensor& S = c->sensors[q];
+    S.g_is_base = true;
+    S.base_mu = h->mu;
+    S.base_beta = h->beta;
+  }
   // size the event-path scratch once (a 64-column downdate on every sensor)
   // so elimination rounds never stop to grow it
   {
@@ -1406,27 +1481,35 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
     }
     c->scratch.reserve(need);
   }
-  // keep a copy for the next run when memory allows (always leave >= 4 GB free)
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  for (int q : fresh) {
-    Sensor& S = c->sensors[q];
-    if (!S.G0.own) S.G0.release();  // never write through a view of another context's factor
-    const size_t bytes = sizeof(double2) * (size_t)S.ldg * S.g_n;
-    if (env_int("RADMM_FACTOR_CACHE", 1) == 0 || (S.G0.n < bytes / sizeof(double2) && free_b < bytes + (4ull << 30)))
-      continue;
-    if (S.G0.n < bytes / sizeof(double2)) {
-      S.G0.alloc(bytes / sizeof(double2), false);
-      free_b -= bytes;
+}
+
+// Keep the full-set factor for the next run before G is first modified: copy
+// G -> G0 when memory allows (always leaves >= 4 GB free).  `modify`: the
+// caller is about to change G (downdate, fold, rebuild), so G stops being
+// the base factor.
+void snapshot_base(radmm_ctx* c, Sensor& S, bool modify) {
+  if (!S.g_is_base) return;
+  if (modify) S.g_is_base = false;
+  if (S.g0_valid && S.g0_mu == S.base_mu && S.g0_beta == S.base_beta && S.g0_ld == S.ldg && S.g0_n == S.g_n) return;
+  if (env_int("RADMM_FACTOR_CACHE", 1) == 0) return;
+  if (!S.G0.own) S.G0.release();  // never write through a view of another context's factor
+  const size_t bytes = sizeof(double2) * (size_t)S.ldg * S.g_n;
+  if (S.G0.n < bytes / sizeof(double2)) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (free_b < bytes + (4ull << 30)) {
+      S.g0_valid = false;
+      return;
     }
-    CK(cudaMemcpyAsync(S.G0.p, S.G.p, bytes, cudaMemcpyDeviceToDevice, c->stream));
-    S.g0_valid = true;
-    S.g0_primal = S.primal;
-    S.g0_mu = h->mu;
-    S.g0_beta = h->beta;
-    S.g0_ld = S.ldg;
-    S.g0_n = S.g_n;
+    S.G0.alloc(bytes / sizeof(double2), false);
   }
+  CK(cudaMemcpyAsync(S.G0.p, S.G.p, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  S.g0_valid = true;
+  S.g0_primal = S.primal;
+  S.g0_mu = S.base_mu;
+  S.g0_beta = S.base_beta;
+  S.g0_ld = S.ldg;
+  S.g0_n = S.g_n;
 }
 
 // Adjoint + x-update.  When KM is so large that one shared copy of w per
@@ -1709,6 +1792,7 @@ uint64_t apply_screen(radmm_ctx* c, const radmm_hyperparams* h, int k, int slot)
       (S.removed_now <= S.rows ? down : rebuild).push_back(q);
     }
   }
+  for (int q : rebuild) snapshot_base(c, c->sensors[q], true);
   full_rebuild(c, rebuild, h->mu, h->beta);
   downdate(c, down, h->mu);
   return notice;
@@ -2358,10 +2442,11 @@ radmm_ctx* frame_ctx(radmm_ctx* p, int f) {
 // Point frame f's factor cache at a full-set factor computed elsewhere (the
 // parent's, or frame 0's): the frame's begin_run then copies it instead of
 // refactorising (the factor depends on A, mu, beta only).
-void share_factor(radmm_ctx* dst, const radmm_ctx* src, double mu, double beta) {
+void share_factor(radmm_ctx* dst, radmm_ctx* src, double mu, double beta) {
   for (int q = 0; q < dst->Q; ++q) {
     Sensor& D = dst->sensors[q];
-    const Sensor& S = src->sensors[q];
+    Sensor& S = src->sensors[q];
+    if (S.g_is_base && S.base_mu == mu && S.base_beta == beta) snapshot_base(src, S, false);
     if (!S.g0_valid || S.g0_mu != mu || S.g0_beta != beta) continue;
     if (D.g0_valid && D.g0_mu == mu && D.g0_beta == beta) continue;
     D.G0.view(S.G0.p, S.G0.n);
@@ -2709,6 +2794,23 @@ int radmm_ctx_create(int device, int n_pixels, int n_sensors, radmm_ctx** out) {
 int radmm_ctx_destroy(radmm_ctx* ctx) {
   return guarded([&] {
     if (ctx && ctx->parent) fail(RADMM_INVALID_ARGUMENT, "frame contexts are owned by their parent context");
+    if (ctx && env_int("RADMM_TRACE_DESTROY", 0)) {
+      auto now = [] { return std::chrono::steady_clock::now(); };
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      const auto t0 = now();
+      cudaSetDevice(ctx->device);
+      cudaDeviceSynchronize();
+      const auto t1 = now();
+      ctx->frames.clear();
+      const auto t2 = now();
+      ctx->sensors.clear();
+      const auto t3 = now();
+      delete ctx;
+      const auto t4 = now();
+      std::fprintf(stderr, "[radmm destroy] sync %.2f ms, frames %.2f ms, sensors %.2f ms, rest %.2f ms\n", ms(t0, t1),
+                   ms(t1, t2), ms(t2, t3), ms(t3, t4));
+      return;
+    }
     delete ctx;
   });
 }
