@@ -612,8 +612,14 @@ __device__ __forceinline__ double2 soft_threshold1(double2 v, double kappa) {
 // contrib(k) returns sensor k's image value at j.
 template <typename Contrib>
 __device__ __forceinline__ void fusion_pixel(const FusionArgs& a, int j, Contrib contrib, double (&q)[5]) {
+  // fixed sensor order (admm.hpp:239); four loads issued together, summed in order
   double2 s = make_double2(0.0, 0.0);
-  for (int k = 0; k < a.Q; ++k) s = c_add(s, contrib(k));  // fixed sensor order (admm.hpp:239)
+  int k = 0;
+  for (; k + 4 <= a.Q; k += 4) {
+    const double2 v0 = contrib(k), v1 = contrib(k + 1), v2 = contrib(k + 2), v3 = contrib(k + 3);
+    s = c_add(c_add(c_add(c_add(s, v0), v1), v2), v3);
+  }
+  for (; k < a.Q; ++k) s = c_add(s, contrib(k));
   s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
   const double2 xgp = a.xg[j];
   const double2 sg = a.sigma[j];
