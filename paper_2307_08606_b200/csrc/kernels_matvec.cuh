@@ -446,9 +446,11 @@ __global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant_
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ unsigned char smem_raw[];
   const FwdJob& jb = jobs.j[blockIdx.z];
-  const int chunk = blockIdx.x;
+  // row tiles fastest: the CTAs that run together cover every row tile of the
+  // same column chunk, so each column is streamed whole (DRAM page / TLB locality)
+  const int chunk = blockIdx.y;
   if (chunk >= jb.n_chunks) return;
-  const int64_t row0 = (int64_t)blockIdx.y * kFwdTile;
+  const int64_t row0 = (int64_t)blockIdx.x * kFwdTile;
   if (row0 >= jb.ld) return;
   const int i0 = chunk * jb.chunk_len;
   const int cnt = min(jb.chunk_len, jb.n - i0);
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant_
       const double2 d = jb.data[i], g = gap[c], xh = jb.x_hat[i], sg = sigma[c];
       v.x = __dsub_rn(__dadd_rn(__dadd_rn(d.x, __dmul_rn(beta, g.x)), __dmul_rn(beta, xh.x)), sg.x);
       v.y = __dsub_rn(__dadd_rn(__dadd_rn(d.y, __dmul_rn(beta, g.y)), __dmul_rn(beta, xh.y)), sg.y);
-      if (blockIdx.y == 0) jb.rhs_out[i] = v;
+      if (blockIdx.x == 0) jb.rhs_out[i] = v;
     } else {
       v = jb.src[c];
     }

@@ -777,7 +777,7 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
       const size_t smem = (size_t)max_len * (sizeof(double2) + sizeof(int));
       if (smem > 48 * 1024)
         CK(cudaFuncSetAttribute(fwd_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      dim3 grid(max_chunks, (unsigned)((ld_max + kFwdTile - 1) / kFwdTile), (unsigned)nb);
+      dim3 grid((unsigned)((ld_max + kFwdTile - 1) / kFwdTile), max_chunks, (unsigned)nb);
       LAUNCH(c, fwd_kernel<MODE>, grid, kFwdThreads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
     dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
