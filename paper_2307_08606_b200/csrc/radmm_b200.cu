@@ -710,7 +710,7 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
-  } else if (env_int("RADMM_HERM_PERSIST", 1)) {
+  } else if (nr == 2 || env_int("RADMM_HERM_PERSIST", 1)) {
     auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
     const size_t smem = herm_persist_smem(nr);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -718,10 +718,8 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
     LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
-  } else if (nr == 1) {
-    LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   } else {
-    LAUNCH(c, herm_gapply_kernel<2>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
+    LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
   LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), 256, 0, pk, go);
 }
