@@ -656,7 +656,9 @@ void coldot(radmm_ctx* c, const std::vector<ColDotJob>& jobs, double mu, double 
 bool herm_enabled() { return env_int("RADMM_HERM", 1) != 0; }
 
 // algorithmic bytes of one G-apply: the Hermitian triangle (or the full matrix)
-double gapply_bytes(int n) { return herm_enabled() ? 8.0 * n * (n + 1.0) : 16.0 * n * (double)n; }
+double gapply_bytes(int n) {
+  return herm_enabled() && n >= env_int("RADMM_HERM_MIN_ROWS", 512) ? 8.0 * n * (n + 1.0) : 16.0 * n * (double)n;
+}
 
 // Job table for the listed (dual) sensors: v = S.v -> w = S.w, plus the work
 // item list, rebuilt only when the batch signature changes.
@@ -724,9 +726,15 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
   LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), 256, 0, pk, go);
 }
 
+// Below this order the triangle's few long strips (one CTA each) are
+// latency-bound: the full-matrix column-dot apply spreads over more CTAs.
+constexpr int kHermMinRows = 512;
+
 void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
   if (qs.empty()) return;
-  if (!herm_enabled() || qs.size() > (size_t)kMaxBatch) {
+  int rows_max = 0;
+  for (int q : qs) rows_max = std::max(rows_max, c->sensors[q].rows);
+  if (!herm_enabled() || qs.size() > (size_t)kMaxBatch || rows_max < env_int("RADMM_HERM_MIN_ROWS", kHermMinRows)) {
     std::vector<ColDotJob> gj;
     for (int q : qs) {
       Sensor& S = c->sensors[q];

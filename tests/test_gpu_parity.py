@@ -104,6 +104,7 @@ def test_dual_solves_hermitian_apply(rows, cols, herm, monkeypatch):
         monkeypatch.setenv("RADMM_ADJ_SPLIT_ROWS", "64")
         monkeypatch.setenv("RADMM_ADJ_SEG", "64")
     monkeypatch.setenv("RADMM_HERM", herm)
+    monkeypatch.setenv("RADMM_HERM_MIN_ROWS", "0")  # the triangle kernels even at these small orders
     rng = np.random.default_rng(rows + cols)
     if (rows, cols) == (256, 1024):
         cfg = scenario.baseline_config("c1")
@@ -366,8 +367,9 @@ def _small_c1(**kw):
 
 DOWNDATE_VARIANTS = {
     "lazy": {},                        # default: columns accumulate in P = G A_D, folded at 64
-    "lazy_folds": {"RADMM_LAZY_MAX": "3"},  # fold into G every few events
-    "lazy_full_gapply": {"RADMM_HERM": "0"},  # pending columns through the column-dot G-apply
+    "lazy_herm": {"RADMM_HERM_MIN_ROWS": "0"},  # single columns ride the triangle G-apply (NR = 2)
+    "lazy_folds": {"RADMM_LAZY_MAX": "3", "RADMM_HERM_MIN_ROWS": "0"},  # fold into G every few events
+    "lazy_full_gapply": {"RADMM_HERM": "0"},  # every column through the column-dot G-apply
     "eager": {"RADMM_LAZY": "0"},      # G rewritten at every event
 }
 
