@@ -486,6 +486,115 @@ __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant
   }
 }
 
+// Gauss-Jordan rank-kb update (kb <= 64), the dominant cost of the explicit
+// inverse: M[i,j] = (j in K ? 0 : M[i,j]) - sum_k F[i,k] R'[k,j] for i not in
+// K, M[i,j] = R'[i-k0, j] for i in K.  The whole K extent of both operands
+// fits in shared memory (F tile 128 x 64, R' tile 64 x 64, complex128, pitches
+// = 2 (mod 8) so a quarter warp's 16-B fragment loads hit distinct banks), so
+// one cp.async batch fills it and the 16 k4-steps of 3M DMMAs run without a
+// barrier.  Same k order and DMMA sequence as gemm_dmma_kernel<GEPI_GJ>:
+// bitwise-identical results.
+constexpr int kGjuBM = 128, kGjuBN = 64, kGjuPF = 130, kGjuPR = 66;
+constexpr size_t kGjuSmem = (size_t)64 * (kGjuPF + kGjuPR) * sizeof(double2);
+
+struct GjUpdJob {
+  double2* M;
+  int64_t ldm;
+  int n;
+  const double2* F;  // n x kb, leading dimension ldf
+  int64_t ldf;
+  const double2* R;  // kb x n, leading dimension 64
+  int k0, kb;
+};
+
+__global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant__ Pack<GjUpdJob> P) {
+  const GjUpdJob& jb = P.j[blockIdx.z];
+  const int m0 = blockIdx.y * kGjuBM, n0 = blockIdx.x * kGjuBN, n = jb.n, kb = jb.kb;
+  if (m0 >= n || n0 >= n) return;
+  extern __shared__ __align__(16) double2 gju[];
+  double2* Fs = gju;                   // [k][kGjuPF]
+  double2* Rs = gju + 64 * kGjuPF;     // [k][kGjuPR]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 64 * kGjuBM; e += 256) {  // F tile: 128 rows x 64 k (column-major source)
+    const int i = e % kGjuBM, k = e / kGjuBM;
+    const bool ok = m0 + i < n && k < kb;
+    cp_async16(Fs + k * kGjuPF + i, ok ? jb.F + (m0 + i) + (int64_t)k * jb.ldf : jb.F, ok);
+  }
+  for (int e = tid; e < 64 * kGjuBN; e += 256) {  // R' tile: 64 k x 64 columns
+    const int k = e % 64, j = e / 64;
+    const bool ok = n0 + j < n && k < kb;
+    cp_async16(Rs + k * kGjuPR + j, ok ? jb.R + k + (int64_t)(n0 + j) * 64 : jb.R, ok);
+  }
+  cp_async_commit();
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32, fr = lane >> 2, fc = lane & 3;
+  double p1[4][4][2], p2[4][4][2], p3[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) p1[a][b][v] = p2[a][b][v] = p3[a][b][v] = 0.0;
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll 1
+  for (int k4 = 0; k4 < 64; k4 += 4) {
+    double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double2 x = Fs[(k4 + fc) * kGjuPF + wm + 8 * a + fr];
+      ar[a] = x.x;
+      ai[a] = x.y;
+      as[a] = ar[a] + ai[a];
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double2 y = Rs[(k4 + fc) * kGjuPR + wn + 8 * b + fr];
+      br[b] = y.x;
+      bi[b] = y.y;
+      bs[b] = br[b] + bi[b];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        dmma884(p1[a][b], ar[a], br[b]);
+        dmma884(p2[a][b], ai[a], bi[b]);
+        dmma884(p3[a][b], as[a], bs[b]);
+      }
+  }
+  // epilogue (gemm_dmma_kernel<GEPI_GJ>), one 8-row block at a time, inputs first
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = m0 + wm + 8 * a + fr;
+    const bool iK = i >= jb.k0 && i < jb.k0 + kb;
+    double2 cin[4][2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = n0 + wn + 8 * b + 2 * fc + v;
+        cin[b][v] = make_double2(0.0, 0.0);
+        if (i >= n || j >= n) continue;
+        if (iK) cin[b][v] = jb.R[(i - jb.k0) + (int64_t)j * 64];
+        else if (!(j >= jb.k0 && j < jb.k0 + kb)) cin[b][v] = jb.M[i + (int64_t)j * jb.ldm];
+      }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = n0 + wn + 8 * b + 2 * fc + v;
+        if (i >= n || j >= n) continue;
+        double2* cp = jb.M + i + (int64_t)j * jb.ldm;
+        if (iK) {
+          *cp = cin[b][v];
+        } else {
+          const double accr = p1[a][b][v] - p2[a][b][v], acci = p3[a][b][v] - p1[a][b][v] - p2[a][b][v];
+          *cp = make_double2(cin[b][v].x - accr, cin[b][v].y - acci);
+        }
+      }
+  }
+}
+
 // C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
 __global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
                                   const double2* __restrict__ ws, int64_t ws_stride) {

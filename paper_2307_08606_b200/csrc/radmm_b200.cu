@@ -954,7 +954,22 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     LAUNCH(c, gj_panel_kernel, dim3(pblocks, (unsigned)T), 256, 0, dj);
     gemm<GEPI_PLAIN>(c, rjobs);
     LAUNCH(c, gj_fix_kernel, dim3((unsigned)T), 256, 0, dj);
-    gemm<GEPI_GJ>(c, ujobs);
+    if (env_int("RADMM_GJ_UPDATE", 1) && ujobs.size() <= (size_t)kMaxBatch) {
+      // rank-kb update with both operands resident in shared memory
+      Pack<GjUpdJob> up;
+      int nmax = 0;
+      for (size_t u = 0; u < ujobs.size(); ++u) {
+        const GemmJob& g = ujobs[u];
+        up.j[u] = GjUpdJob{g.c, g.ldc, g.m, reinterpret_cast<const double2*>(g.a.p), g.a.ld,
+                           reinterpret_cast<const double2*>(g.b.p), g.k0, g.kb};
+        nmax = std::max(nmax, g.m);
+      }
+      CK(cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjuSmem));
+      LAUNCH(c, gj_update_kernel, dim3((unsigned)((nmax + kGjuBN - 1) / kGjuBN), (unsigned)((nmax + kGjuBM - 1) / kGjuBM),
+                                       (unsigned)ujobs.size()), 256, kGjuSmem, up);
+    } else {
+      gemm<GEPI_GJ>(c, ujobs);
+    }
   }
   // flags land after any still-unchecked deferred ones
   if (c->pending_fail + T > (size_t)kFlagCap) {
