@@ -614,17 +614,20 @@ __device__ __forceinline__ double2 soft_threshold1(double2 v, double kappa) {
 // contrib(k) returns sensor k's image value at j.
 template <typename Contrib>
 __device__ __forceinline__ void fusion_pixel(const FusionArgs& a, int j, Contrib contrib, double (&q)[5]) {
-  // fixed sensor order (admm.hpp:239); four loads issued together, summed in order
-  double2 s = make_double2(0.0, 0.0);
-  int k = 0;
-  for (; k + 4 <= a.Q; k += 4) {
-    const double2 v0 = contrib(k), v1 = contrib(k + 1), v2 = contrib(k + 2), v3 = contrib(k + 3);
-    s = c_add(c_add(c_add(c_add(s, v0), v1), v2), v3);
-  }
-  for (; k < a.Q; ++k) s = c_add(s, contrib(k));
-  s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
+  // fixed sensor order (admm.hpp:239); the pixel's previous x_G and sigma and
+  // up to eight sensor values are loaded together, then summed in order
   const double2 xgp = a.xg[j];
   const double2 sg = a.sigma[j];
+  double2 s = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < a.Q; k0 += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = k0 + u < a.Q ? contrib(k0 + u) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < a.Q) s = c_add(s, v[u]);
+  }
+  s = make_double2(__ddiv_rn(s.x, (double)a.Q), __ddiv_rn(s.y, (double)a.Q));
   a.sigma_pre[j] = sg;
   const double2 v = make_double2(__dadd_rn(s.x, __ddiv_rn(sg.x, a.beta)), __dadd_rn(s.y, __ddiv_rn(sg.y, a.beta)));
   const double2 xg = soft_threshold1(v, a.kappa);
