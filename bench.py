@@ -47,7 +47,7 @@ sys.path.insert(0, ROOT)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=400)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
@@ -78,7 +78,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except FileNotFoundError:
@@ -173,7 +173,7 @@ def algorithmic_bytes_per_iteration(cfg, sizes):
 # ---------------------------------------------------------------------------
 # CPU baseline / reference arm (oracle; bounded sample)
 # ---------------------------------------------------------------------------
-def cpu_sample(cfg, iters: int, sample_sensors: int = 2):
+def cpu_sample(cfg, iters: int, sample_sensors: int = 2, budget_s: float = 20.0):
     """fp64 oracle (NumPy/SciPy, all BLAS threads) on `sample_sensors` of the Q
     sensors: time `iters` local updates + the fusion round; extrapolate the
     per-sensor cost x Q (the Jacobi sweep is a sum of independent per-sensor
@@ -197,7 +197,11 @@ def cpu_sample(cfg, iters: int, sample_sensors: int = 2):
     fusion = admm_ref.FusionRef(cfg.N, cfg.Q, h)
     t_local = 0.0
     t_fusion = 0.0
-    for _ in range(iters):
+    done = 0
+    for _ in range(iters):  # bounded: stops once ~budget_s of CPU work is timed
+        if done and t_local + t_fusion > budget_s:
+            break
+        done += 1
         t0 = time.perf_counter()
         for s in sensors:
             s.local_update(fusion.gap, fusion.sigma)
@@ -208,6 +212,7 @@ def cpu_sample(cfg, iters: int, sample_sensors: int = 2):
         t2 = time.perf_counter()
         t_local += t1 - t0
         t_fusion += t2 - t1
+    iters = done
     per_iter = (t_local / sample_sensors) * cfg.Q / iters + t_fusion / iters
     # one more iteration of one sensor on a single BLAS thread (SURVEY 8d asks
     # for the 1-thread figure next to the all-core one)
@@ -328,7 +333,10 @@ def ours(args, cfg):
     # ---- time to tolerance ------------------------------------------------
     ttt, ttt_hyper = None, None
     if not args.no_ttt:
+        clocks_ttt = ClockSampler(local)
+        clocks_ttt.start()
         ttt, ttt_hyper = time_to_tolerance(solver, hyper, args.ttt_max_iter)
+        ttt["clocks"] = clocks_ttt.stop()
     solver.close()
 
     # ---- e2e through the public API with pinned host buffers ---------------
