@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libradmm_b200.so")
+LIB_PATH = os.environ.get("RADMM_LIB_PATH") or os.path.join(_HERE, "libradmm_b200.so")  # override: A/B of builds
 
 OK, INVALID_ARGUMENT, NUMERICAL, TRANSPORT, CUDA, OUT_OF_MEMORY = range(6)
 PTR_HOST, PTR_DEVICE = 0, 1
