@@ -435,11 +435,15 @@ struct FwdJob {
   int chunk_len;
 };
 
+// 256 threads (512-row tiles) up to KM = 4096; 512 threads (1024-row tiles) on
+// taller operators (config 3: 6.0 -> 6.4 TB/s; config 2 prefers 256)
 constexpr int kFwdThreads = 256;
 constexpr int kFwdTile = 2 * kFwdThreads;
+constexpr int kFwdTallRows = 4096;
+__host__ __device__ constexpr int fwd_threads_for(int64_t ld) { return ld > kFwdTallRows ? 512 : 256; }
 
-template <int MODE>
-__global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant__ Pack<FwdJob> jobs,
+template <int MODE, int THREADS>
+__global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ Pack<FwdJob> jobs,
                                                           const double2* __restrict__ gap,
                                                           const double2* __restrict__ sigma, double beta,
                                                           const int* __restrict__ go) {
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(kFwdThreads) fwd_kernel(const __grid_constant_
   // same column chunk, so each column is streamed whole (DRAM page / TLB locality)
   const int chunk = blockIdx.y;
   if (chunk >= jb.n_chunks) return;
-  const int64_t row0 = (int64_t)blockIdx.x * kFwdTile;
+  const int64_t row0 = (int64_t)blockIdx.x * (2 * THREADS);
   if (row0 >= jb.ld) return;
   const int i0 = chunk * jb.chunk_len;
   const int cnt = min(jb.chunk_len, jb.n - i0);

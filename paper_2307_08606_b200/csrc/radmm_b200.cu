@@ -283,7 +283,8 @@ struct radmm_ctx {
   int rank = 0, world = 1;
   int q_max_local = 0;
   int sm_count = 148;
-  int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API)
+  int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API), 256-thread variant
+  int fwd_per_sm_tall = 2;  // the 512-thread variant (operators taller than kFwdTallRows)
   int sweep_clusters = 0;  // clusters of the last fused sweep (= partial chunks it left)
   cudaStream_t stream = nullptr;
   cudaStream_t up_stream = nullptr;  // operator uploads (overlap the previous sensor's Gram)
@@ -483,8 +484,10 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
     fail(RADMM_CUDA, "radmm_b200 requires an sm_100 (Blackwell) GPU; found " + std::string(prop.name));
   }
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS>, kFwdThreads, 16 * 1024));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS, 256>, 256, 16 * 1024));
   c->fwd_per_sm = std::max(1, c->fwd_per_sm);
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 512>, 512, 16 * 1024));
+  c->fwd_per_sm_tall = std::max(1, c->fwd_per_sm_tall);
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->N = n_pixels;
   c->Q = q_local;
@@ -547,8 +550,10 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.bz.alloc(S.ld);
   S.v.alloc(S.ld);
   S.w.alloc(S.ld);
-  const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
-  S.part_chunks = std::max(std::max(1, c->sm_count * c->fwd_per_sm / tiles), (c->N + kMaxChunk - 1) / kMaxChunk) + 1;
+  const int tile = 2 * fwd_threads_for(S.ld);
+  const int tiles = (int)((S.ld + tile - 1) / tile);
+  const int per_sm = fwd_threads_for(S.ld) == 512 ? c->fwd_per_sm_tall : c->fwd_per_sm;
+  S.part_chunks = std::max(std::max(1, c->sm_count * per_sm / tiles), (c->N + kMaxChunk - 1) / kMaxChunk) + 1;
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
   S.g0_valid = false;  // a new operator invalidates the cached factor
@@ -781,10 +786,11 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
     }
     if (max_chunks > 0) {
       const size_t smem = (size_t)max_len * (sizeof(double2) + sizeof(int));
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(fwd_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      dim3 grid((unsigned)((ld_max + kFwdTile - 1) / kFwdTile), max_chunks, (unsigned)nb);
-      LAUNCH(c, fwd_kernel<MODE>, grid, kFwdThreads, smem, pk, c->gap.p, c->sigma.p, beta, go);
+      const int threads = fwd_threads_for(ld_max);
+      auto kern = threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
+      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      dim3 grid((unsigned)((ld_max + 2 * threads - 1) / (2 * threads)), max_chunks, (unsigned)nb);
+      LAUNCH(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
     dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
     LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp, go);
@@ -793,8 +799,9 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
 
 // chunking so one forward launch is exactly one full wave of resident CTAs
 void plan_chunks(radmm_ctx* c, const Sensor& S, int n, int batch, int& n_chunks, int& chunk_len) {
-  const int tiles = (int)((S.ld + kFwdTile - 1) / kFwdTile);
-  const int target = c->sm_count * c->fwd_per_sm;
+  const int tile = 2 * fwd_threads_for(S.ld);
+  const int tiles = (int)((S.ld + tile - 1) / tile);
+  const int target = c->sm_count * (fwd_threads_for(S.ld) == 512 ? c->fwd_per_sm_tall : c->fwd_per_sm);
   const int chunks = std::min(S.part_chunks, std::max(1, target / std::max(1, tiles * batch)));
   chunk_len = (int)std::min<int64_t>(kMaxChunk, round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8));
   n_chunks = (n + chunk_len - 1) / chunk_len;
