@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   while (true) {
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
     const HermJob& jb = P.j[q];
+    const bool has1 = NR > 1 && jb.v1 != nullptr;  // second right-hand side present (else skipped)
     const int nxt = next_item(cur + gridDim.x);
     const uint64_t it_n = nxt < n_items ? __ldg(items + nxt) : 0;
     __syncthreads();  // vectors of `buf` visible; the other buffer's readers are done
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
+          if (c == 1 && !has1) continue;
           const double2 vi = vI[buf][c][t * kHermTile + lane + 32 * h];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
 #pragma unroll
           for (int h = 0; h < 2; ++h) sax[par][c][warp][lane + 32 * h] = make_double2(ar[c][h], ai[c][h]);
         __syncthreads();
-        if (tid < NR * kHermTile) {
+        if (tid < (has1 ? 2 : 1) * kHermTile) {
           const int c = tid / kHermTile, r = tid % kHermTile;
           double2 sum = sax[par][c][0][r];
 #pragma unroll
@@ -293,6 +295,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
       const int gi = (I0 - J) / kHermStrip;
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
+        if (c == 1 && !has1) continue;
         double2* dp = jb.dotp + c * jb.dstride + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[c][k], di[c][k]);
@@ -375,10 +378,34 @@ struct LazyJob {
   const double2* Sinv;  // d x d, leading dimension lds
   int64_t lds;
   double2* w;           // in: u = G v; out: C_D^{-1} v
-  double2* t;           // d (scratch)
+  double2* t;           // d (scratch): t = A_D^H u, then s = mu Sinv t in t + kLazyMax
+  unsigned* cnt;        // arrival counter of the job's dot blocks (zero between launches)
 };
 
-__global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ Pack<LazyJob> P, const int* __restrict__ go) {
+// s = mu Sinv t for one job by one block: four threads per row of Sinv,
+// fixed-order shuffle combine (deterministic)
+__device__ __forceinline__ void lazy_s(const LazyJob& jb, double mu, const double2* t, double2* s) {
+  const int j = threadIdx.x >> 2, sub = threadIdx.x & 3;
+  double re = 0.0, im = 0.0;
+  if (j < jb.d)
+    for (int k = sub; k < jb.d; k += 4) {
+      const double2 m = jb.Sinv[j + (int64_t)k * jb.lds], x = t[k];
+      re = fma(m.x, x.x, re);
+      re = fma(-m.y, x.y, re);
+      im = fma(m.x, x.y, im);
+      im = fma(m.y, x.x, im);
+    }
+  re += __shfl_xor_sync(0xffffffffu, re, 1);
+  im += __shfl_xor_sync(0xffffffffu, im, 1);
+  re += __shfl_xor_sync(0xffffffffu, re, 2);
+  im += __shfl_xor_sync(0xffffffffu, im, 2);
+  if (sub == 0 && j < jb.d) s[j] = make_double2(mu * re, mu * im);
+}
+
+// t = A_D^H u (one block per column); the job's last block to finish also
+// forms s = mu Sinv t (lazy_s), so lazy_axpy_kernel only streams P.
+__global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ Pack<LazyJob> P, double mu,
+                                                       const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;
   const LazyJob& jb = P.j[blockIdx.y];
   const int j = blockIdx.x;
@@ -400,11 +427,25 @@ __global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ P
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { sr[warp] = re; si[warp] = im; }
   __syncthreads();
+  __shared__ bool last;
   if (threadIdx.x == 0) {
     double a0 = sr[0], b0 = si[0];
     for (int k = 1; k < 8; ++k) { a0 += sr[k]; b0 += si[k]; }
     jb.t[j] = make_double2(a0, b0);
+    __threadfence();
+    last = atomicAdd(jb.cnt, 1u) == (unsigned)jb.d - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 ts[kLazyMax];
+  if (threadIdx.x < jb.d) {
+    const volatile double* tv = reinterpret_cast<volatile double*>(jb.t) + 2 * threadIdx.x;
+    ts[threadIdx.x] = make_double2(tv[0], tv[1]);
+  }
+  __syncthreads();
+  lazy_s(jb, mu, ts, jb.t + kLazyMax);
+  if (threadIdx.x == 0) *jb.cnt = 0u;
 }
 
 __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ Pack<LazyJob> P, double mu,
@@ -412,25 +453,8 @@ __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ 
   if (go && __ldg(go) == 0) return;
   const LazyJob& jb = P.j[blockIdx.y];
   if (jb.d <= 0 || (int64_t)blockIdx.x * 256 >= jb.rows) return;
-  __shared__ double2 sv[kLazyMax];
-  // s = mu Sinv t: four threads per row of Sinv, fixed-order shuffle combine
-  {
-    const int j = threadIdx.x >> 2, sub = threadIdx.x & 3;
-    double re = 0.0, im = 0.0;
-    if (j < jb.d)
-      for (int k = sub; k < jb.d; k += 4) {
-        const double2 m = jb.Sinv[j + (int64_t)k * jb.lds], x = jb.t[k];
-        re = fma(m.x, x.x, re);
-        re = fma(-m.y, x.y, re);
-        im = fma(m.x, x.y, im);
-        im = fma(m.y, x.x, im);
-      }
-    re += __shfl_xor_sync(0xffffffffu, re, 1);
-    im += __shfl_xor_sync(0xffffffffu, im, 1);
-    re += __shfl_xor_sync(0xffffffffu, re, 2);
-    im += __shfl_xor_sync(0xffffffffu, im, 2);
-    if (sub == 0 && j < jb.d) sv[j] = make_double2(mu * re, mu * im);
-  }
+  __shared__ double2 sv[kLazyMax];  // s = mu Sinv t, formed by lazy_dot_kernel's last block
+  if (threadIdx.x < jb.d) sv[threadIdx.x] = jb.t[kLazyMax + threadIdx.x];
   __syncthreads();
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= jb.rows) return;

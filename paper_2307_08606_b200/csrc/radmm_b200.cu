@@ -328,6 +328,7 @@ struct radmm_ctx {
   std::vector<cudaEvent_t> ev_steps;
   std::vector<cudaEvent_t> ev_ends;  // recorded after each round's fusion
   DArr<int> go_flags;                // speculation guards, alternating per round
+  DArr<unsigned> lazy_cnt;           // lazy_dot_kernel arrival counters (one per job)
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
@@ -1128,7 +1129,7 @@ void lazy_reserve(Sensor& S) {
     S.lz_P.alloc((size_t)S.ld * kLazyMax, false);
     S.lz_R.alloc((size_t)S.ld * kLazyMax, false);
     S.lz_S.alloc((size_t)kLazyMax * kLazyMax, false);
-    S.lz_t.alloc(kLazyMax, false);
+    S.lz_t.alloc(2 * kLazyMax, false);
     S.lz_pix.alloc(kLazyMax, false);
     S.lz_B.alloc((size_t)kLazyMax * kBorderMax, false);
   }
@@ -1260,12 +1261,16 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
     Sensor& S = c->sensors[q];
     if (S.primal || S.lz_d == 0) continue;
     if (nb >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
-    pk.j[nb++] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax, S.w.p, S.lz_t.p};
+    pk.j[nb] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax, S.w.p, S.lz_t.p,
+                       c->lazy_cnt.p + nb};
+    ++nb;
     dmax = std::max(dmax, S.lz_d);
     rmax = std::max(rmax, S.rows);
   }
   if (!nb) return;
-  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, go);
+  if (c->lazy_cnt.n < (size_t)kMaxBatch) c->lazy_cnt.alloc(kMaxBatch);  // zeroed; the last blocks re-zero
+  for (int i = 0; i < nb; ++i) pk.j[i].cnt = c->lazy_cnt.p + i;
+  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
   LAUNCH(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
 }
 
