@@ -2328,6 +2328,9 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   // the kept counts at the same sync as the round's scalars (no extra round
   // trip), and a screening round that changes no active set does not even
   // cancel the speculative round.
+  constexpr double kPreScreenRatio = 8.0;
+  bool trigger_seen = false;
+  double last_ratio = 1e300;  // pri_res / eps_pri of the last completed round
   auto issue = [&](int kk, const int* go, uint64_t notice) {
     int* go_next = spec ? c->go_flags.p + ((kk + 1) & 1) : nullptr;
     c->pre_screened[kk & 1] = false;
@@ -2337,7 +2340,14 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       local_updates(c, h, go);
       exchange(c, (double)notice);
       const int snp = screen_next_possible();
-      int* sgo = (spec && snp) ? c->sgo_flags.p + (kk & 1) : nullptr;
+      // the guarded screening is enqueued only when the trigger is near: the
+      // last observed primal residual within kPreScreenRatio of its
+      // threshold, or the trigger seen already.  Otherwise (C2's long
+      // approach) the three guarded launches are skipped; if the trigger does
+      // fire, the speculative round is cancelled and screening runs the
+      // synchronous way (screen_all) -- same result.
+      const bool near = trigger_seen || last_ratio <= kPreScreenRatio;
+      int* sgo = (spec && snp && near) ? c->sgo_flags.p + (kk & 1) : nullptr;
       run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, snp, sgo);
       if (sgo) c->pre_screened[kk & 1] = enqueue_screen(c, h, kk & 1, go, sgo, go_next);
     }
@@ -2397,6 +2407,8 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       }
     }
     record_round(c, k, f, notice, sm, sizes, meta_all, t1);
+    trigger_seen = trigger_seen || f.trigger;
+    last_ratio = f.eps_pri > 0 ? f.pri_res / f.eps_pri : 1e300;
     if (o && o->observer) {
       CK(cudaMemcpy(hx.data(), c->xg.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(hs.data(), c->s.p, sizeof(double2) * c->N, cudaMemcpyDeviceToHost));
