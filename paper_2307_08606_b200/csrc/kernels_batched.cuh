@@ -312,26 +312,28 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
 // 256 threads per row block: slice s = tid / 64 sums the partials k = s, s+4, ...
 // of the row's list (4 independent loads in flight), then the 4 slice sums are
 // added in slice order -- deterministic.  blockIdx.z = right-hand side.
-__global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
-                                                         const int* __restrict__ go) {
+constexpr int kHermRedSlices = 8;  // 512 threads: 8 slices x 64 rows, 4 loads in flight each
+
+__global__ void __launch_bounds__(kHermRedSlices * kHermTile) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
+                                                                                const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;
   const HermJob& jb = P.j[blockIdx.y];
   const int c = blockIdx.z;
   double2* const out = c == 0 ? jb.w : jb.w1;
   if (!jb.v || !out || (c == 1 && !jb.v1)) return;
   const int b = blockIdx.x, r = threadIdx.x & 63, sl = threadIdx.x >> 6;
-  __shared__ double2 part[4][kHermTile];
+  __shared__ double2 part[kHermRedSlices][kHermTile];
   if (b >= jb.nb) return;
   const int ng = (jb.nb - b + kHermStrip - 1) / kHermStrip;
   const int total = ng + b;  // dot partials, then ax partials J = 0 .. b-1
   const double2* dbase = jb.dotp + c * jb.dstride + (int64_t)b * jb.groups * kHermTile + r;
   const double2* abase = jb.axp + c * jb.astride + (int64_t)b * (b - 1) / 2 * kHermTile + r;
   double2 s = make_double2(0.0, 0.0);
-  for (int k0 = sl; k0 < total; k0 += 16) {
+  for (int k0 = sl; k0 < total; k0 += 4 * kHermRedSlices) {
     double2 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int k = k0 + 4 * u;
+      const int k = k0 + kHermRedSlices * u;
       v[u] = k < total ? (k < ng ? dbase[(int64_t)k * kHermTile] : abase[(int64_t)(k - ng) * kHermTile])
                        : make_double2(0.0, 0.0);
     }
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(256) herm_reduce_kernel(const __grid_constant_
     const int row = b * kHermTile + r;
     double2 t = part[0][r];
 #pragma unroll
-    for (int u = 1; u < 4; ++u) {
+    for (int u = 1; u < kHermRedSlices; ++u) {
       t.x += part[u][r].x;
       t.y += part[u][r].y;
     }

@@ -729,7 +729,8 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
   } else {
     LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
-  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), 256, 0, pk, go);
+  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
+         pk, go);
 }
 
 // Below this order the triangle's few long strips (one CTA each) are

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for cfg in "RADMM_HERM=1" "RADMM_HERM=2"; do
+for cfg in "RADMM_X=0"; do
   env $cfg timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-ttt --steps 50 > gpurun_out/sweep.tmp 2>&1
   python - "$cfg" <<'PY' >> gpurun_out/sweep.log
 import json,sys
