@@ -24,3 +24,4 @@
 #include "kernels_dense.cuh"
 #include "kernels_batched.cuh"
 #include "kernels_fused.cuh"
+#include "kernels_ozaki.cuh"

@@ -1,0 +1,357 @@
+// kernels_ozaki.cuh: int8 GEMM tile on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, int32 accumulators in tensor memory), the building
+// block of the Ozaki-sliced capacitance Gram.
+//
+//   D[128 x 128] (int32, TMEM) += A[128 x K] . B[128 x K]^T   (int8, both K-major)
+//
+// Operands stream through a kOzStages-deep shared ring with cp.async; each
+// 128-row x 128-byte stage is stored in the canonical K-major SWIZZLE_128B
+// layout (8-row x 128-byte atoms, 16-byte chunk c of row r at c ^ (r & 7)), so
+// one smem descriptor per stage serves four K = 32 MMAs by advancing its
+// start address 32 bytes at a time.  One thread issues the MMAs; each stage's
+// MMAs commit to that stage's mbarrier, which releases the slot for the next
+// copy.  Exact: int8 x int8 products, int32 sums (|sum| < 2^31 for
+// K < 2^17 with operands in [-127, 127]).
+#pragma once
+#include <cstdint>
+
+namespace radmm_oz {
+
+constexpr int kOzBM = 128, kOzBN = 128, kOzBK = 128, kOzStages = 4;
+constexpr int kOzStageBytes = (kOzBM + kOzBN) * kOzBK;  // 32 KB
+constexpr size_t kOzSmem = (size_t)kOzStages * kOzStageBytes + 1024 + 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void oz_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void oz_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void oz_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void oz_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void oz_mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// SWIZZLE_128B K-major smem descriptor (cute UMMA::SmemDescriptor layout):
+// start >> 4 in [0,14), LBO (ignored for swizzled K-major) = 1, SBO = 1024 B
+// between 8-row groups, version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// kind::i8 instruction descriptor: D = S32, A = B = signed int8, both
+// K-major, N = 128, M = 128.
+constexpr uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) |
+                              ((uint32_t)(kOzBM >> 4) << 24);
+
+struct TcI8Tile {
+  uint8_t* ring;       // 1024-aligned: kOzStages x (A 16 KB | B 16 KB)
+  uint64_t* bar;       // kOzStages stage-release barriers
+  uint32_t tmem;       // accumulator base (column 0 of lane 0)
+  uint32_t ncols;
+  uint32_t uses;       // stages issued so far (ring position / barrier phases)
+
+  // n_acc accumulators of 128 columns each (TMEM allocation: power of two)
+  __device__ void init(uint8_t* smem_raw, int n_acc) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    ring = base;
+    bar = reinterpret_cast<uint64_t*>(base + (size_t)kOzStages * kOzStageBytes);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kOzStages);
+    ncols = n_acc <= 1 ? 128u : n_acc <= 2 ? 256u : 512u;
+    uses = 0;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kOzStages; ++s) oz_mbar_init(&bar[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if ((threadIdx.x >> 5) == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tmem = *slot;
+  }
+
+  // stage copy: 8 threads per 128-byte row (coalesced), 16 rows per pass
+  __device__ void load(int s, const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int kb) {
+    const int t = threadIdx.x, c = t & 7;
+    const uint32_t a_s = smem_u32(ring + (size_t)s * kOzStageBytes), b_s = a_s + kOzBM * kOzBK;
+#pragma unroll
+    for (int p = 0; p < kOzBM / 16; ++p) {
+      const int r = (t >> 3) + 16 * p;
+      const uint32_t off = r * kOzBK + ((c ^ (r & 7)) << 4);
+      oz_cp16(a_s + off, A + (int64_t)r * lda + (int64_t)kb * kOzBK + c * 16);
+      oz_cp16(b_s + off, B + (int64_t)r * ldb + (int64_t)kb * kOzBK + c * 16);
+    }
+  }
+
+  // D[acc] (+)= A B^T over K (a multiple of kOzBK); `accumulate` false starts
+  // the accumulator at zero.  Blocks all 128 threads of the CTA.
+  __device__ void run(const int8_t* A, int64_t lda, const int8_t* B, int64_t ldb, int K, int acc, bool accumulate) {
+    const int nk = K / kOzBK;
+#pragma unroll
+    for (int p = 0; p < kOzStages - 1; ++p) {
+      if (p < nk) {
+        const uint32_t u = uses + p;
+        if (u >= kOzStages) oz_mbar_wait(&bar[u % kOzStages], ((u / kOzStages) - 1) & 1);
+        load(u % kOzStages, A, lda, B, ldb, p);
+      }
+      oz_commit();
+    }
+    for (int kb = 0; kb < nk; ++kb) {
+      const int ld_kb = kb + kOzStages - 1;
+      if (ld_kb < nk) {
+        const uint32_t u = uses + ld_kb;
+        if (u >= kOzStages) oz_mbar_wait(&bar[u % kOzStages], ((u / kOzStages) - 1) & 1);
+        load(u % kOzStages, A, lda, B, ldb, ld_kb);
+      }
+      oz_commit();
+      oz_wait<kOzStages - 1>();  // this thread's copies of stage kb landed
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t u = uses + kb;
+        const uint32_t a_s = smem_u32(ring + (size_t)(u % kOzStages) * kOzStageBytes), b_s = a_s + kOzBM * kOzBK;
+#pragma unroll
+        for (int k = 0; k < kOzBK / 32; ++k) {
+          const uint64_t ad = oz_desc(a_s + 32 * k), bd = oz_desc(b_s + 32 * k);
+          const uint32_t en = (accumulate || kb > 0 || k > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+                  tmem + (uint32_t)acc * 128u),
+              "l"(ad), "l"(bd), "r"(kOzIdesc), "r"(en), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+              : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar[u % kOzStages]))
+                     : "memory");
+      }
+    }
+    uses += nk;
+  }
+
+  // wait for every issued MMA (the last stage's barrier covers all earlier ones)
+  __device__ void wait_all() {
+    if (uses > 0) {
+      const uint32_t u = uses - 1;
+      oz_mbar_wait(&bar[u % kOzStages], (u / kOzStages) & 1);
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+
+  // 32 consecutive accumulator columns of the warp's 32 rows (lanes 32w..32w+31)
+  __device__ void load32(int acc, int warp, int col0, uint32_t (&v)[32]) {
+    const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)acc * 128u + (uint32_t)col0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  }
+
+  __device__ void finish() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Ozaki-sliced capacitance Gram  C = A_J A_J^H  (complex64 A, exact-to-fp64
+// level products on the int8 tensor cores).
+//
+// Row r of A_J is scaled by 2^-e_r (e_r: exponent of the row's largest
+// |re|, |im|, so |v| < 1) and split into kOzSlices int8 slices,
+//   v = sum_{s=1..S} d_s 2^{-7s},  d_s in [-127, 127]  (truncation: exact
+//   residuals, |v - sum| < 2^{-7S}),
+// stored K-major with the real and imaginary parts side by side:
+//   P_s = [Re d_s | Im d_s],  Q_s = [Im d_s | -Re d_s]   (rows x 2N bytes),
+// so that for each slice pair (s1, s2)
+//   Re(A A^H) part = P_s1 P_s2^T,  Im part = Q_s1 P_s2^T   (int32, exact).
+// Pairs with s1 + s2 <= kOzSlices + 1 are kept (the dropped tail is below
+// 2^{-7(S+2)} relative per product).  oz_combine_kernel sums the pairs in a
+// fixed order in fp64, scales by 2^{e_i + e_j} and writes the lower tiles
+// with an exact conjugate mirror, like gram_dmma_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kOzSlices = 6;
+constexpr int kOzPairs = kOzSlices * (kOzSlices + 1) / 2;  // s1 + s2 <= S + 1, s1, s2 >= 1
+
+__host__ __device__ inline void oz_pair(int p, int& s1, int& s2) {
+  // pairs ordered by t = s1 + s2 (largest contributions first), then s1
+  int t = 2;
+  while (p >= t - 1) {
+    p -= t - 1;
+    ++t;
+  }
+  s1 = p + 1;
+  s2 = t - s1;
+}
+
+// row maxima of |re|, |im| over the listed columns (float bits: order-preserving
+// for non-negative floats, so atomicMax on the bits is exact)
+__global__ void oz_rowmax_kernel(const float2* __restrict__ A, int64_t ld, int rows, const int* __restrict__ J, int n,
+                                 unsigned* __restrict__ rowmax) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int per = (n + gridDim.y - 1) / gridDim.y;
+  const int c0 = blockIdx.y * per, c1 = min(n, c0 + per);
+  float m = 0.f;
+  for (int c = c0; c < c1; ++c) {
+    const float2 a = A[r + (int64_t)(J ? J[c] : c) * ld];
+    m = fmaxf(m, fmaxf(fabsf(a.x), fabsf(a.y)));
+  }
+  atomicMax(rowmax + r, __float_as_uint(m));
+}
+
+// slices of a 32-column x 64-row block, transposed through shared memory so
+// both the column-major read and the K-major writes are coalesced
+__global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict__ A, int64_t ld, int rows,
+                                                      const int* __restrict__ J, int n, int npad,
+                                                      const unsigned* __restrict__ rowmax, int8_t* __restrict__ P,
+                                                      int8_t* __restrict__ Q, int64_t slice_stride) {
+  __shared__ int8_t sre[kOzSlices][64][33], sim[kOzSlices][64][33];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 32;
+  const int tr = threadIdx.x & 63, tq = threadIdx.x >> 6;  // row in tile, column phase
+  const int r = r0 + tr;
+  int e = 0;
+  if (r < rows) {
+    const float m = __uint_as_float(rowmax[r]);
+    e = m > 0.f ? ilogbf(m) + 1 : 0;
+  }
+  for (int cc = tq; cc < 32; cc += 4) {
+    const int c = c0 + cc;
+    double vr = 0.0, vi = 0.0;
+    if (r < rows && c < n) {
+      const float2 a = A[r + (int64_t)(J ? J[c] : c) * ld];
+      vr = ldexp((double)a.x, -e);
+      vi = ldexp((double)a.y, -e);
+    }
+#pragma unroll
+    for (int sl = 0; sl < kOzSlices; ++sl) {
+      const double dr = trunc(vr * 128.0), di = trunc(vi * 128.0);  // exact: |v| < 1
+      sre[sl][tr][cc] = (int8_t)dr;
+      sim[sl][tr][cc] = (int8_t)di;
+      vr = vr * 128.0 - dr;  // exact remainder, |.| < 1
+      vi = vi * 128.0 - di;
+    }
+  }
+  __syncthreads();
+  // write: row rr, 32 consecutive columns per slice (re half, im half); rows
+  // are npad long per half (zero columns beyond n stay as memset)
+  for (int e2 = threadIdx.x; e2 < 64 * 32; e2 += 256) {
+    const int rr = e2 >> 5, cc = e2 & 31, row = r0 + rr, c = c0 + cc;
+    if (row >= rows || c >= n) continue;
+#pragma unroll
+    for (int sl = 0; sl < kOzSlices; ++sl) {
+      int8_t* Pr = P + sl * slice_stride + (int64_t)row * 2 * npad;
+      int8_t* Qr = Q + sl * slice_stride + (int64_t)row * 2 * npad;
+      const int8_t re = sre[sl][rr][cc], im = sim[sl][rr][cc];
+      Pr[c] = re;
+      Pr[npad + c] = im;
+      Qr[c] = im;
+      Qr[npad + c] = (int8_t)(-re);
+    }
+  }
+}
+
+// One CTA per (lower 128 x 128 tile, slice pair): Re and Im int32 blocks of
+// the pair to R[tile][pair][part][128][128] (rows 128 apart in the tile).
+__global__ void __launch_bounds__(128, 1) oz_gram_pairs_kernel(const int8_t* __restrict__ P,
+                                                              const int8_t* __restrict__ Q, int64_t slice_stride,
+                                                              int rows, int kdim, int32_t* __restrict__ R) {
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  int tile = blockIdx.x, I = 0;
+  while (tile > I) {
+    tile -= I + 1;
+    ++I;
+  }
+  const int Jt = tile, pair = blockIdx.y;
+  int s1, s2;
+  oz_pair(pair, s1, s2);
+  const int64_t ldk = kdim;  // bytes per slice row
+  const int m0 = I * kOzBM, n0 = Jt * kOzBN;
+  TcI8Tile t;
+  t.init(oz_smem, 2);
+  const int8_t* Pa = P + (s1 - 1) * slice_stride + (int64_t)m0 * ldk;
+  const int8_t* Qa = Q + (s1 - 1) * slice_stride + (int64_t)m0 * ldk;
+  const int8_t* Pb = P + (s2 - 1) * slice_stride + (int64_t)n0 * ldk;
+  t.run(Pa, ldk, Pb, ldk, kdim, 0, false);
+  t.run(Qa, ldk, Pb, ldk, kdim, 1, false);
+  t.wait_all();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* out = R + ((int64_t)blockIdx.x * kOzPairs + pair) * 2 * kOzBM * kOzBN;
+  for (int part = 0; part < 2; ++part)
+    for (int c0 = 0; c0 < kOzBN; c0 += 32) {
+      uint32_t v[32];
+      t.load32(part, warp, c0, v);
+      int4* dst = reinterpret_cast<int4*>(out + (int64_t)part * kOzBM * kOzBN + (int64_t)(32 * warp + lane) * kOzBN + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2], (int)v[4 * q + 3]);
+    }
+  t.finish();
+}
+
+// C[i, j] (i >= j, lower tiles) = mu 2^{e_i + e_j} sum_pairs 2^{-7(s1+s2)} (R_re + i R_im)
+// (+ beta on the diagonal, exact real), mirrored conjugate to C[j, i].
+__global__ void oz_combine_kernel(const int32_t* __restrict__ R, const unsigned* __restrict__ rowmax, int rows,
+                                  double2* __restrict__ C, int64_t ldc, double mu, double beta) {
+  const int tile = blockIdx.y;
+  int t = tile, I = 0;
+  while (t > I) {
+    t -= I + 1;
+    ++I;
+  }
+  const int Jt = t;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // element in the 128 x 128 tile
+  if (e >= kOzBM * kOzBN) return;
+  const int ii = e / kOzBN, jj = e % kOzBN, i = I * kOzBM + ii, j = Jt * kOzBN + jj;
+  if (i >= rows || j >= rows || i < j) return;
+  const int32_t* base = R + (int64_t)tile * kOzPairs * 2 * kOzBM * kOzBN + e;
+  double re = 0.0, im = 0.0;
+  for (int p = 0; p < kOzPairs; ++p) {
+    int s1, s2;
+    oz_pair(p, s1, s2);
+    const double sc = ldexp(1.0, -7 * (s1 + s2));
+    re += sc * (double)base[(int64_t)p * 2 * kOzBM * kOzBN];
+    im += sc * (double)base[(int64_t)p * 2 * kOzBM * kOzBN + kOzBM * kOzBN];
+  }
+  const float mi = __uint_as_float(rowmax[i]), mj = __uint_as_float(rowmax[j]);
+  const int ei = mi > 0.f ? ilogbf(mi) + 1 : 0, ej = mj > 0.f ? ilogbf(mj) + 1 : 0;
+  re = ldexp(re, ei + ej);
+  im = ldexp(im, ei + ej);
+  double2 o = make_double2(mu * re, mu * im);
+  if (i == j) {
+    o.x += beta;
+    o.y = 0.0;
+  }
+  C[i + (int64_t)j * ldc] = o;
+  if (i != j) C[j + (int64_t)i * ldc] = make_double2(o.x, -o.y);
+}
+
+}  // namespace radmm_oz

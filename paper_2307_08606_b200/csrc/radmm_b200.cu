@@ -363,6 +363,10 @@ struct radmm_ctx {
   DArr<FrameRhsJob> fb_rhs;
   DArr<double2> fb_part;
   DArr<GramJob> gram_jobs;
+  // Ozaki-sliced Gram scratch (kernels_ozaki.cuh): row maxima, slices, pair blocks
+  DArr<unsigned> oz_rowmax;
+  DArr<int8_t> oz_P, oz_Q;
+  DArr<int32_t> oz_R;
   // fused sweep v4 control (tile arrival counters / flags / norm partials)
   DArr<unsigned> s4_cnt, s4_flag, s4_done;
   DArr<double> s4_norms;
@@ -1026,6 +1030,49 @@ void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
   }
 }
 
+// ---- Ozaki-sliced Gram on the int8 tensor cores (tcgen05, kernels_ozaki.cuh) ----
+bool ozaki_enabled() { return env_int("RADMM_OZAKI", 1) != 0; }
+
+// C = beta I + mu A_J A_J^H (rows x rows, lower tiles + exact mirror) for one
+// sensor; returns false (caller falls back to the fp64 DMMA Gram) when the
+// slices do not fit next to 4 GB of free HBM or the shape is out of range.
+bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_t ldc, double mu, double beta) {
+  using namespace radmm_oz;
+  if (!ozaki_enabled() || n < 1 || n > 65536) return false;
+  const int rows = S.rows;
+  const int T = (rows + kOzBM - 1) / kOzBM, tiles = T * (T + 1) / 2;
+  const int64_t rows_pad = (int64_t)T * kOzBM, npad = round_up(n, 64), kdim = 2 * npad;
+  const size_t slice = (size_t)rows_pad * kdim, pq = (size_t)kOzSlices * slice;
+  const size_t rblk = (size_t)tiles * kOzPairs * 2 * kOzBM * kOzBN;
+  const size_t need = 2 * pq + rblk * 4 + rows_pad * 4;
+  if (c->oz_P.n < pq || c->oz_R.n < rblk || c->oz_rowmax.n < (size_t)rows_pad) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t held = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
+    if (free_b + held < need + (4ull << 30)) return false;
+    if (c->oz_P.n < pq) {
+      c->oz_P.alloc(pq, false);
+      c->oz_Q.alloc(pq, false);
+    }
+    if (c->oz_R.n < rblk) c->oz_R.alloc(rblk, false);
+    if (c->oz_rowmax.n < (size_t)rows_pad) c->oz_rowmax.alloc(rows_pad, false);
+  }
+  CK(cudaMemsetAsync(c->oz_rowmax.p, 0, sizeof(unsigned) * rows_pad, c->stream));
+  CK(cudaMemsetAsync(c->oz_P.p, 0, pq, c->stream));  // padding rows / columns are zero slices
+  CK(cudaMemsetAsync(c->oz_Q.p, 0, pq, c->stream));
+  const int split = std::max(1, std::min(64, n / 256));
+  LAUNCH(c, oz_rowmax_kernel, dim3((unsigned)((rows + 255) / 256), (unsigned)split), 256, 0, S.A.p, S.ld, rows, J, n,
+         c->oz_rowmax.p);
+  LAUNCH(c, oz_slice_kernel, dim3((unsigned)((n + 31) / 32), (unsigned)((rows + 63) / 64)), 256, 0, S.A.p, S.ld, rows,
+         J, n, (int)npad, c->oz_rowmax.p, c->oz_P.p, c->oz_Q.p, (int64_t)slice);
+  CK(cudaFuncSetAttribute(oz_gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
+  LAUNCH(c, oz_gram_pairs_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzSmem, c->oz_P.p, c->oz_Q.p,
+         (int64_t)slice, rows, (int)kdim, c->oz_R.p);
+  LAUNCH(c, oz_combine_kernel, dim3((unsigned)(kOzBM * kOzBN / 256), (unsigned)tiles), 256, 0, c->oz_R.p,
+         c->oz_rowmax.p, rows, C, ldc, mu, beta);
+  return true;
+}
+
 // Full rebuild for the listed sensors (batched): data term + factor.
 void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
   if (qs.empty()) return;
@@ -1053,6 +1100,8 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
       // (same roundings as forming beta I + mu A A^H directly)
       LAUNCH(c, gram_scale_kernel, dim3((unsigned)((int64_t)dim * dim + 255) / 256), 256, 0, S.G.p, ldg, dim, mu,
              beta);
+    } else if (env_int("RADMM_GRAM", 1) && ozaki_gram(c, S, S.J.p, S.n_act, S.G.p, ldg, mu, beta)) {
+      // capacitance beta I + mu A_J A_J^H from int8 slices on the tcgen05 tensor cores
     } else if (env_int("RADMM_GRAM", 1)) {
       // capacitance beta I + mu A_J A_J^H on the fp64 tensor cores
       grams.push_back(GramJob{S.A.p, S.ld, S.J.p, S.n_act, S.rows, S.G.p, ldg});
@@ -2872,6 +2921,13 @@ void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
   S.g_n = S.rows;
   S.primal = false;
   CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)S.ld * S.rows, c->stream));
+  if (ozaki_gram(c, S, nullptr, c->N, S.G.p, S.ld, 1.0, 0.0)) {
+    S.raw_gram = true;
+    if (c->gram_evs.size() < (size_t)c->Q) c->gram_evs.resize(c->Q, nullptr);
+    if (!c->gram_evs[q]) CK(cudaEventCreateWithFlags(&c->gram_evs[q], cudaEventDisableTiming));
+    CK(cudaEventRecord(c->gram_evs[q], c->stream));
+    return;
+  }
   // the job travels as a kernel parameter: a pageable job-table upload would
   // wait for the previous sensor's Gram and serialise the pipeline
   const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, S.G.p, S.ld};
