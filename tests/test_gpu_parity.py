@@ -138,6 +138,21 @@ def test_gauss_jordan_update_kernels_bitwise_equal(rows, cols, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("rows,cols", [(300, 1000), (256, 4096), (130, 700)])
+def test_ozaki_tcgen05_gram_matches_fp64_gram(rows, cols, monkeypatch):
+    """The capacitance Gram from exact int8 slices on the tcgen05 tensor cores
+    (kernels_ozaki.cuh) against the fp64 DMMA Gram: solves agree far inside the
+    dual form's conditioning floor (ragged row counts: padded 128-row tiles)."""
+    rng = np.random.default_rng(rows + cols)
+    a = (rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols))).astype(np.complex64)
+    rhs = rng.normal(size=cols) + 1j * rng.normal(size=cols)
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RADMM_OZAKI", flag)
+        outs[flag] = api.factorize(a.astype(np.complex128), 1.0, 1.0).solve(rhs)
+    assert rel(outs["1"], outs["0"]) < 1e-8, rel(outs["1"], outs["0"])
+
+
 def test_cached_solves_bitwise_reproducible():
     rng = np.random.default_rng(31)
     a = rng.normal(size=(10, 7)) + 1j * rng.normal(size=(10, 7))
