@@ -136,7 +136,10 @@ int radmm_ctx_destroy(radmm_ctx* ctx);
 /* ForwardOperator::from_matrix (forward_model.hpp:126-133).  q is the
  * 0-based LOCAL sensor slot; rows = K*M of that sensor (ragged allowed);
  * a points at a column-major rows x n_pixels matrix with leading
- * dimension lda >= rows.  The device copy is complex64. */
+ * dimension lda >= rows.  The device copy is complex64.  Returns once the
+ * host buffer has been consumed (the reference's copy semantics); the
+ * sensor's full-set capacitance Gram then keeps running on the device,
+ * overlapping the next sensor's upload (consumed by the first radmm_run). */
 int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int64_t lda, int ptr_kind);
 int radmm_set_operator_c128(radmm_ctx* ctx, int q, int rows, const double* a, int64_t lda, int ptr_kind);
 /* Measurement y_q (Problem::measurements), complex128, length rows. */
