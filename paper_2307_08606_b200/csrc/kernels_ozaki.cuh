@@ -13,6 +13,7 @@
 // copy.  Exact: int8 x int8 products, int32 sums (|sum| < 2^31 for
 // K < 2^17 with operands in [-127, 127]).
 #pragma once
+#include <cuda.h>
 #include <cstdint>
 
 namespace radmm_oz {
@@ -315,6 +316,129 @@ __global__ void __launch_bounds__(128, 1) oz_gram_pairs_kernel(const int8_t* __r
       for (int q = 0; q < 8; ++q) dst[q] = make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2], (int)v[4 * q + 3]);
     }
   t.finish();
+}
+
+// TMA + warp-specialised variant of oz_gram_pairs_kernel (default): the
+// slices are read by cp.async.bulk.tensor through SWIZZLE_128B tensor maps
+// (the hardware writes the canonical layout the descriptors expect), one
+// elected thread of warp 0 produces, one of warp 1 issues the MMAs, and each
+// stage carries both A operands (P_s1 and Q_s1 rows of tile I) with one
+// shared B (P_s2 rows of tile J): Re and Im accumulate together.
+constexpr int kOzTStages = 4;
+constexpr int kOzTStageBytes = 3 * kOzBM * kOzBK;  // A_P | A_Q | B, 16 KB each
+constexpr size_t kOzTSmem = (size_t)kOzTStages * kOzTStageBytes + 1024 + 256;
+
+__device__ __forceinline__ void oz_tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1) oz_gram_pairs_tma_kernel(const __grid_constant__ CUtensorMap tP,
+                                                                  const __grid_constant__ CUtensorMap tQ,
+                                                                  int rows_pad, int kdim, int32_t* __restrict__ R) {
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)kOzTStages * kOzTStageBytes);
+  uint64_t* empty = full + kOzTStages;
+  uint64_t* done = empty + kOzTStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  int tile = blockIdx.x, I = 0;
+  while (tile > I) {
+    tile -= I + 1;
+    ++I;
+  }
+  const int Jt = tile, pair = blockIdx.y;
+  int s1, s2;
+  oz_pair(pair, s1, s2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kOzTStages; ++st) {
+      oz_mbar_init(&full[st], 1);
+      oz_mbar_init(&empty[st], 1);
+    }
+    oz_mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int nk = kdim / kOzBK;
+  const int ya = (s1 - 1) * rows_pad + I * kOzBM, yb = (s2 - 1) * rows_pad + Jt * kOzBN;
+  if (warp == 0 && lane == 0) {  // producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kOzTStages;
+      if (kb >= kOzTStages) oz_mbar_wait(&empty[st], ((kb / kOzTStages) - 1) & 1);
+      const uint32_t sa = smem_u32(base + (size_t)st * kOzTStageBytes), fb = smem_u32(&full[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(kOzTStageBytes)
+                   : "memory");
+      oz_tma_2d(sa, &tP, kb * kOzBK, ya, fb);
+      oz_tma_2d(sa + kOzBM * kOzBK, &tQ, kb * kOzBK, ya, fb);
+      oz_tma_2d(sa + 2 * kOzBM * kOzBK, &tP, kb * kOzBK, yb, fb);
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % kOzTStages;
+      oz_mbar_wait(&full[st], (kb / kOzTStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = smem_u32(base + (size_t)st * kOzTStageBytes);
+#pragma unroll
+      for (int k = 0; k < kOzBK / 32; ++k) {
+        const uint32_t en = (kb > 0 || k > 0) ? 1u : 0u;
+        const uint64_t bd = oz_desc(sa + 2 * kOzBM * kOzBK + 32 * k);
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const uint64_t ad = oz_desc(sa + part * kOzBM * kOzBK + 32 * k);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(
+                  tmem + (uint32_t)part * 128u),
+              "l"(ad), "l"(bd), "r"(kOzIdesc), "r"(en), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+              : "memory");
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty[st]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(done))
+                 : "memory");
+  }
+  oz_mbar_wait(done, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  int32_t* out = R + ((int64_t)blockIdx.x * kOzPairs + pair) * 2 * kOzBM * kOzBN;
+  for (int part = 0; part < 2; ++part)
+    for (int c0 = 0; c0 < kOzBN; c0 += 32) {
+      uint32_t v[32];
+      const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)part * 128u + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(addr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      int4* dst =
+          reinterpret_cast<int4*>(out + (int64_t)part * kOzBM * kOzBN + (int64_t)(32 * warp + lane) * kOzBN + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2], (int)v[4 * q + 3]);
+    }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 
 // C[i, j] (i >= j, lower tiles) = mu 2^{e_i + e_j} sum_pairs 2^{-7(s1+s2)} (R_re + i R_im)

@@ -10,6 +10,7 @@
 //   screen_all()         <- SensorCore::screen     admm.hpp:134-159
 //   NCCL exchange        <- run_inproc/run_tcp gather+broadcast (runtime.hpp:362-766)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -1033,6 +1034,32 @@ void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
 // ---- Ozaki-sliced Gram on the int8 tensor cores (tcgen05, kernels_ozaki.cuh) ----
 bool ozaki_enabled() { return env_int("RADMM_OZAKI", 1) != 0; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D int8 map over rows x kdim bytes, 128 x 128-byte boxes, SWIZZLE_128B
+bool slice_tensor_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t kdim) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kdim};
+  const cuuint32_t box[2] = {(cuuint32_t)radmm_oz::kOzBK, (cuuint32_t)radmm_oz::kOzBM};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // C = beta I + mu A_J A_J^H (rows x rows, lower tiles + exact mirror) for one
 // sensor; returns false (caller falls back to the fp64 DMMA Gram) when the
 // slices do not fit next to 4 GB of free HBM or the shape is out of range.
@@ -1065,9 +1092,17 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
          c->oz_rowmax.p);
   LAUNCH(c, oz_slice_kernel, dim3((unsigned)((n + 31) / 32), (unsigned)((rows + 63) / 64)), 256, 0, S.A.p, S.ld, rows,
          J, n, (int)npad, c->oz_rowmax.p, c->oz_P.p, c->oz_Q.p, (int64_t)slice);
-  CK(cudaFuncSetAttribute(oz_gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
-  LAUNCH(c, oz_gram_pairs_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzSmem, c->oz_P.p, c->oz_Q.p,
-         (int64_t)slice, rows, (int)kdim, c->oz_R.p);
+  CUtensorMap tP, tQ;
+  if (env_int("RADMM_OZ_TMA", 1) && slice_tensor_map(&tP, c->oz_P.p, (int64_t)kOzSlices * rows_pad, kdim) &&
+      slice_tensor_map(&tQ, c->oz_Q.p, (int64_t)kOzSlices * rows_pad, kdim)) {
+    CK(cudaFuncSetAttribute(oz_gram_pairs_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzTSmem));
+    LAUNCH(c, oz_gram_pairs_tma_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzTSmem, tP, tQ,
+           (int)rows_pad, (int)kdim, c->oz_R.p);
+  } else {
+    CK(cudaFuncSetAttribute(oz_gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
+    LAUNCH(c, oz_gram_pairs_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzSmem, c->oz_P.p, c->oz_Q.p,
+           (int64_t)slice, rows, (int)kdim, c->oz_R.p);
+  }
   LAUNCH(c, oz_combine_kernel, dim3((unsigned)(kOzBM * kOzBN / 256), (unsigned)tiles), 256, 0, c->oz_R.p,
          c->oz_rowmax.p, rows, C, ldc, mu, beta);
   return true;
