@@ -521,6 +521,15 @@ def stress(args):
                 "compaction_ms_total": ph["screen"]["ms"], "refactor_ms_total": ph["refactor"]["ms"],
                 "phase_ms_note": "compaction/refactor totals from a second, profiled run of the same solve",
                 "screen_calls": ph["screen"]["calls"], "refactor_calls": ph["refactor"]["calls"]}
+        # time to tolerance (the reference stopping rule, admm.hpp:244-256), both modes
+        h_tol = api.Hyperparams(mu=cfg.mu, lambda_=lam, beta=cfg.beta, eps_abs=1e-4, eps_rel=1e-2, max_iter=3000)
+        for mode in (api.Mode.SADMM, api.Mode.ASADMM):
+            r = s.run(h_tol, mode)
+            ms, _ = s.iteration_stats(r.iterations)
+            out[api.mode_name(mode)]["to_tolerance"] = {
+                "converged": r.converged, "iterations": r.iterations, "solve_s_device": float(np.sum(ms)) / 1e3,
+                "total_active_solves": r.report.total_active_solves,
+                "active_sizes_end": r.report.iterations[-1].active_sizes}
         s.close()
         a, p = out["asadmm"], out["sadmm"]
         out["asadmm_vs_sadmm_solve_ratio"] = a["total_active_solves"] / max(1, p["total_active_solves"])
