@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-for cfg in "RADMM_X=0"; do
-  env $cfg timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-ttt --steps 50 > gpurun_out/sweep.tmp 2>&1
+for cfg in "RADMM_SPLIT=0" "RADMM_SPLIT=1"; do
+  env $cfg timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-ttt --steps 400 > gpurun_out/sweep.tmp 2>&1
   python - "$cfg" <<'PY' >> gpurun_out/sweep.log
 import json,sys
 l=[x for x in open('gpurun_out/sweep.tmp') if x.startswith('{')][-1]
