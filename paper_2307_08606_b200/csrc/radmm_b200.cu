@@ -282,6 +282,7 @@ struct radmm_ctx {
   int Q_total = 0;
   int q_begin = 0;
   int rank = 0, world = 1;
+  bool sharded = false;  // NCCL exchange active (world > 1, or forced at world 1 by RADMM_FORCE_NCCL)
   int q_max_local = 0;
   int sm_count = 148;
   int fwd_per_sm = 4;  // resident forward-kernel CTAs per SM (occupancy API), 256-thread variant
@@ -1758,7 +1759,7 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
 // Sharded runs: every rank receives every sensor image (fixed global order),
 // plus per-sensor active sizes / stalled flags and the rank's notice bytes.
 void exchange(radmm_ctx* c, double notice_bytes) {
-  if (c->world <= 1) return;
+  if (!c->sharded) return;
   const size_t N = c->N;
   PhaseScope ps(c, RADMM_PHASE_EXCHANGE, 16.0 * N * c->q_max_local * c->world);
   for (int q = 0; q < c->Q; ++q)
@@ -1957,8 +1958,8 @@ bool sweep4_eligible(radmm_ctx* c) {
 }
 
 bool fused_eligible(radmm_ctx* c) {
-  if (fused_version() == 4 || fused_version() == 5) return c->world <= 1 && sweep4_eligible(c);
-  if (!fused_enabled() || c->world > 1 || c->Q < 1 || c->Q > 8) return false;
+  if (fused_version() == 4 || fused_version() == 5) return !c->sharded && sweep4_eligible(c);
+  if (!fused_enabled() || c->sharded || c->Q < 1 || c->Q > 8) return false;
   if (fused_version() == 3 && !sweep3_eligible(c)) return false;
   for (const Sensor& S : c->sensors)
     if (S.primal || S.ld > 4 * 512) return false;
@@ -2254,7 +2255,7 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
 
 void build_contrib(radmm_ctx* c) {
   std::vector<const double2*> ptrs(c->Q_total);
-  if (c->world <= 1) {
+  if (!c->sharded) {
     for (int q = 0; q < c->Q; ++q) ptrs[q] = c->sensors[q].x_full.p;
   } else {
     for (int g = 0; g < c->Q_total; ++g) {
@@ -2281,7 +2282,7 @@ void record_round(radmm_ctx* c, int k, const FusionScalars& f, uint64_t notice, 
   rec.eps_dual = f.eps_dual;
   uint64_t bytes = notice;
   bool stalled_any = false;
-  if (c->world <= 1) {
+  if (!c->sharded) {
     for (int q = 0; q < c->Q; ++q) {
       sizes[q] = c->sensors[q].n_act;
       stalled_any = stalled_any || c->sensors[q].stalled;
@@ -2404,7 +2405,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   // converged, and no screening staged).  Otherwise they exit at entry and
   // the host re-issues k+1 after screening.  Off for observers / profiling /
   // sharded or fused runs.
-  const bool spec = !(o && o->observer) && c->world <= 1 && !fused_enabled() && !c->profiling &&
+  const bool spec = !(o && o->observer) && !c->sharded && !fused_enabled() && !c->profiling &&
                     env_int("RADMM_SPECULATE", 1) != 0;
   auto screen_next_possible = [&]() { return (asadmm && !disable && c->upd >= c->W) ? 1 : 0; };
   // issue one round: local updates (+ exchange) + fusion; go == nullptr = unconditional
@@ -2534,7 +2535,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
 radmm_ctx* frame_ctx(radmm_ctx* p, int f) {
   if (!p) fail(RADMM_INVALID_ARGUMENT, "null context");
   if (p->parent) fail(RADMM_INVALID_ARGUMENT, "frame contexts cannot hold frames");
-  if (p->world > 1) fail(RADMM_INVALID_ARGUMENT, "multi-frame batches need an unsharded context");
+  if (p->sharded) fail(RADMM_INVALID_ARGUMENT, "multi-frame batches need an unsharded context");
   if (f < 0 || f >= 4096) fail(RADMM_INVALID_ARGUMENT, "frame index out of range");
   while ((int)p->frames.size() <= f) {
     for (int q = 0; q < p->Q; ++q)
@@ -3331,7 +3332,7 @@ int radmm_back_projection(radmm_ctx* ctx, double* image) {
     // per-sensor adjoint images A_q^H y_q: into the exchange send buffer when
     // sharded (then all-gathered), else into a local Q x N buffer
     DArr<double2> local;
-    double2* dst = c->world > 1 ? c->send_buf.p : nullptr;
+    double2* dst = c->sharded ? c->send_buf.p : nullptr;
     if (!dst) {
       local.alloc((size_t)c->Q * N, false);
       dst = local.p;
@@ -3346,7 +3347,7 @@ int radmm_back_projection(radmm_ctx* ctx, double* image) {
     }
     coldot<float2, EPI_STORE>(c, jobs, 1.0, 1.0);
     std::vector<const double2*> ptrs(c->Q_total);
-    if (c->world > 1) {
+    if (c->sharded) {
       g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble,
                                     c->comm, c->stream), "ncclAllGather(back_projection)");
       for (int g = 0; g < c->Q_total; ++g) {
@@ -3426,7 +3427,9 @@ int radmm_ctx_create_sharded(int device, int n_pixels, int q_total, int q_begin,
     c->rank = rank;
     c->world = world_size;
     c->q_max_local = (q_total + world_size - 1) / world_size;
-    if (world_size > 1) {
+    // a one-rank communicator exercises the very same exchange path on one GPU
+    c->sharded = world_size > 1 || (nccl_id && env_int("RADMM_FORCE_NCCL", 0) != 0);
+    if (c->sharded) {
       if (!nccl_id) fail(RADMM_INVALID_ARGUMENT, "null NCCL id");
       g_nccl.load();
       nccl_uid id;

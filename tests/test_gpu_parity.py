@@ -456,6 +456,30 @@ def test_sharded_context_world1_equals_plain():
     assert np.array_equal(r.x_global, plain.x_global) and np.array_equal(r.sigma, plain.sigma)
 
 
+def test_nccl_exchange_path_one_rank_equals_plain(monkeypatch):
+    """The multi-GPU exchange path on real hardware: a one-rank NCCL
+    communicator (RADMM_FORCE_NCCL) runs the same per-iteration all-gather of
+    the sensor images + metadata and the fusion over the gathered buffer as a
+    G-rank run does; results equal the plain single-GPU run bitwise."""
+    from paper_2307_08606_b200 import distributed as D
+    ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=60)
+    hyper = dict(hyper, screening_tol=1e-3)
+    h = api.Hyperparams(**hyper)
+    plain = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    monkeypatch.setenv("RADMM_FORCE_NCCL", "1")
+    s = D.sharded_solver(ops[0].shape[1], len(ops), 0, 1, 0, D.nccl_unique_id())
+    for q, (a, y) in enumerate(zip(ops, ys)):
+        s.set_operator(q, a)
+        s.set_measurement(q, y)
+    r = s.run(h, api.Mode.ASADMM, fixed_iterations=True)
+    s.close()
+    assert plain.downdates + plain.rebuilds > len(ops)  # eliminations happened
+    assert np.array_equal(r.x_global, plain.x_global) and np.array_equal(r.sigma, plain.sigma)
+    for a, b in zip(r.sensor_images, plain.sensor_images):
+        assert np.array_equal(a, b)
+    assert [rec.active_sizes for rec in r.report.iterations] == [rec.active_sizes for rec in plain.report.iterations]
+
+
 def test_apply_and_adjoint_match_host():
     ops, ys, hyper = _small_c1(nside=16, K=16)
     s = api.Solver(ops[0].shape[1], len(ops))
