@@ -259,7 +259,7 @@ def reference_arm(args, cfg):
     v = base["value"]
     out = {"metric": "ASADMM iterations/s", "value": v, "unit": "iterations/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64 complex)",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "dtype_note": "complex128 arithmetic (fp64 NumPy/SciPy oracle)",
            "data": "synthetic (seeded BASELINE dechirp operators, host generator)",
            "impl": "reference",
            "config": workload_config(cfg, 1, lam=None, parallelism=f"host BLAS threads ({base['cores']})"),
@@ -357,7 +357,7 @@ def ours(args, cfg):
     if rank == 0:
         out = {"metric": "ASADMM iterations/s", "value": value, "unit": "iterations/s", "n_gpus": world,
                "steps": K, "warmup": W, "ms_per_step": timed_ms / K, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "c64 operator, fp64 arithmetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "dtype_note": "complex64 operator storage, complex128 (fp64) arithmetic; Gram from exact int8 slices",
                "data": "synthetic (seeded BASELINE dechirp operators generated on device)",
                "config": workload_config(cfg, world, lam),
                "gpu_launches": launches, "clocks": clk, "roofline": roofline,
