@@ -164,6 +164,15 @@ constexpr int kNcclDouble = 8;  // ncclFloat64
 // ---------------------------------------------------------------------------
 // Device state
 // ---------------------------------------------------------------------------
+// forward CTA width: 256 threads (512-row tiles) up to kFwdTallRows, then
+// RADMM_FWD_TALL_THREADS (1024 default: config 3 forward 21.6 -> 20.2 ms; 512)
+int env_int(const char* name, int dflt);
+int fwd_threads(int64_t ld) {
+  if (ld <= kFwdTallRows) return 256;
+  static const int tall = env_int("RADMM_FWD_TALL_THREADS", 1024) == 512 ? 512 : 1024;
+  return tall;
+}
+
 struct Sensor {
   int rows = 0;
   int64_t ld = 0;  // roundup(rows, 64)
@@ -493,7 +502,10 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS, 256>, 256, 16 * 1024));
   c->fwd_per_sm = std::max(1, c->fwd_per_sm);
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 512>, 512, 16 * 1024));
+  if (fwd_threads(1 << 30) == 1024)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 1024>, 1024, 16 * 1024));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 512>, 512, 16 * 1024));
   c->fwd_per_sm_tall = std::max(1, c->fwd_per_sm_tall);
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->N = n_pixels;
@@ -557,9 +569,9 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.bz.alloc(S.ld);
   S.v.alloc(S.ld);
   S.w.alloc(S.ld);
-  const int tile = 2 * fwd_threads_for(S.ld);
+  const int tile = 2 * fwd_threads(S.ld);
   const int tiles = (int)((S.ld + tile - 1) / tile);
-  const int per_sm = fwd_threads_for(S.ld) == 512 ? c->fwd_per_sm_tall : c->fwd_per_sm;
+  const int per_sm = fwd_threads(S.ld) > 256 ? c->fwd_per_sm_tall : c->fwd_per_sm;
   S.part_chunks = std::max(std::max(1, c->sm_count * per_sm / tiles), (c->N + kMaxChunk - 1) / kMaxChunk) + 1;
   S.part.alloc((size_t)S.part_chunks * S.ld, false);
   S.has_op = true;
@@ -794,8 +806,8 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
     }
     if (max_chunks > 0) {
       const size_t smem = (size_t)max_len * (sizeof(double2) + sizeof(int));
-      const int threads = fwd_threads_for(ld_max);
-      auto kern = threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
+      const int threads = fwd_threads(ld_max);
+      auto kern = threads == 1024 ? fwd_kernel<MODE, 1024> : threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
       if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       dim3 grid((unsigned)((ld_max + 2 * threads - 1) / (2 * threads)), max_chunks, (unsigned)nb);
       LAUNCH(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
@@ -807,9 +819,9 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
 
 // chunking so one forward launch is exactly one full wave of resident CTAs
 void plan_chunks(radmm_ctx* c, const Sensor& S, int n, int batch, int& n_chunks, int& chunk_len) {
-  const int tile = 2 * fwd_threads_for(S.ld);
+  const int tile = 2 * fwd_threads(S.ld);
   const int tiles = (int)((S.ld + tile - 1) / tile);
-  const int target = c->sm_count * (fwd_threads_for(S.ld) == 512 ? c->fwd_per_sm_tall : c->fwd_per_sm);
+  const int target = c->sm_count * (fwd_threads(S.ld) > 256 ? c->fwd_per_sm_tall : c->fwd_per_sm);
   const int chunks = std::min(S.part_chunks, std::max(1, target / std::max(1, tiles * batch)));
   chunk_len = (int)std::min<int64_t>(kMaxChunk, round_up(std::max<int64_t>(32, (n + chunks - 1) / chunks), 8));
   n_chunks = (n + chunk_len - 1) / chunk_len;
@@ -1035,6 +1047,16 @@ void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
 // ---- Ozaki-sliced Gram on the int8 tensor cores (tcgen05, kernels_ozaki.cuh) ----
 bool ozaki_enabled() { return env_int("RADMM_OZAKI", 1) != 0; }
 
+// The slices are large for tall operators (config 3: 18.5 GB per sensor); only
+// small scratch (<= 2 GB, config 2: 1.2 GB) is kept between Grams.
+void release_ozaki_scratch(radmm_ctx* c) {
+  const size_t bytes = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
+  if (bytes <= (2ull << 30)) return;
+  c->oz_P.release();
+  c->oz_Q.release();
+  c->oz_R.release();
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -1110,11 +1132,19 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
 }
 
 // Full rebuild for the listed sensors (batched): data term + factor.
+void release_ozaki_scratch(radmm_ctx* c);
+
 void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
   if (qs.empty()) return;
   std::vector<GemmJob> jobs;
   std::vector<GramJob> grams;
   std::vector<InvTarget> inv;
+  for (int q : qs) {  // every factor's storage first: the Ozaki scratch is sized against what is left
+    Sensor& S = c->sensors[q];
+    const bool primal = S.n_act <= S.rows;
+    const int dim = primal ? S.n_act : S.rows;
+    ensure_g(S, dim, primal ? round_up(dim, 32) : S.ld);
+  }
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     S.primal = S.n_act <= S.rows;
@@ -1163,6 +1193,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
            256, kGramSmem, c->gram_jobs.p, mu, beta);
   }
   gemm<GEPI_PLAIN>(c, jobs);
+  release_ozaki_scratch(c);
   size_t need = 0;
   for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
   c->scratch.reserve(need);
@@ -2958,6 +2989,7 @@ void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
   S.primal = false;
   CK(cudaMemsetAsync(S.G.p, 0, sizeof(double2) * (size_t)S.ld * S.rows, c->stream));
   if (ozaki_gram(c, S, nullptr, c->N, S.G.p, S.ld, 1.0, 0.0)) {
+    release_ozaki_scratch(c);
     S.raw_gram = true;
     if (c->gram_evs.size() < (size_t)c->Q) c->gram_evs.resize(c->Q, nullptr);
     if (!c->gram_evs[q]) CK(cudaEventCreateWithFlags(&c->gram_evs[q], cudaEventDisableTiming));

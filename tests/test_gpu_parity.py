@@ -153,6 +153,19 @@ def test_ozaki_tcgen05_gram_matches_fp64_gram(rows, cols, monkeypatch):
     assert rel(outs["1"], outs["0"]) < 1e-8, rel(outs["1"], outs["0"])
 
 
+def test_tall_operator_dual_solve_matches_dense():
+    """A dual solve on an operator taller than 4096 rows (1024-thread forward
+    tiles, as at config 3) against a dense complex128 solve."""
+    rng = np.random.default_rng(9)
+    rows, cols, mu, beta = 4608, 5200, 1.0, 2.0
+    a = (rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols))).astype(np.complex64).astype(np.complex128)
+    rhs = rng.normal(size=cols) + 1j * rng.normal(size=cols)
+    x = api.factorize(a, mu, beta).solve(rhs)
+    cap = beta * np.eye(rows) + mu * a @ a.conj().T
+    ref = (rhs - mu * a.conj().T @ np.linalg.solve(cap, a @ rhs)) / beta
+    assert rel(x, ref) < 1e-8, rel(x, ref)
+
+
 def test_cached_solves_bitwise_reproducible():
     rng = np.random.default_rng(31)
     a = rng.normal(size=(10, 7)) + 1j * rng.normal(size=(10, 7))
