@@ -19,6 +19,9 @@ PHASE_OF = {  # kernel name fragment (mangled or demangled) -> bench phase name
     "coldot_pipe_kernelILi1": "adjoint",
     "coldot_pipe_kernel<1": "adjoint",
     "herm_gapply_persist_kernel": "gapply",
+    "fwd_kernel<0, 256": "forward",
+    "fwd_kernel<0, 512": "forward",
+    "fwd_kernel<0, 1024": "forward",
     "coldot_kernelI6float2Li1": "adjoint",
     "fwd_kernelILi0": "forward",
     "coldot_kernelI7double2Li0": "gapply",
