@@ -488,6 +488,9 @@ void configure_pool(int device) {
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
 }
 
+int occupancy(const void* func, int threads, size_t smem);
+void set_smem_attr(const void* func, int bytes);
+
 void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   c->device = device;
   CK(cudaSetDevice(device));
@@ -500,12 +503,12 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
     fail(RADMM_CUDA, "radmm_b200 requires an sm_100 (Blackwell) GPU; found " + std::string(prop.name));
   }
   CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm, fwd_kernel<MODE_RHS, 256>, 256, 16 * 1024));
+  c->fwd_per_sm = occupancy((const void*)fwd_kernel<MODE_RHS, 256>, 256, 16 * 1024);
   c->fwd_per_sm = std::max(1, c->fwd_per_sm);
   if (fwd_threads(1 << 30) == 1024)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 1024>, 1024, 16 * 1024));
+    c->fwd_per_sm_tall = occupancy((const void*)fwd_kernel<MODE_RHS, 1024>, 1024, 16 * 1024);
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->fwd_per_sm_tall, fwd_kernel<MODE_RHS, 512>, 512, 16 * 1024));
+    c->fwd_per_sm_tall = occupancy((const void*)fwd_kernel<MODE_RHS, 512>, 512, 16 * 1024);
   c->fwd_per_sm_tall = std::max(1, c->fwd_per_sm_tall);
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->N = n_pixels;
@@ -581,6 +584,46 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.has_y = false;
 }
 
+// Kernel attribute / occupancy queries cost microseconds of host time each;
+// the per-iteration launch path (and the host-bound elimination rounds) asks
+// the same questions every time, so the answers are cached per process.
+std::mutex g_attr_mu;
+std::vector<std::pair<const void*, int>> g_smem_attr;
+std::vector<std::pair<std::pair<const void*, int64_t>, int>> g_occ;
+
+void set_smem_attr(const void* func, int bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto& e : g_smem_attr)
+      if (e.first == func) {
+        if (e.second >= bytes) return;
+        break;
+      }
+  }
+  CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto& e : g_smem_attr)
+    if (e.first == func) {
+      e.second = std::max(e.second, bytes);
+      return;
+    }
+  g_smem_attr.push_back({func, bytes});
+}
+
+int occupancy(const void* func, int threads, size_t smem) {
+  const int64_t key = (int64_t)threads << 32 | (int64_t)smem;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto& e : g_occ)
+      if (e.first.first == func && e.first.second == key) return e.second;
+  }
+  int v = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, func, threads, smem));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  g_occ.push_back({{func, key}, v});
+  return v;
+}
+
 #define LAUNCH(c, kern, grid, block, smem, ...)                              \
   do {                                                                        \
     kern<<<(grid), (block), (smem), (c)->stream>>>(__VA_ARGS__);              \
@@ -596,9 +639,9 @@ void coldot_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max
                    double beta, const int* go) {
   auto kern = coldot_kernel<T, EPI, SMEM, CPW, THREADS>;
   if (SMEM && smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    set_smem_attr((const void*)kern, (int)(227 * 1024));
   int per_sm = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, SMEM ? smem : 0));
+  per_sm = occupancy((const void*)kern, THREADS, SMEM ? smem : 0);
   const int target = c->sm_count * std::max(1, per_sm);
   constexpr int kWarps = THREADS / 32;
   const int gx =
@@ -625,9 +668,9 @@ void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int 
   const int minb = env_int("RADMM_PIPE_MINB", 2);  // measured: 2 CTAs/SM (128 regs) streams best
   auto kern = minb >= 4 ? coldot_pipe_kernel<EPI, 256, 4> : minb == 2 ? coldot_pipe_kernel<EPI, 256, 2>
                                                                        : coldot_pipe_kernel<EPI, 256, 3>;
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)(227 * 1024));
   int per_sm = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  per_sm = occupancy((const void*)kern, 256, smem);
   const int slots = c->sm_count * std::max(1, per_sm);
   const int gmax = std::max(1, (n_max + 8 * 2 - 1) / (8 * 2));
   LAUNCH(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
@@ -731,17 +774,16 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
 // nr = 2 when some job carries a second right-hand side (v1 -> w1).
 void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go) {
   if (nr == 1 && env_int("RADMM_HERM", 1) == 2) {
-    CK(cudaFuncSetAttribute(herm_gapply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kHermTmaSmem));
+    set_smem_attr((const void*)herm_gapply_tma_kernel, (int)((int)kHermTmaSmem));
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
   } else if (nr == 2 || env_int("RADMM_HERM_PERSIST", 1)) {
     auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
     const size_t smem = herm_persist_smem(nr);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr((const void*)kern, (int)((int)smem));
     int per_sm = 1;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    per_sm = occupancy((const void*)kern, 256, smem);
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
     LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
   } else {
@@ -808,7 +850,7 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
       const size_t smem = (size_t)max_len * (sizeof(double2) + sizeof(int));
       const int threads = fwd_threads(ld_max);
       auto kern = threads == 1024 ? fwd_kernel<MODE, 1024> : threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
-      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)(227 * 1024));
       dim3 grid((unsigned)((ld_max + 2 * threads - 1) / (2 * threads)), max_chunks, (unsigned)nb);
       LAUNCH(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
@@ -864,15 +906,13 @@ void gemm(radmm_ctx* c, const std::vector<GemmJob>& jobs) {
       continue;
     }
     if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 2) == 2) {
-      CK(cudaFuncSetAttribute(gemm_dmma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kGemmDmmaSmem));
+      set_smem_attr((const void*)gemm_dmma_kernel<EPI>, (int)((int)kGemmDmmaSmem));
       dim3 grid((nn + kDmBN - 1) / kDmBN, (mm + kDmBM - 1) / kDmBM, (unsigned)nb);
       LAUNCH(c, gemm_dmma_kernel<EPI>, grid, 256, kGemmDmmaSmem, pk);
       continue;
     }
     if (EPI != GEPI_SPLIT && mm >= 256 && nn >= 256 && env_int("RADMM_GEMM_BIG", 2)) {
-      CK(cudaFuncSetAttribute(gemm_big_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)kGemmBigSmem));
+      set_smem_attr((const void*)gemm_big_kernel<EPI>, (int)((int)kGemmBigSmem));
       dim3 grid((nn + kBigBN - 1) / kBigBN, (mm + kBigBM - 1) / kBigBM, (unsigned)nb);
       LAUNCH(c, gemm_big_kernel<EPI>, grid, 256, kGemmBigSmem, pk);
       continue;
@@ -935,7 +975,7 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     n_max = std::max(n_max, targets[i].n);
   }
   CK(cudaMemsetAsync(c->fail_flags.p, 0, sizeof(int) * kMaxBatch, c->stream));
-  CK(cudaFuncSetAttribute(gj_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjSmem));
+  set_smem_attr((const void*)gj_diag_kernel, (int)(kGjSmem));
   if (n_max <= kGJB) {
     // every matrix is a single pivot block (the r x r downdate systems):
     // one in-shared-memory Gauss-Jordan, written back in place
@@ -975,7 +1015,7 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
       ujobs.push_back(u);
     }
     if (!live) break;
-    CK(cudaFuncSetAttribute(gj_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjSmem));
+    set_smem_attr((const void*)gj_diag_kernel, (int)(kGjSmem));
     LAUNCH(c, gj_diag_kernel, dim3((unsigned)T), 1024, kGjSmem, dj);
     const int pblocks = (int)std::min<int64_t>(1024, (panel_max + 255) / 256);
     LAUNCH(c, gj_panel_kernel, dim3(pblocks, (unsigned)T), 256, 0, dj);
@@ -991,7 +1031,7 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
                            reinterpret_cast<const double2*>(g.b.p), g.k0, g.kb};
         nmax = std::max(nmax, g.m);
       }
-      CK(cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjuSmem));
+      set_smem_attr((const void*)gj_update_kernel, (int)((int)kGjuSmem));
       LAUNCH(c, gj_update_kernel, dim3((unsigned)((nmax + kGjuBN - 1) / kGjuBN), (unsigned)((nmax + kGjuBM - 1) / kGjuBM),
                                        (unsigned)ujobs.size()), 256, kGjuSmem, up);
     } else {
@@ -1118,11 +1158,11 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
   CUtensorMap tP, tQ;
   if (env_int("RADMM_OZ_TMA", 1) && slice_tensor_map(&tP, c->oz_P.p, (int64_t)kOzSlices * rows_pad, kdim) &&
       slice_tensor_map(&tQ, c->oz_Q.p, (int64_t)kOzSlices * rows_pad, kdim)) {
-    CK(cudaFuncSetAttribute(oz_gram_pairs_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzTSmem));
+    set_smem_attr((const void*)oz_gram_pairs_tma_kernel, (int)((int)kOzTSmem));
     LAUNCH(c, oz_gram_pairs_tma_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzTSmem, tP, tQ,
            (int)rows_pad, (int)kdim, c->oz_R.p);
   } else {
-    CK(cudaFuncSetAttribute(oz_gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOzSmem));
+    set_smem_attr((const void*)oz_gram_pairs_kernel, (int)((int)kOzSmem));
     LAUNCH(c, oz_gram_pairs_kernel, dim3((unsigned)tiles, (unsigned)kOzPairs), 128, kOzSmem, c->oz_P.p, c->oz_Q.p,
            (int64_t)slice, rows, (int)kdim, c->oz_R.p);
   }
@@ -1187,7 +1227,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
                        c->stream));
     int mmax = 0;
     for (const auto& g : grams) mmax = std::max(mmax, g.m);
-    CK(cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
+    set_smem_attr((const void*)gram_dmma_kernel, (int)((int)kGramSmem));
     LAUNCH(c, gram_dmma_kernel, dim3((unsigned)((mmax + kGrBN - 1) / kGrBN), (unsigned)((mmax + kGrBM - 1) / kGrBM),
                                      (unsigned)grams.size()),
            256, kGramSmem, c->gram_jobs.p, mu, beta);
@@ -1269,7 +1309,7 @@ void lazy_finish(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   }
   const unsigned nb = (unsigned)qs.size();
   LAUNCH(c, lazy_border_dots_kernel, dim3((unsigned)dmax, nb), 256, 0, pk);
-  CK(cudaFuncSetAttribute(lazy_border_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBorderSmem));
+  set_smem_attr((const void*)lazy_border_inv_kernel, (int)((int)kBorderSmem));
   LAUNCH(c, lazy_border_inv_kernel, dim3(nb), 256, kBorderSmem, pk, mu);
   if (c->pending_fail + (int)nb > kFlagCap) {
     CK(cudaStreamSynchronize(c->stream));
@@ -2001,7 +2041,7 @@ template <int RPT>
 void launch_sweep(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa, const radmm_hyperparams* h,
                   size_t smem) {
   auto kern = fused_sweep_kernel<RPT>;
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)((int)smem));
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -2055,7 +2095,7 @@ void launch_sweep2(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa,
   cfg.gridDim = dim3((unsigned)c->Q);
   // smem: w (ld complex) + tile table of the largest range (one cluster: N)
   size_t smem = (size_t)ld_max * sizeof(double2) + sizeof(int) * ((size_t)c->N / tile + 2);
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(smem, 200 * 1024)));
+  set_smem_attr((const void*)kern, (int)((int)std::min<size_t>(smem, 200 * 1024)));
   cfg.dynamicSmemBytes = std::min<size_t>(smem, 200 * 1024);
   int clusters = 0;
   CK(cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg));
@@ -2067,7 +2107,7 @@ void launch_sweep2(radmm_ctx* c, const Pack<SweepJob>& pk, const FusionArgs& fa,
   clusters = (c->N + range - 1) / range;
   smem = (size_t)ld_max * sizeof(double2) + sizeof(int) * ((size_t)range / tile + 2);
   if (smem > 200 * 1024) fail(RADMM_INVALID_ARGUMENT, "fused sweep: tile table exceeds shared memory");
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  set_smem_attr((const void*)kern, (int)((int)smem));
   cfg.dynamicSmemBytes = smem;
   cfg.gridDim = dim3((unsigned)(c->Q * clusters));
   if (c->fpart.n < (size_t)5 * c->Q * clusters) c->fpart.alloc((size_t)5 * c->Q * clusters);
@@ -2117,7 +2157,7 @@ void launch_sweep4(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa,
                 v5 ? c->xg_alt.p : nullptr, v5 ? c->sigma_alt.p : nullptr};
   const size_t smem = (size_t)ld * sizeof(double2) + (size_t)kS4Slots * kS4P * ld * sizeof(float2) +
                       kS4Slots * sizeof(uint64_t);
-  CK(cudaFuncSetAttribute(fused_sweep4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  set_smem_attr((const void*)fused_sweep4_kernel, (int)((int)smem));
   double mu = h->mu, beta = h->beta;
   int64_t ldv = ld;
   void* args[] = {(void*)&pk, (void*)&fa, (void*)&ctl, (void*)&mu, (void*)&beta, (void*)&ldv};
@@ -2127,7 +2167,7 @@ void launch_sweep4(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa,
   if (fused_version() == 5) {
     const size_t smem5 = (size_t)ld * sizeof(double2) + (size_t)kS5Slots * kS4P * ld * sizeof(float2) +
                          2 * kS5Slots * sizeof(uint64_t);
-    CK(cudaFuncSetAttribute(fused_sweep5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    set_smem_attr((const void*)fused_sweep5_kernel, (int)((int)smem5));
     CK(cudaLaunchCooperativeKernel((void*)fused_sweep5_kernel, dim3((unsigned)chunks, (unsigned)c->Q),
                                    dim3(kS5Threads), args, smem5, c->stream));
     std::swap(c->xg, c->xg_alt);  // the round's new x_G / sigma
@@ -2152,7 +2192,7 @@ void launch_sweep3(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa,
   // per-sensor tile tables: sized for >= 8 clusters, re-checked below
   const size_t tab_est = sizeof(int) * (size_t)c->Q * ((c->N + 8 * kS3P - 1) / (8 * kS3P) + 2);
   size_t smem = base + tab_est;
-  CK(cudaFuncSetAttribute(fused_sweep3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  set_smem_attr((const void*)fused_sweep3_kernel, (int)((int)smem));
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -2177,7 +2217,7 @@ void launch_sweep3(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa,
   if (tab > tab_est) {
     smem = base + tab;
     if (smem > 227 * 1024) fail(RADMM_INVALID_ARGUMENT, "fused sweep v3: tile tables exceed shared memory");
-    CK(cudaFuncSetAttribute(fused_sweep3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_smem_attr((const void*)fused_sweep3_kernel, (int)((int)smem));
     cfg.dynamicSmemBytes = smem;
   }
   cfg.gridDim = dim3((unsigned)(kS3R * clusters));
@@ -2478,16 +2518,27 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     return false;
   };
   bool k_launched = false;   // iteration k already enqueued (speculatively)
+  const bool trace_host = env_int("RADMM_TRACE_HOST", 0) != 0;  // host time of re-issued rounds (stderr)
+  double host_ev_us = 0, host_issue_us = 0;
+  int host_n = 0;
   int64_t l_k = 0;           // launch counter when iteration k was enqueued
   uint64_t notice_k = 0;
   for (int k = 1; k <= h->max_iter; ++k) {
     if (!k_launched) {
+      const auto tt0 = std::chrono::steady_clock::now();
       l_k = c->launches;
       CK(cudaEventRecord(STEP(k - 1), c->stream));
       notice_k = 0;
       if (asadmm && !disable && staged_trigger)
         notice_k = c->pre_screened[(k - 1) & 1] ? apply_screen(c, h, k, (k - 1) & 1) : screen_all(c, h, k);
+      const auto tt1 = std::chrono::steady_clock::now();
       issue(k, nullptr, notice_k);
+      if (trace_host) {
+        const auto tt2 = std::chrono::steady_clock::now();
+        host_ev_us += std::chrono::duration<double, std::micro>(tt1 - tt0).count();
+        host_issue_us += std::chrono::duration<double, std::micro>(tt2 - tt1).count();
+        ++host_n;
+      }
     }
     const uint64_t notice = notice_k;
     const int64_t l0 = l_k;
@@ -2541,6 +2592,9 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     staged_trigger = f.trigger != 0;
   }
   if (fixed) sm.converged = f.converged;
+  if (trace_host && host_n)
+    std::fprintf(stderr, "[radmm host] %d re-issued rounds: events %.1f us, issue %.1f us per round\n", host_n,
+                 host_ev_us / host_n, host_issue_us / host_n);
   CK(cudaEventRecord(STEP(sm.iterations), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   check_deferred(c);
@@ -2679,22 +2733,20 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
     const bool v2 = env_int("RADMM_FRAME_KERNEL", 2) == 2;
     if (mode != FB_GAP && v2) {  // operator passes: cp.async multistage pipeline
       if (mode == FB_FWD) {
-        CK(cudaFuncSetAttribute(frame_batch2_kernel<FB_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kFb2Smem));
+        set_smem_attr((const void*)frame_batch2_kernel<FB_FWD>, (int)((int)kFb2Smem));
         LAUNCH(p, frame_batch2_kernel<FB_FWD>, grid, 256, kFb2Smem, p->fb_jobs.p, nsplit, mu, beta);
       } else {
-        CK(cudaFuncSetAttribute(frame_batch2_kernel<FB_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kFb2Smem));
+        set_smem_attr((const void*)frame_batch2_kernel<FB_ADJ>, (int)((int)kFb2Smem));
         LAUNCH(p, frame_batch2_kernel<FB_ADJ>, grid, 256, kFb2Smem, p->fb_jobs.p, nsplit, mu, beta);
       }
     } else if (mode == FB_FWD) {
-      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      set_smem_attr((const void*)frame_batch_kernel<FB_FWD>, (int)(sm));
       LAUNCH(p, frame_batch_kernel<FB_FWD>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
     } else if (mode == FB_GAP) {
-      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_GAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      set_smem_attr((const void*)frame_batch_kernel<FB_GAP>, (int)(sm));
       LAUNCH(p, frame_batch_kernel<FB_GAP>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
     } else {
-      CK(cudaFuncSetAttribute(frame_batch_kernel<FB_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      set_smem_attr((const void*)frame_batch_kernel<FB_ADJ>, (int)(sm));
       LAUNCH(p, frame_batch_kernel<FB_ADJ>, grid, 256, kFbSmem, p->fb_jobs.p, nsplit, mu, beta);
     }
     if (mode == FB_ADJ) return;
@@ -2999,7 +3051,7 @@ void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
   // the job travels as a kernel parameter: a pageable job-table upload would
   // wait for the previous sensor's Gram and serialise the pipeline
   const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, S.G.p, S.ld};
-  CK(cudaFuncSetAttribute(gram_dmma1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
+  set_smem_attr((const void*)gram_dmma1_kernel, (int)((int)kGramSmem));
   LAUNCH(c, gram_dmma1_kernel,
          dim3((unsigned)((S.rows + kGrBN - 1) / kGrBN), (unsigned)((S.rows + kGrBM - 1) / kGrBM), 1u), 256,
          kGramSmem, g, 1.0, 0.0);
