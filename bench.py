@@ -349,7 +349,7 @@ def ours(args, cfg):
     # ---- CPU baseline ------------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(cfg, 3)
+        cpu = cpu_sample(cfg, 12, budget_s=12.0)  # about 10-15 s of CPU work
         if ttt is not None:
             ttt["cpu_oracle_time_to_tolerance_s_est"] = ttt["iterations"] / cpu["value"]
 
