@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ P
   if (j >= jb.d) return;
   const float2* a = jb.A + (int64_t)jb.pix[j] * jb.ld;
   double re = 0.0, im = 0.0;
+#pragma unroll 4
   for (int i = threadIdx.x; i < jb.rows; i += 256) {
     const float2 x = a[i];
     const double2 u = jb.w[i];
@@ -461,7 +462,21 @@ __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ 
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= jb.rows) return;
   double re = 0.0, im = 0.0;
-  for (int k = 0; k < jb.d; ++k) {
+  int k = 0;
+  for (; k + 8 <= jb.d; k += 8) {  // eight independent loads in flight, summed in order
+    double2 p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = jb.P[i + (int64_t)(k + u) * jb.ld];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 x = sv[k + u];
+      re = fma(p[u].x, x.x, re);
+      re = fma(-p[u].y, x.y, re);
+      im = fma(p[u].x, x.y, im);
+      im = fma(p[u].y, x.x, im);
+    }
+  }
+  for (; k < jb.d; ++k) {
     const double2 p = jb.P[i + (int64_t)k * jb.ld], x = sv[k];
     re = fma(p.x, x.x, re);
     re = fma(-p.y, x.y, re);
