@@ -283,11 +283,10 @@ __global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__
 // reduction and epilogue, and the epilogue's inputs (rhs, pixel, old x) are
 // fetched at the start of the pair -- so no load bubble opens at column
 // boundaries.  Needs a multiple of four 64-row steps (KM % 256 == 0).
-template <int EPI, int THREADS, int MINB>
+template <int EPI, int THREADS, int MINB, int CPW = 2>
 __global__ void __launch_bounds__(THREADS, MINB) coldot_pipe_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu,
                                                               double beta, const int* __restrict__ go) {
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
-  constexpr int CPW = 2;
   extern __shared__ double2 sv[];
   constexpr int kWarps = THREADS / 32;
   const ColDotJob& jb = jobs.j[blockIdx.y];

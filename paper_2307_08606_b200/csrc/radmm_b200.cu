@@ -666,13 +666,15 @@ template <int EPI>
 void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int n_max, size_t smem, double mu,
                         double beta, const int* go) {
   const int minb = env_int("RADMM_PIPE_MINB", 2);  // measured: 2 CTAs/SM (128 regs) streams best
-  auto kern = minb >= 4 ? coldot_pipe_kernel<EPI, 256, 4> : minb == 2 ? coldot_pipe_kernel<EPI, 256, 2>
+  const int cpw = env_int("RADMM_PIPE_CPW", 4) == 2 ? 2 : 4;  // 4 columns per warp: adjoint 0.346 -> 0.343 ms
+  auto kern = cpw == 4 ? coldot_pipe_kernel<EPI, 256, 2, 4>
+              : minb >= 4 ? coldot_pipe_kernel<EPI, 256, 4> : minb == 2 ? coldot_pipe_kernel<EPI, 256, 2>
                                                                        : coldot_pipe_kernel<EPI, 256, 3>;
   if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)(227 * 1024));
   int per_sm = 1;
   per_sm = occupancy((const void*)kern, 256, smem);
   const int slots = c->sm_count * std::max(1, per_sm);
-  const int gmax = std::max(1, (n_max + 8 * 2 - 1) / (8 * 2));
+  const int gmax = std::max(1, (n_max + 8 * cpw - 1) / (8 * cpw));
   LAUNCH(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
 }
 

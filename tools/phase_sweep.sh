@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for cfg in "RADMM_X=1"; do
+for cfg in "RADMM_PIPE_CPW=2" "RADMM_PIPE_CPW=4"; do
   env $cfg timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-ttt --steps 400 > gpurun_out/sweep.tmp 2>&1
   python - "$cfg" <<'PY' >> gpurun_out/sweep.log
 import json,sys
