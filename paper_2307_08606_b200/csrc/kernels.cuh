@@ -19,8 +19,8 @@
 
 
 // The kernels live in topical headers, included in dependency order.
-#include "kernels_matvec.cuh"
 #include "kernels_async.cuh"
+#include "kernels_matvec.cuh"
 #include "kernels_dense.cuh"
 #include "kernels_batched.cuh"
 #include "kernels_fused.cuh"

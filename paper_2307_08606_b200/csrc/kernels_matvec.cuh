@@ -873,4 +873,133 @@ __global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid
   }
 }
 
+// The same screening in ONE launch: sensor q is one cluster of kScreenCluster
+// CTAs (blockIdx.y = q); each CTA owns a contiguous range of `per` rounds of
+// kScanBlock entries, keeps its flags in a register mask, scans its
+// (round, warp) kept counts in shared memory and reads the other CTAs' kept
+// totals through distributed shared memory for its output offset.  The last
+// sensor to finish (arrival ticket) sets *go_next when no set changed.  Same
+// outputs, same order as screen_flags / screen_scan / screen_scatter.
+constexpr int kScreenCluster = 8;
+constexpr int kScreenMaxE = 8;  // rounds per CTA: n <= 8 * 1024 * 8 = 65536
+
+__device__ __forceinline__ int dsmem_ld_i32(const int* p, unsigned cta) {
+  uint32_t ra;
+  int v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+  return v;
+}
+
+__global__ void __cluster_dims__(kScreenCluster, 1, 1) __launch_bounds__(kScanBlock)
+    screen_fused_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int nq, int W, double tol,
+                        const int* __restrict__ go, const int* __restrict__ sgo, int* totals_host, int* go_next,
+                        unsigned* sync /* [0] arrival ticket, [1] changed; zero between launches */) {
+  if (screen_off(go, sgo)) return;
+  const ScreenJob& jb = jobs.j[blockIdx.y];
+  const unsigned rank = cluster_ctarank();
+  const int n = jb.n;
+  const int per = (n + kScreenCluster * kScanBlock - 1) / (kScreenCluster * kScanBlock);
+  const int base = (int)rank * per * kScanBlock;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int cnt[kScreenMaxE * 32];  // kept count per (round, warp) -> exclusive offset in the CTA
+  __shared__ int wsum[32];
+  __shared__ int blk_total, blk_off, sensor_total;
+
+  int pix[kScreenMaxE];
+#pragma unroll
+  for (int r = 0; r < kScreenMaxE; ++r) {
+    const int i = base + r * kScanBlock + threadIdx.x;
+    pix[r] = (r < per && i < n) ? __ldg(jb.J + i) : -1;
+  }
+  double z[kScreenMaxE];
+#pragma unroll
+  for (int r = 0; r < kScreenMaxE; ++r) {
+    z[r] = 0.0;
+    if (pix[r] >= 0)
+      for (int t = 0; t < W; ++t) {
+        const int slot = (jb.first_slot + t) % W;
+        z[r] += __ldg(jb.ring + (int64_t)slot * jb.ring_stride + pix[r]);
+      }
+  }
+  unsigned kmask = 0;
+#pragma unroll
+  for (int r = 0; r < kScreenMaxE; ++r) {
+    if (r >= per) break;
+    const bool k = pix[r] >= 0 && z[r] / (double)W >= tol;
+    if (k) kmask |= 1u << r;
+    const unsigned b = __ballot_sync(0xffffffffu, k);
+    if (lane == 0) cnt[r * 32 + warp] = __popc(b);
+  }
+  __syncthreads();
+  // exclusive scan of the per*32 counts, round-major (= index order)
+  const int nv = per * 32;
+  const int v = (int)threadIdx.x < nv ? cnt[threadIdx.x] : 0;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = wsum[lane];
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    wsum[lane] = wi - w;
+    if (lane == 31) blk_total = wi;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < nv) cnt[threadIdx.x] = inc - v + wsum[warp];
+  cluster_sync_acqrel();  // every CTA's blk_total is written
+  if (threadIdx.x == 0) {
+    int off = 0, tot = 0;
+    for (unsigned r = 0; r < (unsigned)kScreenCluster; ++r) {
+      const int t = dsmem_ld_i32(&blk_total, r);
+      if (r < rank) off += t;
+      tot += t;
+    }
+    blk_off = off;
+    sensor_total = tot;
+  }
+  cluster_sync_acqrel();  // no CTA leaves while its blk_total may still be read
+  const int off = blk_off;
+#pragma unroll
+  for (int r = 0; r < kScreenMaxE; ++r) {
+    if (r >= per) break;
+    const bool k = (kmask >> r) & 1u;
+    const unsigned b = __ballot_sync(0xffffffffu, k);
+    if (pix[r] < 0) continue;
+    const int i = base + r * kScanBlock + threadIdx.x;
+    const int kept_before = off + cnt[r * 32 + warp] + __popc(b & ((1u << lane) - 1u));
+    if (k) {
+      jb.Jnew[kept_before] = pix[r];
+      jb.keep_pos[kept_before] = i;
+      jb.x_hat_new[kept_before] = jb.x_hat[i];  // x_full[J_new] (admm.hpp:153-156)
+      jb.data_new[kept_before] = jb.data[i];
+    } else {
+      const int rpos = i - kept_before;
+      jb.rem_pix[rpos] = pix[r];
+      jb.rem_pos[rpos] = i;
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    const int s = sensor_total;
+    jb.totals[0] = s;
+    if (totals_host) ((volatile int*)totals_host)[blockIdx.y] = s;
+    if (s != n && s != 0) atomicOr(sync + 1, 1u);
+    __threadfence_system();
+    if (atomicAdd(sync, 1u) == (unsigned)nq - 1) {
+      const unsigned changed = atomicExch(sync + 1, 0u);
+      atomicExch(sync, 0u);
+      if (go_next && !changed) *go_next = 1;
+    }
+  }
+}
+
 }  // namespace radmm_dev

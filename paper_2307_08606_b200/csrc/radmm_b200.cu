@@ -341,6 +341,7 @@ struct radmm_ctx {
   DArr<int> go_flags;                // speculation guards, alternating per round
   DArr<unsigned> lazy_cnt;           // lazy_dot_kernel arrival counters (one per job)
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
+  DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
   DArr<uint64_t> herm_items;         // Hermitian G-apply work items (largest first)
@@ -532,6 +533,7 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
   c->go_flags.alloc(2);
   c->sgo_flags.alloc(2);
+  c->screen_sync.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
   c->h_totals = reinterpret_cast<int*>(c->pinned_block + off_tot);
   CK(cudaHostGetDevicePointer((void**)&c->d_totals, c->h_totals, 0));
@@ -1868,6 +1870,7 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go =
 }
 
 bool fused_enabled();
+int env_int(const char* name, int dflt);
 
 // SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386),
 // device part: zeta, keep flags, compaction into the *_new buffers and the
@@ -1895,6 +1898,12 @@ bool enqueue_screen(radmm_ctx* c, const radmm_hyperparams* h, int slot, const in
   double sb = 0;
   for (int q = 0; q < c->Q; ++q) sb += (double)c->sensors[q].n_act * (8.0 * c->W + 4 + 1 + 4 + 4 + 32);
   PhaseScope ps(c, RADMM_PHASE_SCREEN, sb);
+  // one cluster launch (RADMM_SCREEN_FUSED=0 selects the three-kernel path)
+  if (n_max <= kScreenCluster * kScanBlock * kScreenMaxE && env_int("RADMM_SCREEN_FUSED", 1) != 0) {
+    LAUNCH(c, screen_fused_kernel, dim3(kScreenCluster, c->Q), kScanBlock, 0, pk, c->Q, c->W, h->screening_tol, go,
+           sgo, c->d_totals + (size_t)slot * c->Q, go_next, c->screen_sync.p);
+    return true;
+  }
   LAUNCH(c, screen_flags_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, c->W, h->screening_tol, go, sgo);
   LAUNCH(c, screen_scan_kernel, dim3(1), 256, 0, pk, c->Q, go, sgo, c->d_totals + (size_t)slot * c->Q, go_next);
   LAUNCH(c, screen_scatter_kernel, dim3(nb, c->Q), kScanBlock, 0, pk, go, sgo);

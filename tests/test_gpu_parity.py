@@ -414,6 +414,7 @@ DOWNDATE_VARIANTS = {
     "lazy_folds": {"RADMM_LAZY_MAX": "3", "RADMM_HERM_MIN_ROWS": "0"},  # fold into G every few events
     "lazy_full_gapply": {"RADMM_HERM": "0"},  # every column through the column-dot G-apply
     "eager": {"RADMM_LAZY": "0"},      # G rewritten at every event
+    "three_kernel_screen": {"RADMM_SCREEN_FUSED": "0"},  # flags / scan / scatter instead of the cluster kernel
 }
 
 
@@ -453,6 +454,30 @@ def test_eager_upload_gram_is_bitwise_identical(monkeypatch):
     for a, b in zip(eager.sensor_images, late.sensor_images):
         assert np.array_equal(a, b)
     assert np.array_equal(eager.sigma, late.sigma)
+
+
+@pytest.mark.parametrize("nside,tol", [(100, 3e-4), (181, 1e-4)])
+def test_fused_screening_equals_three_kernel_path(nside, tol, monkeypatch):
+    """The one-launch cluster screening (several 1024-entry rounds per CTA,
+    ragged last CTA: N = 10000 and 32761) compacts exactly like the
+    flags / scan / scatter kernels: same active sets, same states bit for bit,
+    and the sets track the oracle's."""
+    ops, ys, hyper = _small_c1(nside=nside, K=8, n_targets=6, max_iter=40)
+    hyper = dict(hyper, screening_tol=tol)
+    runs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RADMM_SCREEN_FUSED", flag)
+        runs[flag] = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
+    f, t = runs["1"], runs["0"]
+    assert f.downdates + f.rebuilds > len(ops)
+    for rf, rt in zip(f.report.iterations, t.report.iterations):
+        assert rf.active_sizes == rt.active_sizes
+    for a, b in zip(f.sensor_images, t.sensor_images):
+        assert np.array_equal(a, b)
+    assert np.array_equal(f.sigma, t.sigma) and np.array_equal(f.x_global, t.x_global)
+    o = oracle_run(ops, ys, hyper, True, fixed_iterations=True)
+    bad, near = compare_masks(f, o, hyper["screening_tol"], 5)
+    assert bad == 0, (bad, near)
 
 
 def test_sharded_context_world1_equals_plain():
