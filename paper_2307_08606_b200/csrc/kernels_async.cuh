@@ -10,6 +10,14 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch: the iteration kernels are launched with
+// programmatic stream serialisation (LAUNCH_PDL), so a kernel's CTAs may be
+// scheduled while its predecessor drains.  pdl_wait() blocks until the
+// predecessor grid has completed and its memory is visible (a no-op for a
+// normal launch); pdl_trigger() lets the successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void cluster_sync_acqrel() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");

@@ -170,6 +170,8 @@ template <int NR>
 __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                     const uint64_t* __restrict__ items, int n_items,
                                                                     const int* __restrict__ go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ __align__(16) double2 hps[];  // herm_persist_smem(NR) bytes
   double2(*vJ)[NR][kHermTile] = reinterpret_cast<double2(*)[NR][kHermTile]>(hps);
@@ -316,6 +318,8 @@ constexpr int kHermRedSlices = 8;  // 512 threads: 8 slices x 64 rows, 4 loads i
 
 __global__ void __launch_bounds__(kHermRedSlices * kHermTile) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                                 const int* __restrict__ go) {
+  pdl_wait();
+  pdl_trigger();
   if (go && __ldg(go) == 0) return;
   const HermJob& jb = P.j[blockIdx.y];
   const int c = blockIdx.z;

@@ -341,6 +341,7 @@ struct radmm_ctx {
   DArr<int> go_flags;                // speculation guards, alternating per round
   DArr<unsigned> lazy_cnt;           // lazy_dot_kernel arrival counters (one per job)
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
+  bool pdl = true;                   // programmatic dependent launch of the iteration kernels (RADMM_PDL)
   DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
@@ -533,6 +534,7 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
   c->go_flags.alloc(2);
   c->sgo_flags.alloc(2);
+  c->pdl = env_int("RADMM_PDL", 1) != 0;
   c->screen_sync.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
   c->h_totals = reinterpret_cast<int*>(c->pinned_block + off_tot);
@@ -633,6 +635,30 @@ int occupancy(const void* func, int threads, size_t smem) {
     ++(c)->launches;                                                          \
   } while (0)
 
+// Iteration kernels that open with pdl_wait() (kernels_async.cuh) are
+// launched with programmatic stream serialisation: their CTAs are scheduled
+// while the predecessor drains, hiding the launch gap between the forward,
+// G-apply, reduce, adjoint and fusion kernels.  RADMM_PDL=0 turns it off.
+#define LAUNCH_PDL(c, kern, grid, block, smem, ...)                                   \
+  do {                                                                                \
+    if ((c)->pdl) {                                                                   \
+      cudaLaunchConfig_t cfg_{};                                                      \
+      cfg_.gridDim = dim3(grid);                                                      \
+      cfg_.blockDim = dim3(block);                                                    \
+      cfg_.dynamicSmemBytes = (smem);                                                 \
+      cfg_.stream = (c)->stream;                                                      \
+      cudaLaunchAttribute at_[1];                                                     \
+      at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                 \
+      at_[0].val.programmaticStreamSerializationAllowed = 1;                          \
+      cfg_.attrs = at_;                                                               \
+      cfg_.numAttrs = 1;                                                              \
+      CK(cudaLaunchKernelEx(&cfg_, kern, __VA_ARGS__));                               \
+      ++(c)->launches;                                                                \
+    } else {                                                                          \
+      LAUNCH(c, kern, grid, block, smem, __VA_ARGS__);                                \
+    }                                                                                 \
+  } while (0)
+
 // ---- column-dot launches --------------------------------------------------
 // One full wave of resident CTAs split evenly over the batch (occupancy API);
 // every warp then owns a balanced contiguous range of columns.
@@ -677,7 +703,7 @@ void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int 
   per_sm = occupancy((const void*)kern, 256, smem);
   const int slots = c->sm_count * std::max(1, per_sm);
   const int gmax = std::max(1, (n_max + 8 * cpw - 1) / (8 * cpw));
-  LAUNCH(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
+  LAUNCH_PDL(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
 }
 
 int coldot_cpw() {
@@ -789,11 +815,11 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     int per_sm = 1;
     per_sm = occupancy((const void*)kern, 256, smem);
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
-    LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
+    LAUNCH_PDL(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
   } else {
     LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
-  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
+  LAUNCH_PDL(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
          pk, go);
 }
 
@@ -856,10 +882,10 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
       auto kern = threads == 1024 ? fwd_kernel<MODE, 1024> : threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
       if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)(227 * 1024));
       dim3 grid((unsigned)((ld_max + 2 * threads - 1) / (2 * threads)), max_chunks, (unsigned)nb);
-      LAUNCH(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
+      LAUNCH_PDL(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
     dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
-    LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp, go);
+    LAUNCH_PDL(c, reduce_parts_kernel, rg, 256, 0, rp, go);
   }
 }
 
@@ -1866,11 +1892,10 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go =
   a.screen_next_possible = screen_next_possible;
   a.screen_go = screen_go;
   PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
-  LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
+  LAUNCH_PDL(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
 
 bool fused_enabled();
-int env_int(const char* name, int dflt);
 
 // SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386),
 // device part: zeta, keep flags, compaction into the *_new buffers and the
