@@ -17,6 +17,12 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // normal launch); pdl_trigger() lets the successor start launching.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// (Triggering before the wait measured the same: successors cannot become
+// resident before the full-wave predecessors drain anyway.)
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
 
 __device__ __forceinline__ void cluster_sync_acqrel() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");

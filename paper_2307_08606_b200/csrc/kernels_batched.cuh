@@ -170,8 +170,7 @@ template <int NR>
 __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                     const uint64_t* __restrict__ items, int n_items,
                                                                     const int* __restrict__ go) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ __align__(16) double2 hps[];  // herm_persist_smem(NR) bytes
   double2(*vJ)[NR][kHermTile] = reinterpret_cast<double2(*)[NR][kHermTile]>(hps);
@@ -318,8 +317,7 @@ constexpr int kHermRedSlices = 8;  // 512 threads: 8 slices x 64 rows, 4 loads i
 
 __global__ void __launch_bounds__(kHermRedSlices * kHermTile) herm_reduce_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                                 const int* __restrict__ go) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (go && __ldg(go) == 0) return;
   const HermJob& jb = P.j[blockIdx.y];
   const int c = blockIdx.z;
@@ -412,6 +410,7 @@ __device__ __forceinline__ void lazy_s(const LazyJob& jb, double mu, const doubl
 // forms s = mu Sinv t (lazy_s), so lazy_axpy_kernel only streams P.
 __global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ Pack<LazyJob> P, double mu,
                                                        const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;
   const LazyJob& jb = P.j[blockIdx.y];
   const int j = blockIdx.x;
@@ -457,6 +456,7 @@ __global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ P
 
 __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ Pack<LazyJob> P, double mu,
                                                         const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;
   const LazyJob& jb = P.j[blockIdx.y];
   if (jb.d <= 0 || (int64_t)blockIdx.x * 256 >= jb.rows) return;

@@ -286,8 +286,7 @@ __global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__
 template <int EPI, int THREADS, int MINB, int CPW = 2>
 __global__ void __launch_bounds__(THREADS, MINB) coldot_pipe_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu,
                                                               double beta, const int* __restrict__ go) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ double2 sv[];
   constexpr int kWarps = THREADS / 32;
@@ -448,8 +447,7 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __grid_constant__ Pa
                                                           const double2* __restrict__ gap,
                                                           const double2* __restrict__ sigma, double beta,
                                                           const int* __restrict__ go) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ unsigned char smem_raw[];
   const FwdJob& jb = jobs.j[blockIdx.z];
@@ -520,8 +518,7 @@ struct ReduceJob {
 };
 
 __global__ void reduce_parts_kernel(const __grid_constant__ Pack<ReduceJob> jobs, const int* __restrict__ go) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   const ReduceJob& jb = jobs.j[blockIdx.y];
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -730,8 +727,7 @@ __device__ __forceinline__ void fusion_finish(const FusionArgs& a, double (&q)[5
 }
 
 __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter();
   if (a.go && __ldg(a.go) == 0) return;  // cancelled speculative iteration
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double q[5] = {0, 0, 0, 0, 0};

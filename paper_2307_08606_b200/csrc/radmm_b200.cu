@@ -1457,8 +1457,8 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
   if (!nb) return;
   if (c->lazy_cnt.n < (size_t)kMaxBatch) c->lazy_cnt.alloc(kMaxBatch);  // zeroed; the last blocks re-zero
   for (int i = 0; i < nb; ++i) pk.j[i].cnt = c->lazy_cnt.p + i;
-  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
-  LAUNCH(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
+  LAUNCH_PDL(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
+  LAUNCH_PDL(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
 }
 
 void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu);
