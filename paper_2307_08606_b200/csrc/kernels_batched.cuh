@@ -49,6 +49,7 @@ template <int NR>
 __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant__ Pack<HermJob> P,
                                                          const uint64_t* __restrict__ items,
                                                          const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   const uint64_t it = items[blockIdx.x];
   const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
@@ -514,6 +515,7 @@ struct BorderJob {
 };
 
 __global__ void __launch_bounds__(256) lazy_border_dots_kernel(const __grid_constant__ Pack<BorderJob> P) {
+  pdl_enter();
   const BorderJob& jb = P.j[blockIdx.y];
   const int j = blockIdx.x;
   if (j >= jb.d0 + jb.r) return;
@@ -554,6 +556,7 @@ __global__ void __launch_bounds__(256) lazy_border_dots_kernel(const __grid_cons
 constexpr size_t kBorderSmem = (size_t)(kLazyMax * kLazyMax + 3 * kLazyMax * kBorderMax + kBorderMax * kBorderMax) * 16;
 
 __global__ void __launch_bounds__(256) lazy_border_inv_kernel(const __grid_constant__ Pack<BorderJob> P, double mu) {
+  pdl_enter();
   const BorderJob& jb = P.j[blockIdx.x];
   extern __shared__ __align__(16) double2 bsm[];
   double2* S = bsm;                                   // Sinv_old  d0 x d0 (ld kLazyMax)
@@ -659,6 +662,7 @@ constexpr size_t kHermTmaSmem = (size_t)kHermStages * kHermTileBytes + 2 * 8 * k
 __global__ void __launch_bounds__(288, 1) herm_gapply_tma_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                 const uint64_t* __restrict__ items, int n_items,
                                                                 const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;
   extern __shared__ __align__(128) uint8_t hsm[];
   double2* ring = reinterpret_cast<double2*>(hsm);
@@ -792,6 +796,7 @@ __global__ void __launch_bounds__(288, 1) herm_gapply_tma_kernel(const __grid_co
 // One 32 x 32 tile pair (I > J) or diagonal tile per CTA, staged through
 // shared memory so both halves are read and written coalesced.
 __global__ void __launch_bounds__(256) herm_symmetrize_kernel(double2* __restrict__ G, int64_t ld, int n) {
+  pdl_enter();
   __shared__ double2 a[32][33], b[32][33];
   int t = blockIdx.x, I = 0;
   while (t > I) { t -= I + 1; ++I; }
@@ -838,6 +843,7 @@ struct XFinJob {
 
 __global__ void __launch_bounds__(256) xdual_finish_kernel(const __grid_constant__ Pack<XFinJob> P, double mu,
                                                           double beta, const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;
   const XFinJob& jb = P.j[blockIdx.y];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(256) xdual_finish_kernel(const __grid_constant
 // back_projection (forward_model.hpp:203-220): |sum_q A_q^H y_q| for every
 // pixel, summing the per-sensor adjoint images in global sensor order.
 __global__ void bp_sum_kernel(const double2* const* __restrict__ imgs, int Q, int N, double* __restrict__ out) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   double2 acc = make_double2(0.0, 0.0);
@@ -897,6 +904,7 @@ constexpr size_t kFbSmem = (size_t)2 * 2 * kFbBK * (kFbPA + kFbPB) * sizeof(doub
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) frame_batch_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
                                                             double mu, double beta) {
+  pdl_enter();
   constexpr int BK = kFbBK, LA = kFbBM * BK / 256;
   const FrameBatchJob& jb = jobs[blockIdx.z];
   const int m0 = blockIdx.x * kFbBM;
@@ -1038,6 +1046,7 @@ constexpr size_t kFb2Smem = kFbStages * (kFbStageA + kFbStageB) + kFB * 8;
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) frame_batch2_kernel(const FrameBatchJob* __restrict__ jobs, int nsplit,
                                                              double mu, double beta) {
+  pdl_enter();
   constexpr int BK = kFbBK, S = kFbStages;
   const FrameBatchJob& jb = jobs[blockIdx.z];
   const int m0 = blockIdx.x * kFbBM;
@@ -1302,11 +1311,13 @@ __device__ __forceinline__ void gram_dmma_body(const GramJob& jb, double mu, dou
 }
 
 __global__ void __launch_bounds__(256, 1) gram_dmma_kernel(const GramJob* __restrict__ jobs, double mu, double beta) {
+  pdl_enter();
   gram_dmma_body(jobs[blockIdx.z], mu, beta);
 }
 
 // one job passed by value (no job-table upload on the issuing stream)
 __global__ void __launch_bounds__(256, 1) gram_dmma1_kernel(const __grid_constant__ GramJob job, double mu, double beta) {
+  pdl_enter();
   gram_dmma_body(job, mu, beta);
 }
 
@@ -1314,6 +1325,7 @@ __global__ void __launch_bounds__(256, 1) gram_dmma1_kernel(const __grid_constan
 // gram_dmma_kernel applying mu, beta itself (mu * c, then + beta on the
 // diagonal, imaginary diagonal exactly 0).
 __global__ void gram_scale_kernel(double2* __restrict__ C, int64_t ldc, int n, double mu, double beta) {
+  pdl_enter();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * n) return;
   const int i = (int)(e % n), j = (int)(e / n);
@@ -1336,6 +1348,7 @@ struct FrameReduceJob {
 };
 
 __global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
+  pdl_enter();
   const FrameReduceJob& jb = jobs[blockIdx.z];
   const int i = blockIdx.x * blockDim.x + threadIdx.x, f = blockIdx.y;
   if (i >= jb.m || f >= jb.nf) return;
@@ -1360,6 +1373,7 @@ struct FrameRhsJob {
 };
 
 __global__ void frame_rhs_kernel(const FrameRhsJob* __restrict__ jobs, double beta) {
+  pdl_enter();
   const FrameRhsJob& jb = jobs[blockIdx.y];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= jb.n) return;

@@ -62,6 +62,7 @@ constexpr int kGjSmem = (64 * 65 + 128) * 16;
 template <int EPI>
 __global__ void __launch_bounds__(256) gemm_kernel(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
                                                    double2* __restrict__ ws, int64_t ws_stride) {
+  pdl_enter();
   const int split = blockIdx.z % nsplit;
   const GemmJob& jb = jobs.j[blockIdx.z / nsplit];
   const int m0 = blockIdx.y * kGB, n0 = blockIdx.x * kGB;
@@ -194,6 +195,7 @@ constexpr size_t kGemmBigSmem = (size_t)2 * kGK * ((kBigBM + 1) + (kBigBN + 1)) 
 
 template <int EPI>
 __global__ void __launch_bounds__(256, 1) gemm_big_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  pdl_enter();
   constexpr int TM = kBigTM, TN = kBigTN, BM = kBigBM, BN = kBigBN;
   constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;  // prefetched elements per thread
   const GemmJob& jb = jobs.j[blockIdx.z];
@@ -330,6 +332,7 @@ constexpr size_t kGemmDmmaSmem = (size_t)2 * 2 * kGK * (kDmPA + kDmPB) * sizeof(
 
 template <int EPI>
 __global__ void __launch_bounds__(256, 1) gemm_dmma_kernel(const __grid_constant__ Pack<GemmJob> jobs) {
+  pdl_enter();
   constexpr int BM = kDmBM, BN = kDmBN, PA = kDmPA, PB = kDmPB;
   constexpr int LA = BM * kGK / 256, LB = BN * kGK / 256;
   const GemmJob& jb = jobs.j[blockIdx.z];
@@ -508,6 +511,7 @@ struct GjUpdJob {
 };
 
 __global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant__ Pack<GjUpdJob> P) {
+  pdl_enter();
   const GjUpdJob& jb = P.j[blockIdx.z];
   const int m0 = blockIdx.y * kGjuBM, n0 = blockIdx.x * kGjuBN, n = jb.n, kb = jb.kb;
   if (m0 >= n || n0 >= n) return;
@@ -598,6 +602,7 @@ __global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant
 // C = alpha * sum_s ws[job*nsplit + s] + beta0 * C (+ diag), fixed split order.
 __global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, int nsplit,
                                   const double2* __restrict__ ws, int64_t ws_stride) {
+  pdl_enter();
   const GemmJob& jb = jobs.j[blockIdx.y];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)jb.m * jb.n) return;
@@ -638,6 +643,7 @@ struct DiagJob {
 };
 
 __global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  pdl_enter();
   const DiagJob& jb = jobs.j[blockIdx.x];
   if (jb.k0 >= jb.n) return;
   extern __shared__ double2 gj_smem[];
@@ -683,6 +689,7 @@ __global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ P
 
 // F = M[:, K] (pivot column panel), grid-stride over n*kb per job.
 __global__ void gj_panel_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  pdl_enter();
   const DiagJob& jb = jobs.j[blockIdx.y];
   if (jb.k0 >= jb.n) return;
   const int64_t total = (int64_t)jb.n * jb.kb;
@@ -694,6 +701,7 @@ __global__ void gj_panel_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
 
 // R'[:, K] = P (overwrite the pivot columns of the row panel).
 __global__ void gj_fix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  pdl_enter();
   const DiagJob& jb = jobs.j[blockIdx.x];
   if (jb.k0 >= jb.n) return;
   for (int e = threadIdx.x; e < jb.kb * jb.kb; e += blockDim.x) {
@@ -714,6 +722,7 @@ struct SubJob {
 };
 
 __global__ void gather_sub_kernel(const __grid_constant__ Pack<SubJob> jobs) {
+  pdl_enter();
   const SubJob& jb = jobs.j[blockIdx.y];
   const int64_t total = (int64_t)jb.m * jb.n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -725,6 +734,7 @@ __global__ void gather_sub_kernel(const __grid_constant__ Pack<SubJob> jobs) {
 // Utility kernels -----------------------------------------------------------
 __global__ void c128_to_c64_kernel(const double2* __restrict__ src, int64_t lds, float2* __restrict__ dst,
                                    int64_t ldd, int rows, int cols) {
+  pdl_enter();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)rows * cols) return;
   const int r = (int)(e % rows);
@@ -734,11 +744,13 @@ __global__ void c128_to_c64_kernel(const double2* __restrict__ src, int64_t lds,
 }
 
 __global__ void soft_threshold_kernel(const double2* __restrict__ v, int64_t n, double kappa, double2* __restrict__ out) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = soft_threshold1(v[i], kappa);
 }
 
 __global__ void abs_kernel(const double2* __restrict__ v, int n, double* __restrict__ out) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = c_abs(v[i]);
 }
@@ -748,6 +760,7 @@ __global__ void abs_kernel(const double2* __restrict__ v, int n, double* __restr
 // local_updates in radmm_b200.cu).
 __global__ void scaled_diff_kernel(double2* __restrict__ out, const double2* __restrict__ a,
                                    const double2* __restrict__ b, double beta, int64_t n) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = make_double2(beta * (a[i].x - b[i].x), beta * (a[i].y - b[i].y));
 }
@@ -755,6 +768,7 @@ __global__ void scaled_diff_kernel(double2* __restrict__ out, const double2* __r
 // Rb[:, t] = A[:, rem_pix[t]] promoted to complex128 (zero-padded to ld).
 __global__ void gather_cols_c128_kernel(const float2* __restrict__ A, int64_t ld, const int* __restrict__ pix,
                                         int r, double2* __restrict__ out) {
+  pdl_enter();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ld * r) return;
   const int t = (int)(e / ld);
@@ -783,6 +797,7 @@ struct EventJob {
 };
 
 __global__ void event_prep_kernel(const __grid_constant__ Pack<EventJob> P) {
+  pdl_enter();
   const EventJob& jb = P.j[blockIdx.y];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -804,12 +819,14 @@ __global__ void event_prep_kernel(const __grid_constant__ Pack<EventJob> P) {
 }
 
 __global__ void iota_kernel(int* __restrict__ J, int n) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) J[i] = i;
 }
 
 // Gather x_full[J] -> x_hat (and zero a vector) etc.
 __global__ void gather_kernel(const double2* __restrict__ src, const int* __restrict__ idx, int n, double2* __restrict__ dst) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src[idx[i]];
 }
@@ -820,6 +837,7 @@ __global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K,
                                const double* __restrict__ pix, const double* __restrict__ tx,
                                const double* __restrict__ rx, const double* __restrict__ phi,
                                double alpha, double fc, double t_step, double c_light, double two_pi) {
+  pdl_enter();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int rows = M * K;
   if (e >= (int64_t)rows * N) return;

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kSweepThreads) fused_sweep_kernel(const __grid
                                                                     const __grid_constant__ FusionArgs fa, double mu,
                                                                     double beta, int n_clusters, int range, int tile,
                                                                     int prefetch) {
+  pdl_enter();
   extern __shared__ double2 sweep_smem[];
   __shared__ int s_lo, s_hi, s_hi2;
   const int q = (int)cluster_ctarank();
@@ -258,6 +259,7 @@ template <int RPT>  // float4 row chunks per axpy thread: ld <= RPT * 256
 __global__ void __launch_bounds__(kS2Threads, 1) fused_sweep2_kernel(const __grid_constant__ Pack<SweepJob> jobs,
                                                                      const __grid_constant__ FusionArgs fa, double mu,
                                                                      double beta, int range, int tile) {
+  pdl_enter();
   extern __shared__ double2 s2_smem[];
   __shared__ uint64_t bar_dots[kS2Depth], bar_xhat[kS2Depth], bar_fused[kS2Depth], bar_free[kS2Depth];
   __shared__ double2 s_coef[64];
@@ -475,6 +477,7 @@ struct __align__(16) S3Tile {  // one tile, staged by the producer warp (per buf
 __global__ void __launch_bounds__(kS3Threads, 1) fused_sweep3_kernel(const __grid_constant__ Pack<Sweep3Job> jobs,
                                                                      const __grid_constant__ FusionArgs fa, double mu,
                                                                      double beta, int64_t ld, int range) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char s3_raw[];
   __shared__ __align__(8) uint64_t full_bar[2];
   __shared__ S3Tile tiles[2];
@@ -741,6 +744,7 @@ __global__ void __launch_bounds__(kS4Threads, 1) fused_sweep4_kernel(const __gri
                                                                      const __grid_constant__ FusionArgs fa,
                                                                      const __grid_constant__ Sweep4Ctl ctl,
                                                                      double mu, double beta, int64_t ld) {
+  pdl_enter();
   if (fa.go && __ldg(fa.go) == 0) return;  // cancelled speculative iteration
   extern __shared__ __align__(128) uint8_t s4[];
   const int q = blockIdx.y, chunk = blockIdx.x;
@@ -958,6 +962,7 @@ __global__ void __launch_bounds__(kS5Threads, 1) fused_sweep5_kernel(const __gri
                                                                      const __grid_constant__ FusionArgs fa,
                                                                      const __grid_constant__ Sweep4Ctl ctl,
                                                                      double mu, double beta, int64_t ld) {
+  pdl_enter();
   if (fa.go && __ldg(fa.go) == 0) return;
   extern __shared__ __align__(128) uint8_t s5[];
   const int q = blockIdx.y, chunk = blockIdx.x;

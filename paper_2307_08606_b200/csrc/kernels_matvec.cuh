@@ -223,6 +223,7 @@ __device__ __forceinline__ void coldot_epilogue(const ColDotJob& jb, int i, doub
 template <typename T, int EPI, bool SMEM_VEC, int CPW, int THREADS>
 __global__ void __launch_bounds__(THREADS) coldot_kernel(const __grid_constant__ Pack<ColDotJob> jobs, double mu, double beta,
                                                          const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   extern __shared__ double2 sv[];
   constexpr int kWarps = THREADS / 32;
@@ -552,6 +553,7 @@ struct RhsJob {
 
 __global__ void rhs_kernel(const __grid_constant__ Pack<RhsJob> jobs, const double2* __restrict__ gap,
                            const double2* __restrict__ sigma, double beta, const int* __restrict__ go) {
+  pdl_enter();
   if (go && __ldg(go) == 0) return;  // cancelled speculative iteration
   const RhsJob& jb = jobs.j[blockIdx.y];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -738,6 +740,7 @@ __global__ void __launch_bounds__(kFusionThreads) fusion_kernel(FusionArgs a) {
 // One fusion round per frame of a multi-frame batch (blockIdx.y = frame);
 // each frame reduces over its own row of blocks with its own counter.
 __global__ void __launch_bounds__(kFusionThreads) fusion_frames_kernel(const __grid_constant__ Pack<FusionArgs> P) {
+  pdl_enter();
   const FusionArgs& a = P.j[blockIdx.y];
   if (a.go && __ldg(a.go) == 0) return;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -782,6 +785,7 @@ __device__ __forceinline__ bool screen_off(const int* go, const int* sgo) {
 
 __global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int W, double tol,
                                                                 const int* __restrict__ go, const int* __restrict__ sgo) {
+  pdl_enter();
   if (screen_off(go, sgo)) return;
   const ScreenJob& jb = jobs.j[blockIdx.y];
   __shared__ int wc[kScanBlock / 32];
@@ -816,6 +820,7 @@ __global__ void __launch_bounds__(kScanBlock) screen_flags_kernel(const __grid_c
 __global__ void __launch_bounds__(256) screen_scan_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int nq,
                                                           const int* __restrict__ go, const int* __restrict__ sgo,
                                                           int* totals_host, int* go_next) {
+  pdl_enter();
   if (screen_off(go, sgo)) return;
   __shared__ int changed;
   if (threadIdx.x == 0) changed = 0;
@@ -843,6 +848,7 @@ __global__ void __launch_bounds__(256) screen_scan_kernel(const __grid_constant_
 
 __global__ void __launch_bounds__(kScanBlock) screen_scatter_kernel(const __grid_constant__ Pack<ScreenJob> jobs,
                                                                   const int* __restrict__ go, const int* __restrict__ sgo) {
+  pdl_enter();
   if (screen_off(go, sgo)) return;
   const ScreenJob& jb = jobs.j[blockIdx.y];
   __shared__ int woff[kScanBlock / 32];
@@ -899,6 +905,7 @@ __global__ void __cluster_dims__(kScreenCluster, 1, 1) __launch_bounds__(kScanBl
     screen_fused_kernel(const __grid_constant__ Pack<ScreenJob> jobs, int nq, int W, double tol,
                         const int* __restrict__ go, const int* __restrict__ sgo, int* totals_host, int* go_next,
                         unsigned* sync /* [0] arrival ticket, [1] changed; zero between launches */) {
+  pdl_enter();
   if (screen_off(go, sgo)) return;
   const ScreenJob& jb = jobs.j[blockIdx.y];
   const unsigned rank = cluster_ctarank();

@@ -18,6 +18,13 @@
 
 namespace radmm_oz {
 
+// Programmatic dependent launch (see radmm_dev::pdl_enter in kernels_async.cuh):
+// wait for the predecessor grid, then let the successor launch.
+__device__ __forceinline__ void oz_pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int kOzBM = 128, kOzBN = 128, kOzBK = 128, kOzStages = 4;
 constexpr int kOzStageBytes = (kOzBM + kOzBN) * kOzBK;  // 32 KB
 constexpr size_t kOzSmem = (size_t)kOzStages * kOzStageBytes + 1024 + 256;
@@ -218,6 +225,7 @@ __host__ __device__ inline void oz_pair(int p, int& s1, int& s2) {
 // for non-negative floats, so atomicMax on the bits is exact)
 __global__ void oz_rowmax_kernel(const float2* __restrict__ A, int64_t ld, int rows, const int* __restrict__ J, int n,
                                  unsigned* __restrict__ rowmax) {
+  oz_pdl_enter();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int per = (n + gridDim.y - 1) / gridDim.y;
@@ -236,6 +244,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict_
                                                       const int* __restrict__ J, int n, int npad,
                                                       const unsigned* __restrict__ rowmax, int8_t* __restrict__ P,
                                                       int8_t* __restrict__ Q, int64_t slice_stride) {
+  oz_pdl_enter();
   __shared__ int8_t sre[kOzSlices][64][33], sim[kOzSlices][64][33];
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 32;
   const int tr = threadIdx.x & 63, tq = threadIdx.x >> 6;  // row in tile, column phase
@@ -286,6 +295,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict_
 __global__ void __launch_bounds__(128, 1) oz_gram_pairs_kernel(const int8_t* __restrict__ P,
                                                               const int8_t* __restrict__ Q, int64_t slice_stride,
                                                               int rows, int kdim, int32_t* __restrict__ R) {
+  oz_pdl_enter();
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   int tile = blockIdx.x, I = 0;
   while (tile > I) {
@@ -339,6 +349,7 @@ __device__ __forceinline__ void oz_tma_2d(uint32_t dst, const CUtensorMap* map, 
 __global__ void __launch_bounds__(128, 1) oz_gram_pairs_tma_kernel(const __grid_constant__ CUtensorMap tP,
                                                                   const __grid_constant__ CUtensorMap tQ,
                                                                   int rows_pad, int kdim, int32_t* __restrict__ R) {
+  oz_pdl_enter();
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)kOzTStages * kOzTStageBytes);
@@ -445,6 +456,7 @@ __global__ void __launch_bounds__(128, 1) oz_gram_pairs_tma_kernel(const __grid_
 // (+ beta on the diagonal, exact real), mirrored conjugate to C[j, i].
 __global__ void oz_combine_kernel(const int32_t* __restrict__ R, const unsigned* __restrict__ rowmax, int rows,
                                   double2* __restrict__ C, int64_t ldc, double mu, double beta) {
+  oz_pdl_enter();
   const int tile = blockIdx.y;
   int t = tile, I = 0;
   while (t > I) {

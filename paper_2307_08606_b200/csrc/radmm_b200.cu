@@ -341,7 +341,7 @@ struct radmm_ctx {
   DArr<int> go_flags;                // speculation guards, alternating per round
   DArr<unsigned> lazy_cnt;           // lazy_dot_kernel arrival counters (one per job)
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
-  bool pdl = true;                   // programmatic dependent launch of the iteration kernels (RADMM_PDL)
+  bool pdl = false;                  // programmatic dependent launch: on inside the iteration loop (RADMM_PDL)
   DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
@@ -534,7 +534,6 @@ void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
   std::memset(c->fs_host, 0, 2 * sizeof(FusionScalars));
   c->go_flags.alloc(2);
   c->sgo_flags.alloc(2);
-  c->pdl = env_int("RADMM_PDL", 1) != 0;
   c->screen_sync.alloc(2);
   CK(cudaHostGetDevicePointer((void**)&c->fs_host_dev, c->fs_host, 0));
   c->h_totals = reinterpret_cast<int*>(c->pinned_block + off_tot);
@@ -628,18 +627,21 @@ int occupancy(const void* func, int threads, size_t smem) {
   return v;
 }
 
-#define LAUNCH(c, kern, grid, block, smem, ...)                              \
+#define LAUNCH_PLAIN(c, kern, grid, block, smem, ...)                        \
   do {                                                                        \
     kern<<<(grid), (block), (smem), (c)->stream>>>(__VA_ARGS__);              \
     CK(cudaGetLastError());                                                   \
     ++(c)->launches;                                                          \
   } while (0)
 
-// Iteration kernels that open with pdl_wait() (kernels_async.cuh) are
-// launched with programmatic stream serialisation: their CTAs are scheduled
-// while the predecessor drains, hiding the launch gap between the forward,
-// G-apply, reduce, adjoint and fusion kernels.  RADMM_PDL=0 turns it off.
-#define LAUNCH_PDL(c, kern, grid, block, smem, ...)                                   \
+// Every kernel opens with pdl_enter() (griddepcontrol.wait, then
+// launch_dependents; kernels_async.cuh), so inside the iteration loop
+// (c->pdl, see do_run) context-stream launches use programmatic stream
+// serialisation: a kernel's CTAs are scheduled while its predecessor drains,
+// hiding the launch gaps between the forward, G-apply, reduce, adjoint,
+// fusion, screening, lazy-correction and event kernels.  RADMM_PDL=0 turns it
+// off; outside the loop the wait is a no-op.
+#define LAUNCH(c, kern, grid, block, smem, ...)                                       \
   do {                                                                                \
     if ((c)->pdl) {                                                                   \
       cudaLaunchConfig_t cfg_{};                                                      \
@@ -655,7 +657,7 @@ int occupancy(const void* func, int threads, size_t smem) {
       CK(cudaLaunchKernelEx(&cfg_, kern, __VA_ARGS__));                               \
       ++(c)->launches;                                                                \
     } else {                                                                          \
-      LAUNCH(c, kern, grid, block, smem, __VA_ARGS__);                                \
+      LAUNCH_PLAIN(c, kern, grid, block, smem, __VA_ARGS__);                          \
     }                                                                                 \
   } while (0)
 
@@ -703,7 +705,7 @@ void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int 
   per_sm = occupancy((const void*)kern, 256, smem);
   const int slots = c->sm_count * std::max(1, per_sm);
   const int gmax = std::max(1, (n_max + 8 * cpw - 1) / (8 * cpw));
-  LAUNCH_PDL(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
+  LAUNCH(c, kern, dim3(wave_grid(slots, (int)nb, gmax), (unsigned)nb), 256, smem, pk, mu, beta, go);
 }
 
 int coldot_cpw() {
@@ -815,11 +817,11 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     int per_sm = 1;
     per_sm = occupancy((const void*)kern, 256, smem);
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
-    LAUNCH_PDL(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
+    LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
   } else {
     LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
-  LAUNCH_PDL(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
+  LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
          pk, go);
 }
 
@@ -882,10 +884,10 @@ void forward(radmm_ctx* c, const std::vector<FwdJob>& jobs, const std::vector<Re
       auto kern = threads == 1024 ? fwd_kernel<MODE, 1024> : threads == 512 ? fwd_kernel<MODE, 512> : fwd_kernel<MODE, 256>;
       if (smem > 48 * 1024) set_smem_attr((const void*)kern, (int)(227 * 1024));
       dim3 grid((unsigned)((ld_max + 2 * threads - 1) / (2 * threads)), max_chunks, (unsigned)nb);
-      LAUNCH_PDL(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
+      LAUNCH(c, kern, grid, threads, smem, pk, c->gap.p, c->sigma.p, beta, go);
     }
     dim3 rg((unsigned)((ld_max + 255) / 256), (unsigned)nb);
-    LAUNCH_PDL(c, reduce_parts_kernel, rg, 256, 0, rp, go);
+    LAUNCH(c, reduce_parts_kernel, rg, 256, 0, rp, go);
   }
 }
 
@@ -1457,8 +1459,8 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
   if (!nb) return;
   if (c->lazy_cnt.n < (size_t)kMaxBatch) c->lazy_cnt.alloc(kMaxBatch);  // zeroed; the last blocks re-zero
   for (int i = 0; i < nb; ++i) pk.j[i].cnt = c->lazy_cnt.p + i;
-  LAUNCH_PDL(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
-  LAUNCH_PDL(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
+  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
+  LAUNCH(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
 }
 
 void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu);
@@ -1892,7 +1894,7 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go =
   a.screen_next_possible = screen_next_possible;
   a.screen_go = screen_go;
   PhaseScope ps(c, RADMM_PHASE_FUSION, 16.0 * c->N * (c->Q_total + 7));
-  LAUNCH_PDL(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
+  LAUNCH(c, fusion_kernel, dim3((c->N + kFusionThreads - 1) / kFusionThreads), kFusionThreads, 0, a);
 }
 
 bool fused_enabled();
@@ -2559,6 +2561,13 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   int host_n = 0;
   int64_t l_k = 0;           // launch counter when iteration k was enqueued
   uint64_t notice_k = 0;
+  // PDL inside the iteration loop only (iterations, screening, events): the
+  // setup kernels (Gram, Gauss-Jordan, Ozaki) measured ~2 ms slower with it
+  struct PdlScope {
+    radmm_ctx* c;
+    explicit PdlScope(radmm_ctx* cc) : c(cc) { c->pdl = env_int("RADMM_PDL", 1) != 0; }
+    ~PdlScope() { c->pdl = false; }
+  } pdl_scope(c);
   for (int k = 1; k <= h->max_iter; ++k) {
     if (!k_launched) {
       const auto tt0 = std::chrono::steady_clock::now();
