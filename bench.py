@@ -278,6 +278,8 @@ def ours(args, cfg):
     import __graft_entry__
     __graft_entry__.build()
     rank, world, local = D.env_rank_world()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     dist = None
     if world > 1:
         import torch.distributed as tdist
@@ -638,8 +640,31 @@ def frames(args):
           flush=True)
 
 
+def spawn_ranks(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch this
+    command as N ranks (one process per GPU) through torch.distributed.run on
+    127.0.0.1; rank 0 prints the line.  Returns True when it did (the caller
+    exits with the launcher's status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init lines (nranks) visible in the log
+    rc = subprocess.call(cmd, env=env)
+    if rc != 0:
+        sys.exit(rc)
+    return True
+
+
 def main():
     args = parse()
+    if spawn_ranks(args):
+        return
     from paper_2307_08606_b200 import scenario
     if args.stress:
         stress(args)

@@ -88,6 +88,12 @@ typedef struct {
   int32_t fixed_iterations;   /* build-only: never stop on convergence */
   radmm_observer_fn observer; /* slow path: D2H of x_G, s, sigma per iteration */
   void* observer_user;
+  /* build-only precision switch: 0 (default) = every dual (Woodbury) solve
+   * takes one step of KM-space iterative refinement with the exact
+   * capacitance, which makes it backward stable like the reference's
+   * Cholesky (solver_core.hpp:41-51); 1 = the bare explicit-inverse apply
+   * (faster, ~eps cond(C)^2 forward error -- DESIGN.md section 3). */
+  int32_t skip_refinement;
 } radmm_run_options;
 
 /* RunResult scalars, admm.hpp:324-335 + ConvergenceReport totals :297-300. */
@@ -102,6 +108,7 @@ typedef struct {
   int64_t kernel_launches;   /* library kernels launched by the last run */
   int64_t rebuilds;          /* full refactorizations */
   int64_t downdates;         /* low-rank active-set downdates */
+  int64_t refine_skipped;    /* dual sensors solved without refinement (packed C did not fit) */
 } radmm_run_summary;
 
 typedef enum {
@@ -145,9 +152,11 @@ int radmm_set_operator_c128(radmm_ctx* ctx, int q, int rows, const double* a, in
 /* Measurement y_q (Problem::measurements), complex128, length rows. */
 int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind);
 /* Device generator for the BASELINE dechirped-LFM operator of one sensor:
- * A[m*K+k, n] = exp(j 2 pi (alpha tau t_k + fc tau)) exp(j phi_n),
- * tau = (|tx - p_n| + |rx_m - p_n|)/c, t_k = k*T/K.  pix: N x 3, rx: M x 3,
- * tx: 3, phi: N (host arrays). */
+ * A[m*K+k, n] = exp(j 2 pi (alpha tau t_k + fc tau + phi_n)),
+ * tau = (|tx - p_n| + |rx_m - p_n|)/c, t_k = k*T/K; phi_n in TURNS (cycles,
+ * [0,1)).  pix: N x 3, rx: M x 3, tx: 3, phi: N (host arrays).  IEEE basic
+ * operations only (portable sincos), bitwise equal to the host generator
+ * scenario.baseline_operator on any machine. */
 int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const double* pix,
                                     const double* tx, const double* rx, const double* phi,
                                     double fc, double bw, double pulse);

@@ -115,6 +115,9 @@ class LocalSolve:
             form = "primal" if nq <= rows else "dual"
         self.form, self.size, self.mu, self.beta = form, nq, mu, beta
         self.a_hat = a_hat
+        # A_hat^H kept contiguous once (speed only: NumPy would otherwise
+        # materialise the conjugate transpose on every solve)
+        self.a_hat_h = np.ascontiguousarray(a_hat.conj().T) if form == "dual" else None
         if form == "primal":
             gram = mu * (a_hat.conj().T @ a_hat)       # solver_core.hpp:39
             gram[np.diag_indices(nq)] += beta           # :40
@@ -131,7 +134,7 @@ class LocalSolve:
             return sla.cho_solve(self.fac, rhs, check_finite=False)
         v = self.a_hat @ rhs
         w = sla.cho_solve(self.fac, v, check_finite=False)
-        return cdiv(rhs - self.mu * (self.a_hat.conj().T @ w), self.beta)
+        return cdiv(rhs - self.mu * (self.a_hat_h @ w), self.beta)
 
 
 class SensorRef:
@@ -198,7 +201,7 @@ class SensorRef:
     def rebuild(self) -> None:
         """admm.hpp:171-179."""
         j = self.active
-        a_hat = self.a[:, j]
+        a_hat = self.a if j.size == self.n else self.a[:, j]   # (no copy while every pixel is active)
         frozen = self.x_full.copy()
         frozen[j] = 0.0
         y_eff = self.y - self.a @ frozen

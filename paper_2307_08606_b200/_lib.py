@@ -69,14 +69,14 @@ OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(View))
 
 class Options(C.Structure):
     _fields_ = [("mode", C.c_int), ("disable_screening", C.c_int32), ("fixed_iterations", C.c_int32),
-                ("observer", OBSERVER), ("observer_user", C.c_void_p)]
+                ("observer", OBSERVER), ("observer_user", C.c_void_p), ("skip_refinement", C.c_int32)]
 
 
 class Summary(C.Structure):
     _fields_ = [("converged", C.c_int32), ("screening_stalled", C.c_int32), ("iterations", C.c_int32),
                 ("total_active_solves", C.c_uint64), ("total_bytes", C.c_uint64),
                 ("setup_ms", C.c_double), ("solve_ms", C.c_double), ("kernel_launches", C.c_int64),
-                ("rebuilds", C.c_int64), ("downdates", C.c_int64)]
+                ("rebuilds", C.c_int64), ("downdates", C.c_int64), ("refine_skipped", C.c_int64)]
 
 
 class PhaseStat(C.Structure):

@@ -187,6 +187,7 @@ class RunResult:
     downdates: int = 0
     active_sets: list = field(default_factory=list)
     removal_log: np.ndarray = None
+    refine_skipped: int = 0   # dual sensors solved without KM-space refinement (memory)
 
 
 @dataclass
@@ -335,7 +336,7 @@ class Solver:
         return v
 
     def run_frames(self, hypers, mode: Mode = Mode.ASADMM, disable_screening: bool = False,
-                   fixed_iterations: bool = False, fetch: bool = True) -> list:
+                   fixed_iterations: bool = False, fetch: bool = True, skip_refinement: bool = False) -> list:
         """Solve frames 0..F-1 (F = len(hypers)) in lockstep on the resident
         operators; frame f behaves exactly like run(problem_f, hypers[f])
         (admm.hpp:357-445).  Returns one RunResult per frame."""
@@ -344,7 +345,7 @@ class Solver:
         arr = (_lib.Hyper * F)(*[h._c() for h in hypers])
         summ = (_lib.Summary * F)()
         opts = _lib.Options(int(mode), int(bool(disable_screening)), int(bool(fixed_iterations)),
-                            _lib.OBSERVER(), None)
+                            _lib.OBSERVER(), None, int(bool(skip_refinement)))
         _lib.check(_lib.lib().radmm_run_frames(self._h, F, arr, C.byref(opts), summ))
         out = []
         for f in range(F):
@@ -352,7 +353,7 @@ class Solver:
             res = RunResult(converged=bool(sm.converged), screening_stalled=bool(sm.screening_stalled),
                             iterations=int(sm.iterations), setup_ms=sm.setup_ms, solve_ms=sm.solve_ms,
                             kernel_launches=int(sm.kernel_launches), rebuilds=int(sm.rebuilds),
-                            downdates=int(sm.downdates))
+                            downdates=int(sm.downdates), refine_skipped=int(sm.refine_skipped))
             res.report.total_active_solves = int(sm.total_active_solves)
             res.report.total_bytes = int(sm.total_bytes)
             if fetch:
@@ -386,7 +387,7 @@ class Solver:
     # ---- run -----------------------------------------------------------
     def run(self, hyper: Hyperparams, mode: Mode = Mode.ASADMM, observer=None,
             disable_screening: bool = False, fixed_iterations: bool = False,
-            fetch: bool = True) -> RunResult:
+            fetch: bool = True, skip_refinement: bool = False) -> RunResult:
         L = _lib.lib()
         hc = hyper._c()
         cb = OBSERVER_NONE = _lib.OBSERVER()
@@ -402,14 +403,15 @@ class Solver:
 
             cb = _lib.OBSERVER(_obs)
             del Qt
-        opts = _lib.Options(int(mode), int(bool(disable_screening)), int(bool(fixed_iterations)), cb, None)
+        opts = _lib.Options(int(mode), int(bool(disable_screening)), int(bool(fixed_iterations)), cb, None,
+                            int(bool(skip_refinement)))
         summ = _lib.Summary()
         _lib.check(L.radmm_run(self._h, C.byref(hc), C.byref(opts), C.byref(summ)))
         del OBSERVER_NONE
         res = RunResult(converged=bool(summ.converged), screening_stalled=bool(summ.screening_stalled),
                         iterations=int(summ.iterations), setup_ms=summ.setup_ms, solve_ms=summ.solve_ms,
                         kernel_launches=int(summ.kernel_launches), rebuilds=int(summ.rebuilds),
-                        downdates=int(summ.downdates))
+                        downdates=int(summ.downdates), refine_skipped=int(summ.refine_skipped))
         res.report.total_active_solves = int(summ.total_active_solves)
         res.report.total_bytes = int(summ.total_bytes)
         if fetch:

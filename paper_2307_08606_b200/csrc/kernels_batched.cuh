@@ -35,7 +35,18 @@ struct HermJob {
   double2* dotp;     // [NR][nb][groups][64], column stride dstride
   double2* axp;      // [NR][nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J, column stride astride
   int64_t dstride, astride;
+  int packed;          // G is a packed lower-tile array (cap_pack_kernel), not column-major ld
+  const double2* base; // right-hand side 0 output: w = base + sgn * (G v) (nullptr: w = G v)
+  double sgn;
 };
+
+// Packed lower-tile storage of a Hermitian matrix (the dual capacitance C,
+// kept next to its explicit inverse for the KM-space refinement): tile (I, J),
+// I >= J, at tile slot I (I + 1) / 2 + J, 64 x 64 column-major (ld 64),
+// zero-padded past n.  Only the lower triangle is stored.
+__host__ __device__ inline int64_t herm_packed_tile(int I, int J) {
+  return ((int64_t)I * (I + 1) / 2 + J) * (int64_t)(kHermTile * kHermTile);
+}
 
 // item word: q (16) | J (16) | I0 (16) | nt (16)
 __host__ __device__ inline uint64_t herm_item(int q, int J, int I0, int nt) {
@@ -210,8 +221,16 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   auto load_tile = [&](uint64_t it, int I) {
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF);
     const HermJob& jb = P.j[q];
-    const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
     const int ib = I * kHermTile;
+    if (jb.packed) {  // tile-contiguous: 64 KB per tile, zero-padded
+      const double2* Gt = jb.G + herm_packed_tile(I, J) + (int64_t)c0 * kHermTile;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) g[k][h] = __ldg(Gt + k * kHermTile + lane + 32 * h);
+      return;
+    }
+    const double2* Gc = jb.G + (int64_t)(J * kHermTile + c0) * jb.ld;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -356,7 +375,13 @@ __global__ void __launch_bounds__(kHermRedSlices * kHermTile) herm_reduce_kernel
       t.x += part[u][r].x;
       t.y += part[u][r].y;
     }
-    if (row < jb.n) out[row] = t;
+    if (row < jb.n) {
+      if (c == 0 && jb.base) {  // refinement: residual v - C w, or correction w + G rho
+        const double2 b = jb.base[row];
+        t = make_double2(b.x + jb.sgn * t.x, b.y + jb.sgn * t.y);
+      }
+      out[row] = t;
+    }
   }
 }
 
@@ -385,6 +410,8 @@ struct LazyJob {
   double2* w;           // in: u = G v; out: C_D^{-1} v
   double2* t;           // d (scratch): t = A_D^H u, then s = mu Sinv t in t + kLazyMax
   unsigned* cnt;        // arrival counter of the job's dot blocks (zero between launches)
+  int ident;            // refinement residual: s = mu t (no Sinv), then dst += A_D s
+  double2* dst;         //   (lazy_resid_axpy_kernel; w is only read)
 };
 
 // s = mu Sinv t for one job by one block: four threads per row of Sinv,
@@ -451,7 +478,11 @@ __global__ void __launch_bounds__(256) lazy_dot_kernel(const __grid_constant__ P
     ts[threadIdx.x] = make_double2(tv[0], tv[1]);
   }
   __syncthreads();
-  lazy_s(jb, mu, ts, jb.t + kLazyMax);
+  if (jb.ident) {
+    if (threadIdx.x < jb.d) jb.t[kLazyMax + threadIdx.x] = make_double2(mu * ts[threadIdx.x].x, mu * ts[threadIdx.x].y);
+  } else {
+    lazy_s(jb, mu, ts, jb.t + kLazyMax);
+  }
   if (threadIdx.x == 0) *jb.cnt = 0u;
 }
 
@@ -490,6 +521,150 @@ __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ 
   }
   const double2 u = jb.w[i];
   jb.w[i] = make_double2(u.x + re, u.y + im);
+}
+
+// ---------------------------------------------------------------------------
+// KM-space iterative refinement of the dual solve.  The explicit inverse G
+// (Gauss-Jordan) applies C^{-1} with an error ~eps cond(C) |G| in every
+// direction; the Woodbury x-update r - mu A^H w cancels in the operator's
+// dominant directions and amplifies it by mu sigma^2 / beta (C2: 5.7e-6 per
+// solve).  One step of fixed-precision refinement with the exact capacitance
+//   rho = v - C_D w1,   w = w1 + C_D^{-1} rho,
+//   C_D = C - mu A_D A_D^H  (C: packed lower tiles, kept next to G),
+// makes the solve backward stable -- the accuracy of the reference's Cholesky
+// (solver_core.hpp:41-51; DESIGN.md section 3 has the measurements).
+// The C w1 product is the Hermitian apply over the packed tiles
+// (herm_gapply_persist_kernel, packed = 1) with the reduce writing v - C w1;
+// the kernels below add the lazy term and maintain C.
+// ---------------------------------------------------------------------------
+
+// dst += A_D s,  s = mu A_D^H w1 from lazy_dot_kernel (ident = 1)
+__global__ void __launch_bounds__(256) lazy_resid_axpy_kernel(const __grid_constant__ Pack<LazyJob> P,
+                                                              const int* __restrict__ go) {
+  pdl_enter();
+  if (go && __ldg(go) == 0) return;
+  const LazyJob& jb = P.j[blockIdx.y];
+  if (jb.d <= 0 || (int64_t)blockIdx.x * 256 >= jb.rows) return;
+  __shared__ double2 sv[kLazyMax];
+  __shared__ int px[kLazyMax];
+  if (threadIdx.x < jb.d) {
+    sv[threadIdx.x] = jb.t[kLazyMax + threadIdx.x];
+    px[threadIdx.x] = jb.pix[threadIdx.x];
+  }
+  __syncthreads();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= jb.rows) return;
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < jb.d; ++k) {
+    const float2 a = jb.A[i + (int64_t)px[k] * jb.ld];
+    const double2 x = sv[k];
+    re = fma((double)a.x, x.x, re);
+    re = fma(-(double)a.y, x.y, re);
+    im = fma((double)a.x, x.y, im);
+    im = fma((double)a.y, x.x, im);
+  }
+  const double2 u = jb.dst[i];
+  jb.dst[i] = make_double2(u.x + re, u.y + im);
+}
+
+// C (column-major, ldc, Hermitian: lower tiles valid) -> packed lower tiles
+__global__ void __launch_bounds__(256) cap_pack_kernel(const double2* __restrict__ C, int64_t ldc, int n,
+                                                       double2* __restrict__ Cp) {
+  pdl_enter();
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  double2* dst = Cp + herm_packed_tile(I, J);
+  for (int e = threadIdx.x; e < kHermTile * kHermTile; e += 256) {
+    const int r = e & 63, cc = e >> 6, i = I * kHermTile + r, j = J * kHermTile + cc;
+    dst[e] = (i < n && j < n) ? C[i + (int64_t)j * ldc] : make_double2(0.0, 0.0);
+  }
+}
+
+// Packed C <- C - mu A_R A_R^H over the lower tiles (columns R = pix[0..r) of
+// the complex64 operator): the capacitance of the smaller active set after a
+// fold or eager downdate.  One CTA per (tile, job); 64-column chunks of R in
+// shared memory (16 at a time), fp64 products of the promoted entries, fixed order.
+struct CapJob {
+  double2* Cp;
+  const float2* A;
+  int64_t ld;
+  int n;
+  const int* pix;
+  int r;
+};
+
+__global__ void __launch_bounds__(256) cap_update_kernel(const __grid_constant__ Pack<CapJob> P, double mu) {
+  pdl_enter();
+  const CapJob& jb = P.j[blockIdx.y];
+  const int nb = (jb.n + kHermTile - 1) / kHermTile;
+  if ((int64_t)blockIdx.x >= (int64_t)nb * (nb + 1) / 2 || jb.r <= 0) return;
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  constexpr int kCh = 16;  // columns of R per shared stage
+  __shared__ double2 ai[kCh][kHermTile + 1], aj[kCh][kHermTile + 1];
+  const int tr = threadIdx.x & 63, tc = threadIdx.x >> 6;  // row, column phase (4)
+  double accr[16], acci[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) accr[u] = acci[u] = 0.0;
+  for (int k0 = 0; k0 < jb.r; k0 += kCh) {
+    const int kn = min(kCh, jb.r - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kCh * kHermTile; e += 256) {
+      const int k = e >> 6, rr = e & 63;
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (k < kn) {
+        const int64_t col = (int64_t)jb.pix[k0 + k] * jb.ld;
+        const int i = I * kHermTile + rr, j = J * kHermTile + rr;
+        if (i < jb.n) { const float2 a = jb.A[col + i]; x = make_double2(a.x, a.y); }
+        if (j < jb.n) { const float2 a = jb.A[col + j]; y = make_double2(a.x, a.y); }
+      }
+      ai[k][rr] = x;
+      aj[k][rr] = y;
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      const double2 x = ai[k][tr];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const double2 y = aj[k][tc + 4 * u];
+        // x * conj(y)
+        accr[u] = fma(x.x, y.x, accr[u]);
+        accr[u] = fma(x.y, y.y, accr[u]);
+        acci[u] = fma(x.y, y.x, acci[u]);
+        acci[u] = fma(-x.x, y.y, acci[u]);
+      }
+    }
+  }
+  double2* dst = jb.Cp + herm_packed_tile(I, J);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tc + 4 * u, i = I * kHermTile + tr, j = J * kHermTile + cc;
+    if (i >= jb.n || j >= jb.n) continue;
+    double2 v = dst[tr + cc * kHermTile];
+    v.x -= mu * accr[u];
+    v.y -= mu * acci[u];
+    if (i == j) v.y = 0.0;  // the diagonal of a Hermitian matrix stays real
+    dst[tr + cc * kHermTile] = v;
+  }
+}
+
+// w[i] += dw[i] for the listed vectors (refinement correction after the lazy
+// terms were applied to dw)
+struct VaddJob {
+  double2* w;
+  const double2* dw;
+  int n;
+};
+__global__ void __launch_bounds__(256) vadd_kernel(const __grid_constant__ Pack<VaddJob> P, const int* __restrict__ go) {
+  pdl_enter();
+  if (go && __ldg(go) == 0) return;
+  const VaddJob& jb = P.j[blockIdx.y];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= jb.n) return;
+  const double2 a = jb.w[i], b = jb.dw[i];
+  jb.w[i] = make_double2(a.x + b.x, a.y + b.y);
 }
 
 // Bordered update of Sinv when r <= kBorderMax columns join D (d0 -> d0 + r):
@@ -1345,6 +1520,8 @@ struct FrameReduceJob {
   int64_t ldp;
   int m, nf, nsplit;
   double2* out[kFB];
+  const double2* base[kFB];  // refinement: out = base + sgn * sum (nullptr: out = sum)
+  double sgn;
 };
 
 __global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
@@ -1358,7 +1535,36 @@ __global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
     s.x += v.x;
     s.y += v.y;
   }
+  if (jb.base[f]) {
+    const double2 b = jb.base[f][i];
+    s = make_double2(b.x + jb.sgn * s.x, b.y + jb.sgn * s.y);
+  }
   jb.out[f][i] = s;
+}
+
+// packed lower tiles -> full Hermitian matrix (column-major, ld), for the
+// frame-batched refinement pass R = V - C W on the fp64 tensor cores
+__global__ void __launch_bounds__(256) cap_unpack_kernel(const double2* __restrict__ Cp, int n,
+                                                         double2* __restrict__ C, int64_t ldc) {
+  pdl_enter();
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  const double2* src = Cp + herm_packed_tile(I, J);
+  for (int e = threadIdx.x; e < kHermTile * kHermTile; e += 256) {
+    const int r = e & 63, cc = e >> 6, i = I * kHermTile + r, j = J * kHermTile + cc;
+    if (i >= n || j >= n) continue;
+    const double2 v = src[e];
+    if (I == J) {
+      if (i >= j) {
+        C[i + (int64_t)j * ldc] = v;
+        C[j + (int64_t)i * ldc] = make_double2(v.x, -v.y);
+      }
+    } else {
+      C[i + (int64_t)j * ldc] = v;
+      C[j + (int64_t)i * ldc] = make_double2(v.x, -v.y);
+    }
+  }
 }
 
 // rhs_f[j] = data_f[j] + beta gap_f[j] + beta x_hat_f[j] - sigma_f[j] for the

@@ -831,12 +831,50 @@ __global__ void gather_kernel(const double2* __restrict__ src, const int* __rest
   if (i < n) dst[i] = src[idx[i]];
 }
 
-// BASELINE dechirped-LFM operator generator (mirrors scenario.baseline_operator
-// operation by operation, no FMA contraction).
+// Portable (cos 2 pi t, sin 2 pi t), t in [0, 1): the exact operation sequence of
+// scenario.sincos_turns -- octant reduction, Taylor polynomials on [0, pi/4] in
+// Horner form, every op a separately rounded fp64 op (no FMA contraction) -- so
+// the device operator is bitwise the host one (tests/test_gpu_parity.py).
+__device__ __forceinline__ void sincos_turns(double t, double* c_out, double* s_out) {
+  const double t8 = __dmul_rn(t, 8.0);
+  const double o = floor(t8);
+  const double f = __dsub_rn(t8, o);
+  const int oi = (int)o;
+  const double h = (oi & 1) ? __dsub_rn(1.0, f) : f;
+  const double x = __dmul_rn(h, 0.7853981633974483);
+  const double x2 = __dmul_rn(x, x);
+  double p = 2.8114572543455206e-15;
+  p = __dadd_rn(-7.647163731819816e-13, __dmul_rn(x2, p));
+  p = __dadd_rn(1.6059043836821613e-10, __dmul_rn(x2, p));
+  p = __dadd_rn(-2.505210838544172e-08, __dmul_rn(x2, p));
+  p = __dadd_rn(2.7557319223985893e-06, __dmul_rn(x2, p));
+  p = __dadd_rn(-0.0001984126984126984, __dmul_rn(x2, p));
+  p = __dadd_rn(0.008333333333333333, __dmul_rn(x2, p));
+  p = __dadd_rn(-0.16666666666666666, __dmul_rn(x2, p));
+  const double sx = __dadd_rn(x, __dmul_rn(__dmul_rn(x, x2), p));
+  double r = -1.5619206968586225e-16;
+  r = __dadd_rn(4.779477332387385e-14, __dmul_rn(x2, r));
+  r = __dadd_rn(-1.1470745597729725e-11, __dmul_rn(x2, r));
+  r = __dadd_rn(2.08767569878681e-09, __dmul_rn(x2, r));
+  r = __dadd_rn(-2.755731922398589e-07, __dmul_rn(x2, r));
+  r = __dadd_rn(2.48015873015873e-05, __dmul_rn(x2, r));
+  r = __dadd_rn(-0.001388888888888889, __dmul_rn(x2, r));
+  r = __dadd_rn(0.041666666666666664, __dmul_rn(x2, r));
+  r = __dadd_rn(-0.5, __dmul_rn(x2, r));
+  const double cx = __dadd_rn(1.0, __dmul_rn(x2, r));
+  const bool sw = ((oi + 1) >> 1) & 1;
+  const double sa = sw ? cx : sx, ca = sw ? sx : cx;
+  *s_out = (oi >= 4) ? -sa : sa;
+  *c_out = (oi >= 2 && oi <= 5) ? -ca : ca;
+}
+
+// BASELINE dechirped-LFM operator generator: scenario.baseline_operator
+// operation by operation (no FMA contraction), phases in turns; bitwise equal
+// to the host generator.
 __global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K, int N,
                                const double* __restrict__ pix, const double* __restrict__ tx,
-                               const double* __restrict__ rx, const double* __restrict__ phi,
-                               double alpha, double fc, double t_step, double c_light, double two_pi) {
+                               const double* __restrict__ rx, const double* __restrict__ turns,
+                               double alpha, double fc, double t_step, double c_light) {
   pdl_enter();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int rows = M * K;
@@ -853,9 +891,10 @@ __global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K,
   const double tk = __dmul_rn((double)k, t_step);
   double cyc = __dadd_rn(__dmul_rn(__dmul_rn(alpha, tau), tk), __dmul_rn(fc, tau));
   cyc = __dsub_rn(cyc, floor(cyc));
-  const double ang = __dadd_rn(__dmul_rn(two_pi, cyc), phi[n]);
+  double t = __dadd_rn(cyc, turns[n]);
+  t = __dsub_rn(t, floor(t));
   double s, c;
-  sincos(ang, &s, &c);
+  sincos_turns(t, &c, &s);
   A[r + (int64_t)n * ld] = make_float2(__double2float_rn(c), __double2float_rn(s));
 }
 

@@ -202,23 +202,40 @@ struct TcI8Tile {
 //   P_s = [Re d_s | Im d_s],  Q_s = [Im d_s | -Re d_s]   (rows x 2N bytes),
 // so that for each slice pair (s1, s2)
 //   Re(A A^H) part = P_s1 P_s2^T,  Im part = Q_s1 P_s2^T   (int32, exact).
-// Pairs with s1 + s2 <= kOzSlices + 1 are kept (the dropped tail is below
-// 2^{-7(S+2)} relative per product).  oz_combine_kernel sums the pairs in a
+// Pairs with s1 + s2 <= kOzSlices + 3 are kept: every complex64 entry whose
+// |re|, |im| lies within 2^-25 of its row maximum is represented exactly by
+// its 7 slices (24-bit mantissa), and the dropped pairs are below 2^-56
+// relative per product -- so C matches an fp64 Gram to ~1e-16 relative, which
+// the KM-space refinement of the dual solve needs (its residual uses this C;
+// a 6-slice / s1 + s2 <= 7 Gram left ~2^-42 and cost three decades of solve
+// accuracy).  oz_combine_kernel sums the pairs in a
 // fixed order in fp64, scales by 2^{e_i + e_j} and writes the lower tiles
 // with an exact conjugate mirror, like gram_dmma_kernel.
 // ---------------------------------------------------------------------------
-constexpr int kOzSlices = 6;
-constexpr int kOzPairs = kOzSlices * (kOzSlices + 1) / 2;  // s1 + s2 <= S + 1, s1, s2 >= 1
+constexpr int kOzSlices = 7;
+constexpr int kOzMaxSum = kOzSlices + 3;
+constexpr int oz_pair_count() {
+  int n = 0;
+  for (int t = 2; t <= kOzMaxSum; ++t)
+    for (int s1 = 1; s1 <= kOzSlices; ++s1)
+      if (t - s1 >= 1 && t - s1 <= kOzSlices) ++n;
+  return n;
+}
+constexpr int kOzPairs = oz_pair_count();  // 39
 
 __host__ __device__ inline void oz_pair(int p, int& s1, int& s2) {
   // pairs ordered by t = s1 + s2 (largest contributions first), then s1
-  int t = 2;
-  while (p >= t - 1) {
-    p -= t - 1;
-    ++t;
-  }
-  s1 = p + 1;
-  s2 = t - s1;
+  for (int t = 2; t <= kOzMaxSum; ++t)
+    for (int a = 1; a <= kOzSlices; ++a) {
+      const int b = t - a;
+      if (b < 1 || b > kOzSlices) continue;
+      if (p-- == 0) {
+        s1 = a;
+        s2 = b;
+        return;
+      }
+    }
+  s1 = s2 = 1;
 }
 
 // row maxima of |re|, |im| over the listed columns (float bits: order-preserving

@@ -229,6 +229,11 @@ struct Sensor {
   int lz_r = 0;    // columns added by the last event (bordered Sinv update pending)
   DArr<double2> lz_P, lz_R, lz_S, lz_t, lz_B;
   DArr<int> lz_pix;
+  // KM-space refinement of the dual solve (refine(), kernels_batched.cuh):
+  // the capacitance C of G's base set in packed lower tiles (Cp; Cp0 next to
+  // the cached factor G0), residual rho and correction dw
+  DArr<double2> Cp, Cp0, rho, dw;
+  bool cp_valid = false, cp0_valid = false;
 };
 
 constexpr int kFlagCap = 4 * kMaxBatch;  // pinned pivot-flag slots
@@ -342,6 +347,8 @@ struct radmm_ctx {
   DArr<unsigned> lazy_cnt;           // lazy_dot_kernel arrival counters (one per job)
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
   bool pdl = false;                  // programmatic dependent launch: on inside the iteration loop (RADMM_PDL)
+  bool refine = true;                // KM-space refinement of the dual solves (radmm_run_options.skip_refinement)
+  int64_t refine_skipped = 0;        // dual sensors whose packed C did not fit (solved unrefined)
   DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
   DArr<double2> split_ws;            // split-K partial tiles
@@ -375,6 +382,9 @@ struct radmm_ctx {
   DArr<FrameReduceJob> fb_red;
   DArr<FrameRhsJob> fb_rhs;
   DArr<double2> fb_part;
+  std::vector<DArr<double2>> fb_cap;  // full capacitances for the batched refinement pass
+  bool fb_cap_ok = false;             // fb_cap holds this run's base C (reset per run_frames)
+  double fb_cap_mu = 0, fb_cap_beta = 0;
   DArr<GramJob> gram_jobs;
   // Ozaki-sliced Gram scratch (kernels_ozaki.cuh): row maxima, slices, pair blocks
   DArr<unsigned> oz_rowmax;
@@ -804,13 +814,14 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
 }
 
 // nr = 2 when some job carries a second right-hand side (v1 -> w1).
-void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go) {
-  if (nr == 1 && env_int("RADMM_HERM", 1) == 2) {
+void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go,
+                 bool packed = false) {
+  if (nr == 1 && !packed && env_int("RADMM_HERM", 1) == 2) {
     set_smem_attr((const void*)herm_gapply_tma_kernel, (int)((int)kHermTmaSmem));
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
-  } else if (nr == 2 || env_int("RADMM_HERM_PERSIST", 1)) {
+  } else if (nr == 2 || packed || env_int("RADMM_HERM_PERSIST", 1)) {
     auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
     const size_t smem = herm_persist_smem(nr);
     set_smem_attr((const void*)kern, (int)((int)smem));
@@ -1203,6 +1214,145 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
   return true;
 }
 
+// ---- KM-space refinement of the dual solve (see kernels_batched.cuh) --------
+size_t cap_tiles(int n) {
+  const size_t nb = (size_t)(n + kHermTile - 1) / kHermTile;
+  return nb * (nb + 1) / 2;
+}
+
+// Keep C = beta I + mu A_J A_J^H of a dual sensor (in S.G, lower tiles valid,
+// right before the in-place inversion) as packed lower tiles.  Skipped --
+// and the sensor solved unrefined, counted in refine_skipped -- only when the
+// tiles would not fit next to 1 GB of free HBM.
+void cap_keep(radmm_ctx* c, Sensor& S) {
+  S.cp_valid = false;
+  if (S.primal) return;
+  const size_t need = cap_tiles(S.rows) * kHermTile * kHermTile;
+  if (S.Cp.n < need) {
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (free_b < need * sizeof(double2) + (1ull << 30)) {
+      ++c->refine_skipped;
+      return;
+    }
+    S.Cp.alloc(need, false);
+  }
+  LAUNCH(c, cap_pack_kernel, dim3((unsigned)cap_tiles(S.rows)), 256, 0, S.G.p, S.ldg, S.rows, S.Cp.p);
+  S.cp_valid = true;
+}
+
+// C <- C - mu A_R A_R^H for the packed capacitances (fold / eager downdate):
+// pix lists the removed columns of each job.
+void cap_update(radmm_ctx* c, const std::vector<CapJob>& jobs, double mu) {
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<CapJob> pk;
+    size_t tiles = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = jobs[b0 + i];
+      tiles = std::max(tiles, cap_tiles(pk.j[i].n));
+    }
+    LAUNCH(c, cap_update_kernel, dim3((unsigned)tiles, (unsigned)nb), 256, 0, pk, mu);
+  }
+}
+
+void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go, bool on_dw = false);
+
+// rho += mu A_D (A_D^H w) for sensors with accumulated lazy columns: the
+// residual against C_D = C - mu A_D A_D^H, the capacitance the lazy inverse
+// (G + P Sinv P^H terms) inverts.
+void lazy_resid(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go) {
+  Pack<LazyJob> pk;
+  int nb = 0, dmax = 0, rmax = 0;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    if (S.primal || S.lz_d == 0) continue;
+    if (nb >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
+    if (c->lazy_cnt.n < (size_t)kMaxBatch) c->lazy_cnt.alloc(kMaxBatch);
+    LazyJob j{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax, S.w.p, S.lz_t.p,
+              c->lazy_cnt.p + nb};
+    j.ident = 1;
+    j.dst = S.rho.p;
+    pk.j[nb++] = j;
+    dmax = std::max(dmax, S.lz_d);
+    rmax = std::max(rmax, S.rows);
+  }
+  if (!nb) return;
+  LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
+  LAUNCH(c, lazy_resid_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, go);
+}
+
+// One step of fixed-precision iterative refinement of w = C_D^{-1} v for the
+// listed dual sensors (after gapply + lazy_correct left w1 in S.w):
+//   rho = v - C w1 + mu A_D A_D^H w1     (packed C, Hermitian apply)
+//   dw  = G rho + lazy terms             (the same apply as w1's)
+//   w   = w1 + dw
+// It makes the explicit-inverse solve backward stable: C2 5.7e-6 -> 2.5e-10
+// against the primal-Cholesky solution.  Algorithmic
+// bytes: one more pass over C's and G's lower triangles.
+void refine(radmm_ctx* c, const std::vector<int>& gq, double mu, const int* go) {
+  if (!c->refine) return;
+  std::vector<int> qs;
+  for (int q : gq)
+    if (!c->sensors[q].primal && c->sensors[q].cp_valid) qs.push_back(q);
+  for (size_t b0 = 0; b0 < qs.size(); b0 += kMaxBatch) {
+    const std::vector<int> part(qs.begin() + b0, qs.begin() + std::min(qs.size(), b0 + kMaxBatch));
+    int rows_max = 0;
+    bool any_lazy = false;
+    for (int q : part) {
+      Sensor& S = c->sensors[q];
+      if (S.rho.n < (size_t)S.ld) S.rho.alloc(S.ld);
+      if (S.dw.n < (size_t)S.ld) S.dw.alloc(S.ld);
+      rows_max = std::max(rows_max, S.rows);
+      any_lazy = any_lazy || S.lz_d > 0;
+    }
+    // rho = v - C w1
+    Pack<HermJob> pk;
+    const int nb_max = herm_pack(c, part, pk);
+    for (size_t i = 0; i < part.size(); ++i) {
+      Sensor& S = c->sensors[part[i]];
+      HermJob& h = pk.j[i];
+      h.G = S.Cp.p; h.ld = kHermTile; h.packed = 1;
+      h.v = S.w.p; h.w = S.rho.p; h.v1 = nullptr; h.w1 = nullptr;
+      h.base = S.v.p; h.sgn = -1.0;
+    }
+    herm_launch(c, pk, part.size(), nb_max, 1, go, true);
+    if (any_lazy) lazy_resid(c, part, mu, go);
+    // dw = C_D^{-1} rho (w += dw directly when no lazy terms follow)
+    const bool herm = herm_enabled() && rows_max >= env_int("RADMM_HERM_MIN_ROWS", kHermMinRows);
+    if (herm) {
+      Pack<HermJob> pg;
+      herm_pack(c, part, pg);
+      for (size_t i = 0; i < part.size(); ++i) {
+        Sensor& S = c->sensors[part[i]];
+        HermJob& h = pg.j[i];
+        h.v = S.rho.p; h.v1 = nullptr; h.w1 = nullptr;
+        if (S.lz_d > 0) { h.w = S.dw.p; h.base = nullptr; }
+        else { h.w = S.w.p; h.base = S.w.p; h.sgn = 1.0; }
+      }
+      herm_launch(c, pg, part.size(), nb_max, 1, go);
+    } else {
+      std::vector<ColDotJob> gj;
+      for (int q : part) {
+        Sensor& S = c->sensors[q];
+        ColDotJob g{};
+        g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.rho.p; g.out = S.dw.p; g.scale = 1.0;
+        gj.push_back(g);
+      }
+      coldot<double2, EPI_STORE>(c, gj, 1.0, 1.0, go);
+    }
+    if (any_lazy) lazy_correct(c, part, mu, go, true);
+    Pack<VaddJob> va;
+    int nva = 0;
+    for (int q : part) {
+      Sensor& S = c->sensors[q];
+      if (herm && S.lz_d == 0) continue;  // already folded into the reduce
+      va.j[nva++] = VaddJob{S.w.p, S.dw.p, S.rows};
+    }
+    if (nva) LAUNCH(c, vadd_kernel, dim3((unsigned)((rows_max + 255) / 256), (unsigned)nva), 256, 0, va, go);
+  }
+}
+
 // Full rebuild for the listed sensors (batched): data term + factor.
 void release_ozaki_scratch(radmm_ctx* c);
 
@@ -1266,6 +1416,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
   }
   gemm<GEPI_PLAIN>(c, jobs);
   release_ozaki_scratch(c);
+  for (int q : qs) cap_keep(c, c->sensors[q]);  // C itself, before the in-place inversion
   size_t need = 0;
   for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
   c->scratch.reserve(need);
@@ -1360,6 +1511,7 @@ void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   for (int q : qs) need += (size_t)c->sensors[q].ld * kLazyMax * sizeof(double2) + 1024;
   c->scratch.reserve(need);
   std::vector<GemmJob> st3, st4;
+  std::vector<CapJob> cj;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     const int m = S.rows, d = S.lz_d;
@@ -1368,11 +1520,13 @@ void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     st4.push_back(gjob(m, m, d, mref(T, S.ld, false), mref(S.lz_P.p, S.ld, false, true, true), S.G.p, S.ldg, mu,
                        1.0));
     st4.back().herm = 1;
+    if (S.cp_valid) cj.push_back(CapJob{S.Cp.p, S.A.p, S.ld, S.rows, S.lz_pix.p, d});
     S.lz_d = 0;
     S.lz_new = 0;
   }
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
+  cap_update(c, cj, mu);  // the base capacitance follows G's base set
 }
 
 // Append this event's removed columns to D.  A single column rides the next
@@ -1443,15 +1597,15 @@ void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
 }
 
 // w <- C_D^{-1} v from u = G v for every listed sensor with accumulated columns.
-void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go) {
+void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go, bool on_dw) {
   Pack<LazyJob> pk;
   int nb = 0, dmax = 0, rmax = 0;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     if (S.primal || S.lz_d == 0) continue;
     if (nb >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
-    pk.j[nb] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax, S.w.p, S.lz_t.p,
-                       c->lazy_cnt.p + nb};
+    pk.j[nb] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax,
+                       on_dw ? S.dw.p : S.w.p, S.lz_t.p, c->lazy_cnt.p + nb};
     ++nb;
     dmax = std::max(dmax, S.lz_d);
     rmax = std::max(rmax, S.rows);
@@ -1510,6 +1664,7 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   int nsub = 0;
   int64_t sub_max = 0;
   std::vector<double2*> Pm(qs.size()), Tm(qs.size()), Sm(qs.size());
+  std::vector<CapJob> capj;
   for (size_t t = 0; t < qs.size(); ++t) {
     Sensor& S = c->sensors[qs[t]];
     const int r = S.removed_now;
@@ -1550,6 +1705,7 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
                          S.ldg, mu, 1.0));
       st4.back().herm = 1;
+      if (S.cp_valid) capj.push_back(CapJob{S.Cp.p, S.A.p, S.ld, S.rows, S.rem_pix.p, r});
     } else {
       const int nn = S.n_act;  // kept
       const int64_t ld_new = round_up(nn, 32);
@@ -1590,6 +1746,7 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   c->defer_fail_check = false;
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
+  cap_update(c, capj, mu);
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     if (S.primal) {
@@ -1677,6 +1834,15 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
       S.primal = S.g0_primal;
       S.ldg = S.g0_ld;
       S.g_n = S.g0_n;
+      S.cp_valid = false;
+      if (!S.primal && S.cp0_valid) {
+        const size_t cn = cap_tiles(S.rows) * kHermTile * kHermTile;
+        if (S.Cp.n < cn) S.Cp.alloc(cn, false);
+        CK(cudaMemcpyAsync(S.Cp.p, S.Cp0.p, cn * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+        S.cp_valid = true;
+      } else if (!S.primal) {
+        ++c->refine_skipped;
+      }
       S.g_is_base = true;
       S.base_mu = h->mu;
       S.base_beta = h->beta;
@@ -1726,6 +1892,25 @@ void snapshot_base(radmm_ctx* c, Sensor& S, bool modify) {
     S.G0.alloc(bytes / sizeof(double2), false);
   }
   CK(cudaMemcpyAsync(S.G0.p, S.G.p, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  // the packed capacitance of the same base set travels with it (refinement)
+  S.cp0_valid = false;
+  if (S.cp_valid) {
+    const size_t cn = cap_tiles(S.rows) * kHermTile * kHermTile;
+    if (!S.Cp0.own) S.Cp0.release();
+    bool ok = S.Cp0.n >= cn;
+    if (!ok) {
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      if (free_b >= cn * sizeof(double2) + (4ull << 30)) {
+        S.Cp0.alloc(cn, false);
+        ok = true;
+      }
+    }
+    if (ok) {
+      CK(cudaMemcpyAsync(S.Cp0.p, S.Cp.p, cn * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+      S.cp0_valid = true;
+    }
+  }
   S.g0_valid = true;
   S.g0_primal = S.primal;
   S.g0_mu = S.base_mu;
@@ -1847,6 +2032,7 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
         }
       lazy_finish(c, fin, h->mu);
       lazy_correct(c, gq, h->mu, go);
+      refine(c, gq, h->mu, go);
     }
     PhaseScope ps(c, RADMM_PHASE_ADJOINT, a_bytes);
     adjoint(c, aj, gq, h->mu, h->beta, go);  // gq lists the same dual sensors in the same order
@@ -2460,6 +2646,8 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   c->have_result = false;
   c->launches = 0;
   c->rebuilds = c->downdates = 0;
+  c->refine = !(o && o->skip_refinement);
+  c->refine_skipped = 0;
   c->iter_ms.clear();
   c->iter_launches.clear();
   c->marks.clear();
@@ -2650,6 +2838,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   sm.kernel_launches = c->launches;
   sm.rebuilds = c->rebuilds;
   sm.downdates = c->downdates;
+  sm.refine_skipped = c->refine ? c->refine_skipped : 0;
   c->summary = sm;
   c->have_result = true;
   if (out) *out = sm;
@@ -2711,6 +2900,8 @@ void share_factor(radmm_ctx* dst, radmm_ctx* src, double mu, double beta) {
     if (!S.g0_valid || S.g0_mu != mu || S.g0_beta != beta) continue;
     if (D.g0_valid && D.g0_mu == mu && D.g0_beta == beta) continue;
     D.G0.view(S.G0.p, S.G0.n);
+    D.cp0_valid = S.cp0_valid;
+    if (S.cp0_valid) D.Cp0.view(S.Cp0.p, S.Cp0.n);
     D.g0_valid = true;
     D.g0_primal = S.g0_primal;
     D.g0_mu = mu;
@@ -2831,8 +3022,55 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
     }
   }
   {
-    PhaseScope ps(p, RADMM_PHASE_GAPPLY, 16.0 * ld_max * ld_max * Q);
+    PhaseScope ps(p, RADMM_PHASE_GAPPLY, 16.0 * ld_max * ld_max * Q * (fs[0]->refine ? 3 : 1));
     run_pass(FB_GAP, sp_gap);
+    // KM-space refinement for every frame (see refine()): R = V - C W, then
+    // W += G R -- two more DMMA passes over the frames' right-hand sides,
+    // with C unpacked once per run into a full matrix (frame 0's base C).
+    bool can = fs[0]->refine;
+    for (int q = 0; q < Q && can; ++q) can = fs[0]->sensors[q].cp_valid && !fs[0]->sensors[q].primal;
+    if (can) {
+      if (p->fb_cap.size() < (size_t)Q) p->fb_cap.resize(Q);
+      for (int q = 0; q < Q; ++q) {
+        const Sensor& H = fs[0]->sensors[q];
+        DArr<double2>& Cf = p->fb_cap[q];
+        if (!p->fb_cap_ok || p->fb_cap_mu != mu || p->fb_cap_beta != beta || Cf.n < (size_t)H.ldg * H.rows) {
+          if (Cf.n < (size_t)H.ldg * H.rows) Cf.alloc((size_t)H.ldg * H.rows, false);
+          LAUNCH(p, cap_unpack_kernel, dim3((unsigned)cap_tiles(H.rows)), 256, 0, H.Cp.p, H.rows, Cf.p, H.ldg);
+        }
+      }
+      p->fb_cap_ok = true;
+      p->fb_cap_mu = mu;
+      p->fb_cap_beta = beta;
+      for (int q = 0; q < Q; ++q) {  // R = V - C W  (into rho)
+        FrameBatchJob& j = jobs[q];
+        j.A = p->fb_cap[q].p;
+        FrameReduceJob& r = red[q];
+        for (int f = 0; f < nf; ++f) {
+          j.B[f] = fs[f]->sensors[q].w.p;
+          if (fs[f]->sensors[q].rho.n < (size_t)fs[f]->sensors[q].ld) fs[f]->sensors[q].rho.alloc(fs[f]->sensors[q].ld);
+          r.out[f] = fs[f]->sensors[q].rho.p;
+          r.base[f] = fs[f]->sensors[q].v.p;
+        }
+        r.sgn = -1.0;
+      }
+      run_pass(FB_GAP, sp_gap);
+      for (int q = 0; q < Q; ++q) {  // W = W + G R
+        const Sensor& H = fs[0]->sensors[q];
+        FrameBatchJob& j = jobs[q];
+        j.A = H.G.p;
+        FrameReduceJob& r = red[q];
+        for (int f = 0; f < nf; ++f) {
+          j.B[f] = fs[f]->sensors[q].rho.p;
+          r.out[f] = fs[f]->sensors[q].w.p;
+          r.base[f] = fs[f]->sensors[q].w.p;
+        }
+        r.sgn = 1.0;
+      }
+      run_pass(FB_GAP, sp_gap);
+      for (int q = 0; q < Q; ++q)
+        for (int f = 0; f < nf; ++f) red[q].base[f] = nullptr;
+    }
   }
   // X = (RHS - mu A^H W) / beta + epilogue
   for (int q = 0; q < Q; ++q) {
@@ -2878,6 +3116,7 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
                                          " has no measurement");
   }
   std::vector<radmm_run_summary> sm(F);
+  p->fb_cap_ok = false;
   p->marks.clear();
   p->ev_used = 0;
   for (int i = 0; i < RADMM_PHASE_COUNT; ++i) {  // parent stats = this call's batched passes
@@ -2896,6 +3135,8 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
     c->have_result = false;
     c->launches = 0;
     c->rebuilds = c->downdates = 0;
+    c->refine = !(o && o->skip_refinement);
+    c->refine_skipped = 0;
     c->iter_ms.clear();
     c->iter_launches.clear();
     c->marks.clear();
@@ -2989,6 +3230,7 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
     sm[f].kernel_launches = c->launches;
     sm[f].rebuilds = c->rebuilds;
     sm[f].downdates = c->downdates;
+    sm[f].refine_skipped = c->refine ? c->refine_skipped : 0;
     c->summary = sm[f];
     c->have_result = true;
     if (outs) outs[f] = sm[f];
@@ -3224,9 +3466,8 @@ int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const d
     CK(cudaMemcpyAsync(drx.p, rx, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(dphi.p, phi, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
     const int64_t total = (int64_t)M * K * N;
-    const double pi = 3.141592653589793238462643383279502884;
     LAUNCH(ctx, dechirp_kernel, dim3((unsigned)((total + 255) / 256)), 256, 0, S.A.p, S.ld, M, K, N, dpix.p, dtx.p,
-           drx.p, dphi.p, bw / pulse, fc, pulse / K, 299792458.0, 2.0 * pi);
+           drx.p, dphi.p, bw / pulse, fc, pulse / K, 299792458.0);
     CK(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -3378,6 +3619,7 @@ int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
       plan_chunks(c, S, sc->cols, 1, f.n_chunks, f.chunk_len);
       forward<MODE_GATHER>(c, {f}, {ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, nullptr, S.v.p, 1.0}}, 0.0);
       gapply(c, {0});
+      refine(c, {0}, sc->mu, nullptr);
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = sc->cols; a.cols = S.J.p; a.pix = S.J.p; a.vec = S.w.p;
       a.rhs = S.rhs.p; a.x_hat = sc->x.p; a.x_full = sc->tmp.p; a.ring_slot = sc->ring.p;

@@ -432,18 +432,63 @@ def baseline_geometry(cfg: BaselineConfig):
 
 
 def baseline_phases(cfg: BaselineConfig, q: int) -> np.ndarray:
-    """phi_qn ~ U(0, 2 pi) from stream mix_seed(seed, 1000 + q)."""
-    return 2.0 * PI * uniform01(MT19937_64(mix_seed(cfg.seed, 1000 + q)), cfg.N)
+    """phi_qn = 2 pi u_qn, u_qn ~ U(0, 1) from stream mix_seed(seed, 1000 + q),
+    returned in turns (u_qn): the generators add it to the cycle count before
+    the portable sincos, so no 2 pi rounding enters the phase."""
+    return uniform01(MT19937_64(mix_seed(cfg.seed, 1000 + q)), cfg.N)
+
+
+# Taylor coefficients of sin(x)/x - 1 (x^2 .. x^16) and cos(x) - 1 (x^2 .. x^18);
+# the CUDA generator (kernels_dense.cuh, sincos_turns) carries the same literals.
+_SIN_COEF = [(-1.0) ** k / math.factorial(2 * k + 1) for k in range(1, 9)]
+_COS_COEF = [(-1.0) ** k / math.factorial(2 * k) for k in range(1, 10)]
+_PI_4 = 0.7853981633974483
+
+
+def sincos_turns(t: np.ndarray):
+    """(cos 2 pi t, sin 2 pi t) for t in [0, 1), from IEEE +, -, *, floor only.
+
+    Octant reduction (exact: t*8 and t8 - floor(t8)) and Taylor polynomials on
+    [0, pi/4] in Horner form, every operation a separately rounded fp64 op.
+    The device generator performs the same operations in the same order with
+    __dmul_rn/__dadd_rn (no FMA contraction), so host and device operators are
+    bitwise identical on any machine -- which libm sin/cos are not -- and the
+    committed oracle fixtures (tests/golden/) can be checked against operators
+    generated on the GPU.  Error < 2 ulp of fp64 (tests/test_oracle_pins.py)."""
+    t8 = t * 8.0
+    o = np.floor(t8)
+    f = t8 - o
+    oi = o.astype(np.int64)
+    odd = (oi & 1) == 1
+    h = np.where(odd, 1.0 - f, f)
+    x = h * _PI_4
+    x2 = x * x
+    p = np.full_like(x, _SIN_COEF[-1])
+    for c in reversed(_SIN_COEF[:-1]):
+        p = c + x2 * p
+    sx = x + (x * x2) * p
+    r = np.full_like(x, _COS_COEF[-1])
+    for c in reversed(_COS_COEF[:-1]):
+        r = c + x2 * r
+    cx = 1.0 + x2 * r
+    # angle = o pi/4 + f pi/4; odd octants use x' = (1 - f) pi/4 from the next axis
+    sw = ((oi + 1) >> 1) & 1 == 1          # octants 1, 2, 5, 6: sin <-> cos
+    s_abs = np.where(sw, cx, sx)
+    c_abs = np.where(sw, sx, cx)
+    s_neg = oi >= 4                        # octants 4..7: sin < 0
+    c_neg = (oi >= 2) & (oi <= 5)          # octants 2..5: cos < 0
+    return np.where(c_neg, -c_abs, c_abs), np.where(s_neg, -s_abs, s_abs)
 
 
 def baseline_operator(cfg: BaselineConfig, q: int) -> np.ndarray:
-    """A_q[m*K+k, n] = exp(j 2 pi (alpha tau t_k + fc tau)) e^{j phi_qn}, complex64.
+    """A_q[m*K+k, n] = exp(j 2 pi (alpha tau t_k + fc tau + u_qn)), complex64.
 
-    t_k = k T / K; the phase is reduced modulo one cycle in fp64 before the
-    sincos so the fp32 entries do not inherit the ~5e3-cycle carrier offset.
-    """
+    t_k = k T / K; the cycle count is reduced modulo one turn in fp64, the
+    per-pixel phase u_qn (turns) added and reduced again, then the portable
+    ``sincos_turns`` -- bitwise equal to the device generator
+    (radmm_generate_dechirp_operator)."""
     pix, tx, rx = baseline_geometry(cfg)
-    phi = baseline_phases(cfg, q)
+    u = baseline_phases(cfg, q)
     alpha = cfg.bw / cfg.pulse
     tk = np.arange(cfg.K, dtype=np.float64) * (cfg.pulse / cfg.K)
     a = np.empty((cfg.KM, cfg.N), dtype=np.complex64)
@@ -452,8 +497,12 @@ def baseline_operator(cfg: BaselineConfig, q: int) -> np.ndarray:
         tau = (d_tx + _dist(rx[q, m][None, :], pix)) / SPEED_OF_LIGHT
         cyc = (alpha * tau)[None, :] * tk[:, None] + (cfg.fc * tau)[None, :]
         cyc = cyc - np.floor(cyc)
-        ang = 2.0 * PI * cyc + phi[None, :]
-        a[m * cfg.K:(m + 1) * cfg.K] = (np.cos(ang) + 1j * np.sin(ang)).astype(np.complex64)
+        t = cyc + u[None, :]
+        t = t - np.floor(t)
+        c, s = sincos_turns(t)
+        blk = a[m * cfg.K:(m + 1) * cfg.K]
+        blk.real = c.astype(np.float32)
+        blk.imag = s.astype(np.float32)
     return a
 
 

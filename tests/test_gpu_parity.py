@@ -375,9 +375,8 @@ def test_device_generator_matches_host():
                                     cfg.fc, cfg.bw, cfg.pulse)
         dev = s.get_operator(q)
         host = scenario.baseline_operator(cfg, q)
-        d = np.abs(dev - host)
-        assert d.max() <= 2 * np.finfo(np.float32).eps
-        assert np.count_nonzero(d) <= 1e-3 * d.size
+        # portable sincos (IEEE basic ops only): bitwise, not "within ulps"
+        assert np.array_equal(dev.view(np.uint32), host.view(np.uint32))
     s.close()
 
 
