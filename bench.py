@@ -365,6 +365,7 @@ def ours(args, cfg):
                "gpu_launches": launches, "clocks": clk, "roofline": roofline,
                "iteration_GBps_algorithmic": bytes_iter * value / 1e9,
                "cpu_baseline": cpu, "e2e": e2e, "time_to_tolerance": ttt,
+               "refinement": {"km_space_refinement": True, "sensors_unrefined": res.refine_skipped},
                "active_sizes_end": None}
         print(json.dumps(out), flush=True)
     if dist is not None:

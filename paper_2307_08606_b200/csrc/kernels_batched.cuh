@@ -641,12 +641,75 @@ __global__ void __launch_bounds__(256) cap_update_kernel(const __grid_constant__
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int cc = tc + 4 * u, i = I * kHermTile + tr, j = J * kHermTile + cc;
-    if (i >= jb.n || j >= jb.n) continue;
+    if (i >= jb.n || j >= jb.n || (I == J && i < j)) continue;  // diagonal tiles: lower half + exact mirror
     double2 v = dst[tr + cc * kHermTile];
     v.x -= mu * accr[u];
     v.y -= mu * acci[u];
     if (i == j) v.y = 0.0;  // the diagonal of a Hermitian matrix stays real
     dst[tr + cc * kHermTile] = v;
+    if (I == J && i > j) dst[cc + tr * kHermTile] = make_double2(v.x, -v.y);
+  }
+}
+
+// Packed lower tiles of a Hermitian G <- G + alpha X Y^H (X, Y: ld x d,
+// complex128): the lazy fold / eager downdate of a packed dual factor
+// (G + mu (P Sinv) P^H).  One CTA per (tile, job), fixed order.
+struct PackedUpdJob {
+  double2* Gp;
+  const double2* X;
+  const double2* Y;
+  int64_t ld;
+  int n, d;
+};
+
+__global__ void __launch_bounds__(256) herm_packed_update_kernel(const __grid_constant__ Pack<PackedUpdJob> P,
+                                                                 double alpha) {
+  pdl_enter();
+  const PackedUpdJob& jb = P.j[blockIdx.y];
+  const int nb = (jb.n + kHermTile - 1) / kHermTile;
+  if ((int64_t)blockIdx.x >= (int64_t)nb * (nb + 1) / 2 || jb.d <= 0) return;
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  constexpr int kCh = 16;
+  __shared__ double2 xi[kCh][kHermTile + 1], yj[kCh][kHermTile + 1];
+  const int tr = threadIdx.x & 63, tc = threadIdx.x >> 6;
+  double accr[16], acci[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) accr[u] = acci[u] = 0.0;
+  for (int k0 = 0; k0 < jb.d; k0 += kCh) {
+    const int kn = min(kCh, jb.d - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kCh * kHermTile; e += 256) {
+      const int k = e >> 6, rr = e & 63;
+      const int i = I * kHermTile + rr, j = J * kHermTile + rr;
+      xi[k][rr] = (k < kn && i < jb.n) ? jb.X[i + (int64_t)(k0 + k) * jb.ld] : make_double2(0.0, 0.0);
+      yj[k][rr] = (k < kn && j < jb.n) ? jb.Y[j + (int64_t)(k0 + k) * jb.ld] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      const double2 x = xi[k][tr];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const double2 y = yj[k][tc + 4 * u];
+        accr[u] = fma(x.x, y.x, accr[u]);
+        accr[u] = fma(x.y, y.y, accr[u]);
+        acci[u] = fma(x.y, y.x, acci[u]);
+        acci[u] = fma(-x.x, y.y, acci[u]);
+      }
+    }
+  }
+  double2* dst = jb.Gp + herm_packed_tile(I, J);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tc + 4 * u, i = I * kHermTile + tr, j = J * kHermTile + cc;
+    if (i >= jb.n || j >= jb.n || (I == J && i < j)) continue;  // diagonal tiles: lower half + exact mirror
+    double2 v = dst[tr + cc * kHermTile];
+    v.x += alpha * accr[u];
+    v.y += alpha * acci[u];
+    if (i == j) v.y = 0.0;
+    dst[tr + cc * kHermTile] = v;
+    if (I == J && i > j) dst[cc + tr * kHermTile] = make_double2(v.x, -v.y);
   }
 }
 

@@ -201,6 +201,7 @@ struct Sensor {
   double base_mu = 0, base_beta = 0;
   int64_t g0_ld = 0;
   int g0_n = 0;
+  size_t g0_elems = 0;
   int64_t ldg = 0;
   int g_n = 0;
   // forward partials / KM-space vectors
@@ -224,6 +225,7 @@ struct Sensor {
   // raw full-set Gram A A^H computed right after the operator upload (overlaps
   // the next sensor's upload); the run's first factorization scales it
   bool raw_gram = false;
+  bool raw_packed = false;  // the raw Gram sits in Cp (packed factor) instead of G
   int lz_d = 0;    // |D|
   int lz_new = 0;  // 1: P[:, d-1] = G a is formed by the next G-apply (second right-hand side)
   int lz_r = 0;    // columns added by the last event (bordered Sinv update pending)
@@ -234,6 +236,10 @@ struct Sensor {
   // the cached factor G0), residual rho and correction dw
   DArr<double2> Cp, Cp0, rho, dw;
   bool cp_valid = false, cp0_valid = false;
+  // dual factor stored as packed lower tiles (herm_packed_tile) instead of a
+  // full ld x rows matrix: half the HBM (config 3 fits with C next to it) and
+  // tile-contiguous reads for the Hermitian apply; g0_packed: G0's layout
+  bool gpacked = false, g0_packed = false;
 };
 
 constexpr int kFlagCap = 4 * kMaxBatch;  // pinned pivot-flag slots
@@ -382,8 +388,12 @@ struct radmm_ctx {
   DArr<FrameReduceJob> fb_red;
   DArr<FrameRhsJob> fb_rhs;
   DArr<double2> fb_part;
+  std::vector<DArr<double2>> gtmp;    // full rows x rows temporaries: Gram + Gauss-Jordan of packed factors
+  std::vector<DArr<double2>> fb_g;    // full copies of packed factors for the frame-batched DMMA passes
   std::vector<DArr<double2>> fb_cap;  // full capacitances for the batched refinement pass
   bool fb_cap_ok = false;             // fb_cap holds this run's base C (reset per run_frames)
+  bool fb_g_ok = false;               // fb_g holds this run's unpacked base factors
+  double fb_g_mu = 0, fb_g_beta = 0;
   double fb_cap_mu = 0, fb_cap_beta = 0;
   DArr<GramJob> gram_jobs;
   // Ozaki-sliced Gram scratch (kernels_ozaki.cuh): row maxima, slices, pair blocks
@@ -500,6 +510,22 @@ void configure_pool(int device) {
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
 }
 
+// Bytes an allocation can still get: free device memory plus what the
+// stream-ordered pool holds reserved but unused (freed blocks it keeps up to
+// the release threshold -- invisible to cudaMemGetInfo).
+size_t mem_available(int device) {
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+      free_b += (size_t)(reserved - used);
+  }
+  return free_b;
+}
+
 int occupancy(const void* func, int threads, size_t smem);
 void set_smem_attr(const void* func, int bytes);
 
@@ -594,6 +620,8 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   S.g0_valid = false;  // a new operator invalidates the cached factor
   S.g_is_base = false;
   S.raw_gram = false;
+  S.raw_packed = false;
+  S.cp_valid = S.cp0_valid = false;
   S.has_y = false;
 }
 
@@ -777,7 +805,7 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
   for (size_t i = 0; i < qs.size(); ++i) {
     Sensor& S = c->sensors[qs[i]];
     HermJob h{};
-    h.G = S.G.p; h.ld = S.ldg; h.n = S.rows;
+    h.G = S.G.p; h.ld = S.gpacked ? kHermTile : S.ldg; h.packed = S.gpacked ? 1 : 0; h.n = S.rows;
     h.nb = (S.rows + kHermTile - 1) / kHermTile;
     h.groups = (h.nb + kHermStrip - 1) / kHermStrip;
     const size_t nd = (size_t)h.nb * h.groups * kHermTile,
@@ -816,6 +844,7 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
 // nr = 2 when some job carries a second right-hand side (v1 -> w1).
 void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go,
                  bool packed = false) {
+  for (size_t i = 0; i < nq; ++i) packed = packed || pk.j[i].packed;  // only the persistent kernel reads tiles
   if (nr == 1 && !packed && env_int("RADMM_HERM", 1) == 2) {
     set_smem_attr((const void*)herm_gapply_tma_kernel, (int)((int)kHermTmaSmem));
     const int grid = std::min(c->herm_n_items, c->sm_count);
@@ -1121,7 +1150,7 @@ void symmetrize(radmm_ctx* c, const std::vector<int>& qs) {
   if (env_int("RADMM_SYMM", 1) == 0) return;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
-    if (S.primal || S.g_n <= 0) continue;
+    if (S.primal || S.gpacked || S.g_n <= 0) continue;  // packed: the lower tiles define G
     const int nt = (S.g_n + 31) / 32;
     LAUNCH(c, herm_symmetrize_kernel, dim3((unsigned)((int64_t)nt * (nt + 1) / 2)), 256, 0, S.G.p, S.ldg, S.g_n);
   }
@@ -1179,8 +1208,7 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
   const size_t rblk = (size_t)tiles * kOzPairs * 2 * kOzBM * kOzBN;
   const size_t need = 2 * pq + rblk * 4 + rows_pad * 4;
   if (c->oz_P.n < pq || c->oz_R.n < rblk || c->oz_rowmax.n < (size_t)rows_pad) {
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = mem_available(c->device);
     const size_t held = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
     if (free_b + held < need + (4ull << 30)) return false;
     if (c->oz_P.n < pq) {
@@ -1224,21 +1252,45 @@ size_t cap_tiles(int n) {
 // right before the in-place inversion) as packed lower tiles.  Skipped --
 // and the sensor solved unrefined, counted in refine_skipped -- only when the
 // tiles would not fit next to 1 GB of free HBM.
-void cap_keep(radmm_ctx* c, Sensor& S) {
+void cap_keep(radmm_ctx* c, Sensor& S, const double2* C, int64_t ldc) {
   S.cp_valid = false;
   if (S.primal) return;
   const size_t need = cap_tiles(S.rows) * kHermTile * kHermTile;
   if (S.Cp.n < need) {
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = mem_available(c->device);
     if (free_b < need * sizeof(double2) + (1ull << 30)) {
       ++c->refine_skipped;
       return;
     }
     S.Cp.alloc(need, false);
   }
-  LAUNCH(c, cap_pack_kernel, dim3((unsigned)cap_tiles(S.rows)), 256, 0, S.G.p, S.ldg, S.rows, S.Cp.p);
+  LAUNCH(c, cap_pack_kernel, dim3((unsigned)cap_tiles(S.rows)), 256, 0, C, ldc, S.rows, S.Cp.p);
   S.cp_valid = true;
+}
+
+// Elements of G's storage (packed lower tiles or a full ldg x g_n matrix).
+size_t g_elems(const Sensor& S) {
+  return S.gpacked ? cap_tiles(S.rows) * kHermTile * kHermTile : (size_t)S.ldg * S.g_n;
+}
+
+// A dual factor of this sensor is stored packed (callers check dual-ness).
+bool use_gpacked(const radmm_ctx* c, const Sensor& S) {
+  return herm_enabled() && S.rows >= env_int("RADMM_HERM_MIN_ROWS", kHermMinRows) && c->Q <= kMaxBatch &&
+         env_int("RADMM_GPACK", 1) != 0;
+}
+
+// Full rows x rows temporaries for `count` packed factorizations at once.
+void gtmp_reserve(radmm_ctx* c, int count, size_t elems) {
+  if ((int)c->gtmp.size() < count) c->gtmp.resize(count);
+  for (int i = 0; i < count; ++i)
+    if (c->gtmp[i].n < elems) c->gtmp[i].alloc(elems, false);
+}
+
+void gtmp_release(radmm_ctx* c) {
+  size_t held = 0;
+  for (auto& t : c->gtmp) held += t.n * sizeof(double2);
+  if (held <= (2ull << 30)) return;
+  c->gtmp.clear();
 }
 
 // C <- C - mu A_R A_R^H for the packed capacitances (fold / eager downdate):
@@ -1253,6 +1305,20 @@ void cap_update(radmm_ctx* c, const std::vector<CapJob>& jobs, double mu) {
       tiles = std::max(tiles, cap_tiles(pk.j[i].n));
     }
     LAUNCH(c, cap_update_kernel, dim3((unsigned)tiles, (unsigned)nb), 256, 0, pk, mu);
+  }
+}
+
+// G <- G + alpha X Y^H on packed factors (lazy fold / eager downdate).
+void packed_update(radmm_ctx* c, const std::vector<PackedUpdJob>& jobs, double alpha) {
+  for (size_t b0 = 0; b0 < jobs.size(); b0 += kMaxBatch) {
+    const size_t nb = std::min<size_t>(kMaxBatch, jobs.size() - b0);
+    Pack<PackedUpdJob> pk;
+    size_t tiles = 0;
+    for (size_t i = 0; i < nb; ++i) {
+      pk.j[i] = jobs[b0 + i];
+      tiles = std::max(tiles, cap_tiles(pk.j[i].n));
+    }
+    LAUNCH(c, herm_packed_update_kernel, dim3((unsigned)tiles, (unsigned)nb), 256, 0, pk, alpha);
   }
 }
 
@@ -1356,7 +1422,17 @@ void refine(radmm_ctx* c, const std::vector<int>& gq, double mu, const int* go) 
 // Full rebuild for the listed sensors (batched): data term + factor.
 void release_ozaki_scratch(radmm_ctx* c);
 
-void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
+void rebuild_packed(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta);
+
+void full_rebuild(radmm_ctx* c, const std::vector<int>& qs0, double mu, double beta) {
+  if (qs0.empty()) return;
+  std::vector<int> qs, packed;
+  for (int q : qs0) {
+    Sensor& S = c->sensors[q];
+    S.primal = S.n_act <= S.rows;
+    (!S.primal && use_gpacked(c, S) ? packed : qs).push_back(q);
+  }
+  rebuild_packed(c, packed, mu, beta);
   if (qs.empty()) return;
   std::vector<GemmJob> jobs;
   std::vector<GramJob> grams;
@@ -1373,7 +1449,9 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
     S.lz_d = S.lz_new = 0;  // a fresh factor of the current set
     const int dim = S.primal ? S.n_act : S.rows;
     const int64_t ldg = S.primal ? round_up(dim, 32) : S.ld;
-    const bool raw = S.raw_gram && !S.primal && S.n_act == c->N && S.ldg == ldg;
+    const bool raw = S.raw_gram && !S.raw_packed && !S.primal && S.n_act == c->N && S.ldg == ldg && !S.gpacked;
+    if (S.gpacked) S.G.release();  // was packed (layout switch): a full matrix now
+    S.gpacked = false;
     ensure_g(S, dim, ldg);
     S.ldg = ldg;
     S.g_n = dim;
@@ -1383,7 +1461,7 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
       jobs.push_back(gjob(dim, dim, S.rows, mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p),
                           mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p), S.G.p, ldg, mu, 0.0, beta));
       jobs.back().herm = 1;  // Hermitian: lower tiles + mirror
-    } else if (S.raw_gram && S.n_act == c->N && S.ldg == ldg) {
+    } else if (raw) {
       // the full-set Gram was formed at upload (eager_gram): scale it in place
       // (same roundings as forming beta I + mu A A^H directly)
       LAUNCH(c, gram_scale_kernel, dim3((unsigned)((int64_t)dim * dim + 255) / 256), 256, 0, S.G.p, ldg, dim, mu,
@@ -1416,12 +1494,112 @@ void full_rebuild(radmm_ctx* c, const std::vector<int>& qs, double mu, double be
   }
   gemm<GEPI_PLAIN>(c, jobs);
   release_ozaki_scratch(c);
-  for (int q : qs) cap_keep(c, c->sensors[q]);  // C itself, before the in-place inversion
+  for (int q : qs) cap_keep(c, c->sensors[q], c->sensors[q].G.p, c->sensors[q].ldg);  // C, before the in-place inversion
   size_t need = 0;
   for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
   c->scratch.reserve(need);
   gj_invert(c, inv, "factorize");
   symmetrize(c, qs);
+}
+
+// Dual factors in packed lower tiles: per chunk of sensors, the capacitance
+// is formed in full temporaries (upload-time raw Gram unpacked and scaled, or
+// a fresh Ozaki / DMMA Gram), kept packed (Cp, refinement), inverted in place
+// by Gauss-Jordan and packed into S.G.  Chunks are sized so the temporaries
+// fit next to everything resident (config 3 on one GPU: 171 GB).
+void rebuild_packed(radmm_ctx* c, const std::vector<int>& qs, double mu, double beta) {
+  if (qs.empty()) return;
+  size_t full = 0;
+  for (int q : qs) {
+    Sensor& S = c->sensors[q];
+    S.lz_d = S.lz_new = 0;
+    const size_t ge = cap_tiles(S.rows) * kHermTile * kHermTile;
+    if (!S.gpacked || S.G.n < ge) {
+      S.G.release();
+      S.G.alloc(ge, false);
+    }
+    S.gpacked = true;
+    S.ldg = kHermTile;
+    S.g_n = S.rows;
+    full = std::max(full, (size_t)S.ld * S.rows);
+  }
+  for (int q : qs) {  // C's packed tiles before the temporaries take what is left
+    Sensor& S = c->sensors[q];
+    const size_t cn = cap_tiles(S.rows) * kHermTile * kHermTile;
+    if (S.Cp.n < cn && mem_available(c->device) >= cn * sizeof(double2) + (4ull << 30)) S.Cp.alloc(cn, false);
+  }
+  const size_t free_b = mem_available(c->device);
+  size_t held = 0;
+  for (auto& t : c->gtmp) held += t.n * sizeof(double2);
+  const size_t room = free_b + held > (6ull << 30) ? free_b + held - (6ull << 30) : 0;
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(qs.size(), room / (full * sizeof(double2))));
+  gtmp_reserve(c, chunk, full);
+  for (size_t b0 = 0; b0 < qs.size(); b0 += chunk) {
+    const size_t nb = std::min<size_t>(chunk, qs.size() - b0);
+    std::vector<GemmJob> jobs;
+    std::vector<GramJob> grams;
+    std::vector<InvTarget> inv;
+    for (size_t i = 0; i < nb; ++i) {
+      Sensor& S = c->sensors[qs[b0 + i]];
+      double2* T = c->gtmp[i].p;
+      const int64_t ldt = S.ld;
+      const int dim = S.rows;
+      if (S.raw_gram && S.raw_packed && S.cp_valid && S.n_act == c->N) {
+        // the raw full-set Gram A A^H formed at upload (eager_gram, packed in Cp)
+        CK(cudaMemsetAsync(T, 0, sizeof(double2) * (size_t)ldt * dim, c->stream));
+        LAUNCH(c, cap_unpack_kernel, dim3((unsigned)cap_tiles(dim)), 256, 0, S.Cp.p, dim, T, ldt);
+        LAUNCH(c, gram_scale_kernel, dim3((unsigned)((int64_t)dim * dim + 255) / 256), 256, 0, T, ldt, dim, mu,
+               beta);
+      } else {
+        CK(cudaMemsetAsync(T, 0, sizeof(double2) * (size_t)ldt * dim, c->stream));
+        if (env_int("RADMM_GRAM", 1) && ozaki_gram(c, S, S.J.p, S.n_act, T, ldt, mu, beta)) {
+        } else if (env_int("RADMM_GRAM", 1)) {
+          grams.push_back(GramJob{S.A.p, S.ld, S.J.p, S.n_act, S.rows, T, ldt});
+        } else {
+          jobs.push_back(gjob(dim, dim, S.n_act, mref(S.A.p, S.ld, true, false, false, nullptr, S.J.p),
+                              mref(S.A.p, S.ld, true, true, true, nullptr, S.J.p), T, ldt, mu, 0.0, beta));
+          jobs.back().herm = 1;
+        }
+      }
+      inv.push_back({T, ldt, dim});
+      S.raw_gram = false;
+      ++c->rebuilds;
+    }
+    if (!grams.empty()) {
+      if (c->gram_jobs.n < grams.size()) c->gram_jobs.alloc(grams.size(), false);
+      CK(cudaMemcpyAsync(c->gram_jobs.p, grams.data(), sizeof(GramJob) * grams.size(), cudaMemcpyHostToDevice,
+                         c->stream));
+      int mmax = 0;
+      for (const auto& g : grams) mmax = std::max(mmax, g.m);
+      set_smem_attr((const void*)gram_dmma_kernel, (int)((int)kGramSmem));
+      LAUNCH(c, gram_dmma_kernel,
+             dim3((unsigned)((mmax + kGrBN - 1) / kGrBN), (unsigned)((mmax + kGrBM - 1) / kGrBM),
+                  (unsigned)grams.size()),
+             256, kGramSmem, c->gram_jobs.p, mu, beta);
+    }
+    gemm<GEPI_PLAIN>(c, jobs);
+    for (size_t i = 0; i < nb; ++i) {
+      Sensor& S = c->sensors[qs[b0 + i]];
+      cap_keep(c, S, c->gtmp[i].p, S.ld);
+    }
+    size_t need = 0;
+    for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
+    c->scratch.reserve(need);
+    gj_invert(c, inv, "factorize");
+    for (size_t i = 0; i < nb; ++i) {
+      Sensor& S = c->sensors[qs[b0 + i]];
+      // Hermitian projection first (see symmetrize): the packed apply reads the
+      // diagonal tiles whole, so they must be the projected factor's
+      if (env_int("RADMM_SYMM", 1) != 0) {
+        const int nt = (S.rows + 31) / 32;
+        LAUNCH(c, herm_symmetrize_kernel, dim3((unsigned)((int64_t)nt * (nt + 1) / 2)), 256, 0, c->gtmp[i].p, S.ld,
+               S.rows);
+      }
+      LAUNCH(c, cap_pack_kernel, dim3((unsigned)cap_tiles(S.rows)), 256, 0, c->gtmp[i].p, S.ld, S.rows, S.G.p);
+    }
+  }
+  release_ozaki_scratch(c);
+  gtmp_release(c);
 }
 
 // Data term mu A_J^H y_eff for the listed sensors (admm.hpp:177).
@@ -1512,20 +1690,26 @@ void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   c->scratch.reserve(need);
   std::vector<GemmJob> st3, st4;
   std::vector<CapJob> cj;
+  std::vector<PackedUpdJob> pu;
   for (int q : qs) {
     Sensor& S = c->sensors[q];
     const int m = S.rows, d = S.lz_d;
     double2* T = c->scratch.take<double2>((size_t)S.ld * kLazyMax);
     st3.push_back(gjob(m, d, d, mref(S.lz_P.p, S.ld, false), mref(S.lz_S.p, kLazyMax, false), T, S.ld, 1.0, 0.0));
-    st4.push_back(gjob(m, m, d, mref(T, S.ld, false), mref(S.lz_P.p, S.ld, false, true, true), S.G.p, S.ldg, mu,
-                       1.0));
-    st4.back().herm = 1;
+    if (S.gpacked) {
+      pu.push_back(PackedUpdJob{S.G.p, T, S.lz_P.p, S.ld, m, d});
+    } else {
+      st4.push_back(gjob(m, m, d, mref(T, S.ld, false), mref(S.lz_P.p, S.ld, false, true, true), S.G.p, S.ldg, mu,
+                         1.0));
+      st4.back().herm = 1;
+    }
     if (S.cp_valid) cj.push_back(CapJob{S.Cp.p, S.A.p, S.ld, S.rows, S.lz_pix.p, d});
     S.lz_d = 0;
     S.lz_new = 0;
   }
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
+  packed_update(c, pu, mu);
   cap_update(c, cj, mu);  // the base capacitance follows G's base set
 }
 
@@ -1665,6 +1849,9 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   int64_t sub_max = 0;
   std::vector<double2*> Pm(qs.size()), Tm(qs.size()), Sm(qs.size());
   std::vector<CapJob> capj;
+  std::vector<PackedUpdJob> pupd;
+  std::vector<int> hp_q;                 // packed dual sensors: P = G R by Hermitian applies
+  std::vector<double2*> hp_R, hp_P;
   for (size_t t = 0; t < qs.size(); ++t) {
     Sensor& S = c->sensors[qs[t]];
     const int r = S.removed_now;
@@ -1677,8 +1864,16 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       Tm[t] = c->scratch.take<double2>((size_t)S.ld * r);
       // P = G R: few columns -> r Hermitian matvecs G a_t through the streaming
       // column-dot kernel (G read once per removed column, all sensors batched);
-      // many columns -> tiled GEMM
-      if (r <= env_int("RADMM_DD_MATVEC", kDowndateMatvecMax)) {
+      // many columns -> tiled GEMM; packed factors -> Hermitian applies, two
+      // columns per pass over the lower tiles
+      if (S.gpacked) {
+        double2* Rb = c->scratch.take<double2>((size_t)S.ld * r);
+        LAUNCH(c, gather_cols_c128_kernel, dim3((unsigned)((S.ld * r + 255) / 256)), 256, 0, S.A.p, S.ld,
+               S.rem_pix.p, r, Rb);
+        hp_q.push_back(qs[t]);
+        hp_R.push_back(Rb);
+        hp_P.push_back(Pm[t]);
+      } else if (r <= env_int("RADMM_DD_MATVEC", kDowndateMatvecMax)) {
         double2* Rb = c->scratch.take<double2>((size_t)S.ld * r);
         LAUNCH(c, gather_cols_c128_kernel, dim3((unsigned)((S.ld * r + 255) / 256)), 256, 0, S.A.p, S.ld,
                S.rem_pix.p, r, Rb);
@@ -1702,9 +1897,13 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       // G += mu T P^H: a Hermitian rank-r update, applied to the lower tiles
       // with an exact conjugate mirror -- G stays exactly Hermitian (no
       // projection pass needed after a downdate)
-      st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
-                         S.ldg, mu, 1.0));
-      st4.back().herm = 1;
+      if (S.gpacked) {
+        pupd.push_back(PackedUpdJob{S.G.p, Tm[t], Pm[t], S.ld, m, r});
+      } else {
+        st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
+                           S.ldg, mu, 1.0));
+        st4.back().herm = 1;
+      }
       if (S.cp_valid) capj.push_back(CapJob{S.Cp.p, S.A.p, S.ld, S.rows, S.rem_pix.p, r});
     } else {
       const int nn = S.n_act;  // kept
@@ -1739,6 +1938,28 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     LAUNCH(c, gather_sub_kernel, dim3(std::max(1, blocks), nsub), 256, 0, sub);
   }
   for (const auto& jobs : p_by_col) coldot<double2, EPI_STORE>(c, jobs, mu, 1.0);
+  if (!hp_q.empty()) {
+    Pack<HermJob> pk;
+    const int nb_max = herm_pack(c, hp_q, pk);
+    int rmax = 0;
+    for (int q : hp_q) rmax = std::max(rmax, c->sensors[q].removed_now);
+    for (int u0 = 0; u0 < rmax; u0 += 2) {
+      for (size_t i = 0; i < hp_q.size(); ++i) {
+        Sensor& S = c->sensors[hp_q[i]];
+        HermJob& h = pk.j[i];
+        h.v = h.v1 = nullptr;
+        h.w = h.w1 = nullptr;
+        h.base = nullptr;
+        for (int tcol = 0; tcol < 2; ++tcol) {
+          const int u = u0 + tcol;
+          if (u >= S.removed_now) break;
+          (tcol ? h.v1 : h.v) = hp_R[i] + (size_t)u * S.ld;
+          (tcol ? h.w1 : h.w) = hp_P[i] + (size_t)u * S.ld;
+        }
+      }
+      herm_launch(c, pk, hp_q.size(), nb_max, 2, nullptr);
+    }
+  }
   gemm<GEPI_PLAIN>(c, st1);
   gemm<GEPI_PLAIN>(c, st2);
   c->defer_fail_check = true;  // the r x r pivots are checked after the iteration's sync
@@ -1746,6 +1967,7 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   c->defer_fail_check = false;
   gemm<GEPI_PLAIN>(c, st3);
   gemm<GEPI_PLAIN>(c, st4);
+  packed_update(c, pupd, mu);
   cap_update(c, capj, mu);
   for (int q : qs) {
     Sensor& S = c->sensors[q];
@@ -1825,12 +2047,16 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
   std::vector<int> fresh;
   for (int q : all) {
     Sensor& S = c->sensors[q];
-    if (S.g_is_base && S.base_mu == h->mu && S.base_beta == h->beta) {
+    // the layout this run would factor the full set in (a cached factor of
+    // the other layout -- RADMM_HERM / RADMM_GPACK changed -- is refactored)
+    const bool want_packed = c->N > S.rows && use_gpacked(c, S);
+    if (S.g_is_base && S.base_mu == h->mu && S.base_beta == h->beta && S.gpacked == want_packed) {
       ++c->factor_cache_hits;  // G is untouched since its full-set factorization
-    } else if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta) {
-      if (S.G.n < (size_t)S.g0_ld * S.g0_n) S.G.alloc((size_t)S.g0_ld * S.g0_n);
-      CK(cudaMemcpyAsync(S.G.p, S.G0.p, sizeof(double2) * (size_t)S.g0_ld * S.g0_n, cudaMemcpyDeviceToDevice,
-                         c->stream));
+    } else if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta && S.g0_packed == want_packed) {
+      if (S.gpacked != S.g0_packed) S.G.release();
+      if (S.G.n < S.g0_elems) S.G.alloc(S.g0_elems);
+      CK(cudaMemcpyAsync(S.G.p, S.G0.p, sizeof(double2) * S.g0_elems, cudaMemcpyDeviceToDevice, c->stream));
+      S.gpacked = S.g0_packed;
       S.primal = S.g0_primal;
       S.ldg = S.g0_ld;
       S.g_n = S.g0_n;
@@ -1878,13 +2104,14 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
 void snapshot_base(radmm_ctx* c, Sensor& S, bool modify) {
   if (!S.g_is_base) return;
   if (modify) S.g_is_base = false;
-  if (S.g0_valid && S.g0_mu == S.base_mu && S.g0_beta == S.base_beta && S.g0_ld == S.ldg && S.g0_n == S.g_n) return;
+  if (S.g0_valid && S.g0_mu == S.base_mu && S.g0_beta == S.base_beta && S.g0_ld == S.ldg && S.g0_n == S.g_n &&
+      S.g0_packed == S.gpacked)
+    return;
   if (env_int("RADMM_FACTOR_CACHE", 1) == 0) return;
   if (!S.G0.own) S.G0.release();  // never write through a view of another context's factor
-  const size_t bytes = sizeof(double2) * (size_t)S.ldg * S.g_n;
+  const size_t bytes = sizeof(double2) * g_elems(S);
   if (S.G0.n < bytes / sizeof(double2)) {
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = mem_available(c->device);
     if (free_b < bytes + (4ull << 30)) {
       S.g0_valid = false;
       return;
@@ -1899,8 +2126,7 @@ void snapshot_base(radmm_ctx* c, Sensor& S, bool modify) {
     if (!S.Cp0.own) S.Cp0.release();
     bool ok = S.Cp0.n >= cn;
     if (!ok) {
-      size_t free_b = 0, total_b = 0;
-      CK(cudaMemGetInfo(&free_b, &total_b));
+      const size_t free_b = mem_available(c->device);
       if (free_b >= cn * sizeof(double2) + (4ull << 30)) {
         S.Cp0.alloc(cn, false);
         ok = true;
@@ -1913,6 +2139,8 @@ void snapshot_base(radmm_ctx* c, Sensor& S, bool modify) {
   }
   S.g0_valid = true;
   S.g0_primal = S.primal;
+  S.g0_packed = S.gpacked;
+  S.g0_elems = g_elems(S);
   S.g0_mu = S.base_mu;
   S.g0_beta = S.base_beta;
   S.g0_ld = S.ldg;
@@ -1999,6 +2227,8 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, S.data_lag ? S.bz.p : nullptr, S.v.p, 1.0});
       gq.push_back(q);
       g_bytes += gapply_bytes(S.rows);
+      if (c->refine && S.cp_valid)  // refinement: packed C pass + second G pass
+        g_bytes += 16.0 * cap_tiles(S.rows) * kHermTile * kHermTile + gapply_bytes(S.rows);
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = S.n_act; a.cols = S.J.p; a.pix = S.J.p;
       a.vec = S.w.p; a.rhs = S.rhs.p; a.x_hat = S.x_hat.p; a.x_full = S.x_full.p; a.ring_slot = ring_slot;
@@ -2898,12 +3128,14 @@ void share_factor(radmm_ctx* dst, radmm_ctx* src, double mu, double beta) {
     Sensor& S = src->sensors[q];
     if (S.g_is_base && S.base_mu == mu && S.base_beta == beta) snapshot_base(src, S, false);
     if (!S.g0_valid || S.g0_mu != mu || S.g0_beta != beta) continue;
-    if (D.g0_valid && D.g0_mu == mu && D.g0_beta == beta) continue;
+    if (D.g0_valid && D.g0_mu == mu && D.g0_beta == beta && D.g0_packed == S.g0_packed) continue;
     D.G0.view(S.G0.p, S.G0.n);
     D.cp0_valid = S.cp0_valid;
     if (S.cp0_valid) D.Cp0.view(S.Cp0.p, S.Cp0.n);
     D.g0_valid = true;
     D.g0_primal = S.g0_primal;
+    D.g0_packed = S.g0_packed;
+    D.g0_elems = S.g0_elems;
     D.g0_mu = mu;
     D.g0_beta = beta;
     D.g0_ld = S.g0_ld;
@@ -3009,11 +3241,26 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
     PhaseScope ps(p, RADMM_PHASE_FORWARD, 8.0 * ld_max * N * Q);
     run_pass(FB_FWD, sp_fwd);
   }
-  // W = G V on the shared factor
+  // W = G V on the shared factor (a packed factor is unpacked once per run
+  // into a full matrix for the DMMA pass)
+  if (p->fb_g.size() < (size_t)Q) p->fb_g.resize(Q);
+  const bool fb_g_fresh = !(p->fb_g_ok && p->fb_g_mu == mu && p->fb_g_beta == beta);
+  for (int q = 0; q < Q; ++q) {
+    const Sensor& H = fs[0]->sensors[q];
+    if (!H.gpacked || !fb_g_fresh) continue;
+    DArr<double2>& Gf = p->fb_g[q];
+    if (Gf.n < (size_t)H.ld * H.rows) Gf.alloc((size_t)H.ld * H.rows, false);
+    LAUNCH(p, cap_unpack_kernel, dim3((unsigned)cap_tiles(H.rows)), 256, 0, H.G.p, H.rows, Gf.p, H.ld);
+  }
+  p->fb_g_ok = true;
+  p->fb_g_mu = mu;
+  p->fb_g_beta = beta;
+  auto g_full = [&](int q) -> const double2* { return fs[0]->sensors[q].gpacked ? p->fb_g[q].p : fs[0]->sensors[q].G.p; };
+  auto g_ld = [&](int q) -> int64_t { return fs[0]->sensors[q].gpacked ? fs[0]->sensors[q].ld : fs[0]->sensors[q].ldg; };
   for (int q = 0; q < Q; ++q) {
     const Sensor& H = fs[0]->sensors[q];
     FrameBatchJob& j = jobs[q];
-    j.A = H.G.p; j.lda = H.ldg; j.m = H.rows; j.k = H.rows;
+    j.A = g_full(q); j.lda = g_ld(q); j.m = H.rows; j.k = H.rows;
     FrameReduceJob& r = red[q];
     r.nsplit = sp_gap;
     for (int f = 0; f < nf; ++f) {
@@ -3034,9 +3281,9 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
       for (int q = 0; q < Q; ++q) {
         const Sensor& H = fs[0]->sensors[q];
         DArr<double2>& Cf = p->fb_cap[q];
-        if (!p->fb_cap_ok || p->fb_cap_mu != mu || p->fb_cap_beta != beta || Cf.n < (size_t)H.ldg * H.rows) {
-          if (Cf.n < (size_t)H.ldg * H.rows) Cf.alloc((size_t)H.ldg * H.rows, false);
-          LAUNCH(p, cap_unpack_kernel, dim3((unsigned)cap_tiles(H.rows)), 256, 0, H.Cp.p, H.rows, Cf.p, H.ldg);
+        if (!p->fb_cap_ok || p->fb_cap_mu != mu || p->fb_cap_beta != beta || Cf.n < (size_t)H.ld * H.rows) {
+          if (Cf.n < (size_t)H.ld * H.rows) Cf.alloc((size_t)H.ld * H.rows, false);
+          LAUNCH(p, cap_unpack_kernel, dim3((unsigned)cap_tiles(H.rows)), 256, 0, H.Cp.p, H.rows, Cf.p, H.ld);
         }
       }
       p->fb_cap_ok = true;
@@ -3045,6 +3292,7 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
       for (int q = 0; q < Q; ++q) {  // R = V - C W  (into rho)
         FrameBatchJob& j = jobs[q];
         j.A = p->fb_cap[q].p;
+        j.lda = fs[0]->sensors[q].ld;
         FrameReduceJob& r = red[q];
         for (int f = 0; f < nf; ++f) {
           j.B[f] = fs[f]->sensors[q].w.p;
@@ -3056,9 +3304,9 @@ void frame_batch_updates(radmm_ctx* p, const std::vector<radmm_ctx*>& fs, double
       }
       run_pass(FB_GAP, sp_gap);
       for (int q = 0; q < Q; ++q) {  // W = W + G R
-        const Sensor& H = fs[0]->sensors[q];
         FrameBatchJob& j = jobs[q];
-        j.A = H.G.p;
+        j.A = g_full(q);
+        j.lda = g_ld(q);
         FrameReduceJob& r = red[q];
         for (int f = 0; f < nf; ++f) {
           j.B[f] = fs[f]->sensors[q].rho.p;
@@ -3117,6 +3365,7 @@ void run_frames(radmm_ctx* p, int F, const radmm_hyperparams* hs, const radmm_ru
   }
   std::vector<radmm_run_summary> sm(F);
   p->fb_cap_ok = false;
+  p->fb_g_ok = false;
   p->marks.clear();
   p->ev_used = 0;
   for (int i = 0; i < RADMM_PHASE_COUNT; ++i) {  // parent stats = this call's batched passes
@@ -3322,6 +3571,40 @@ int radmm_ctx_destroy(radmm_ctx* ctx) {
 void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
   if (c->parent || S.rows >= c->N || !env_int("RADMM_EAGER_GRAM", 1) || !env_int("RADMM_GRAM", 1)) return;
   if (ev) CK(cudaStreamWaitEvent(c->stream, ev, 0));
+  if (use_gpacked(c, S)) {
+    // packed factor: the raw Gram goes through one full temporary into Cp
+    // (rebuild_packed unpacks and scales it)
+    const size_t cn = cap_tiles(S.rows) * kHermTile * kHermTile;
+    const size_t free_b = mem_available(c->device);
+    const size_t tmp = (size_t)S.ld * S.rows;
+    const size_t held = c->gtmp.empty() ? 0 : c->gtmp[0].n;
+    if (free_b + held * sizeof(double2) < (tmp + (S.Cp.n < cn ? cn : 0)) * sizeof(double2) + (6ull << 30)) return;
+    if (S.Cp.n < cn) S.Cp.alloc(cn, false);
+    gtmp_reserve(c, 1, tmp);
+    double2* T = c->gtmp[0].p;
+    CK(cudaMemsetAsync(T, 0, sizeof(double2) * tmp, c->stream));
+    if (ozaki_gram(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0)) {
+      release_ozaki_scratch(c);
+    } else {
+      const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, T, S.ld};
+      set_smem_attr((const void*)gram_dmma1_kernel, (int)((int)kGramSmem));
+      LAUNCH(c, gram_dmma1_kernel,
+             dim3((unsigned)((S.rows + kGrBN - 1) / kGrBN), (unsigned)((S.rows + kGrBM - 1) / kGrBM), 1u), 256,
+             kGramSmem, g, 1.0, 0.0);
+    }
+    LAUNCH(c, cap_pack_kernel, dim3((unsigned)cap_tiles(S.rows)), 256, 0, T, S.ld, S.rows, S.Cp.p);
+    S.cp_valid = true;  // raw A A^H (raw_gram) until the first run scales it
+    S.raw_gram = true;
+    S.raw_packed = true;
+    S.primal = false;
+    if (c->gram_evs.size() < (size_t)c->Q) c->gram_evs.resize(c->Q, nullptr);
+    if (!c->gram_evs[q]) CK(cudaEventCreateWithFlags(&c->gram_evs[q], cudaEventDisableTiming));
+    CK(cudaEventRecord(c->gram_evs[q], c->stream));
+    return;
+  }
+  if (S.gpacked) S.G.release();
+  S.gpacked = false;
+  S.raw_packed = false;
   ensure_g(S, S.rows, S.ld);
   S.ldg = S.ld;
   S.g_n = S.rows;

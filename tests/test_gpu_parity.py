@@ -376,7 +376,7 @@ def test_device_generator_matches_host():
         dev = s.get_operator(q)
         host = scenario.baseline_operator(cfg, q)
         # portable sincos (IEEE basic ops only): bitwise, not "within ulps"
-        assert np.array_equal(dev.view(np.uint32), host.view(np.uint32))
+        assert np.array_equal(np.ascontiguousarray(dev).view(np.uint32), np.ascontiguousarray(host).view(np.uint32))
     s.close()
 
 
