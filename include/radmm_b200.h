@@ -247,6 +247,12 @@ typedef struct {
   double bytes;      /* algorithmic bytes moved */
 } radmm_phase_stat;
 
+/* Page-locked host memory for operator buffers (cudaHostAlloc, portable):
+ * what a caller stages large problems in so the uploads run at PCIe/C2C
+ * speed (config 3: 137 GB of operators).  Not part of the reference API. */
+int radmm_host_alloc(size_t bytes, void** out);
+int radmm_host_free(void* p);
+
 int radmm_set_profiling(radmm_ctx* ctx, int enabled);
 /* out[RADMM_PHASE_COUNT], accumulated over the last run. */
 int radmm_get_phase_stats(radmm_ctx* ctx, radmm_phase_stat* out);

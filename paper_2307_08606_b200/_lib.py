@@ -124,6 +124,8 @@ SIGNATURES = {
     "radmm_apply_operator": (C.c_int, [_VP, C.c_int, _DP, _DP]),
     "radmm_apply_adjoint": (C.c_int, [_VP, C.c_int, _DP, _DP]),
     "radmm_back_projection": (C.c_int, [_VP, _DP]),
+    "radmm_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_VP)]),
+    "radmm_host_free": (C.c_int, [_VP]),
     "radmm_set_profiling": (C.c_int, [_VP, C.c_int]),
     "radmm_get_phase_stats": (C.c_int, [_VP, C.POINTER(PhaseStat)]),
     "radmm_get_iteration_stats": (C.c_int, [_VP, _DP, C.POINTER(C.c_int64), C.c_int]),

@@ -295,8 +295,15 @@ class Solver:
     def get_operator(self, q: int) -> np.ndarray:
         rows = self.rows[q]
         out = np.empty((self.N, rows), dtype=np.complex64)  # column-major rows x N
+        return self.get_operator_into(q, out).T
+
+    def get_operator_into(self, q: int, out: np.ndarray) -> np.ndarray:
+        """Copy sensor q's device operator into ``out`` (N x rows C-contiguous
+        complex64, i.e. the rows x N column-major matrix), e.g. a PinnedBuffer."""
+        if out.shape != (self.N, self.rows[q]) or out.dtype != np.complex64 or not out.flags.c_contiguous:
+            raise ValueError("get_operator_into: need an (N, rows) C-contiguous complex64 buffer")
         _lib.check(_lib.lib().radmm_get_operator_c64(self._h, q, out.ctypes.data_as(C.c_void_p)))
-        return out.T
+        return out
 
     def apply(self, q: int, x) -> np.ndarray:
         """ForwardOperator::apply (forward_model.hpp:147-160) on the GPU."""
@@ -464,6 +471,33 @@ class Solver:
         log = np.empty(max(1, 3 * m.value), dtype=np.int32)
         _lib.check(L.radmm_get_removal_log(self._h, log.ctypes.data_as(C.POINTER(C.c_int32)), m.value))
         res.removal_log = log[:3 * m.value].reshape(m.value, 3)
+
+
+class PinnedBuffer:
+    """Page-locked host memory (radmm_host_alloc) viewed as a NumPy array --
+    where callers stage large operators so uploads run at full host-link
+    speed.  ``free()`` (or garbage collection) releases it."""
+
+    def __init__(self, shape, dtype=np.complex64):
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * dtype.itemsize
+        p = C.c_void_p()
+        _lib.check(_lib.lib().radmm_host_alloc(n, C.byref(p)))
+        self._p = p
+        buf = (C.c_char * n).from_address(p.value) if n else bytearray()
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def free(self) -> None:
+        if getattr(self, "_p", None) is not None and self._p.value:
+            self.array = None
+            _lib.check(_lib.lib().radmm_host_free(self._p))
+        self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def run(problem: Problem, hyper: Hyperparams, mode: Mode = Mode.ASADMM, observer=None,

@@ -4054,6 +4054,27 @@ int radmm_get_iteration_stats(radmm_ctx* ctx, double* device_ms, int64_t* launch
   });
 }
 
+int radmm_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (bytes == 0) return;
+    void* p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(RADMM_OUT_OF_MEMORY, std::string("radmm_host_alloc: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+  });
+}
+
+int radmm_host_free(void* p) {
+  return guarded([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
 int radmm_nccl_unique_id(uint8_t out[128]) {
   return guarded([&] {
     if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");

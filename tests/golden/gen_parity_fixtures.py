@@ -9,10 +9,10 @@ bit-identical on both sides: the operators come from the portable generator
 SHA-256 of every sensor's complex64 operator is stored and checked on the GPU
 box), and the measurements y and lambda are stored in the fixture.
 
-    python tests/golden/gen_parity_fixtures.py [c2_fixed c2_ttt c4_masks c3_q2 c5_frames]
+    python tests/golden/gen_parity_fixtures.py [c2_fixed c2_ttt c4_masks c3_q2 c5_frames lambdas]
 
-Cost here (8 cores): c2_fixed ~1 min, c2_ttt ~4 min, c4_masks ~5 min,
-c3_q2 ~8 min, c5_frames ~3 min.
+Cost here (8 cores): c2_fixed ~2 min, c2_ttt ~23 min, c4_masks ~5 min,
+c3_q2 ~10 min, c5_frames ~5 min, lambdas ~5 min.
 """
 from __future__ import annotations
 
@@ -40,8 +40,9 @@ def op_digest(a64: np.ndarray) -> str:
 
 def problem(cfg, q_count=None):
     """Host operators (portable generator), seeded scene, measurements, lambda."""
+    from oracle import gen  # the C host generator: bitwise scenario.baseline_operator, ~100x faster
     q_count = q_count or cfg.Q
-    ops = [scenario.baseline_operator(cfg, q) for q in range(q_count)]
+    ops = [gen.baseline_operator(cfg, q) for q in range(q_count)]
     per_sensor = scenario.baseline_scene(cfg)[:q_count]
     ys = scenario.baseline_measurements(cfg, ops, per_sensor)
     lam = scenario.baseline_lambda(cfg, ops, ys)
@@ -178,6 +179,27 @@ def gen_c5_frames(frames=(1, 2), iters=100):
         out[f"f{f}_sigma"] = o.sigma
     save("c5_frames", digests=np.array([op_digest(a) for a in ops]), frames=np.array(frames),
          iters=np.int64(iters), **out)
+
+
+def gen_lambdas():
+    """lambda = 0.05 max_q |A_q^H y_q|_inf of every BASELINE config (host
+    generator): the reference arm of bench.py prints the same lambda as the
+    GPU arm without regenerating all 32 config-3 operators (~2 min)."""
+    import json
+    from oracle import gen
+    out = {}
+    for name in ("c1", "c2", "c3", "c4_sparse", "c4_dense"):
+        cfg = scenario.baseline_config(name)
+        per_sensor = scenario.baseline_scene(cfg)
+        m = 0.0
+        for q in range(cfg.Q):
+            a = gen.baseline_operator(cfg, q)
+            y = scenario.simulate_measurement(a, per_sensor[q], cfg.snr_db, scenario.mix_seed(cfg.seed, q + 1))[0]
+            m = max(m, float(np.abs(a.conj().T @ y).max()))
+        out[name] = cfg.lambda_frac * m
+        print(name, out[name], flush=True)
+    with open(os.path.join(HERE, "baseline_lambdas.json"), "w") as f:
+        json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
