@@ -160,6 +160,15 @@ int radmm_set_measurement(radmm_ctx* ctx, int q, const double* y, int ptr_kind);
 int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const double* pix,
                                     const double* tx, const double* rx, const double* phi,
                                     double fc, double bw, double pulse);
+/* Device assembly of the reference's own operator, EchoKernel::entry +
+ * ForwardOperator::dense (forward_model.hpp:32-114): row m*K + k, pixel n,
+ *   tau = (|tx - p_n| + |rx_m - p_n|)/c,  t = k/fs - tau,
+ *   a = exp(j(-2 pi fc tau + pi alpha t^2)) for 0 <= t <= T, else 0,
+ * stored as complex64.  pix: N x 3, rx: M x 3, tx: 3 (host arrays); K from
+ * the reference's derive_sample_count (host side). */
+int radmm_generate_echo_operator(radmm_ctx* ctx, int q, int M, int K, const double* pix, const double* tx,
+                                 const double* rx, double fc, double sample_rate, double chirp_rate,
+                                 double pulse_duration);
 /* Copy a sensor's device operator back (complex64, column-major, ld = rows). */
 int radmm_get_operator_c64(radmm_ctx* ctx, int q, float* out);
 
@@ -263,6 +272,11 @@ int radmm_get_iteration_stats(radmm_ctx* ctx, double* device_ms, int64_t* launch
 /* ---- sharded runs over NCCL (runtime.hpp:768-775 analogue) ------------- */
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
 int radmm_nccl_unique_id(uint8_t out[128]);
+/* Transport timeout of a sharded context (default 60000 ms; env
+ * RADMM_NCCL_TIMEOUT_MS at creation): a collective or iteration that does not
+ * complete in time aborts the communicator and returns RADMM_TRANSPORT -- the
+ * reference's tcp_timeout_ms / TransportError (runtime.hpp:540-545,739-775). */
+int radmm_set_transport_timeout(radmm_ctx* ctx, int timeout_ms);
 int radmm_ctx_create_sharded(int device, int n_pixels, int q_total, int q_begin, int q_end,
                              int rank, int world_size, const uint8_t nccl_id[128],
                              radmm_ctx** out);

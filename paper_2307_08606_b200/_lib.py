@@ -103,6 +103,8 @@ SIGNATURES = {
     "radmm_set_measurement": (C.c_int, [_VP, C.c_int, _VP, C.c_int]),
     "radmm_generate_dechirp_operator": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _DP, _DP, _DP, _DP,
                                                   C.c_double, C.c_double, C.c_double]),
+    "radmm_generate_echo_operator": (C.c_int, [_VP, C.c_int, C.c_int, C.c_int, _DP, _DP, _DP, C.c_double,
+                                               C.c_double, C.c_double, C.c_double]),
     "radmm_get_operator_c64": (C.c_int, [_VP, C.c_int, _VP]),
     "radmm_run": (C.c_int, [_VP, C.POINTER(Hyper), C.POINTER(Options), C.POINTER(Summary)]),
     "radmm_set_frame_measurement": (C.c_int, [_VP, C.c_int, C.c_int, _VP, C.c_int]),
@@ -130,6 +132,7 @@ SIGNATURES = {
     "radmm_get_phase_stats": (C.c_int, [_VP, C.POINTER(PhaseStat)]),
     "radmm_get_iteration_stats": (C.c_int, [_VP, _DP, C.POINTER(C.c_int64), C.c_int]),
     "radmm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "radmm_set_transport_timeout": (C.c_int, [_VP, C.c_int]),
     "radmm_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(C.c_uint8), C.POINTER(_VP)]),
 }

@@ -292,6 +292,22 @@ class Solver:
                                                               _dptr(rx), _dptr(phi), fc, bw, pulse))
         self.rows[q] = M * K
 
+    def generate_echo_operator(self, q: int, grid, sensor, waveform, k_samples: int | None = None) -> None:
+        """ForwardOperator::dense(EchoKernel(grid, sensor, waveform))
+        (forward_model.hpp:32-114) assembled on the device (complex64).
+        ``grid``/``sensor``/``waveform``: scenario.SceneGrid / SensorArray /
+        Waveform; K defaults to the reference's derive_sample_count."""
+        from . import scenario as _sc
+        k = int(k_samples) if k_samples is not None else _sc.derive_sample_count(grid, sensor, waveform)
+        pix = np.ascontiguousarray(grid.centers(), dtype=np.float64)
+        tx = np.ascontiguousarray(sensor.tx_position, dtype=np.float64)
+        rx = np.ascontiguousarray(np.asarray(sensor.rx_positions, dtype=np.float64).reshape(-1, 3))
+        M = rx.shape[0]
+        _lib.check(_lib.lib().radmm_generate_echo_operator(self._h, q, M, k, _dptr(pix), _dptr(tx), _dptr(rx),
+                                                           waveform.fc, waveform.sample_rate, waveform.chirp_rate,
+                                                           waveform.pulse_duration))
+        self.rows[q] = M * k
+
     def get_operator(self, q: int) -> np.ndarray:
         rows = self.rows[q]
         out = np.empty((self.N, rows), dtype=np.complex64)  # column-major rows x N

@@ -898,4 +898,44 @@ __global__ void dechirp_kernel(float2* __restrict__ A, int64_t ld, int M, int K,
   A[r + (int64_t)n * ld] = make_float2(__double2float_rn(c), __double2float_rn(s));
 }
 
+// The reference's own operator on the device: EchoKernel::entry
+// (forward_model.hpp:64-71) assembled densely like ForwardOperator::dense
+// (:91-114), row r = m K + k.  The delay and phase are the reference's
+// expression evaluated operation by operation (no FMA contraction, the same
+// order as scenario.echo_operator):
+//   tau   = (|tx - p_n| + |rx_m - p_n|) / c
+//   t     = k / fs - tau;  zero outside [0, T]
+//   phase = ((-2 pi) fc) tau + ((pi alpha) t) t
+// then std::polar(1, phase) -> CUDA's fp64 sincos (full range reduction),
+// stored as complex64.  Entries equal the host generator's to within one
+// fp32 rounding (tests/test_gpu_parity.py::test_device_echo_operator_*).
+__global__ void echo_kernel(float2* __restrict__ A, int64_t ld, int M, int K, int N,
+                            const double* __restrict__ pix, const double* __restrict__ tx,
+                            const double* __restrict__ rx, double fc, double fs, double alpha, double T,
+                            double c_light, double pi) {
+  pdl_enter();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = M * K;
+  if (e >= (int64_t)rows * N) return;
+  const int r = (int)(e % rows);
+  const int n = (int)(e / rows);
+  const int m = r / K, k = r % K;
+  const double px = pix[3 * n], py = pix[3 * n + 1], pz = pix[3 * n + 2];
+  double dx = __dsub_rn(tx[0], px), dy = __dsub_rn(tx[1], py), dz = __dsub_rn(tx[2], pz);
+  const double dtx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  dx = __dsub_rn(rx[3 * m], px); dy = __dsub_rn(rx[3 * m + 1], py); dz = __dsub_rn(rx[3 * m + 2], pz);
+  const double drx = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  const double tau = __ddiv_rn(__dadd_rn(dtx, drx), c_light);
+  const double t = __dsub_rn(__ddiv_rn((double)k, fs), tau);
+  float2 out = make_float2(0.f, 0.f);
+  if (!(t < 0.0 || t > T)) {
+    const double carrier = __dmul_rn(__dmul_rn(-2.0 * pi, fc), tau);
+    const double chirp = __dmul_rn(__dmul_rn(__dmul_rn(pi, alpha), t), t);
+    double s, c;
+    sincos(__dadd_rn(carrier, chirp), &s, &c);
+    out = make_float2(__double2float_rn(c), __double2float_rn(s));
+  }
+  A[r + (int64_t)n * ld] = out;
+}
+
 }  // namespace radmm_dev

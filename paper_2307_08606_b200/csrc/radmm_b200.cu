@@ -15,8 +15,10 @@
 
 #include <algorithm>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -129,12 +131,30 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 // ---------------------------------------------------------------------------
 typedef struct { char internal[128]; } nccl_uid;
 typedef void* nccl_comm;
+// ncclConfig_t as of NCCL 2.27 (versioned by size/version: newer libraries
+// accept it); only `blocking` is set -- a non-blocking communicator, so the
+// host can poll ncclCommGetAsyncError and enforce a timeout instead of
+// hanging in a collective when a peer dies (runtime.hpp:540-545, 739-760).
+struct nccl_config {
+  size_t size;
+  unsigned int magic;
+  unsigned int version;
+  int blocking, cgaClusterSize, minCTAs, maxCTAs;
+  const char* netName;
+  int splitShare, trafficClass;
+  const char* commName;
+  int collnetEnable, CTAPolicy, shrinkShare, nvlsCTAs;
+};
+constexpr int kNcclInProgress = 7;
 struct Nccl {
   void* h = nullptr;
   int (*GetUniqueId)(nccl_uid*) = nullptr;
   int (*CommInitRank)(nccl_comm*, int, nccl_uid, int) = nullptr;
+  int (*CommInitRankConfig)(nccl_comm*, int, nccl_uid, int, nccl_config*) = nullptr;
   int (*AllGather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t) = nullptr;
   int (*CommDestroy)(nccl_comm) = nullptr;
+  int (*CommAbort)(nccl_comm) = nullptr;
+  int (*GetAsyncError)(nccl_comm, int*) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   void load() {
     if (h) return;
@@ -148,14 +168,41 @@ struct Nccl {
     CommInitRank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
     AllGather = (int (*)(const void*, void*, size_t, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllGather");
     CommDestroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+    CommInitRankConfig = (int (*)(nccl_comm*, int, nccl_uid, int, nccl_config*))dlsym(h, "ncclCommInitRankConfig");
+    CommAbort = (int (*)(nccl_comm))dlsym(h, "ncclCommAbort");
+    GetAsyncError = (int (*)(nccl_comm, int*))dlsym(h, "ncclCommGetAsyncError");
     GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
     if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy)
       fail(RADMM_TRANSPORT, "libnccl is missing required symbols");
   }
   void check(int r, const char* what) {
-    if (r != 0)
+    if (r != 0 && r != kNcclInProgress)
       fail(RADMM_TRANSPORT, std::string("NCCL error in ") + what + ": " +
                                 (GetErrorString ? GetErrorString(r) : std::to_string(r)));
+  }
+  // Wait until a non-blocking communicator leaves ncclInProgress (after init
+  // or an enqueue); abort it and raise RADMM_TRANSPORT on an error or after
+  // timeout_ms -- the reference's TransportError / receive timeout.
+  void settle(nccl_comm comm, const char* what, int timeout_ms) {
+    if (!GetAsyncError) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      int st = 0;
+      const int r = GetAsyncError(comm, &st);
+      if (r != 0) st = r;
+      if (st == 0) return;
+      if (st != kNcclInProgress) {
+        if (CommAbort) CommAbort(comm);
+        fail(RADMM_TRANSPORT, std::string("NCCL error in ") + what + ": " +
+                                  (GetErrorString ? GetErrorString(st) : std::to_string(st)));
+      }
+      if (std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() > timeout_ms) {
+        if (CommAbort) CommAbort(comm);
+        fail(RADMM_TRANSPORT, std::string("NCCL timeout in ") + what + " after " + std::to_string(timeout_ms) +
+                                  " ms (a peer is gone or stalled)");
+      }
+      std::this_thread::yield();
+    }
   }
 };
 Nccl g_nccl;
@@ -331,6 +378,11 @@ struct radmm_ctx {
   nccl_comm comm = nullptr;
   DArr<double2> send_buf, gathered;
   DArr<double> size_send, size_recv;
+  int nccl_timeout_ms = 60000;     // transport timeout (radmm_set_transport_timeout)
+  bool sync_meta = false;          // observer runs: per-iteration metadata all-gather (else once at run end)
+  double* meta_host = nullptr;     // pinned, 2 slots of (2 q_max_local + 1) doubles (sync_meta)
+  size_t meta_bytes = 0;
+  std::vector<double> shard_meta;  // per completed iteration: local n_act, stalled flags, notice bytes
   // results of the last run
   std::vector<radmm_iteration_record> records;
   std::vector<int32_t> active_log;
@@ -424,6 +476,7 @@ struct radmm_ctx {
     for (cudaEvent_t e : ev_ends) cudaEventDestroy(e);
     mark("events");
     if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+    if (meta_host) pinned_put(reinterpret_cast<char*>(meta_host), meta_bytes);
     pinned_put(pinned_block, pinned_bytes);  // fs_host / h_totals / h_flags live in it
     mark("host");
     if (stream && own_stream) cudaStreamDestroy(stream);
@@ -2275,27 +2328,69 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
   ++c->upd;
 }
 
-// Sharded runs: every rank receives every sensor image (fixed global order),
-// plus per-sensor active sizes / stalled flags and the rank's notice bytes.
-void exchange(radmm_ctx* c, double notice_bytes) {
+// Sharded runs: every rank receives every sensor image (fixed global order)
+// in ONE all-gather per iteration; the per-sensor active sizes, stall flags
+// and notice bytes (records only) are gathered once at the end of the run
+// (finish_sharded_records) -- or per iteration when an observer needs them.
+// Images travel as complex128: s is a near-cancelling mean of the images in
+// the degenerate BASELINE problems, so rounding them to
+// complex64 would cost s its parity with the oracle.
+void exchange(radmm_ctx* c, double notice_bytes, int k) {
   if (!c->sharded) return;
   const size_t N = c->N;
   PhaseScope ps(c, RADMM_PHASE_EXCHANGE, 16.0 * N * c->q_max_local * c->world);
   for (int q = 0; q < c->Q; ++q)
     CK(cudaMemcpyAsync(c->send_buf.p + (size_t)q * N, c->sensors[q].x_full.p, sizeof(double2) * N,
                        cudaMemcpyDeviceToDevice, c->stream));
-  std::vector<double> meta(2 * c->q_max_local + 1, 0.0);
+  g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble, c->comm,
+                                c->stream), "ncclAllGather(contributions)");
+  g_nccl.settle(c->comm, "ncclAllGather(contributions)", c->nccl_timeout_ms);
+  ++c->launches;
+  if (!c->sync_meta) return;
+  const size_t stride = 2 * (size_t)c->q_max_local + 1;
+  double* meta = c->meta_host + (size_t)(k & 1) * stride;  // two slots: the copy of round k-1 may be in flight
+  std::fill(meta, meta + stride, 0.0);
   for (int q = 0; q < c->Q; ++q) {
     meta[2 * q] = c->sensors[q].n_act;
     meta[2 * q + 1] = c->sensors[q].stalled ? 1.0 : 0.0;
   }
   meta[2 * c->q_max_local] = notice_bytes;
-  CK(cudaMemcpyAsync(c->size_send.p, meta.data(), sizeof(double) * meta.size(), cudaMemcpyHostToDevice, c->stream));
-  g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble, c->comm,
-                                c->stream), "ncclAllGather(contributions)");
-  g_nccl.check(g_nccl.AllGather(c->size_send.p, c->size_recv.p, meta.size(), kNcclDouble, c->comm, c->stream),
+  CK(cudaMemcpyAsync(c->size_send.p, meta, sizeof(double) * stride, cudaMemcpyHostToDevice, c->stream));
+  g_nccl.check(g_nccl.AllGather(c->size_send.p, c->size_recv.p, stride, kNcclDouble, c->comm, c->stream),
                "ncclAllGather(meta)");
-  c->launches += 2;
+  g_nccl.settle(c->comm, "ncclAllGather(meta)", c->nccl_timeout_ms);
+  ++c->launches;
+}
+
+// Wait for a round's completion event; in sharded runs poll the NCCL
+// communicator meanwhile, so a failed or vanished peer surfaces as
+// RADMM_TRANSPORT within the timeout instead of a hang.
+void wait_round(radmm_ctx* c, cudaEvent_t e) {
+  if (!c->sharded || !g_nccl.GetAsyncError) {
+    CK(cudaEventSynchronize(e));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t r = cudaEventQuery(e);
+    if (r == cudaSuccess) return;
+    if (r != cudaErrorNotReady) CK(r);
+    int st = 0;
+    if (g_nccl.GetAsyncError(c->comm, &st) != 0 || (st != 0 && st != kNcclInProgress)) {
+      if (g_nccl.CommAbort) g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      fail(RADMM_TRANSPORT, std::string("NCCL asynchronous error during the iteration: ") +
+                                (g_nccl.GetErrorString ? g_nccl.GetErrorString(st) : std::to_string(st)));
+    }
+    if (std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() >
+        c->nccl_timeout_ms) {
+      if (g_nccl.CommAbort) g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      fail(RADMM_TRANSPORT, "iteration did not complete within " + std::to_string(c->nccl_timeout_ms) +
+                                " ms (a peer rank is gone or stalled)");
+    }
+    std::this_thread::yield();
+  }
 }
 
 FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k);
@@ -2812,10 +2907,28 @@ void record_round(radmm_ctx* c, int k, const FusionScalars& f, uint64_t notice, 
       sizes[q] = c->sensors[q].n_act;
       stalled_any = stalled_any || c->sensors[q].stalled;
     }
+  } else if (!c->sync_meta) {
+    // local view now (rank-local sensors), the global records at the end of
+    // the run (finish_sharded_records): no per-iteration host round trip
+    const size_t stride = 2 * (size_t)c->q_max_local + 1;
+    const size_t base = c->shard_meta.size();
+    c->shard_meta.resize(base + stride, 0.0);
+    for (int q = 0; q < c->Q; ++q) {
+      c->shard_meta[base + 2 * q] = c->sensors[q].n_act;
+      c->shard_meta[base + 2 * q + 1] = c->sensors[q].stalled ? 1.0 : 0.0;
+    }
+    c->shard_meta[base + 2 * c->q_max_local] = (double)notice;
+    rec.bytes_sent = notice;
+    rec.ms_elapsed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+    c->records.push_back(rec);
+    return;
   } else {
+    // observer runs: this round's metadata all-gather completed with END(k)
     const int stride = 2 * c->q_max_local + 1;
     meta_all.resize((size_t)stride * c->world);
-    CK(cudaMemcpy(meta_all.data(), c->size_recv.p, sizeof(double) * meta_all.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(meta_all.data(), c->size_recv.p, sizeof(double) * meta_all.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     bytes = 0;
     for (int r = 0; r < c->world; ++r) {
       const int begin = (int)((int64_t)r * c->Q_total / c->world);
@@ -2840,6 +2953,51 @@ void record_round(radmm_ctx* c, int k, const FusionScalars& f, uint64_t notice, 
   rec.ms_elapsed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
   sm.total_bytes += bytes;
   c->records.push_back(rec);
+  sm.screening_stalled = stalled_any ? 1 : 0;
+}
+
+// Sharded runs without an observer: one all-gather of every rank's
+// per-iteration metadata at the end of the run, then the records' global
+// fields (admm.hpp:397-420) exactly as the per-iteration path computes them.
+void finish_sharded_records(radmm_ctx* c, radmm_run_summary& sm) {
+  if (!c->sharded || c->sync_meta) return;
+  const size_t stride = 2 * (size_t)c->q_max_local + 1, K = c->records.size();
+  if (K == 0) return;
+  DArr<double> dsend, drecv;
+  dsend.alloc(K * stride, false);
+  drecv.alloc(K * stride * c->world, false);
+  CK(cudaMemcpyAsync(dsend.p, c->shard_meta.data(), sizeof(double) * K * stride, cudaMemcpyHostToDevice, c->stream));
+  g_nccl.check(g_nccl.AllGather(dsend.p, drecv.p, K * stride, kNcclDouble, c->comm, c->stream),
+               "ncclAllGather(records)");
+  g_nccl.settle(c->comm, "ncclAllGather(records)", c->nccl_timeout_ms);
+  std::vector<double> all(K * stride * c->world);
+  CK(cudaMemcpyAsync(all.data(), drecv.p, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->active_log.clear();
+  sm.total_active_solves = 0;
+  sm.total_bytes = 0;
+  bool stalled_any = false;
+  for (size_t k = 0; k < K; ++k) {
+    uint64_t bytes = 0;
+    int max_active = 0;
+    for (int r = 0; r < c->world; ++r) {
+      const double* m = all.data() + ((size_t)r * K + k) * stride;
+      const int begin = (int)((int64_t)r * c->Q_total / c->world);
+      const int end = (int)((int64_t)(r + 1) * c->Q_total / c->world);
+      bytes += (uint64_t)m[2 * c->q_max_local];
+      for (int g = begin; g < end; ++g) {
+        const int32_t sz = (int32_t)m[2 * (g - begin)];
+        stalled_any = stalled_any || m[2 * (g - begin) + 1] != 0.0;
+        bytes += contribution_size((size_t)sz);
+        max_active = std::max(max_active, (int)sz);
+        sm.total_active_solves += (uint64_t)sz;
+        c->active_log.push_back(sz);
+      }
+    }
+    c->records[k].bytes_sent = bytes;
+    c->records[k].active_fraction = (double)max_active / c->N;
+    sm.total_bytes += bytes;
+  }
   sm.screening_stalled = stalled_any ? 1 : 0;
 }
 
@@ -2932,8 +3090,18 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   // converged, and no screening staged).  Otherwise they exit at entry and
   // the host re-issues k+1 after screening.  Off for observers / profiling /
   // sharded or fused runs.
-  const bool spec = !(o && o->observer) && !c->sharded && !fused_enabled() && !c->profiling &&
-                    env_int("RADMM_SPECULATE", 1) != 0;
+  // Sharded runs speculate too: every host decision below depends only on the
+  // fusion scalars, which are bitwise identical on all ranks, so every rank
+  // issues the same rounds (one all-gather each) -- except the pre-enqueued
+  // screening, whose "did any set change" is rank-local: sharded runs screen
+  // the synchronous way (screen_all) instead.
+  const bool spec = !(o && o->observer) && !fused_enabled() && !c->profiling && env_int("RADMM_SPECULATE", 1) != 0;
+  c->sync_meta = c->sharded && o && o->observer;
+  if (c->sync_meta && !c->meta_host) {
+    c->meta_bytes = pinned_class(2 * sizeof(double) * (2 * (size_t)c->q_max_local + 1));
+    c->meta_host = reinterpret_cast<double*>(pinned_get(c->meta_bytes));
+  }
+  c->shard_meta.clear();
   auto screen_next_possible = [&]() { return (asadmm && !disable && c->upd >= c->W) ? 1 : 0; };
   // issue one round: local updates (+ exchange) + fusion; go == nullptr = unconditional
   // With speculation the next round's screening is enqueued right behind this
@@ -2951,7 +3119,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       fused_iteration(c, h, kk);
     } else {
       local_updates(c, h, go);
-      exchange(c, (double)notice);
+      exchange(c, (double)notice, kk);
       const int snp = screen_next_possible();
       // the guarded screening is enqueued only when the trigger is near: the
       // last observed primal residual within kPreScreenRatio of its
@@ -2960,7 +3128,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       // fire, the speculative round is cancelled and screening runs the
       // synchronous way (screen_all) -- same result.
       const bool near = trigger_seen || last_ratio <= kPreScreenRatio;
-      int* sgo = (spec && snp && near) ? c->sgo_flags.p + (kk & 1) : nullptr;
+      int* sgo = (spec && snp && near && !c->sharded) ? c->sgo_flags.p + (kk & 1) : nullptr;
       run_fusion(c, h, kk, go, go_next, fixed ? 0 : 1, snp, sgo);
       if (sgo) c->pre_screened[kk & 1] = enqueue_screen(c, h, kk & 1, go, sgo, go_next);
     }
@@ -3013,7 +3181,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       CK(cudaEventRecord(STEP(k), c->stream));
       issue(k + 1, c->go_flags.p + ((k + 1) & 1), 0);
     }
-    CK(cudaEventSynchronize(END(k)));
+    wait_round(c, END(k));
     check_deferred(c);             // pivots of a downdate issued before iteration k
     if (k >= 2) step_time(k - 1);  // STEP(k-1) precedes iteration k's kernels: complete
     c->iter_launches.push_back(l_end - l0);
@@ -3062,6 +3230,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
   CK(cudaStreamSynchronize(c->stream));
   check_deferred(c);
   finish_removal_log(c);
+  finish_sharded_records(c, sm);
   if (sm.iterations >= 1) step_time(sm.iterations);
   const auto t2 = std::chrono::steady_clock::now();
   sm.solve_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -3755,6 +3924,28 @@ int radmm_generate_dechirp_operator(radmm_ctx* ctx, int q, int M, int K, const d
   });
 }
 
+int radmm_generate_echo_operator(radmm_ctx* ctx, int q, int M, int K, const double* pix, const double* tx,
+                                 const double* rx, double fc, double sample_rate, double chirp_rate,
+                                 double pulse_duration) {
+  return guarded([&] {
+    Sensor& S = sensor_at(ctx, q);
+    if (M < 1 || K < 1 || !pix || !tx || !rx) fail(RADMM_INVALID_ARGUMENT, "bad generator arguments");
+    if (!(sample_rate > 0.0) || !(pulse_duration > 0.0)) fail(RADMM_INVALID_ARGUMENT, "Waveform: bad parameters");
+    set_device(ctx);
+    prepare_operator(ctx, S, M * K);
+    const int N = ctx->N;
+    DArr<double> dpix, dtx, drx;
+    dpix.alloc(3 * (size_t)N, false); dtx.alloc(3, false); drx.alloc(3 * (size_t)M, false);
+    CK(cudaMemcpyAsync(dpix.p, pix, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(dtx.p, tx, sizeof(double) * 3, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(drx.p, rx, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t total = (int64_t)M * K * N;
+    LAUNCH(ctx, echo_kernel, dim3((unsigned)((total + 255) / 256)), 256, 0, S.A.p, S.ld, M, K, N, dpix.p, dtx.p,
+           drx.p, fc, sample_rate, chirp_rate, pulse_duration, 299792458.0, 3.141592653589793238462643383279502884);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int radmm_get_operator_c64(radmm_ctx* ctx, int q, float* out) {
   return guarded([&] {
     Sensor& S = sensor_at(ctx, q);
@@ -4004,6 +4195,7 @@ int radmm_back_projection(radmm_ctx* ctx, double* image) {
     if (c->sharded) {
       g_nccl.check(g_nccl.AllGather(c->send_buf.p, c->gathered.p, (size_t)c->q_max_local * N * 2, kNcclDouble,
                                     c->comm, c->stream), "ncclAllGather(back_projection)");
+      g_nccl.settle(c->comm, "ncclAllGather(back_projection)", c->nccl_timeout_ms);
       for (int g = 0; g < c->Q_total; ++g) {
         int r = 0;
         while (r + 1 < c->world && (int64_t)(r + 1) * c->Q_total / c->world <= g) ++r;
@@ -4075,6 +4267,14 @@ int radmm_host_free(void* p) {
   });
 }
 
+int radmm_set_transport_timeout(radmm_ctx* ctx, int timeout_ms) {
+  return guarded([&] {
+    if (!ctx) fail(RADMM_INVALID_ARGUMENT, "null context");
+    if (timeout_ms < 1) fail(RADMM_INVALID_ARGUMENT, "transport timeout must be >= 1 ms");
+    ctx->nccl_timeout_ms = timeout_ms;
+  });
+}
+
 int radmm_nccl_unique_id(uint8_t out[128]) {
   return guarded([&] {
     if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
@@ -4090,7 +4290,9 @@ int radmm_ctx_create_sharded(int device, int n_pixels, int q_total, int q_begin,
   return guarded([&] {
     if (!out) fail(RADMM_INVALID_ARGUMENT, "null output");
     if (world_size < 1 || rank < 0 || rank >= world_size) fail(RADMM_INVALID_ARGUMENT, "bad rank / world size");
-    if (q_total < world_size) fail(RADMM_INVALID_ARGUMENT, "fewer sensors than ranks");
+    if (q_total < 1) fail(RADMM_INVALID_ARGUMENT, "Problem: at least one sensor");
+    // Q < G: the ranks past the sensors hold none -- they join the exchange
+    // with empty blocks and run the (redundant) fusion like every rank
     const int b = (int)((int64_t)rank * q_total / world_size);
     const int e = (int)((int64_t)(rank + 1) * q_total / world_size);
     if (q_begin != b || q_end != e)
@@ -4109,7 +4311,15 @@ int radmm_ctx_create_sharded(int device, int n_pixels, int q_total, int q_begin,
       g_nccl.load();
       nccl_uid id;
       std::memcpy(id.internal, nccl_id, 128);
-      g_nccl.check(g_nccl.CommInitRank(&c->comm, world_size, id, rank), "ncclCommInitRank");
+      c->nccl_timeout_ms = std::max(1000, env_int("RADMM_NCCL_TIMEOUT_MS", c->nccl_timeout_ms));
+      if (g_nccl.CommInitRankConfig && g_nccl.GetAsyncError) {
+        nccl_config cfg{sizeof(nccl_config), 0xcafebeef, 22703, 0 /* non-blocking */, INT32_MIN, INT32_MIN,
+                        INT32_MIN, nullptr, INT32_MIN, INT32_MIN, nullptr, INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
+        g_nccl.check(g_nccl.CommInitRankConfig(&c->comm, world_size, id, rank, &cfg), "ncclCommInitRankConfig");
+        g_nccl.settle(c->comm, "ncclCommInitRankConfig", c->nccl_timeout_ms);
+      } else {
+        g_nccl.check(g_nccl.CommInitRank(&c->comm, world_size, id, rank), "ncclCommInitRank");
+      }
       c->send_buf.alloc((size_t)c->q_max_local * n_pixels);
       c->gathered.alloc((size_t)c->q_max_local * n_pixels * world_size);
       c->size_send.alloc(2 * (size_t)c->q_max_local + 1);

@@ -26,8 +26,10 @@ def shard_range(q_total: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous sensor block of ``rank`` (same formula as the C runtime)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank / world size")
-    if q_total < world:
-        raise ValueError("fewer sensors than ranks")
+    if q_total < 1:
+        raise ValueError("Problem: at least one sensor")
+    # Q < G: ranks past the sensors get an empty block (they join the
+    # exchange and the redundant fusion; SURVEY 8e: C1 beyond 4 GPUs)
     return rank * q_total // world, (rank + 1) * q_total // world
 
 
@@ -55,28 +57,33 @@ def broadcast_unique_id(rank: int, world: int) -> bytes | None:
 
 
 def sharded_solver(n_pixels: int, q_total: int, rank: int, world: int, device: int,
-                   uid: bytes | None) -> Solver:
+                   uid: bytes | None, tcp_timeout_ms: int | None = None) -> Solver:
     b, e = shard_range(q_total, rank, world)
     h = C.c_void_p()
     ids = (C.c_uint8 * 128)(*(uid or bytes(128)))
     _lib.check(_lib.lib().radmm_ctx_create_sharded(device, n_pixels, q_total, b, e, rank, world, ids,
                                                    C.byref(h)))
+    if tcp_timeout_ms is not None:
+        _lib.check(_lib.lib().radmm_set_transport_timeout(h, int(tcp_timeout_ms)))
     return Solver(n_pixels, e - b, device, _ctx=h, q_total=q_total, q_begin=b)
 
 
 def run_distributed(problem: Problem, hyper: Hyperparams, mode: Mode = Mode.ASADMM, *,
-                    fixed_iterations: bool = False):
+                    fixed_iterations: bool = False, tcp_timeout_ms: int = 60000):
     """run_distributed (runtime.hpp:768-775) over the torch.distributed world.
 
     Every rank passes the whole Problem (as the reference does) and uploads
     only its own sensors; every rank returns the same global state (x_G, s,
     sigma, report); ``sensor_images`` holds the rank's own sensors.
+    ``tcp_timeout_ms`` keeps the reference's name: a collective or iteration
+    that does not complete in time raises TransportError (a dead peer does
+    not hang the job).
     """
     problem.validate()
     hyper.validate()
     rank, world, local = env_rank_world()
     uid = broadcast_unique_id(rank, world)
-    solver = sharded_solver(problem.pixel_count(), problem.sensor_count(), rank, world, local, uid)
+    solver = sharded_solver(problem.pixel_count(), problem.sensor_count(), rank, world, local, uid, tcp_timeout_ms)
     try:
         b, e = shard_range(problem.sensor_count(), rank, world)
         for q in range(b, e):

@@ -319,6 +319,44 @@ def test_desk_parity(desk):
     assert abs(api.nmse_db(g.image, truth) - (-13.70)) < 0.01
 
 
+def test_device_echo_operator_matches_host():
+    """EchoKernel::entry on the device (forward_model.hpp:64-71, dense
+    assembly :91-114) against the host restatement on the reference's desk
+    scenario: the same fp64 phase, sincos within an ulp, stored as complex64
+    -- entries equal up to one fp32 rounding, on a vanishing fraction."""
+    sc = scenario.desk_scenario()
+    sim = scenario.build_simulation(sc)
+    s = api.Solver(sc.grid.pixel_count, len(sc.sensors))
+    try:
+        for q, sensor in enumerate(sc.sensors):
+            s.generate_echo_operator(q, sc.grid, sensor, sc.waveform)
+            dev = s.get_operator(q)
+            host = np.asarray(sim.ops[q]).astype(np.complex64)
+            assert dev.shape == host.shape  # K = derive_sample_count (6142/6105/6105/6142)
+            d = np.abs(dev.astype(np.complex128) - host.astype(np.complex128))
+            assert d.max() <= 2.0 ** -23, d.max()
+            assert np.count_nonzero(d) <= 1e-5 * d.size, np.count_nonzero(d)
+    finally:
+        s.close()
+
+
+def test_desk_pin_with_device_built_operators():
+    """The reference's published desk numbers (17 iterations, NMSE -13.70 dB,
+    proj/test_output.txt:21-23) with the operators assembled on the GPU."""
+    sc = scenario.desk_scenario()
+    sim = scenario.build_simulation(sc)
+    s = api.Solver(sc.grid.pixel_count, len(sc.sensors))
+    try:
+        for q, sensor in enumerate(sc.sensors):
+            s.generate_echo_operator(q, sc.grid, sensor, sc.waveform)
+            s.set_measurement(q, sim.ys[q])
+        r = s.run(api.Hyperparams(**sc.hyper), api.Mode.ASADMM)
+    finally:
+        s.close()
+    assert r.iterations == 17 and r.converged
+    assert abs(api.nmse_db(r.image, sim.composite) - (-13.70)) < 0.01
+
+
 def test_back_projection_desk(desk):
     """back_projection on the GPU (forward_model.hpp:201-220) against the host
     restatement on the same complex64 operators: the desk's published BP NMSE
