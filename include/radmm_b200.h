@@ -128,6 +128,13 @@ typedef struct radmm_solve_cache radmm_solve_cache;
 
 const char* radmm_last_error(void);
 int radmm_version(void);
+/* Tuning switches (RADMM_* names: A/B knobs and
+ * build-only paths; defaults are the shipped configuration).  The environment
+ * is read once per ABI call, never on a launch path; radmm_set_tuning
+ * overrides it (clear != 0 removes the override). */
+int radmm_set_tuning(const char* name, int value, int clear);
+/* Bit 0: built with the parked experimental kernels (RADMM_EXPERIMENTAL). */
+int radmm_build_features(void);
 
 /* Hyperparams defaults / validate (admm.hpp:32-57). */
 int radmm_hyperparams_default(radmm_hyperparams* out);

@@ -94,6 +94,8 @@ _IP = C.POINTER(C.c_int32)
 SIGNATURES = {
     "radmm_last_error": (C.c_char_p, []),
     "radmm_version": (C.c_int, []),
+    "radmm_build_features": (C.c_int, []),
+    "radmm_set_tuning": (C.c_int, [C.c_char_p, C.c_int, C.c_int]),
     "radmm_hyperparams_default": (C.c_int, [C.POINTER(Hyper)]),
     "radmm_hyperparams_validate": (C.c_int, [C.POINTER(Hyper)]),
     "radmm_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(_VP)]),

@@ -489,6 +489,12 @@ class Solver:
         res.removal_log = log[:3 * m.value].reshape(m.value, 3)
 
 
+def set_tuning(name: str, value: int | None) -> None:
+    """Override a RADMM_* tuning switch for this
+    process; ``None`` removes the override (the environment applies again)."""
+    _lib.check(_lib.lib().radmm_set_tuning(name.encode(), int(value or 0), int(value is None)))
+
+
 class PinnedBuffer:
     """Page-locked host memory (radmm_host_alloc) viewed as a NumPy array --
     where callers stage large operators so uploads run at full host-link

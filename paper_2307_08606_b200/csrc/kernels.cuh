@@ -23,5 +23,7 @@
 #include "kernels_matvec.cuh"
 #include "kernels_dense.cuh"
 #include "kernels_batched.cuh"
-#include "kernels_fused.cuh"
+#if RADMM_EXPERIMENTAL
+#include "kernels_fused.cuh"  // parked single-pass sweeps (not shipped)
+#endif
 #include "kernels_ozaki.cuh"

@@ -53,6 +53,7 @@ __host__ __device__ inline uint64_t herm_item(int q, int J, int I0, int nt) {
   return (uint64_t)q << 48 | (uint64_t)J << 32 | (uint64_t)I0 << 16 | (uint64_t)nt;
 }
 
+#if RADMM_EXPERIMENTAL  // one CTA per item (superseded by the persistent kernel below)
 // NR right-hand sides per pass of G: NR = 1 is the iteration's w = G v; NR = 2
 // also forms a lazy-downdate column P[:, u] = G a_u from the same tile reads
 // (see lazy_* below).  A missing second column (v1 == nullptr) is zero.
@@ -168,6 +169,8 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
     }
   }
 }
+
+#endif
 
 constexpr size_t herm_persist_smem(int nr) {
   return (size_t)(2 * nr * kHermTile + 2 * nr * kHermStrip * kHermTile + 2 * nr * 8 * kHermTile) * 16;
@@ -888,6 +891,7 @@ __global__ void __launch_bounds__(256) lazy_border_inv_kernel(const __grid_const
   }
 }
 
+#if RADMM_EXPERIMENTAL  // TMA-ring variant (RADMM_HERM=2), measured slower
 // TMA-staged variant: persistent CTAs (one per SM) walk the item list
 // round-robin; warp 8 streams each 64 x 64 tile (64 column segments of
 // <= 1 KB) into a kHermStages-deep shared ring with cp.async.bulk, and the
@@ -1028,6 +1032,7 @@ __global__ void __launch_bounds__(288, 1) herm_gapply_tma_kernel(const __grid_co
     }
   }
 }
+#endif
 
 // Hermitian projection of a factor in place: G <- (G + G^H) / 2 (the nearest
 // Hermitian matrix; never increases the Frobenius error of an inverse).

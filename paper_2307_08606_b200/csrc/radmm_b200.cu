@@ -28,6 +28,9 @@
 #include <string>
 #include <vector>
 
+#ifndef RADMM_EXPERIMENTAL
+#define RADMM_EXPERIMENTAL 0
+#endif
 #include "../../include/radmm_b200.h"
 #include "kernels.cuh"
 
@@ -56,9 +59,45 @@ void check_cuda(cudaError_t e, const char* what, int line) {
 
 int env_int(const char* name, int dflt);
 
+// ---------------------------------------------------------------------------
+// Tuning switches (RADMM_* names: A/B knobs and build-only paths, defaults in
+// DESIGN.md section 10).  Nothing reads the environment on a launch path:
+// every ABI call refreshes one snapshot of the environment (tune_refresh,
+// from guarded()), radmm_set_tuning() overrides it programmatically, and
+// env_int() only looks the snapshot up.
+// ---------------------------------------------------------------------------
+struct TuneEntry {
+  std::string name;
+  bool env_set = false, api_set = false;
+  int env_val = 0, api_val = 0;
+};
+std::mutex g_tune_mu;
+std::vector<TuneEntry> g_tune;  // grows as switches are first consulted
+
+TuneEntry& tune_entry(const char* name) {  // caller holds g_tune_mu
+  for (TuneEntry& t : g_tune)
+    if (t.name == name) return t;
+  g_tune.push_back(TuneEntry{name});
+  TuneEntry& t = g_tune.back();
+  const char* e = std::getenv(name);
+  t.env_set = e != nullptr;
+  t.env_val = e ? std::atoi(e) : 0;
+  return t;
+}
+
+void tune_refresh() {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  for (TuneEntry& t : g_tune) {
+    const char* e = std::getenv(t.name.c_str());
+    t.env_set = e != nullptr;
+    t.env_val = e ? std::atoi(e) : 0;
+  }
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
+    tune_refresh();
     f();
     return RADMM_OK;
   } catch (const Failure& e) {
@@ -459,7 +498,7 @@ struct radmm_ctx {
   DArr<double2> xg_alt, sigma_alt;  // v5 writes the new x_G / sigma here, then they swap
 
   ~radmm_ctx() {
-    const bool tr = std::getenv("RADMM_TRACE_DESTROY") != nullptr;
+    const bool tr = env_int("RADMM_TRACE_DESTROY", 0) != 0;
     auto t = std::chrono::steady_clock::now();
     auto mark = [&](const char* what) {
       if (!tr) return;
@@ -800,12 +839,8 @@ void coldot_pipe_launch(radmm_ctx* c, const Pack<ColDotJob>& pk, size_t nb, int 
 }
 
 int coldot_cpw() {
-  static int v = [] {
-    const char* e = std::getenv("RADMM_CPW");
-    const int x = e ? std::atoi(e) : 0;
-    return (x == 1 || x == 2 || x == 4) ? x : 0;
-  }();
-  return v;
+  const int x = env_int("RADMM_CPW", 0);
+  return (x == 1 || x == 2 || x == 4) ? x : 0;
 }
 
 template <typename T, int EPI>
@@ -898,12 +933,17 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
 void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, int nr, const int* go,
                  bool packed = false) {
   for (size_t i = 0; i < nq; ++i) packed = packed || pk.j[i].packed;  // only the persistent kernel reads tiles
+#if RADMM_EXPERIMENTAL  // superseded variants (TMA ring, one CTA per item), measured slower
   if (nr == 1 && !packed && env_int("RADMM_HERM", 1) == 2) {
     set_smem_attr((const void*)herm_gapply_tma_kernel, (int)((int)kHermTmaSmem));
     const int grid = std::min(c->herm_n_items, c->sm_count);
     LAUNCH(c, herm_gapply_tma_kernel, dim3((unsigned)grid), 288, kHermTmaSmem, pk, c->herm_items.p,
            c->herm_n_items, go);
-  } else if (nr == 2 || packed || env_int("RADMM_HERM_PERSIST", 1)) {
+  } else if (nr == 1 && !packed && !env_int("RADMM_HERM_PERSIST", 1)) {
+    LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
+  } else
+#endif
+  {
     auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
     const size_t smem = herm_persist_smem(nr);
     set_smem_attr((const void*)kern, (int)((int)smem));
@@ -911,8 +951,6 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     per_sm = occupancy((const void*)kern, 256, smem);
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
     LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
-  } else {
-    LAUNCH(c, herm_gapply_kernel<1>, dim3((unsigned)c->herm_n_items), 256, 0, pk, c->herm_items.p, go);
   }
   LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
          pk, go);
@@ -2553,18 +2591,45 @@ void note_stalls(radmm_ctx* c, int slot) {
 
 // ---- single-pass fused sweep (one GPU, all sensors dual, Q <= 8) ------------
 int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  const TuneEntry& t = tune_entry(name);
+  return t.api_set ? t.api_val : t.env_set ? t.env_val : dflt;
 }
 
+FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
+  FusionArgs a;
+  a.contrib = c->contrib.p;
+  a.Q = c->Q_total;
+  a.N = c->N;
+  a.s = c->s.p; a.xg = c->xg.p; a.sigma = c->sigma.p; a.sigma_pre = c->sigma_pre.p; a.gap = c->gap.p;
+  a.beta = h->beta;
+  a.kappa = h->lambda / h->beta;
+  a.root_n_eps_abs = std::sqrt((double)c->N) * h->eps_abs;
+  a.eps_rel = h->eps_rel;
+  a.has_prev = k > 1 ? 1 : 0;
+  a.iteration = k;
+  a.partials = c->fpart.p;
+  a.counter = c->fcounter.p;
+  a.out_dev = c->fs_dev.p;
+  a.out_host = c->fs_host_dev + (k & 1);  // two slots: round k+1 may finish before the host reads round k
+  a.go = nullptr;
+  a.go_next = nullptr;
+  a.stop_on_converge = 1;
+  a.screen_next_possible = 0;
+  a.screen_go = nullptr;
+  return a;
+}
+
+#if RADMM_EXPERIMENTAL
+// ---- parked experiment: single-pass fused sweeps ------
+// Compiled only with -DRADMM_EXPERIMENTAL=1 (__graft_entry__.build(experimental=True));
+// every variant measured slower than the two-pass default, none carries the
+// KM-space refinement, and the product library does not ship them.
 constexpr int kDefaultSweepTile = 16;
 
 // RADMM_FUSED: 0 = two-pass local updates (default), 1 = synchronous cluster
 // sweep (v1), 2 = asynchronous warp-specialised sweep (v2).
-int fused_version() {
-  const char* e = std::getenv("RADMM_FUSED");  // read per call: tests switch it
-  return e ? std::atoi(e) : 0;                  // experimental: see DESIGN.md section 9
-}
+int fused_version() { return env_int("RADMM_FUSED", 0); }
 
 bool fused_enabled() { return fused_version() != 0; }
 
@@ -2781,29 +2846,6 @@ void launch_sweep3(radmm_ctx* c, const Pack<SweepJob>& sp, const FusionArgs& fa,
   c->sweep_clusters = clusters;
 }
 
-FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
-  FusionArgs a;
-  a.contrib = c->contrib.p;
-  a.Q = c->Q_total;
-  a.N = c->N;
-  a.s = c->s.p; a.xg = c->xg.p; a.sigma = c->sigma.p; a.sigma_pre = c->sigma_pre.p; a.gap = c->gap.p;
-  a.beta = h->beta;
-  a.kappa = h->lambda / h->beta;
-  a.root_n_eps_abs = std::sqrt((double)c->N) * h->eps_abs;
-  a.eps_rel = h->eps_rel;
-  a.has_prev = k > 1 ? 1 : 0;
-  a.iteration = k;
-  a.partials = c->fpart.p;
-  a.counter = c->fcounter.p;
-  a.out_dev = c->fs_dev.p;
-  a.out_host = c->fs_host_dev + (k & 1);  // two slots: round k+1 may finish before the host reads round k
-  a.go = nullptr;
-  a.go_next = nullptr;
-  a.stop_on_converge = 1;
-  a.screen_next_possible = 0;
-  a.screen_go = nullptr;
-  return a;
-}
 
 // One iteration on the fused path: v for every sensor (left by the previous
 // sweep, or a fresh forward pass after an active-set change / at k = 1), the
@@ -2872,6 +2914,14 @@ void fused_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k) {
   for (Sensor& S : c->sensors) S.v_ready = true;
   ++c->upd;
 }
+
+#else
+bool fused_enabled() { return false; }
+bool fused_eligible(radmm_ctx*) { return false; }
+void fused_iteration(radmm_ctx*, const radmm_hyperparams*, int) {
+  fail(RADMM_INVALID_ARGUMENT, "fused sweeps are an experiment: build with RADMM_EXPERIMENTAL=1");
+}
+#endif  // RADMM_EXPERIMENTAL
 
 void build_contrib(radmm_ctx* c) {
   std::vector<const double2*> ptrs(c->Q_total);
@@ -3683,7 +3733,9 @@ struct radmm_solve_cache {
 extern "C" {
 
 const char* radmm_last_error(void) { return g_last_error.c_str(); }
-int radmm_version(void) { return 1; }
+int radmm_version(void) { return 2; }
+
+int radmm_build_features(void) { return RADMM_EXPERIMENTAL ? 1 : 0; }
 
 int radmm_hyperparams_default(radmm_hyperparams* out) {
   return guarded([&] {
@@ -4264,6 +4316,16 @@ int radmm_host_alloc(size_t bytes, void** out) {
 int radmm_host_free(void* p) {
   return guarded([&] {
     if (p) CK(cudaFreeHost(p));
+  });
+}
+
+int radmm_set_tuning(const char* name, int value, int clear) {
+  return guarded([&] {
+    if (!name || std::strncmp(name, "RADMM_", 6) != 0) fail(RADMM_INVALID_ARGUMENT, "tuning switches are RADMM_*");
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    TuneEntry& t = tune_entry(name);
+    t.api_set = clear == 0;
+    t.api_val = value;
   });
 }
 

@@ -574,9 +574,13 @@ def test_apply_and_adjoint_match_host():
 
 @pytest.mark.parametrize("fused", ["1", "2", "3", "4", "5"])
 def test_fused_sweeps_match_oracle(fused, monkeypatch):
-    """The experimental single-kernel sweeps (RADMM_FUSED=1|2|3) reproduce the
-    oracle, including elimination (masks) -- on a shape every variant accepts
-    (Q=4 dual sensors, KM=512, N=1024)."""
+    """The parked single-kernel sweeps (RADMM_FUSED=1..5)
+    reproduce the oracle, including elimination (masks) -- on a shape every
+    variant accepts (Q=4 dual sensors, KM=512, N=1024).  Only in a library
+    built with RADMM_EXPERIMENTAL=1; the shipped one does not contain them."""
+    from paper_2307_08606_b200 import _lib
+    if not _lib.lib().radmm_build_features() & 1:
+        pytest.skip("parked experiment not compiled (RADMM_EXPERIMENTAL=0)")
     ops, ys, hyper = _small_c1(nside=32, K=64, M=8, n_targets=6, max_iter=120)
     hyper = dict(hyper, screening_tol=1e-3)
     monkeypatch.setenv("RADMM_FUSED", fused)
