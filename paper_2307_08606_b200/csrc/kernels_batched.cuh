@@ -38,9 +38,6 @@ struct HermJob {
   int packed;          // G is a packed lower-tile array (cap_pack_kernel), not column-major ld
   const double2* base; // right-hand side 0 output: w = base + sgn * (G v) (nullptr: w = G v)
   double sgn;
-  unsigned* cnt;       // nb arrival counters (zero between launches): the apply reduces its own
-                       // row blocks (the last item to finish one sums its partials); nullptr:
-                       // herm_reduce_kernel does it in a second launch
 };
 
 // Packed lower-tile storage of a Hermitian matrix (the dual capacitance C,
@@ -174,57 +171,6 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
 }
 
 #endif
-
-// Sum row block b's partials (its dot partials, then the ax partials of tiles
-// (b, J < b)) in a fixed order -- 4 slices of 64 rows, then the slices in
-// order -- and write w (+ base / sgn): the deterministic reduction of
-// herm_reduce_kernel, done by whichever CTA finishes the row block last.
-// Partials written by other SMs are read through L2 (__ldcg).
-template <int NR>
-__device__ __forceinline__ void herm_reduce_block(const HermJob& jb, int b, bool has1, double2* scratch) {
-  const int tid = threadIdx.x, r = tid & 63, sl = tid >> 6;  // 256 threads: 4 slices
-  const int ng = (jb.nb - b + kHermStrip - 1) / kHermStrip, total = ng + b;
-#pragma unroll
-  for (int c = 0; c < NR; ++c) {
-    if (c == 1 && !has1) continue;
-    const double2* dbase = jb.dotp + c * jb.dstride + (int64_t)b * jb.groups * kHermTile + r;
-    const double2* abase = jb.axp + c * jb.astride + (int64_t)b * (b - 1) / 2 * kHermTile + r;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k0 = sl; k0 < total; k0 += 16) {
-      double2 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = k0 + 4 * u;
-        v[u] = k < total ? __ldcg(k < ng ? dbase + (int64_t)k * kHermTile : abase + (int64_t)(k - ng) * kHermTile)
-                         : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc.x += v[u].x;
-        acc.y += v[u].y;
-      }
-    }
-    scratch[sl * kHermTile + r] = acc;
-    __syncthreads();
-    if (sl == 0) {
-      const int row = b * kHermTile + r;
-      double2 t = scratch[r];
-#pragma unroll
-      for (int u = 1; u < 4; ++u) {
-        t.x += scratch[u * kHermTile + r].x;
-        t.y += scratch[u * kHermTile + r].y;
-      }
-      if (row < jb.n) {
-        if (c == 0 && jb.base) {
-          const double2 bb = jb.base[row];
-          t = make_double2(bb.x + jb.sgn * t.x, bb.y + jb.sgn * t.y);
-        }
-        (c == 0 ? jb.w : jb.w1)[row] = t;
-      }
-    }
-    __syncthreads();
-  }
-}
 
 constexpr size_t herm_persist_smem(int nr) {
   return (size_t)(2 * nr * kHermTile + 2 * nr * kHermStrip * kHermTile + 2 * nr * 8 * kHermTile) * 16;
@@ -377,33 +323,6 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
         double2* dp = jb.dotp + c * jb.dstride + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[c][k], di[c][k]);
-      }
-    }
-    if (jb.cnt) {
-      // arrival per touched row block (dot: J; ax: the strip's tiles I != J);
-      // the CTA completing a row block reduces it -- no second launch
-      __shared__ int red_list[kHermStrip + 1];
-      __shared__ int red_n;
-      __threadfence();  // this item's partials, device-wide, before the counts
-      __syncthreads();
-      if (tid == 0) {
-        int n = 0;
-        auto arrive = [&](int b) {
-          const unsigned expect = (unsigned)((jb.nb - b + kHermStrip - 1) / kHermStrip + b);
-          if (atomicAdd(jb.cnt + b, 1u) == expect - 1u) red_list[n++] = b;
-        };
-        arrive(J);
-        for (int t = 0; t < nt; ++t)
-          if (I0 + t != J) arrive(I0 + t);
-        red_n = n;
-      }
-      __syncthreads();
-      const int nred = red_n;
-      for (int i = 0; i < nred; ++i) {
-        const int b = red_list[i];
-        __threadfence();
-        herm_reduce_block<NR>(jb, b, has1, &sax[0][0][0][0]);
-        if (tid == 0) jb.cnt[b] = 0u;  // zero again for the next launch
       }
     }
     if (nxt >= n_items) break;

@@ -303,7 +303,6 @@ struct Sensor {
   bool data_lag = false;
   // Hermitian G-apply partials (dot: nb x groups x 64, ax: nb(nb-1)/2 x 64)
   DArr<double2> hdot, hax;
-  DArr<unsigned> hcnt;  // per row block arrival counters of the folded reduction
   DArr<double2> apart;  // row-segmented adjoint partials (nseg x N)
   // Lazy Woodbury downdates (dual form, see lazy_dot_kernel): G stays the
   // factor of the base active set; the eliminated columns D accumulate in
@@ -901,9 +900,7 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
                  na = std::max<size_t>((size_t)h.nb * (h.nb - 1) / 2 * kHermTile, 1);
     if (S.hdot.n < 2 * nd) S.hdot.alloc(2 * nd, false);  // two right-hand sides
     if (S.hax.n < 2 * na) S.hax.alloc(2 * na, false);
-    if (S.hcnt.n < (size_t)h.nb) S.hcnt.alloc(h.nb);  // zeroed; the reducing CTAs re-zero
     h.v = S.v.p; h.w = S.w.p; h.dotp = S.hdot.p; h.axp = S.hax.p;
-    h.cnt = env_int("RADMM_HERM_FOLD", 1) ? S.hcnt.p : nullptr;
     h.dstride = (int64_t)nd; h.astride = (int64_t)na;
     pk.j[i] = h;
     nb_max = std::max(nb_max, h.nb);
@@ -954,9 +951,6 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
     per_sm = occupancy((const void*)kern, 256, smem);
     const int grid = std::min(c->herm_n_items, c->sm_count * std::max(1, per_sm));
     LAUNCH(c, kern, dim3((unsigned)grid), 256, smem, pk, c->herm_items.p, c->herm_n_items, go);
-    bool folded = true;
-    for (size_t i = 0; i < nq; ++i) folded = folded && pk.j[i].cnt != nullptr;
-    if (folded) return;  // the persistent kernel reduced its own row blocks
   }
   LAUNCH(c, herm_reduce_kernel, dim3((unsigned)nb_max, (unsigned)nq, (unsigned)nr), kHermRedSlices * kHermTile, 0,
          pk, go);
