@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--stress", action="store_true", help="BASELINE config 4 elimination-stress report")
     p.add_argument("--stress-iters", type=int, default=400)
     p.add_argument("--frames", type=int, default=0, help="BASELINE config 5: F frames sharing the operators")
+    p.add_argument("--paper", action="store_true", help="ASADMM vs SADMM on the reference's full and clean-desk "
+                   "scenarios (PAPER.md:69,77)")
     return p.parse_args()
 
 
@@ -767,6 +769,52 @@ def spawn_ranks(args) -> bool:
     return True
 
 
+def paper(args):
+    """The paper's comparison on the reference's own scenarios,
+    ASADMM vs SADMM to tolerance on the GPU (operators assembled by the device
+    EchoKernel generator, forward_model.hpp:32-114):
+      full   -- scenario.hpp:328-363 (64 x 64, Q=4, M=8; defaults mu=3,
+                lambda=20, beta=100, eps 1e-4/1e-2, W=5, tol=1e-5);
+      clean  -- the x10 noiseless desk with tol 1e-3 (test_screening_scenario.cpp:14-35).
+    Reports iterations, device time, solve counts and the active-fraction
+    trace of both modes (one auxiliary JSON line per scenario)."""
+    import __graft_entry__
+    from paper_2307_08606_b200 import api, scenario
+    __graft_entry__.build()
+    runs = []
+    full = scenario.full_scenario()
+    runs.append(("full", full, {}))
+    clean = scenario.desk_scenario()
+    clean.snr_db = math.inf
+    for t in clean.targets:
+        t.base_amplitude *= 10
+    runs.append(("clean_desk_x10", clean, {"screening_tol": 1e-3}))
+    for name, sc, hyp in runs:
+        sim = scenario.build_simulation(sc)  # measurements (and the reference-side operators for the shapes)
+        s = api.Solver(sc.grid.pixel_count, len(sc.sensors))
+        for q, sensor in enumerate(sc.sensors):
+            s.generate_echo_operator(q, sc.grid, sensor, sc.waveform)
+            s.set_measurement(q, sim.ys[q])
+        h = api.Hyperparams(**{**sc.hyper, **hyp})
+        s.run(h, api.Mode.ASADMM, fetch=False)  # warm-up (factor cache, kernel loading)
+        out = {"scenario": name, "pixels": sc.grid.pixel_count, "sensors": len(sc.sensors),
+               "rows": [s.rows[q] for q in range(len(sc.sensors))], "hyper": h.__dict__}
+        for mode in (api.Mode.SADMM, api.Mode.ASADMM):
+            r = s.run(h, mode)
+            ms, _ = s.iteration_stats(r.iterations)
+            fr = [rec.active_fraction for rec in r.report.iterations]
+            out[api.mode_name(mode)] = {
+                "iterations": r.iterations, "converged": r.converged, "solve_ms_device": float(np.sum(ms)),
+                "total_active_solves": r.report.total_active_solves,
+                "final_active_fraction": fr[-1], "active_fraction_trace": fr,
+                "nmse_db": api.nmse_db(r.image, sim.composite)}
+        a, b = out["asadmm"], out["sadmm"]
+        out["asadmm_vs_sadmm_time_ratio"] = a["solve_ms_device"] / max(1e-9, b["solve_ms_device"])
+        out["asadmm_vs_sadmm_solve_ratio"] = a["total_active_solves"] / max(1, b["total_active_solves"])
+        s.close()
+        print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if spawn_ranks(args):
@@ -777,6 +825,9 @@ def main():
         return
     if args.frames:
         frames(args)
+        return
+    if args.paper:
+        paper(args)
         return
     cfg = scenario.baseline_config(args.config)
     if args.impl == "reference":
