@@ -27,3 +27,4 @@
 #include "kernels_fused.cuh"  // parked single-pass sweeps (not shipped)
 #endif
 #include "kernels_ozaki.cuh"
+#include "kernels_small.cuh"
