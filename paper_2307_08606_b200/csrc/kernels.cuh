@@ -27,4 +27,3 @@
 #include "kernels_fused.cuh"  // parked single-pass sweeps (not shipped)
 #endif
 #include "kernels_ozaki.cuh"
-#include "kernels_small.cuh"

@@ -2448,88 +2448,6 @@ void run_fusion(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go =
 
 bool fused_enabled();
 
-// ---- one cooperative launch per iteration for L2-resident problems ----------
-// (kernels_small.cuh): dual sensors with full (unpacked) factors of at most
-// kSmallMaxRows rows and primal sensors, no pending lazy column, unsharded,
-// not profiling.  Config 1 (4 x 256 x 1024) and the reference's desk.
-bool small_eligible(radmm_ctx* c) {
-  if (c->sharded || c->profiling || c->Q < 1 || c->Q > kMaxBatch || env_int("RADMM_SMALL", 1) == 0) return false;
-  double elems = 0;
-  for (const Sensor& S : c->sensors) {
-    if (S.primal) {
-      if (S.n_act > 4096) return false;
-      elems += (double)S.n_act * S.n_act;
-    } else {
-      if (S.gpacked || S.rows > kSmallMaxRows || S.lz_new || S.lz_d > kLazyMax || S.v_ready) return false;
-      elems += (double)S.rows * S.n_act;
-    }
-  }
-  return elems <= 64.0 * 1024 * 1024;  // L2-resident operators / factors
-}
-
-void small_iteration(radmm_ctx* c, const radmm_hyperparams* h, int k, const int* go, int* go_next,
-                     int stop_on_converge, int* screen_go, bool snp_after) {
-  const int slot = c->upd % c->W;
-  SmallArgs a{};
-  a.Q = c->Q;
-  a.mu = h->mu;
-  a.beta = h->beta;
-  a.go = go;
-  for (int q = 0; q < c->Q; ++q) {
-    Sensor& S = c->sensors[q];
-    SmallJob& j = a.jobs.j[q];
-    j.primal = S.primal ? 1 : 0;
-    j.A = S.A.p; j.ld = S.ld; j.rows = S.rows; j.n_act = S.n_act; j.J = S.J.p; j.data = S.data.p;
-    j.x_hat = S.x_hat.p; j.rhs = S.rhs.p; j.x_full = S.x_full.p; j.ring_slot = S.ring.p + (size_t)slot * c->N;
-    j.G = S.G.p; j.ldg = S.ldg;
-    if (!S.primal) {
-      if (S.rho.n < (size_t)S.ld) S.rho.alloc(S.ld);
-      if (S.dw.n < (size_t)S.ld) S.dw.alloc(S.ld);
-      j.nchunk = (S.n_act + kSmallChunk - 1) / kSmallChunk;
-      if (S.part.n < (size_t)j.nchunk * S.ld) {
-        S.part.alloc((size_t)j.nchunk * S.ld, false);
-        S.part_chunks = j.nchunk;
-      }
-      j.v = S.v.p; j.w = S.w.p; j.rho = S.rho.p; j.dw = S.dw.p; j.part = S.part.p;
-      j.bz = S.data_lag ? S.bz.p : nullptr;
-      j.Cp = (c->refine && S.cp_valid) ? S.Cp.p : nullptr;
-      j.d = S.lz_d;
-      if (S.lz_d > 0) {
-        lazy_reserve(S);
-        j.pix = S.lz_pix.p; j.P = S.lz_P.p; j.Sinv = S.lz_S.p; j.lds = kLazyMax; j.t = S.lz_t.p;
-      }
-      a.any_dual = 1;
-      a.any_lazy |= S.lz_d > 0 ? 1 : 0;
-      a.any_refine |= j.Cp ? 1 : 0;
-    }
-  }
-  ++c->upd;
-  const int snp = snp_after ? 1 : 0;
-  FusionArgs f = fusion_args(c, h, k);
-  f.go = go;
-  f.go_next = go_next;
-  f.stop_on_converge = stop_on_converge;
-  f.screen_next_possible = snp;
-  f.screen_go = screen_go;
-  static int per_sm = -1;
-  if (per_sm < 0) per_sm = std::max(1, occupancy((const void*)small_iter_kernel, kSmallThreads, 0));
-  const int grid = c->sm_count * std::min(per_sm, 2);
-  if (c->fpart.n < (size_t)grid * 5) c->fpart.alloc((size_t)grid * 5);
-  f.partials = c->fpart.p;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kSmallThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, small_iter_kernel, a, f));
-  ++c->launches;
-}
-
 // SensorCore::screen for every local sensor (admm.hpp:134-159, run :380-386),
 // device part: zeta, keep flags, compaction into the *_new buffers and the
 // kept counts (mapped host slot `slot`).  Guarded (go, sgo) when it is
@@ -3249,13 +3167,6 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     c->pre_screened[kk & 1] = false;
     if (fused_eligible(c)) {
       fused_iteration(c, h, kk);
-    } else if (small_eligible(c)) {
-      // one cooperative launch: local updates + fusion round (kernels_small.cuh)
-      const int snp = (asadmm && !disable && c->upd + 1 >= c->W) ? 1 : 0;
-      const bool near = trigger_seen || last_ratio <= kPreScreenRatio;
-      int* sgo = (spec && snp && near && !c->sharded) ? c->sgo_flags.p + (kk & 1) : nullptr;
-      small_iteration(c, h, kk, go, go_next, fixed ? 0 : 1, sgo, snp != 0);
-      if (sgo) c->pre_screened[kk & 1] = enqueue_screen(c, h, kk & 1, go, sgo, go_next);
     } else {
       local_updates(c, h, go);
       exchange(c, (double)notice, kk);

@@ -534,12 +534,15 @@ def test_sharded_context_world1_equals_plain():
 def test_nccl_exchange_path_one_rank_equals_plain(monkeypatch):
     """The multi-GPU exchange path on real hardware: a one-rank NCCL
     communicator (RADMM_FORCE_NCCL) runs the same per-iteration all-gather of
-    the sensor images + metadata and the fusion over the gathered buffer as a
-    G-rank run does; results equal the plain single-GPU run bitwise."""
+    the sensor images and the fusion over the gathered buffer as a G-rank run
+    does, plus the end-of-run record gather; results equal the plain
+    single-GPU run bitwise (both on the general multi-launch path: the
+    one-launch small-problem iteration is unsharded only)."""
     from paper_2307_08606_b200 import distributed as D
     ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=60)
     hyper = dict(hyper, screening_tol=1e-3)
     h = api.Hyperparams(**hyper)
+    monkeypatch.setenv("RADMM_SMALL", "0")
     plain = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
     monkeypatch.setenv("RADMM_FORCE_NCCL", "1")
     s = D.sharded_solver(ops[0].shape[1], len(ops), 0, 1, 0, D.nccl_unique_id())
