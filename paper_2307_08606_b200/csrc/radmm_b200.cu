@@ -1738,7 +1738,7 @@ void lazy_reserve(Sensor& S) {
     S.lz_P.alloc((size_t)S.ld * kLazyMax, false);
     S.lz_R.alloc((size_t)S.ld * kLazyMax, false);
     S.lz_S.alloc((size_t)kLazyMax * kLazyMax, false);
-    S.lz_t.alloc(3 * kLazyMax, false);  // lazy_dot scratch; small_iter_kernel uses three slots
+    S.lz_t.alloc(2 * kLazyMax, false);
     S.lz_pix.alloc(kLazyMax, false);
     S.lz_B.alloc((size_t)kLazyMax * kBorderMax, false);
   }
