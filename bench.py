@@ -166,12 +166,15 @@ def build_workload(cfg, solver, q_begin: int, q_end: int, dist=None):
     return ys, cfg.lambda_frac * lam_local
 
 
-def algorithmic_bytes_per_iteration(cfg, sizes):
-    """Dual form: 2 passes over the active columns + the Hermitian triangle of
-    the KM x KM capacitance inverse (c128, KM(KM+1)/2 entries) + O(N) vectors
-    (SURVEY 8d)."""
+def algorithmic_bytes_per_iteration(cfg, sizes, refined: bool = True):
+    """Dual form: 2 passes over the active columns + the packed lower 64 x 64
+    tiles of the capacitance inverse G (complex128), and with the KM-space
+    refinement two more tile passes (C, then G) + O(N)
+    vectors."""
     km = cfg.KM
-    return sum(2.0 * km * n * 8 + km * (km + 1) * 8 for n in sizes) + 12.0 * cfg.N * 16
+    nb = -(-km // 64)
+    tiles = 64 * 64 * 16.0 * nb * (nb + 1) / 2
+    return sum(2.0 * km * n * 8 + (3 if refined else 1) * tiles for n in sizes) + 12.0 * cfg.N * 16
 
 
 # ---------------------------------------------------------------------------

@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <thread>
 #include <type_traits>
@@ -73,6 +74,7 @@ struct TuneEntry {
 };
 std::mutex g_tune_mu;
 std::vector<TuneEntry> g_tune;  // grows as switches are first consulted
+std::atomic<unsigned> g_tune_gen{1};  // bumped by every refresh / override
 
 TuneEntry& tune_entry(const char* name) {  // caller holds g_tune_mu
   for (TuneEntry& t : g_tune)
@@ -87,11 +89,16 @@ TuneEntry& tune_entry(const char* name) {  // caller holds g_tune_mu
 
 void tune_refresh() {
   std::lock_guard<std::mutex> lk(g_tune_mu);
+  bool changed = false;
   for (TuneEntry& t : g_tune) {
     const char* e = std::getenv(t.name.c_str());
-    t.env_set = e != nullptr;
-    t.env_val = e ? std::atoi(e) : 0;
+    const bool set = e != nullptr;
+    const int val = e ? std::atoi(e) : 0;
+    changed = changed || set != t.env_set || val != t.env_val;
+    t.env_set = set;
+    t.env_val = val;
   }
+  if (changed) g_tune_gen.fetch_add(1, std::memory_order_release);
 }
 
 template <class F>
@@ -2591,9 +2598,32 @@ void note_stalls(radmm_ctx* c, int slot) {
 
 // ---- single-pass fused sweep (one GPU, all sensors dual, Q <= 8) ------------
 int env_int(const char* name, int dflt) {
-  std::lock_guard<std::mutex> lk(g_tune_mu);
-  const TuneEntry& t = tune_entry(name);
-  return t.api_set ? t.api_val : t.env_set ? t.env_val : dflt;
+  // launch paths call this a few dozen times per round: a per-thread cache
+  // keyed by the name literal's address answers without the lock while the
+  // switch table is unchanged (generation counter)
+  struct Hit { const char* name; int dflt; unsigned gen; int value; };
+  thread_local Hit cache[64];
+  thread_local int used = 0;
+  const unsigned gen = g_tune_gen.load(std::memory_order_acquire);
+  for (int i = 0; i < used; ++i)
+    if (cache[i].name == name && cache[i].dflt == dflt) {
+      if (cache[i].gen == gen) return cache[i].value;
+      break;
+    }
+  int value;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    const TuneEntry& t = tune_entry(name);
+    value = t.api_set ? t.api_val : t.env_set ? t.env_val : dflt;
+  }
+  for (int i = 0; i < used; ++i)
+    if (cache[i].name == name && cache[i].dflt == dflt) {
+      cache[i].gen = gen;
+      cache[i].value = value;
+      return value;
+    }
+  if (used < 64) cache[used++] = Hit{name, dflt, gen, value};
+  return value;
 }
 
 FusionArgs fusion_args(radmm_ctx* c, const radmm_hyperparams* h, int k) {
@@ -4326,6 +4356,7 @@ int radmm_set_tuning(const char* name, int value, int clear) {
     TuneEntry& t = tune_entry(name);
     t.api_set = clear == 0;
     t.api_val = value;
+    g_tune_gen.fetch_add(1, std::memory_order_release);
   });
 }
 
