@@ -119,6 +119,21 @@ int guarded(F&& f) {
   }
 }
 
+// One non-blocking stream per device for allocation-time work (DArr).
+cudaStream_t alloc_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!streams[dev]) {  // highest priority: its fills go ahead of queued CTAs of long kernels
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, hi));
+  }
+  return streams[dev];
+}
+
 template <typename T>
 struct DArr {
   T* p = nullptr;
@@ -146,7 +161,7 @@ struct DArr {
   void release() {
     if (p && own) {
       cudaDeviceSynchronize();
-      cudaFreeAsync(p, 0);
+      cudaFreeAsync(p, alloc_stream());
     }
     p = nullptr;
     n = 0;
@@ -155,15 +170,14 @@ struct DArr {
   void alloc(size_t count, bool zero = true) {
     release();
     if (count == 0) return;
-    CK(cudaMallocAsync(&p, count * sizeof(T), 0));
-    CK(cudaStreamSynchronize(0));  // usable from any stream from here on
+    // allocation-side work on a private non-blocking stream: the legacy
+    // default stream made these waits include the context stream's running
+    // work (config 3: every upload waited for the previous sensor's Gram)
+    cudaStream_t as = alloc_stream();
+    CK(cudaMallocAsync(&p, count * sizeof(T), as));
     n = count;
-    if (zero) {
-      // legacy-stream memset: context streams are non-blocking, so finish it
-      // before any of their work can touch the buffer
-      CK(cudaMemset(p, 0, count * sizeof(T)));
-      CK(cudaStreamSynchronize(0));
-    }
+    if (zero) CK(cudaMemsetAsync(p, 0, count * sizeof(T), as));
+    CK(cudaStreamSynchronize(as));  // usable (and zeroed) from any stream from here on
   }
   void ensure(size_t count) {
     if (count > n) alloc(count);
@@ -452,6 +466,7 @@ struct radmm_ctx {
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
   bool pdl = false;                  // programmatic dependent launch: on inside the iteration loop (RADMM_PDL)
   bool refine = true;                // KM-space refinement of the dual solves (radmm_run_options.skip_refinement)
+  int oz_eager = -1;                 // upload-time Grams on the Ozaki path (-1: not decided yet, see eager_gram)
   int64_t refine_skipped = 0;        // dual sensors whose packed C did not fit (solved unrefined)
   DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
   bool pre_screened[2] = {false, false};  // screening enqueued behind round k (slot k & 1)
@@ -705,11 +720,14 @@ void prepare_operator(radmm_ctx* c, Sensor& S, int rows) {
   if (S.ld > rows)  // zero padding rows (ordered before the upload on the context stream)
     CK(cudaMemset2DAsync(S.A.p + rows, S.ld * sizeof(float2), 0, (S.ld - rows) * sizeof(float2), c->N,
                          c->stream));
-  S.y_eff.alloc(S.ld);
-  S.y_eff_s.alloc(S.ld);
-  S.bz.alloc(S.ld);
-  S.v.alloc(S.ld);
-  S.w.alloc(S.ld);
+  // no zero fill: a fill is a kernel, and behind an eager Gram that occupies
+  // every SM it would wait for the Gram (begin_run writes y_eff; v, w, bz,
+  // y_eff_s are written before they are read)
+  if (S.y_eff.n != (size_t)S.ld) S.y_eff.alloc(S.ld, false);
+  if (S.y_eff_s.n != (size_t)S.ld) S.y_eff_s.alloc(S.ld, false);
+  if (S.bz.n != (size_t)S.ld) S.bz.alloc(S.ld, false);
+  if (S.v.n != (size_t)S.ld) S.v.alloc(S.ld, false);
+  if (S.w.n != (size_t)S.ld) S.w.alloc(S.ld, false);
   const int tile = 2 * fwd_threads(S.ld);
   const int tiles = (int)((S.ld + tile - 1) / tile);
   const int per_sm = fwd_threads(S.ld) > 256 ? c->fwd_per_sm_tall : c->fwd_per_sm;
@@ -1291,6 +1309,14 @@ bool slice_tensor_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Scratch of one Ozaki Gram (slices, pair blocks, row maxima) in bytes.
+double ozaki_scratch_bytes(int rows, int n) {
+  using namespace radmm_oz;
+  const int T = (rows + kOzBM - 1) / kOzBM, tiles = T * (T + 1) / 2;
+  const double rows_pad = (double)T * kOzBM, kdim = 2.0 * round_up(n, 64);
+  return 2.0 * kOzSlices * rows_pad * kdim + 4.0 * tiles * kOzPairs * 2 * kOzBM * kOzBN + 4.0 * rows_pad;
 }
 
 // C = beta I + mu A_J A_J^H (rows x rows, lower tiles + exact mirror) for one
@@ -3834,9 +3860,21 @@ void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
     gtmp_reserve(c, 1, tmp);
     double2* T = c->gtmp[0].p;
     CK(cudaMemsetAsync(T, 0, sizeof(double2) * tmp, c->stream));
-    if (ozaki_gram(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0)) {
-      release_ozaki_scratch(c);
-    } else {
+    // The Ozaki slices are only worth it if they can stay allocated across the
+    // uploads: releasing a multi-GB scratch synchronises the device, which
+    // would serialise every upload behind the previous sensor's Gram (config
+    // 3: 0.6 s per sensor).  Project the whole problem's residency (every
+    // sensor like this one) once per context; if the slices do not fit next to
+    // it, the uploads use the fp64 DMMA Gram, which needs no scratch.
+    if (c->oz_eager < 0) {
+      size_t free_now = 0, total = 0;
+      CK(cudaMemGetInfo(&free_now, &total));
+      const double per_sensor = (double)S.ld * c->N * sizeof(float2) + 2.0 * cn * sizeof(double2) + 64.0 * c->N * 16;
+      c->oz_eager = (per_sensor * c->Q + ozaki_scratch_bytes(S.rows, c->N) + tmp * 16.0 + (8.0 * (1ull << 30)) <
+                     (double)total) ? 1 : 0;
+    }
+    const bool oz = c->oz_eager == 1 && ozaki_gram(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0);
+    if (!oz) {  // (the Ozaki scratch stays allocated for the next upload; the first run releases it)
       const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, T, S.ld};
       set_smem_attr((const void*)gram_dmma1_kernel, (int)((int)kGramSmem));
       LAUNCH(c, gram_dmma1_kernel,
@@ -3888,7 +3926,9 @@ int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int6
     if (!a) fail(RADMM_INVALID_ARGUMENT, "null operator");
     if (lda < rows) fail(RADMM_INVALID_ARGUMENT, "lda < rows");
     set_device(ctx);
+    const auto tp0 = std::chrono::steady_clock::now();
     prepare_operator(ctx, S, rows);
+    const auto tp1 = std::chrono::steady_clock::now();
     const cudaMemcpyKind kind = ptr_kind == RADMM_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     // host operators upload on their own stream (the data rows; the padding
     // rows are zeroed on the context stream), so the previous sensor's eager
@@ -3907,9 +3947,17 @@ int radmm_set_operator_c64(radmm_ctx* ctx, int q, int rows, const float* a, int6
       CK(cudaMemcpy2DAsync(S.A.p, S.ld * sizeof(float2), a, lda * sizeof(float2), rows * sizeof(float2), ctx->N,
                            kind, st));
     if (host) CK(cudaEventRecord(ctx->up_event, st));
+    const auto tp2 = std::chrono::steady_clock::now();
     eager_gram(ctx, S, q, host ? ctx->up_event : nullptr);
+    const auto tp3 = std::chrono::steady_clock::now();
     if (host) CK(cudaStreamSynchronize(st));
     else CK(cudaStreamSynchronize(ctx->stream));
+    if (env_int("RADMM_DEBUG", 0)) {
+      const auto tp4 = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[radmm] set_operator q=%d: prepare %.2f ms, copy enqueue %.2f, eager gram %.2f, sync %.2f\n",
+                   q, ms(tp0, tp1), ms(tp1, tp2), ms(tp2, tp3), ms(tp3, tp4));
+    }
   });
 }
 
