@@ -36,6 +36,7 @@ struct HermJob {
   double2* axp;      // [NR][nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J, column stride astride
   int64_t dstride, astride;
   int packed;          // G is a packed lower-tile array (cap_pack_kernel), not column-major ld
+  const float2* G32;   // packed complex64 copy of G read instead of G (refinement's correction pass)
   const double2* base; // right-hand side 0 output: w = base + sgn * (G v) (nullptr: w = G v)
   double sgn;
 };
@@ -225,7 +226,18 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF);
     const HermJob& jb = P.j[q];
     const int ib = I * kHermTile;
-    if (jb.packed) {  // tile-contiguous: 64 KB per tile, zero-padded
+    if (jb.packed) {  // tile-contiguous: 64 KB per tile (32 KB in complex64), zero-padded
+      if (jb.G32) {
+        const float2* Gt = jb.G32 + herm_packed_tile(I, J) + (int64_t)c0 * kHermTile;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float2 x = __ldg(Gt + k * kHermTile + lane + 32 * h);
+            g[k][h] = make_double2(x.x, x.y);
+          }
+        return;
+      }
       const double2* Gt = jb.G + herm_packed_tile(I, J) + (int64_t)c0 * kHermTile;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -1608,6 +1620,18 @@ __global__ void frame_reduce_kernel(const FrameReduceJob* __restrict__ jobs) {
     s = make_double2(b.x + jb.sgn * s.x, b.y + jb.sgn * s.y);
   }
   jb.out[f][i] = s;
+}
+
+// packed complex128 tiles -> packed complex64 tiles (the refinement's
+// correction pass only needs modest relative accuracy: its input is the small
+// residual)
+__global__ void __launch_bounds__(256) pack_to_c64_kernel(const double2* __restrict__ Gp, float2* __restrict__ G32,
+                                                          int64_t n) {
+  pdl_enter();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = Gp[i];
+    G32[i] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+  }
 }
 
 // packed lower tiles -> full Hermitian matrix (column-major, ld), for the

@@ -347,6 +347,10 @@ struct Sensor {
   // full ld x rows matrix: half the HBM (config 3 fits with C next to it) and
   // tile-contiguous reads for the Hermitian apply; g0_packed: G0's layout
   bool gpacked = false, g0_packed = false;
+  // complex64 copy of a packed G for the refinement's correction pass (half
+  // its bytes); re-derived lazily whenever G changes (g32_valid)
+  DArr<float2> G32;
+  bool g32_valid = false;
 };
 
 constexpr int kFlagCap = 4 * kMaxBatch;  // pinned pivot-flag slots
@@ -1472,6 +1476,24 @@ void lazy_resid(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* 
   LAUNCH(c, lazy_resid_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, go);
 }
 
+// Re-derive the complex64 copy of a packed G after it changed (memory
+// permitting; RADMM_G32=0 keeps the correction in fp64).  The correction
+// pass's input is the residual, ~eps cond(C) of v, so fp32 factor entries
+// cost nothing measurable (C2 single solve: 1.8e-9 vs 6.7e-10).
+bool g32_refresh(radmm_ctx* c, Sensor& S) {
+  if (!S.gpacked || env_int("RADMM_G32", 1) == 0) return false;
+  if (S.g32_valid) return true;
+  const size_t n = cap_tiles(S.rows) * kHermTile * kHermTile;
+  if (S.G32.n < n) {
+    if (mem_available(c->device) < n * sizeof(float2) + (4ull << 30)) return false;
+    S.G32.alloc(n, false);
+  }
+  LAUNCH(c, pack_to_c64_kernel, dim3((unsigned)std::min<size_t>((n + 255) / 256, 4096)), 256, 0, S.G.p, S.G32.p,
+         (int64_t)n);
+  S.g32_valid = true;
+  return true;
+}
+
 // One step of fixed-precision iterative refinement of w = C_D^{-1} v for the
 // listed dual sensors (after gapply + lazy_correct left w1 in S.w):
 //   rho = v - C w1 + mu A_D A_D^H w1     (packed C, Hermitian apply)
@@ -1508,7 +1530,8 @@ void refine(radmm_ctx* c, const std::vector<int>& gq, double mu, const int* go) 
     }
     herm_launch(c, pk, part.size(), nb_max, 1, go, true);
     if (any_lazy) lazy_resid(c, part, mu, go);
-    // dw = C_D^{-1} rho (w += dw directly when no lazy terms follow)
+    // dw = C_D^{-1} rho (w += dw directly when no lazy terms follow), through
+    // the complex64 copy of a packed G where it fits (g32_refresh)
     const bool herm = herm_enabled() && rows_max >= env_int("RADMM_HERM_MIN_ROWS", kHermMinRows);
     if (herm) {
       Pack<HermJob> pg;
@@ -1516,6 +1539,7 @@ void refine(radmm_ctx* c, const std::vector<int>& gq, double mu, const int* go) 
       for (size_t i = 0; i < part.size(); ++i) {
         Sensor& S = c->sensors[part[i]];
         HermJob& h = pg.j[i];
+        h.G32 = g32_refresh(c, S) ? S.G32.p : nullptr;
         h.v = S.rho.p; h.v1 = nullptr; h.w1 = nullptr;
         if (S.lz_d > 0) { h.w = S.dw.p; h.base = nullptr; }
         else { h.w = S.w.p; h.base = S.w.p; h.sgn = 1.0; }
@@ -1643,6 +1667,7 @@ void rebuild_packed(radmm_ctx* c, const std::vector<int>& qs, double mu, double 
       S.G.alloc(ge, false);
     }
     S.gpacked = true;
+    S.g32_valid = false;
     S.ldg = kHermTile;
     S.g_n = S.rows;
     full = std::max(full, (size_t)S.ld * S.rows);
@@ -1821,6 +1846,7 @@ void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     double2* T = c->scratch.take<double2>((size_t)S.ld * kLazyMax);
     st3.push_back(gjob(m, d, d, mref(S.lz_P.p, S.ld, false), mref(S.lz_S.p, kLazyMax, false), T, S.ld, 1.0, 0.0));
     if (S.gpacked) {
+      S.g32_valid = false;
       pu.push_back(PackedUpdJob{S.G.p, T, S.lz_P.p, S.ld, m, d});
     } else {
       st4.push_back(gjob(m, m, d, mref(T, S.ld, false), mref(S.lz_P.p, S.ld, false, true, true), S.G.p, S.ldg, mu,
@@ -2022,6 +2048,7 @@ void eager_downdate(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       // with an exact conjugate mirror -- G stays exactly Hermitian (no
       // projection pass needed after a downdate)
       if (S.gpacked) {
+        S.g32_valid = false;
         pupd.push_back(PackedUpdJob{S.G.p, Tm[t], Pm[t], S.ld, m, r});
       } else {
         st4.push_back(gjob(m, m, r, mref(Tm[t], S.ld, false), mref(Pm[t], S.ld, false, true, true), S.G.p,
@@ -2178,6 +2205,7 @@ void begin_run(radmm_ctx* c, const radmm_hyperparams* h) {
       ++c->factor_cache_hits;  // G is untouched since its full-set factorization
     } else if (S.g0_valid && S.g0_mu == h->mu && S.g0_beta == h->beta && S.g0_packed == want_packed) {
       if (S.gpacked != S.g0_packed) S.G.release();
+      S.g32_valid = false;
       if (S.G.n < S.g0_elems) S.G.alloc(S.g0_elems);
       CK(cudaMemcpyAsync(S.G.p, S.G0.p, sizeof(double2) * S.g0_elems, cudaMemcpyDeviceToDevice, c->stream));
       S.gpacked = S.g0_packed;
@@ -2351,8 +2379,9 @@ void local_updates(radmm_ctx* c, const radmm_hyperparams* h, const int* go = nul
       rj.push_back(ReduceJob{S.part.p, f.n_chunks, S.ld, S.rows, S.data_lag ? S.bz.p : nullptr, S.v.p, 1.0});
       gq.push_back(q);
       g_bytes += gapply_bytes(S.rows);
-      if (c->refine && S.cp_valid)  // refinement: packed C pass + second G pass
-        g_bytes += 16.0 * cap_tiles(S.rows) * kHermTile * kHermTile + gapply_bytes(S.rows);
+      if (c->refine && S.cp_valid)  // refinement: packed C pass + correction pass (complex64 G when it fits)
+        g_bytes += 16.0 * cap_tiles(S.rows) * kHermTile * kHermTile +
+                   (S.gpacked && S.g32_valid ? 8.0 * cap_tiles(S.rows) * kHermTile * kHermTile : gapply_bytes(S.rows));
       ColDotJob a{};
       a.M = S.A.p; a.ld = S.ld; a.len = S.rows; a.n_out = S.n_act; a.cols = S.J.p; a.pix = S.J.p;
       a.vec = S.w.p; a.rhs = S.rhs.p; a.x_hat = S.x_hat.p; a.x_full = S.x_full.p; a.ring_slot = ring_slot;
