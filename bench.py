@@ -238,6 +238,23 @@ def cpu_sample(cfg, lam, budget_s: float = 20.0, a0=None, max_steps: int | None 
         sample = (f"fp64 NumPy/SciPy oracle (Woodbury form, LAPACK Cholesky), all {cfg.Q} sensors + fusion, "
                   f"{len(times)} full iterations timed (median), setup excluded; {cfg.name} shapes, "
                   f"lambda = {lam:.6g}")
+        # the same iteration on ONE host thread (SURVEY 8d asks for both figures)
+        one = None
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                t1 = []
+                while not t1 or (sum(t1) < budget_s / 2 and len(t1) < 5):
+                    t0 = time.perf_counter()
+                    for s in sensors:
+                        s.local_update(fusion.gap, fusion.sigma)
+                    for q, s in enumerate(sensors):
+                        fusion.set_contribution(q + 1, s.active, s.x_hat)
+                    fusion.round()
+                    t1.append(time.perf_counter() - t0)
+            one = 1.0 / float(np.median(t1))
+        except Exception:
+            pass
     else:
         a = np.asarray(host_operator(cfg, 0) if a0 is None else a0, dtype=np.complex128)
         y = scenario.simulate_measurement(a, per_sensor[0], cfg.snr_db, scenario.mix_seed(cfg.seed, 1))[0]
@@ -271,8 +288,11 @@ def cpu_sample(cfg, lam, budget_s: float = 20.0, a0=None, max_steps: int | None 
                   f"extrapolated x{cfg.Q} + the timed fusion round (SURVEY 8d: config 3 does not fit host "
                   "memory); placeholder triangular factor (LAPACK potrs cost is value-independent); "
                   f"lambda = {lam:.6g}")
-    return {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": int(cores), "kind": "port",
-            "extrapolated": bool(extrapolate), "steps_timed": len(times), "sample": sample}
+    out = {"value": 1.0 / per_iter, "unit": "iterations/s", "cores": int(cores), "kind": "port",
+           "extrapolated": bool(extrapolate), "steps_timed": len(times), "sample": sample}
+    if not extrapolate:
+        out["value_1thread"] = one
+    return out
 
 
 def workload_config(cfg, world, lam, parallelism=None):
