@@ -3277,6 +3277,8 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     return false;
   };
   bool k_launched = false;   // iteration k already enqueued (speculatively)
+  bool prev_event = false;   // the screening before the current round changed an active set
+  const int spec_after_event = env_int("RADMM_SPEC_AFTER_EVENT", 0);
   const bool trace_host = env_int("RADMM_TRACE_HOST", 0) != 0;  // host time of re-issued rounds (stderr)
   double host_ev_us = 0, host_issue_us = 0;
   int host_n = 0;
@@ -3297,6 +3299,7 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
       notice_k = 0;
       if (asadmm && !disable && staged_trigger)
         notice_k = c->pre_screened[(k - 1) & 1] ? apply_screen(c, h, k, (k - 1) & 1) : screen_all(c, h, k);
+      prev_event = notice_k > 0;
       const auto tt1 = std::chrono::steady_clock::now();
       issue(k, nullptr, notice_k);
       if (trace_host) {
@@ -3309,7 +3312,11 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     const uint64_t notice = notice_k;
     const int64_t l0 = l_k;
     const int64_t l_end = c->launches;
-    bool spec_next = spec && k < h->max_iter;
+    // Right after an elimination event the next screening most likely changes
+    // a set again (C4: 382 of 400 rounds), and a speculative round would only
+    // be cancelled -- a dozen no-op launches on the device.  Skip it then: the
+    // pre-enqueued screening still runs behind this round's fusion.
+    bool spec_next = spec && k < h->max_iter && !(prev_event && spec_after_event == 0);
     int upd_before_next = c->upd;
     if (spec_next) {
       l_k = c->launches;
