@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) herm_gapply_kernel(const __grid_constant_
 #endif
 
 constexpr size_t herm_persist_smem(int nr) {
-  return (size_t)(2 * nr * kHermTile + 2 * nr * kHermStrip * kHermTile + 2 * nr * 8 * kHermTile) * 16;
+  return (size_t)(2 * nr * kHermTile + 2 * nr * kHermStrip * kHermTile + kHermStrip * nr * 8 * kHermTile) * 16;
 }
 
 // Persistent variant: a fixed grid (resident CTAs) walks the item list
@@ -192,6 +192,8 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   double2(*vJ)[NR][kHermTile] = reinterpret_cast<double2(*)[NR][kHermTile]>(hps);
   double2(*vI)[NR][kHermStrip * kHermTile] =
       reinterpret_cast<double2(*)[NR][kHermStrip * kHermTile]>(hps + 2 * NR * kHermTile);
+  // per-warp axpy partials of every tile of the strip: summed once at the end
+  // of the item (one barrier per item instead of one per tile)
   double2(*sax)[NR][8][kHermTile] =
       reinterpret_cast<double2(*)[NR][8][kHermTile]>(hps + 2 * NR * kHermTile + 2 * NR * kHermStrip * kHermTile);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -260,7 +262,6 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   int buf = 0;
   load_vec(buf, it);
   load_tile(it, (int)(it >> 16 & 0xFFFF));
-  int par = 0;
   while (true) {
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
     const HermJob& jb = P.j[q];
@@ -299,25 +300,29 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
           }
         }
       }
-      if (t + 1 < nt) load_tile(it, I + 1);                       // in flight across the reduction below
+      if (t + 1 < nt) load_tile(it, I + 1);                       // in flight across the work below
       else if (nxt < n_items) load_tile(it_n, (int)(it_n >> 16 & 0xFFFF));  // the next item's first tile
       if (I != J) {
 #pragma unroll
         for (int c = 0; c < NR; ++c)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) sax[par][c][warp][lane + 32 * h] = make_double2(ar[c][h], ai[c][h]);
-        __syncthreads();
-        if (tid < (has1 ? 2 : 1) * kHermTile) {
-          const int c = tid / kHermTile, r = tid % kHermTile;
-          double2 sum = sax[par][c][0][r];
+          for (int h = 0; h < 2; ++h) sax[t][c][warp][lane + 32 * h] = make_double2(ar[c][h], ai[c][h]);
+      }
+    }
+    __syncthreads();  // every warp's axpy partials of the strip are in shared memory
+    {
+      const int nc = has1 ? 2 : 1;
+      for (int e = tid; e < nt * nc * kHermTile; e += 256) {
+        const int t = e / (nc * kHermTile), c = (e / kHermTile) % nc, r = e % kHermTile;
+        const int I = I0 + t;
+        if (I == J) continue;
+        double2 sum = sax[t][c][0][r];
 #pragma unroll
-          for (int w8 = 1; w8 < 8; ++w8) {
-            sum.x += sax[par][c][w8][r].x;
-            sum.y += sax[par][c][w8][r].y;
-          }
-          jb.axp[c * jb.astride + ((int64_t)I * (I - 1) / 2 + J) * kHermTile + r] = sum;
+        for (int w8 = 1; w8 < 8; ++w8) {
+          sum.x += sax[t][c][w8][r].x;
+          sum.y += sax[t][c][w8][r].y;
         }
-        par ^= 1;
+        jb.axp[c * jb.astride + ((int64_t)I * (I - 1) / 2 + J) * kHermTile + r] = sum;
       }
     }
 #pragma unroll
