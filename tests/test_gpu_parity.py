@@ -882,3 +882,58 @@ def test_c2_full_size_first_iterations_match_oracle(c2_solver):
         assert errs[k] < 1e-4, errs  # measured ~1e-5 (tools/c2_oracle_diag.py: 6.4e-6 / 4.5e-6 / 1.2e-5)
     for rg, ro in zip(g.report.iterations, o.records):
         assert abs(rg.pri_res - ro.pri_res) <= 1e-6 * ro.pri_res
+
+
+# ---- round-2 switches and ABI additions ------------------------------------------
+def test_factor_layouts_and_tuning_api_agree_with_oracle():
+    """The packed lower-tile factor (default for >= 512 rows) and the full
+    column-major factor (RADMM_GPACK=0 through radmm_set_tuning) both match
+    the oracle; the shipped library carries no parked experiments."""
+    from paper_2307_08606_b200 import _lib
+    assert _lib.lib().radmm_build_features() & 1 == 0
+    cfg = scenario.baseline_config("c1", nside=32, K=128, M=4, n_targets=6, max_iter=40)  # KM = 512: packed
+    ops, ys, _, hyper = scenario.baseline_problem(cfg)
+    hyper = dict(hyper, screening_tol=1e-3)
+    o = oracle_run(quantize(ops), ys, hyper, True, fixed_iterations=True)
+    res = {}
+    for gpack in (1, 0):
+        api.set_tuning("RADMM_GPACK", gpack)
+        try:
+            res[gpack] = gpu_run(quantize(ops), ys, hyper, True, fixed_iterations=True)
+        finally:
+            api.set_tuning("RADMM_GPACK", None)
+        bad, near = compare_masks(res[gpack], o, 1e-3, 5)
+        assert bad == 0, (gpack, bad, near)
+        errs = state_errors(res[gpack], o)
+        assert errs["sensor_images"] < 1e-8, (gpack, errs)
+    assert rel(np.concatenate(res[0].sensor_images), np.concatenate(res[1].sensor_images)) < 1e-9
+
+
+def test_pinned_host_buffer_feeds_the_solver():
+    """api.PinnedBuffer (radmm_host_alloc): page-locked operators upload and
+    solve exactly like pageable ones."""
+    cfg = scenario.baseline_config("c1", nside=16, K=32, n_targets=4, max_iter=15)
+    ops, ys, _, hyper = scenario.baseline_problem(cfg)
+    buf = api.PinnedBuffer((cfg.Q, cfg.N, cfg.KM), np.complex64)
+    try:
+        for q, a in enumerate(ops):
+            buf.array[q][:] = np.asarray(a).T
+        pinned = gpu_run([buf.array[q].T for q in range(cfg.Q)], ys, hyper, True, fixed_iterations=True)
+        plain = gpu_run(quantize(ops), ys, hyper, True, fixed_iterations=True)
+    finally:
+        buf.free()
+    assert np.array_equal(np.concatenate(pinned.sensor_images), np.concatenate(plain.sensor_images))
+
+
+def test_transport_timeout_setter_and_validation():
+    """radmm_set_transport_timeout (run_distributed's tcp_timeout_ms): accepted
+    on a sharded context, rejected when < 1 ms."""
+    from paper_2307_08606_b200 import _lib, distributed as D
+    import ctypes as C
+    s = D.sharded_solver(64, 2, 0, 1, 0, D.nccl_unique_id(), tcp_timeout_ms=5000)
+    try:
+        with pytest.raises(api.InvalidArgument):
+            _lib.check(_lib.lib().radmm_set_transport_timeout(s._h, 0))
+    finally:
+        s.close()
+    del C
