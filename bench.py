@@ -362,6 +362,9 @@ def init_dist(args):
     rank, world, local = D.env_rank_world()
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:  # NCCL's init lines (nranks, transports) stay in the log for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist = None
     if world > 1:
         import torch.distributed as tdist
@@ -786,6 +789,7 @@ def spawn_ranks(args) -> bool:
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init lines (nranks) visible in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rc = subprocess.call(cmd, env=env)
     if rc != 0:
         sys.exit(rc)
