@@ -536,13 +536,11 @@ def test_nccl_exchange_path_one_rank_equals_plain(monkeypatch):
     communicator (RADMM_FORCE_NCCL) runs the same per-iteration all-gather of
     the sensor images and the fusion over the gathered buffer as a G-rank run
     does, plus the end-of-run record gather; results equal the plain
-    single-GPU run bitwise (both on the general multi-launch path: the
-    one-launch small-problem iteration is unsharded only)."""
+    single-GPU run bitwise."""
     from paper_2307_08606_b200 import distributed as D
     ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=60)
     hyper = dict(hyper, screening_tol=1e-3)
     h = api.Hyperparams(**hyper)
-    monkeypatch.setenv("RADMM_SMALL", "0")
     plain = gpu_run(ops, ys, hyper, True, fixed_iterations=True)
     monkeypatch.setenv("RADMM_FORCE_NCCL", "1")
     s = D.sharded_solver(ops[0].shape[1], len(ops), 0, 1, 0, D.nccl_unique_id())
@@ -937,3 +935,37 @@ def test_transport_timeout_setter_and_validation():
     finally:
         s.close()
     del C
+
+
+def test_sharded_observer_run_sees_every_iteration(monkeypatch):
+    """Observer runs of a sharded context take the per-iteration metadata
+    all-gather (pinned double-buffered slots): the views and records equal the
+    plain run's, eliminations included."""
+    from paper_2307_08606_b200 import distributed as D
+    ops, ys, hyper = _small_c1(nside=16, K=16, n_targets=4, max_iter=40)
+    hyper = dict(hyper, screening_tol=1e-3)
+    h = api.Hyperparams(**hyper)
+    seen_plain, seen_sharded = [], []
+    plain = api.Solver(ops[0].shape[1], len(ops))
+    try:
+        for q, (a, y) in enumerate(zip(ops, ys)):
+            plain.set_operator(q, a)
+            plain.set_measurement(q, y)
+        rp = plain.run(h, api.Mode.ASADMM, observer=lambda v: seen_plain.append(list(v.active_sizes)),
+                       fixed_iterations=True)
+    finally:
+        plain.close()
+    monkeypatch.setenv("RADMM_FORCE_NCCL", "1")
+    s = D.sharded_solver(ops[0].shape[1], len(ops), 0, 1, 0, D.nccl_unique_id())
+    try:
+        for q, (a, y) in enumerate(zip(ops, ys)):
+            s.set_operator(q, a)
+            s.set_measurement(q, y)
+        rs = s.run(h, api.Mode.ASADMM, observer=lambda v: seen_sharded.append(list(v.active_sizes)),
+                   fixed_iterations=True)
+    finally:
+        s.close()
+    assert seen_sharded == seen_plain and len(seen_plain) == 40
+    assert any(sz != seen_plain[0] for sz in seen_plain)  # eliminations happened
+    assert [r.bytes_sent for r in rs.report.iterations] == [r.bytes_sent for r in rp.report.iterations]
+    assert np.array_equal(rs.sigma, rp.sigma)
