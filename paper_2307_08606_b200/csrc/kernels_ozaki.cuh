@@ -260,7 +260,9 @@ __global__ void oz_rowmax_kernel(const float2* __restrict__ A, int64_t ld, int r
 __global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict__ A, int64_t ld, int rows,
                                                       const int* __restrict__ J, int n, int npad,
                                                       const unsigned* __restrict__ rowmax, int8_t* __restrict__ P,
-                                                      int8_t* __restrict__ Q, int64_t slice_stride) {
+                                                      int8_t* __restrict__ Q, int64_t slice_stride, int col0) {
+  // columns col0 .. col0 + n of the list (a pixel chunk of the chunked Gram;
+  // col0 = 0, n = all for the one-pass Gram) land in slice columns 0 .. n
   oz_pdl_enter();
   __shared__ int8_t sre[kOzSlices][64][33], sim[kOzSlices][64][33];
   const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 32;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict_
     const int c = c0 + cc;
     double vr = 0.0, vi = 0.0;
     if (r < rows && c < n) {
-      const float2 a = A[r + (int64_t)(J ? J[c] : c) * ld];
+      const float2 a = A[r + (int64_t)(J ? J[col0 + c] : col0 + c) * ld];
       vr = ldexp((double)a.x, -e);
       vi = ldexp((double)a.y, -e);
     }
@@ -301,8 +303,10 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const float2* __restrict_
       const int8_t re = sre[sl][rr][cc], im = sim[sl][rr][cc];
       Pr[c] = re;
       Pr[npad + c] = im;
-      Qr[c] = im;
-      Qr[npad + c] = (int8_t)(-re);
+      if (Q) {  // the chunked Gram needs no negated copy
+        Qr[c] = im;
+        Qr[npad + c] = (int8_t)(-re);
+      }
     }
   }
 }
@@ -499,6 +503,206 @@ __global__ void oz_combine_kernel(const int32_t* __restrict__ R, const unsigned*
   re = ldexp(re, ei + ej);
   im = ldexp(im, ei + ej);
   double2 o = make_double2(mu * re, mu * im);
+  if (i == j) {
+    o.x += beta;
+    o.y = 0.0;
+  }
+  C[i + (int64_t)j * ldc] = o;
+  if (i != j) C[j + (int64_t)i * ldc] = make_double2(o.x, -o.y);
+}
+
+// ---------------------------------------------------------------------------
+// Chunked Gram for problems whose one-pass scratch (all slices + one int32
+// block per tile and pair: config 3, 26 GB per sensor) does not fit next to
+// the resident operators, and whose one-pass pair kernel is bound by the
+// L2 -> SM operand feed (48 KB per 4.2 M MACs; measured 47% tensor pipe at
+// config-3 shapes).  The pixels are processed kOzChunk at a time: a chunk is
+// sliced into a small scratch holding only P_s = [Re d_s | Im d_s]
+// (7 x rows x 2*kOzChunk bytes), and oz_gram_chunk_kernel -- ONE CTA per lower
+// 128 x 128 tile -- walks all 39 slice pairs of the chunk.  A stage carries
+// the Re and Im halves of both operands (4 x 16 KB) and feeds FOUR real
+// products,
+//   Re += Re_a Re_b^T + Im_a Im_b^T,  X += Im_a Re_b^T,  Y += Re_a Im_b^T,
+//   Im = X - Y  (in the epilogue: no negated slices are stored),
+// i.e. 64 KB per 8.4 M MACs.  Pairs with the same t = s1 + s2 carry the same
+// weight 2^-7t, so they accumulate in the same TMEM accumulators (exact: at
+// most 7 pairs x 2*kOzChunk x 127^2 < 2^31); after each of the 9 weight
+// groups the four epilogue warps add the group's int32 blocks, scaled, to
+// fp64 accumulators in C (chunk-major, then t ascending: a fixed order).
+// oz_gram_finish_kernel then scales by mu 2^{e_i+e_j}, adds beta and mirrors,
+// like oz_combine_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kOzChunk = 8192;  // pixels per chunk: 7 * 2 * 8192 * 127^2 = 1.85e9 < 2^31
+constexpr int kOzGroups = kOzMaxSum - 1;  // t = 2 .. kOzMaxSum
+constexpr int kOzCThreads = 192;  // warps 0-3: epilogue (TMEM lanes 32w..), warp 4: TMA producer, warp 5: MMA issuer
+constexpr int kOzCStages = 3;
+constexpr int kOzCStageBytes = 4 * kOzBM * kOzBK;  // Re_a | Im_a | Re_b | Im_b, 16 KB each
+constexpr size_t kOzCSmem = (size_t)kOzCStages * kOzCStageBytes + 1024 + 256;
+
+__device__ __forceinline__ void oz_mma_i8(uint32_t d, uint64_t ad, uint64_t bd, uint32_t en) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(kOzIdesc), "r"(en), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+__device__ __forceinline__ void oz_tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+// tP: 2-D int8 map over the chunk's P slices, [kOzSlices * rows_pad] rows x
+// (2 * half) bytes; half = chunk columns (a multiple of kOzBK): Re at byte
+// columns [0, half), Im at [half, 2 half).
+__global__ void __launch_bounds__(kOzCThreads, 1) oz_gram_chunk_kernel(const __grid_constant__ CUtensorMap tP,
+                                                                      int rows_pad, int half, int rows,
+                                                                      double2* __restrict__ C, int64_t ldc) {
+  oz_pdl_enter();
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)kOzCStages * kOzCStageBytes);
+  uint64_t* empty = full + kOzCStages;
+  uint64_t* accfull = empty + kOzCStages;  // a weight group's MMAs are complete
+  uint64_t* accfree = accfull + 1;         // the epilogue has drained the accumulators
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accfree + 1);
+  int tile = blockIdx.x, I = 0;
+  while (tile > I) {
+    tile -= I + 1;
+    ++I;
+  }
+  const int Jt = tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kOzCStages; ++st) {
+      oz_mbar_init(&full[st], 1);
+      oz_mbar_init(&empty[st], 1);
+    }
+    oz_mbar_init(accfull, 1);
+    oz_mbar_init(accfree, 4);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int nk = half / kOzBK;
+  if (warp == 4 && lane == 0) {  // producer: every (group, pair, k block) in order
+    uint32_t it = 0;
+    for (int t = 2; t <= kOzMaxSum; ++t)
+      for (int s1 = 1; s1 <= kOzSlices; ++s1) {
+        const int s2 = t - s1;
+        if (s2 < 1 || s2 > kOzSlices) continue;
+        const int ya = (s1 - 1) * rows_pad + I * kOzBM, yb = (s2 - 1) * rows_pad + Jt * kOzBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % kOzCStages;
+          if (it >= (uint32_t)kOzCStages) oz_mbar_wait(&empty[st], ((it / kOzCStages) - 1) & 1);
+          const uint32_t sa = smem_u32(base + (size_t)st * kOzCStageBytes), fb = smem_u32(&full[st]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(kOzCStageBytes)
+                       : "memory");
+          oz_tma_2d(sa, &tP, kb * kOzBK, ya, fb);
+          oz_tma_2d(sa + kOzBM * kOzBK, &tP, half + kb * kOzBK, ya, fb);
+          oz_tma_2d(sa + 2 * kOzBM * kOzBK, &tP, kb * kOzBK, yb, fb);
+          oz_tma_2d(sa + 3 * kOzBM * kOzBK, &tP, half + kb * kOzBK, yb, fb);
+        }
+      }
+  } else if (warp == 5 && lane == 0) {  // MMA issuer
+    uint32_t it = 0;
+    int g = 0;
+    for (int t = 2; t <= kOzMaxSum; ++t, ++g) {
+      if (g >= 1) {  // the epilogue has read the previous group
+        oz_mbar_wait(accfree, (g - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      bool fresh = true;  // the group's first MMAs overwrite the accumulators
+      for (int s1 = 1; s1 <= kOzSlices; ++s1) {
+        const int s2 = t - s1;
+        if (s2 < 1 || s2 > kOzSlices) continue;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % kOzCStages;
+          oz_mbar_wait(&full[st], (it / kOzCStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(base + (size_t)st * kOzCStageBytes);
+#pragma unroll
+          for (int k = 0; k < kOzBK / 32; ++k) {
+            const uint32_t first = (fresh && k == 0) ? 0u : 1u;
+            const uint64_t re_a = oz_desc(sa + 32 * k), im_a = oz_desc(sa + kOzBM * kOzBK + 32 * k);
+            const uint64_t re_b = oz_desc(sa + 2 * kOzBM * kOzBK + 32 * k), im_b = oz_desc(sa + 3 * kOzBM * kOzBK + 32 * k);
+            oz_mma_i8(tmem, re_a, re_b, first);         // Re += Re_a Re_b^T
+            oz_mma_i8(tmem, im_a, im_b, 1u);            // Re += Im_a Im_b^T
+            oz_mma_i8(tmem + 128u, im_a, re_b, first);  // X  += Im_a Re_b^T
+            oz_mma_i8(tmem + 256u, re_a, im_b, first);  // Y  += Re_a Im_b^T
+          }
+          fresh = false;
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(accfull))
+                   : "memory");
+    }
+  } else if (warp < 4) {  // epilogue: row i of the tile per thread
+    const int i = I * kOzBM + 32 * warp + lane;
+    for (int g = 0; g < kOzGroups; ++g) {
+      oz_mbar_wait(accfull, g & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const double sc = __longlong_as_double((long long)(1023 - 7 * (g + 2)) << 52);  // 2^-7t
+      for (int c0 = 0; c0 < kOzBN; c0 += 16) {
+        uint32_t vr[16], vx[16], vy[16];
+        const uint32_t ar = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0;
+        oz_tmem_ld16(ar, vr);
+        oz_tmem_ld16(ar + 128u, vx);
+        oz_tmem_ld16(ar + 256u, vy);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // a warp's 32 rows are consecutive in a column of C: 512-byte accesses
+        double2 acc[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = Jt * kOzBN + c0 + jj;
+          acc[jj] = (i < rows && j < rows) ? C[i + (int64_t)j * ldc] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = Jt * kOzBN + c0 + jj;
+          if (i < rows && j < rows)  // |X - Y| < 2^31: the difference is exact in int64, then in fp64
+            C[i + (int64_t)j * ldc] =
+                make_double2(fma(sc, (double)(int)vr[jj], acc[jj].x),
+                             fma(sc, (double)((long long)(int)vx[jj] - (long long)(int)vy[jj]), acc[jj].y));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accfree)) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// C[i, j] (i >= j) <- mu 2^{e_i + e_j} acc[i, j] (+ beta on the diagonal, exact
+// real), mirrored conjugate to C[j, i]; acc is what oz_gram_chunk_kernel left.
+__global__ void oz_gram_finish_kernel(const unsigned* __restrict__ rowmax, int rows, double2* __restrict__ C,
+                                      int64_t ldc, double mu, double beta) {
+  oz_pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i >= rows || j >= rows || i < j) return;
+  const float mi = __uint_as_float(rowmax[i]), mj = __uint_as_float(rowmax[j]);
+  const int ei = mi > 0.f ? ilogbf(mi) + 1 : 0, ej = mj > 0.f ? ilogbf(mj) + 1 : 0;
+  const double2 a = C[i + (int64_t)j * ldc];
+  double2 o = make_double2(mu * ldexp(a.x, ei + ej), mu * ldexp(a.y, ei + ej));
   if (i == j) {
     o.x += beta;
     o.y = 0.0;

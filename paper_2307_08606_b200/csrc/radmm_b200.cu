@@ -1323,26 +1323,83 @@ double ozaki_scratch_bytes(int rows, int n) {
   return 2.0 * kOzSlices * rows_pad * kdim + 4.0 * tiles * kOzPairs * 2 * kOzBM * kOzBN + 4.0 * rows_pad;
 }
 
+// Scratch of the chunked Gram: the P slices of one pixel chunk + row maxima.
+double ozaki_chunk_scratch_bytes(int rows, int n) {
+  using namespace radmm_oz;
+  const double rows_pad = (double)round_up(rows, kOzBM);
+  const double half = (double)std::min<int64_t>(kOzChunk, round_up(n, kOzBK));
+  return kOzSlices * rows_pad * 2.0 * half + 4.0 * rows_pad;
+}
+
+// RADMM_OZ_CHUNK: 0 = one-pass Gram only, 1 (default) = chunked Gram when the
+// one-pass scratch does not fit, 2 = always chunked (tests).
+int ozaki_chunk_mode() { return env_int("RADMM_OZ_CHUNK", 1); }
+
+// The chunked Gram (kernels_ozaki.cuh, oz_gram_chunk_kernel): C must be zeroed
+// by the caller (it holds the fp64 accumulators between chunks).
+bool ozaki_gram_chunked(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_t ldc, double mu, double beta) {
+  using namespace radmm_oz;
+  const int rows = S.rows;
+  const int T = (rows + kOzBM - 1) / kOzBM, tiles = T * (T + 1) / 2;
+  const int64_t rows_pad = (int64_t)T * kOzBM;
+  const int half = (int)std::min<int64_t>(kOzChunk, round_up(n, kOzBK));  // slice columns per part
+  const size_t pbytes = (size_t)kOzSlices * rows_pad * 2 * half;
+  if (c->oz_P.n < pbytes || c->oz_rowmax.n < (size_t)rows_pad) {
+    const size_t free_b = mem_available(c->device);
+    const size_t held = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
+    if (free_b + held < pbytes + rows_pad * 4 + (3ull << 30)) return false;
+    if (c->oz_P.n < pbytes) {
+      c->oz_Q.release();
+      c->oz_R.release();
+      c->oz_P.alloc(pbytes, false);
+    }
+    if (c->oz_rowmax.n < (size_t)rows_pad) c->oz_rowmax.alloc(rows_pad, false);
+  }
+  CUtensorMap tP;
+  if (!slice_tensor_map(&tP, c->oz_P.p, (int64_t)kOzSlices * rows_pad, 2 * (int64_t)half)) return false;
+  CK(cudaMemsetAsync(c->oz_rowmax.p, 0, sizeof(unsigned) * rows_pad, c->stream));
+  CK(cudaMemsetAsync(c->oz_P.p, 0, pbytes, c->stream));  // padding rows / columns are zero slices
+  const int split = std::max(1, std::min(64, n / 256));
+  LAUNCH(c, oz_rowmax_kernel, dim3((unsigned)((rows + 255) / 256), (unsigned)split), 256, 0, S.A.p, S.ld, rows, J, n,
+         c->oz_rowmax.p);
+  set_smem_attr((const void*)oz_gram_chunk_kernel, (int)((int)kOzCSmem));
+  const int64_t slice = rows_pad * 2 * half;
+  for (int c0 = 0; c0 < n; c0 += half) {
+    const int cn = std::min(half, n - c0);
+    if (cn < half && c0 > 0)  // a short last chunk: the columns past it must read as zero
+      CK(cudaMemsetAsync(c->oz_P.p, 0, pbytes, c->stream));
+    LAUNCH(c, oz_slice_kernel, dim3((unsigned)((cn + 31) / 32), (unsigned)((rows + 63) / 64)), 256, 0, S.A.p, S.ld,
+           rows, J, cn, half, c->oz_rowmax.p, c->oz_P.p, (int8_t*)nullptr, slice, c0);
+    LAUNCH(c, oz_gram_chunk_kernel, dim3((unsigned)tiles), kOzCThreads, kOzCSmem, tP, (int)rows_pad, half, rows, C,
+           ldc);
+  }
+  LAUNCH(c, oz_gram_finish_kernel, dim3((unsigned)((rows + 255) / 256), (unsigned)rows), 256, 0, c->oz_rowmax.p, rows,
+         C, ldc, mu, beta);
+  return true;
+}
+
 // C = beta I + mu A_J A_J^H (rows x rows, lower tiles + exact mirror) for one
 // sensor; returns false (caller falls back to the fp64 DMMA Gram) when the
-// slices do not fit next to 4 GB of free HBM or the shape is out of range.
+// slices do not fit next to the resident problem or the shape is out of range.
+// C arrives zeroed.
 bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_t ldc, double mu, double beta) {
   using namespace radmm_oz;
   if (!ozaki_enabled() || n < 1 || n > 65536) return false;
+  const int chunk_mode = ozaki_chunk_mode();
+  if (chunk_mode == 2) return ozaki_gram_chunked(c, S, J, n, C, ldc, mu, beta);
   const int rows = S.rows;
   const int T = (rows + kOzBM - 1) / kOzBM, tiles = T * (T + 1) / 2;
   const int64_t rows_pad = (int64_t)T * kOzBM, npad = round_up(n, 64), kdim = 2 * npad;
   const size_t slice = (size_t)rows_pad * kdim, pq = (size_t)kOzSlices * slice;
   const size_t rblk = (size_t)tiles * kOzPairs * 2 * kOzBM * kOzBN;
   const size_t need = 2 * pq + rblk * 4 + rows_pad * 4;
-  if (c->oz_P.n < pq || c->oz_R.n < rblk || c->oz_rowmax.n < (size_t)rows_pad) {
+  if (c->oz_P.n < pq || c->oz_Q.n < pq || c->oz_R.n < rblk || c->oz_rowmax.n < (size_t)rows_pad) {
     const size_t free_b = mem_available(c->device);
     const size_t held = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
-    if (free_b + held < need + (4ull << 30)) return false;
-    if (c->oz_P.n < pq) {
-      c->oz_P.alloc(pq, false);
-      c->oz_Q.alloc(pq, false);
-    }
+    if (free_b + held < need + (4ull << 30))
+      return chunk_mode == 1 && ozaki_gram_chunked(c, S, J, n, C, ldc, mu, beta);
+    if (c->oz_P.n < pq) c->oz_P.alloc(pq, false);
+    if (c->oz_Q.n < pq) c->oz_Q.alloc(pq, false);
     if (c->oz_R.n < rblk) c->oz_R.alloc(rblk, false);
     if (c->oz_rowmax.n < (size_t)rows_pad) c->oz_rowmax.alloc(rows_pad, false);
   }
@@ -1353,7 +1410,7 @@ bool ozaki_gram(radmm_ctx* c, Sensor& S, const int* J, int n, double2* C, int64_
   LAUNCH(c, oz_rowmax_kernel, dim3((unsigned)((rows + 255) / 256), (unsigned)split), 256, 0, S.A.p, S.ld, rows, J, n,
          c->oz_rowmax.p);
   LAUNCH(c, oz_slice_kernel, dim3((unsigned)((n + 31) / 32), (unsigned)((rows + 63) / 64)), 256, 0, S.A.p, S.ld, rows,
-         J, n, (int)npad, c->oz_rowmax.p, c->oz_P.p, c->oz_Q.p, (int64_t)slice);
+         J, n, (int)npad, c->oz_rowmax.p, c->oz_P.p, c->oz_Q.p, (int64_t)slice, 0);
   CUtensorMap tP, tQ;
   if (env_int("RADMM_OZ_TMA", 1) && slice_tensor_map(&tP, c->oz_P.p, (int64_t)kOzSlices * rows_pad, kdim) &&
       slice_tensor_map(&tQ, c->oz_Q.p, (int64_t)kOzSlices * rows_pad, kdim)) {
@@ -3906,10 +3963,16 @@ void eager_gram(radmm_ctx* c, Sensor& S, int q, cudaEvent_t ev) {
       size_t free_now = 0, total = 0;
       CK(cudaMemGetInfo(&free_now, &total));
       const double per_sensor = (double)S.ld * c->N * sizeof(float2) + 2.0 * cn * sizeof(double2) + 64.0 * c->N * 16;
-      c->oz_eager = (per_sensor * c->Q + ozaki_scratch_bytes(S.rows, c->N) + tmp * 16.0 + (8.0 * (1ull << 30)) <
-                     (double)total) ? 1 : 0;
+      // 1: the one-pass Gram's scratch fits; 2: only the chunked Gram's does
+      // (config 3: 0.94 GB instead of 26 GB); 0: neither (fp64 DMMA Gram)
+      const double base = per_sensor * c->Q + tmp * 16.0 + (8.0 * (1ull << 30));
+      const int mode = ozaki_chunk_mode();
+      c->oz_eager = (mode != 2 && base + ozaki_scratch_bytes(S.rows, c->N) < (double)total) ? 1
+                    : (mode >= 1 && base + ozaki_chunk_scratch_bytes(S.rows, c->N) < (double)total) ? 2 : 0;
     }
-    const bool oz = c->oz_eager == 1 && ozaki_gram(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0);
+    const bool oz = (c->oz_eager == 1 && ozaki_gram(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0)) ||
+                    (c->oz_eager == 2 && ozaki_enabled() && c->N <= 65536 &&
+                     ozaki_gram_chunked(c, S, nullptr, c->N, T, S.ld, 1.0, 0.0));
     if (!oz) {  // (the Ozaki scratch stays allocated for the next upload; the first run releases it)
       const GramJob g{S.A.p, S.ld, nullptr, c->N, S.rows, T, S.ld};
       set_smem_attr((const void*)gram_dmma1_kernel, (int)((int)kGramSmem));

@@ -198,7 +198,7 @@ def test_c4_elimination_masks_at_c2_geometry():
         assert errs["sensor_images"] < NORTH_STAR_TOL, errs
 
 
-@pytest.mark.parametrize("ozaki", [True, False])
+@pytest.mark.parametrize("ozaki", [True, "chunked", False])
 def test_c3_shapes_two_sensors(ozaki, monkeypatch):
     """Config 3 shapes (KM = 8192, N = 65536) with Q = 2 against the oracle:
     the tall-forward / row-segmented-adjoint paths and both Gram paths (int8
@@ -209,13 +209,15 @@ def test_c3_shapes_two_sensors(ozaki, monkeypatch):
     ys = fx["ys"]
     if not ozaki:
         monkeypatch.setenv("RADMM_OZAKI", "0")
+    if ozaki == "chunked":  # the Gram config 3 itself uses at Q = 32 (one-pass scratch does not fit)
+        monkeypatch.setenv("RADMM_OZ_CHUNK", "2")
     s = device_problem(cfg, ys.shape[0], fx["digests"], ys)
     try:
         g = s.run(fixture_hyper(fx), api.Mode.ASADMM, fixed_iterations=True)
     finally:
         s.close()
     errs = state_vs(g, fx)
-    print(f"C3 shapes, Q=2, {'ozaki' if ozaki else 'dmma'} Gram: {errs}")
+    print(f"C3 shapes, Q=2, {('ozaki ' + str(ozaki)) if ozaki else 'dmma'} Gram: {errs}")
     for k, v in errs.items():
         assert v < NORTH_STAR_TOL, errs
     assert errs["sensor_images"] < 1e-7, errs

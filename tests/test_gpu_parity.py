@@ -153,6 +153,27 @@ def test_ozaki_tcgen05_gram_matches_fp64_gram(rows, cols, monkeypatch):
     assert rel(outs["1"], outs["0"]) < 1e-8, rel(outs["1"], outs["0"])
 
 
+@pytest.mark.parametrize("rows,cols", [(300, 1000), (256, 20000), (130, 700), (1100, 9000)])
+def test_ozaki_chunked_gram_matches_fp64_gram(rows, cols, monkeypatch):
+    """The chunked Gram (RADMM_OZ_CHUNK=2: 8192-pixel chunks, one CTA per tile
+    walking all slice pairs, four real int8 products per stage, fp64
+    accumulation across chunks; config 3's upload-time Gram) against the fp64
+    DMMA Gram: one chunk, several chunks with a short last one, ragged rows."""
+    rng = np.random.default_rng(rows + cols)
+    a = (rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols))).astype(np.complex64)
+    a[:, ::7] *= 1e-3  # columns of very different magnitude: deep slices matter
+    rhs = rng.normal(size=cols) + 1j * rng.normal(size=cols)
+    outs = {}
+    monkeypatch.setenv("RADMM_OZ_CHUNK", "2")
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RADMM_OZAKI", flag)
+        outs[flag] = api.factorize(a.astype(np.complex128), 1.0, 1.0).solve(rhs)
+    assert rel(outs["1"], outs["0"]) < 1e-8, rel(outs["1"], outs["0"])
+    cap = np.eye(rows) + a.astype(np.complex128) @ a.astype(np.complex128).conj().T
+    ref = rhs - a.astype(np.complex128).conj().T @ np.linalg.solve(cap, a.astype(np.complex128) @ rhs)
+    assert rel(outs["1"], ref) < 1e-8, rel(outs["1"], ref)
+
+
 def test_tall_operator_dual_solve_matches_dense():
     """A dual solve on an operator taller than 4096 rows (1024-thread forward
     tiles, as at config 3) against a dense complex128 solve."""

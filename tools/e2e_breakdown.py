@@ -21,12 +21,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--fixed", type=int, default=0, help="fixed iteration count (0: to tolerance)")
+    ap.add_argument("--q", type=int, default=0, help="override the sensor count (setup probes at config-3 shapes)")
     a = ap.parse_args()
     import torch
 
     import bench
     from paper_2307_08606_b200 import api, scenario
-    cfg = scenario.baseline_config(a.config)
+    cfg = scenario.baseline_config(a.config, **({"Q": a.q} if a.q else {}))
     gen = api.Solver(cfg.N, cfg.Q)
     ys, lam = bench.build_workload(cfg, gen, 0, cfg.Q)
     hyper = api.Hyperparams(mu=cfg.mu, lambda_=lam, beta=cfg.beta, eps_abs=cfg.eps_abs, eps_rel=cfg.eps_rel,
