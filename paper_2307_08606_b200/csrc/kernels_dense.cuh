@@ -510,11 +510,17 @@ struct GjUpdJob {
   int k0, kb;
 };
 
+// HERM: the Hermitian sweep (gj_invert, herm = true): F = T = M[:, K] P,
+// R[k, j] = conj(M[j, K][k]); only tiles that touch the lower triangle
+// (n0 < m0 + 128) are updated, M[i, j] -= (T R)[i, j] everywhere in them; the
+// pivot rows / columns are rewritten afterwards by gj_hfix_kernel.
+template <bool HERM>
 __global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant__ Pack<GjUpdJob> P) {
   pdl_enter();
   const GjUpdJob& jb = P.j[blockIdx.z];
   const int m0 = blockIdx.y * kGjuBM, n0 = blockIdx.x * kGjuBN, n = jb.n, kb = jb.kb;
   if (m0 >= n || n0 >= n) return;
+  if (HERM && n0 >= m0 + kGjuBM) return;  // strictly upper tile: never read
   extern __shared__ __align__(16) double2 gju[];
   double2* Fs = gju;                   // [k][kGjuPF]
   double2* Rs = gju + 64 * kGjuPF;     // [k][kGjuPR]
@@ -570,7 +576,7 @@ __global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int i = m0 + wm + 8 * a + fr;
-    const bool iK = i >= jb.k0 && i < jb.k0 + kb;
+    const bool iK = !HERM && i >= jb.k0 && i < jb.k0 + kb;
     double2 cin[4][2];
 #pragma unroll
     for (int b = 0; b < 4; ++b)
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(256, 1) gj_update_kernel(const __grid_constant
         cin[b][v] = make_double2(0.0, 0.0);
         if (i >= n || j >= n) continue;
         if (iK) cin[b][v] = jb.R[(i - jb.k0) + (int64_t)j * 64];
-        else if (!(j >= jb.k0 && j < jb.k0 + kb)) cin[b][v] = jb.M[i + (int64_t)j * jb.ldm];
+        else if (HERM || !(j >= jb.k0 && j < jb.k0 + kb)) cin[b][v] = jb.M[i + (int64_t)j * jb.ldm];
       }
 #pragma unroll
     for (int b = 0; b < 4; ++b)
@@ -640,6 +646,7 @@ struct DiagJob {
   double2* R;     // row panel R' (kb x n), ld = ldr
   int64_t ldr;
   int* fail;
+  int herm;       // Hermitian sweep: the pivot block and its inverse are made exactly Hermitian
 };
 
 __global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
@@ -656,6 +663,23 @@ __global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ P
     S[r][c] = jb.M[(jb.k0 + r) + (int64_t)(jb.k0 + c) * jb.ld];
   }
   __syncthreads();
+  // Hermitian sweep: the row panel is taken as the conjugate transpose of the
+  // column panel M[:, K] P, which is only consistent if P is exactly
+  // Hermitian -- an unsymmetric rounding-level defect of P compounds from
+  // block to block (measured on config 2's capacitance, cond 2e5: |G C - I|
+  // 4.7e3 without this, 2e-7 with it; the general sweep: 1.3e-6).
+  auto hermitize = [&]() {
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+      const int r = e % kb, c = e / kb;
+      if (r < c) continue;
+      const double2 a = S[r][c], b = S[c][r];
+      const double2 m = r == c ? make_double2(a.x, 0.0) : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      S[r][c] = m;
+      S[c][r] = make_double2(m.x, -m.y);
+    }
+    __syncthreads();
+  };
+  if (jb.herm) hermitize();
   for (int p = 0; p < kb; ++p) {
     const double2 piv = S[p][p];
     if (threadIdx.x == 0 && !(piv.x > 0.0 && isfinite(piv.x) && isfinite(piv.y))) atomicExch(jb.fail, 1);
@@ -681,6 +705,7 @@ __global__ void __launch_bounds__(1024) gj_diag_kernel(const __grid_constant__ P
     }
     __syncthreads();
   }
+  if (jb.herm) hermitize();
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
     const int r = e % kb, c = e / kb;
     jb.P[r + (int64_t)c * jb.ldp] = S[r][c];
@@ -707,6 +732,96 @@ __global__ void gj_fix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
   for (int e = threadIdx.x; e < jb.kb * jb.kb; e += blockDim.x) {
     const int r = e % jb.kb, c = e / jb.kb;
     jb.R[r + (int64_t)(jb.k0 + c) * jb.ldr] = jb.P[r + (int64_t)c * jb.ldp];
+  }
+}
+
+// ---- Hermitian sweep (blocked symmetric Gauss-Jordan for HPD matrices) -------
+// Sweeping pivot block K of a Hermitian M:  M_KK <- -inv(M_KK) = -P,
+// M_iK <- M_iK P,  M_ij <- M_ij - M_iK P M_Kj; every intermediate matrix is
+// Hermitian, so only the lower triangle is kept and updated (half the DMMA
+// work and half the memory traffic of the general sweep), and after the last
+// block M = -inv(M0).
+//
+// F[i, c] = M[i, k0 + c] read from the lower triangle (rows above the pivot
+// block come from the conjugate of the pivot rows), and R[c, i] = conj(F[i, c])
+// (the update's right operand).
+__global__ void gj_hpanel_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  pdl_enter();
+  const DiagJob& jb = jobs.j[blockIdx.y];
+  if (jb.k0 >= jb.n) return;
+  const int kb = jb.kb, k0 = jb.k0;
+  // rows at / below the pivot block: column segments of M (row index fastest)
+  const int64_t low = (int64_t)(jb.n - k0) * kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < low; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = k0 + (int)(e % (jb.n - k0)), c = (int)(e / (jb.n - k0));
+    const double2 v = jb.M[i + (int64_t)(k0 + c) * jb.ld];
+    jb.F[i + (int64_t)c * jb.ldf] = v;
+    jb.R[c + (int64_t)i * jb.ldr] = make_double2(v.x, -v.y);
+  }
+  // rows above: conj of the pivot rows (pivot-row index fastest: contiguous in M)
+  const int64_t up = (int64_t)k0 * kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < up; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % kb), i = (int)(e / kb);
+    const double2 v = jb.M[(k0 + c) + (int64_t)i * jb.ld];
+    jb.F[i + (int64_t)c * jb.ldf] = make_double2(v.x, -v.y);
+    jb.R[c + (int64_t)i * jb.ldr] = v;
+  }
+}
+
+// After the update: M[i, K] = T[i, :] below the pivot block, M[K, i] = T[i, :]^H
+// left of it, M_KK = -P.  T = F P (n x kb, ld = ldf) travels in jb.F.
+__global__ void gj_hfix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
+  pdl_enter();
+  const DiagJob& jb = jobs.j[blockIdx.y];
+  if (jb.k0 >= jb.n) return;
+  const int kb = jb.kb, k0 = jb.k0;
+  const int64_t low = (int64_t)(jb.n - k0) * kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < low; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = k0 + (int)(e % (jb.n - k0)), c = (int)(e / (jb.n - k0));
+    double2 v;
+    if (i < k0 + kb) {
+      const double2 p = jb.P[(i - k0) + (int64_t)c * jb.ldp];
+      v = make_double2(-p.x, -p.y);
+    } else {
+      v = jb.F[i + (int64_t)c * jb.ldf];
+    }
+    const_cast<double2*>(jb.M)[i + (int64_t)(k0 + c) * jb.ld] = v;
+  }
+  const int64_t up = (int64_t)k0 * kb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < up; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % kb), i = (int)(e / kb);
+    const double2 v = jb.F[i + (int64_t)c * jb.ldf];
+    const_cast<double2*>(jb.M)[(k0 + c) + (int64_t)i * jb.ld] = make_double2(v.x, -v.y);
+  }
+}
+
+// M <- -M on the lower triangle, mirrored conjugate to the upper one, real
+// diagonal: the inverse, exactly Hermitian.  One 32 x 32 tile (I >= J) per CTA.
+__global__ void __launch_bounds__(256) gj_hfinish_kernel(double2* __restrict__ G, int64_t ld, int n) {
+  pdl_enter();
+  __shared__ double2 a[32][33];
+  int t = blockIdx.x, I = 0;
+  while (t > I) { t -= I + 1; ++I; }
+  const int J = t;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;  // tile (I, J): column j, row i
+    double2 v = (i < n && j < n) ? G[i + (int64_t)j * ld] : make_double2(0.0, 0.0);
+    if (I == J && i < j) {  // upper half of a diagonal tile: from its mirror, below
+      v = (i < n && j < n) ? G[j + (int64_t)i * ld] : make_double2(0.0, 0.0);
+      v.y = -v.y;
+    }
+    v = make_double2(-v.x, -v.y);
+    if (i == j) v.y = 0.0;
+    a[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = I * 32 + tx, j = J * 32 + r;
+    if (i < n && j < n) G[i + (int64_t)j * ld] = a[r][tx];
+    const int i2 = J * 32 + tx, j2 = I * 32 + r;  // tile (J, I) = conj transpose
+    const double2 v = a[tx][r];
+    if (I != J && i2 < n && j2 < n) G[i2 + (int64_t)j2 * ld] = make_double2(v.x, -v.y);
   }
 }
 

@@ -536,6 +536,7 @@ constexpr int kOzChunk = 8192;  // pixels per chunk: 7 * 2 * 8192 * 127^2 = 1.85
 constexpr int kOzGroups = kOzMaxSum - 1;  // t = 2 .. kOzMaxSum
 constexpr int kOzCThreads = 192;  // warps 0-3: epilogue (TMEM lanes 32w..), warp 4: TMA producer, warp 5: MMA issuer
 constexpr int kOzCStages = 3;
+constexpr int kOzBand = 12;  // tile rows per band of the launch order
 constexpr int kOzCStageBytes = 4 * kOzBM * kOzBK;  // Re_a | Im_a | Re_b | Im_b, 16 KB each
 constexpr size_t kOzCSmem = (size_t)kOzCStages * kOzCStageBytes + 1024 + 256;
 
@@ -571,12 +572,35 @@ __global__ void __launch_bounds__(kOzCThreads, 1) oz_gram_chunk_kernel(const __g
   uint64_t* accfull = empty + kOzCStages;  // a weight group's MMAs are complete
   uint64_t* accfree = accfull + 1;         // the epilogue has drained the accumulators
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accfree + 1);
-  int tile = blockIdx.x, I = 0;
-  while (tile > I) {
-    tile -= I + 1;
-    ++I;
+  // Tile order: bands of kOzBand tile rows, column by column inside a band, so
+  // the ~148 CTAs resident together cover a ~12 x 12 block of tiles and share
+  // 12 + 12 row blocks of slices through L2 (row-major order: 3 + 40).
+  int I, Jt;
+  {
+    const int T = rows_pad / kOzBM;
+    int idx = blockIdx.x, r0 = 0, h = min(kOzBand, T);
+    for (;;) {  // band [r0, r0 + h): sum_{I in band} (I + 1) tiles
+      const int cnt = h * r0 + h * (h + 1) / 2;
+      if (idx < cnt) break;
+      idx -= cnt;
+      r0 += h;
+      h = min(kOzBand, T - r0);
+    }
+    const int full = (r0 + 1) * h;  // columns 0 .. r0: every row of the band
+    if (idx < full) {
+      Jt = idx / h;
+      I = r0 + idx % h;
+    } else {  // columns r0 + 1 ..: rows Jt .. r0 + h - 1
+      idx -= full;
+      int col = 1;
+      while (idx >= h - col) {
+        idx -= h - col;
+        ++col;
+      }
+      Jt = r0 + col;
+      I = Jt + idx;
+    }
   }
-  const int Jt = tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kOzCStages; ++st) {

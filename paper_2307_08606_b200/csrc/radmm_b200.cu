@@ -1142,20 +1142,26 @@ constexpr int kGJB = 64;
 void check_deferred(radmm_ctx* c);
 
 // Inverts every target in place; raises RADMM_NUMERICAL if a pivot fails.
-void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* what) {
+// herm = true: the Hermitian sweep (kernels_dense.cuh, gj_hpanel_kernel): the
+// targets are HPD with a valid lower triangle (and diagonal 64-blocks); only
+// lower tiles are updated -- half the work -- and the result is written
+// exactly Hermitian (no projection pass needed).  Needs one more n x 64 panel
+// of scratch per target.
+void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* what, bool herm = false) {
   if (targets.empty()) return;
   if (targets.size() > kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many matrices in one batch");
   const size_t T = targets.size();
-  // scratch: P (64x64), F (n x 64), R (64 x n) per target
+  // scratch: P (64x64), F (n x 64), R (64 x n) (+ T = F P, n x 64) per target
   size_t need = 0;
-  for (const auto& t : targets) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 3 * 256;
+  for (const auto& t : targets)
+    need += (64 * 64 + (herm ? 3 : 2) * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 4 * 256;
   Scratch& sc = c->scratch;
   const size_t base_off = sc.off;
   if (sc.off + need > sc.buf.n) {
     // grow: preserve nothing (callers take scratch before gj only for inputs they own)
     fail(RADMM_OUT_OF_MEMORY, "scratch arena too small for Gauss-Jordan inverse");
   }
-  std::vector<double2*> P(T), F(T), R(T);
+  std::vector<double2*> P(T), F(T), R(T), TP(T);
   std::vector<int64_t> ldf(T);
   int n_max = 0;
   for (size_t i = 0; i < T; ++i) {
@@ -1163,9 +1169,11 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     P[i] = sc.take<double2>(64 * 64);
     F[i] = sc.take<double2>((size_t)nn * 64);
     R[i] = sc.take<double2>((size_t)nn * 64);
+    TP[i] = herm ? sc.take<double2>((size_t)nn * 64) : nullptr;
     ldf[i] = nn;
     n_max = std::max(n_max, targets[i].n);
   }
+  if (herm && n_max <= kGJB) herm = false;  // single pivot block: the in-shared-memory inverse below
   CK(cudaMemsetAsync(c->fail_flags.p, 0, sizeof(int) * kMaxBatch, c->stream));
   set_smem_attr((const void*)gj_diag_kernel, (int)(kGjSmem));
   if (n_max <= kGJB) {
@@ -1193,6 +1201,7 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
       d.kb = std::max(0, std::min(kGJB, targets[i].n - k0));
       d.P = P[i]; d.ldp = 64; d.F = F[i]; d.ldf = ldf[i]; d.R = R[i]; d.ldr = 64;
       d.fail = c->fail_flags.p + i;
+      d.herm = herm ? 1 : 0;
       dj.j[i] = d;
       if (d.kb <= 0) continue;
       ++live;
@@ -1210,6 +1219,31 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
     set_smem_attr((const void*)gj_diag_kernel, (int)(kGjSmem));
     LAUNCH(c, gj_diag_kernel, dim3((unsigned)T), 1024, kGjSmem, dj);
     const int pblocks = (int)std::min<int64_t>(1024, (panel_max + 255) / 256);
+    if (herm) {
+      // F = M[:, K] (from the lower triangle), R = F^H; T = F P; M -= T R on
+      // the lower tiles; then the pivot rows / columns and -P
+      LAUNCH(c, gj_hpanel_kernel, dim3(pblocks, (unsigned)T), 256, 0, dj);
+      std::vector<GemmJob> tjobs;
+      Pack<DiagJob> fx = dj;
+      Pack<GjUpdJob> up;
+      int nu = 0, nmax = 0;
+      for (size_t i = 0; i < T; ++i) {
+        const DiagJob& d = dj.j[i];
+        fx.j[i].F = TP[i];
+        if (d.kb <= 0) continue;
+        tjobs.push_back(gjob(d.n, d.kb, d.kb, mref(F[i], ldf[i], false), mref(P[i], 64, false), TP[i], ldf[i], 1.0,
+                             0.0));
+        up.j[nu++] = GjUpdJob{targets[i].M, targets[i].ld, d.n, TP[i], ldf[i], R[i], k0, d.kb};
+        nmax = std::max(nmax, d.n);
+      }
+      gemm<GEPI_PLAIN>(c, tjobs);
+      set_smem_attr((const void*)gj_update_kernel<true>, (int)((int)kGjuSmem));
+      LAUNCH(c, gj_update_kernel<true>,
+             dim3((unsigned)((nmax + kGjuBN - 1) / kGjuBN), (unsigned)((nmax + kGjuBM - 1) / kGjuBM), (unsigned)nu), 256,
+             kGjuSmem, up);
+      LAUNCH(c, gj_hfix_kernel, dim3(pblocks, (unsigned)T), 256, 0, fx);
+      continue;
+    }
     LAUNCH(c, gj_panel_kernel, dim3(pblocks, (unsigned)T), 256, 0, dj);
     gemm<GEPI_PLAIN>(c, rjobs);
     LAUNCH(c, gj_fix_kernel, dim3((unsigned)T), 256, 0, dj);
@@ -1223,13 +1257,19 @@ void gj_invert(radmm_ctx* c, const std::vector<InvTarget>& targets, const char* 
                            reinterpret_cast<const double2*>(g.b.p), g.k0, g.kb};
         nmax = std::max(nmax, g.m);
       }
-      set_smem_attr((const void*)gj_update_kernel, (int)((int)kGjuSmem));
-      LAUNCH(c, gj_update_kernel, dim3((unsigned)((nmax + kGjuBN - 1) / kGjuBN), (unsigned)((nmax + kGjuBM - 1) / kGjuBM),
+      set_smem_attr((const void*)gj_update_kernel<false>, (int)((int)kGjuSmem));
+      LAUNCH(c, gj_update_kernel<false>, dim3((unsigned)((nmax + kGjuBN - 1) / kGjuBN), (unsigned)((nmax + kGjuBM - 1) / kGjuBM),
                                        (unsigned)ujobs.size()), 256, kGjuSmem, up);
     } else {
       gemm<GEPI_GJ>(c, ujobs);
     }
   }
+  if (herm)  // M = -inv: negate the lower triangle and mirror it
+    for (size_t i = 0; i < T; ++i) {
+      const int nt = (targets[i].n + 31) / 32;
+      LAUNCH(c, gj_hfinish_kernel, dim3((unsigned)((int64_t)nt * (nt + 1) / 2)), 256, 0, targets[i].M, targets[i].ld,
+             targets[i].n);
+    }
   // flags land after any still-unchecked deferred ones
   if (c->pending_fail + T > (size_t)kFlagCap) {
     CK(cudaStreamSynchronize(c->stream));
@@ -1789,14 +1829,18 @@ void rebuild_packed(radmm_ctx* c, const std::vector<int>& qs, double mu, double 
       cap_keep(c, S, c->gtmp[i].p, S.ld);
     }
     size_t need = 0;
-    for (const auto& t : inv) need += (64 * 64 + 2 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
+    for (const auto& t : inv) need += (64 * 64 + 3 * (size_t)round_up(t.n, 64) * 64) * sizeof(double2) + 1024;
     c->scratch.reserve(need);
-    gj_invert(c, inv, "factorize");
+    // Hermitian sweep (RADMM_GJ_HERM=0: the general sweep + projection): the
+    // capacitances are HPD and only their lower tiles are kept
+    const bool hsweep = env_int("RADMM_GJ_HERM", 1) != 0;
+    gj_invert(c, inv, "factorize", hsweep);
     for (size_t i = 0; i < nb; ++i) {
       Sensor& S = c->sensors[qs[b0 + i]];
       // Hermitian projection first (see symmetrize): the packed apply reads the
-      // diagonal tiles whole, so they must be the projected factor's
-      if (env_int("RADMM_SYMM", 1) != 0) {
+      // diagonal tiles whole, so they must be the projected factor's (the
+      // Hermitian sweep's result is exactly Hermitian already)
+      if (!hsweep && env_int("RADMM_SYMM", 1) != 0) {
         const int nt = (S.rows + 31) / 32;
         LAUNCH(c, herm_symmetrize_kernel, dim3((unsigned)((int64_t)nt * (nt + 1) / 2)), 256, 0, c->gtmp[i].p, S.ld,
                S.rows);

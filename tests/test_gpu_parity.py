@@ -174,6 +174,44 @@ def test_ozaki_chunked_gram_matches_fp64_gram(rows, cols, monkeypatch):
     assert rel(outs["1"], ref) < 1e-8, rel(outs["1"], ref)
 
 
+@pytest.mark.parametrize("rows,cols", [(1100, 3000), (576, 2000), (2048, 4096)])
+def test_hermitian_sweep_matches_general_sweep(rows, cols, monkeypatch):
+    """Packed dual factors are inverted by the Hermitian sweep (lower tiles
+    only, half the DMMA work of the general Gauss-Jordan sweep): same solves
+    as the general sweep + projection and as a dense LAPACK solve (ragged last
+    pivot block, odd tile counts)."""
+    rng = np.random.default_rng(rows)
+    a = (rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols))).astype(np.complex64).astype(np.complex128)
+    rhs = rng.normal(size=cols) + 1j * rng.normal(size=cols)
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RADMM_GJ_HERM", flag)
+        outs[flag] = api.factorize(a, 0.7, 1.3).solve(rhs)
+    cap = 1.3 * np.eye(rows) + 0.7 * a @ a.conj().T
+    ref = (rhs - 0.7 * a.conj().T @ np.linalg.solve(cap, a @ rhs)) / 1.3
+    assert rel(outs["1"], ref) < 1e-9, rel(outs["1"], ref)
+    assert rel(outs["0"], ref) < 1e-9, rel(outs["0"], ref)
+
+
+def test_hermitian_sweep_ill_conditioned(monkeypatch):
+    """The Hermitian sweep on a capacitance of condition ~3e5 (config 2's is
+    2e5): with the pivot inverses made exactly Hermitian it is as accurate as
+    the general sweep (without that it diverges: |G C - I| ~ 1e3)."""
+    rng = np.random.default_rng(77)
+    rows, cols = 1024, 3000
+    u, _, vh = np.linalg.svd(rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols)), full_matrices=False)
+    a = ((u * np.logspace(2.75, 0, rows)) @ vh).astype(np.complex64).astype(np.complex128)
+    rhs = rng.normal(size=cols) + 1j * rng.normal(size=cols)
+    cap = np.eye(rows) + a @ a.conj().T
+    ref = rhs - a.conj().T @ np.linalg.solve(cap, a @ rhs)
+    errs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RADMM_GJ_HERM", flag)
+        errs[flag] = rel(api.factorize(a, 1.0, 1.0).solve(rhs), ref)
+    print(f"cond {np.linalg.cond(cap):.2e}: Hermitian sweep {errs['1']:.2e}, general sweep {errs['0']:.2e}")
+    assert errs["1"] < 1e-8 and errs["0"] < 1e-8, errs
+
+
 def test_tall_operator_dual_solve_matches_dense():
     """A dual solve on an operator taller than 4096 rows (1024-thread forward
     tiles, as at config 3) against a dense complex128 solve."""
