@@ -1323,7 +1323,10 @@ bool ozaki_enabled() { return env_int("RADMM_OZAKI", 1) != 0; }
 // small scratch (<= 2 GB, config 2: 1.2 GB) is kept between Grams.
 void release_ozaki_scratch(radmm_ctx* c) {
   const size_t bytes = c->oz_P.n + c->oz_Q.n + c->oz_R.n * 4;
-  if (bytes <= (2ull << 30)) return;
+  if (bytes == 0) return;
+  // small scratch is kept for the next Gram -- unless the device is nearly
+  // full (config 3 on one GPU), where every GB goes back before the run
+  if (bytes <= (2ull << 30) && mem_available(c->device) > (12ull << 30)) return;
   c->oz_P.release();
   c->oz_Q.release();
   c->oz_R.release();
