@@ -445,16 +445,19 @@ def ours(args, cfg):
     W, K = args.warmup, args.steps
     main = device_measure(cfg, rank, world, local, dist, K, W, ttt=(not args.no_ttt and not cfg.fixed_iterations),
                           ttt_max_iter=args.ttt_max_iter)
-    # CPU baseline (rank 0, N = 1): the oracle on a bounded sample of this workload
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(cfg, main["lam"], budget_s=15.0)
-    # e2e through the public API with host (pinned) buffers
+    # e2e through the public API with host (pinned) buffers -- before the CPU
+    # baseline: its 16-thread complex128 sample leaves the host's memory in a
+    # state that slowed the next upload and teardown by seconds (config 3:
+    # 3.3 -> 4.8 s and 0.9 -> 3.3 s)
     e2e = None
     if not args.no_e2e:
         tol = main["ttt_hyper"] is not None
         e2e = e2e_run(cfg, main["ttt_hyper"] or main["hyper"], main["ys"], to_tolerance=tol,
                       q0=main["q0"], q1=main["q1"], dist=dist, reps=1 if cfg.name == "c3" else 3)
+    # CPU baseline (rank 0, N = 1): the oracle on a bounded sample of this workload
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg, main["lam"], budget_s=15.0)
     # config 2 alongside config 3: its own device value, time-to-tolerance and e2e
     extra = None
     if cfg.name == "c3" and not args.no_c2:
