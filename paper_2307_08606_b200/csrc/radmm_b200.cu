@@ -470,6 +470,8 @@ struct radmm_ctx {
   DArr<int> sgo_flags;               // "next round screens" flags, alternating per round
   bool pdl = false;                  // programmatic dependent launch: on inside the iteration loop (RADMM_PDL)
   bool refine = true;                // KM-space refinement of the dual solves (radmm_run_options.skip_refinement)
+  double trace_us[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // RADMM_TRACE_HOST: host time of the event stages
+  int trace_n = 0;
   int oz_eager = -1;                 // upload-time Grams on the Ozaki path (-1: not decided yet, see eager_gram)
   int64_t refine_skipped = 0;        // dual sensors whose packed C did not fit (solved unrefined)
   DArr<unsigned> screen_sync;        // screen_fused_kernel arrival ticket + changed flag (zero between launches)
@@ -1972,6 +1974,9 @@ void lazy_fold(radmm_ctx* c, const std::vector<int>& qs, double mu) {
 // more columns are formed now, two per pass of G's lower triangle.
 void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   if (qs.empty()) return;
+  auto clk = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  const auto l0 = clk();
   std::vector<int> now;
   int passes = 0;
   std::vector<EventJob> ej;
@@ -1993,6 +1998,8 @@ void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     ++c->downdates;
   }
   event_prep(c, ej);
+  const auto l1 = clk();
+  c->trace_us[3] += us(l0, l1);
   if (now.empty()) return;
   std::vector<int> dual;  // the iteration's G-apply batch (same item table)
   for (int q = 0; q < c->Q; ++q)
@@ -2013,6 +2020,7 @@ void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
   } else {
     Pack<HermJob> pk;
     const int nb_max = herm_pack(c, dual, pk);
+    c->trace_us[4] += us(l1, clk());
     for (int p = 0; p < passes; ++p) {
       for (size_t i = 0; i < dual.size(); ++i) {
         Sensor& S = c->sensors[dual[i]];
@@ -2031,7 +2039,10 @@ void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
       herm_launch(c, pk, dual.size(), nb_max, 2, nullptr);
     }
   }
+  const auto l2 = clk();
+  c->trace_us[5] += us(l1, l2);
   lazy_finish(c, now, mu);
+  c->trace_us[6] += us(l2, clk());
 }
 
 // w <- C_D^{-1} v from u = G v for every listed sensor with accumulated columns.
@@ -2707,7 +2718,12 @@ uint64_t apply_screen(radmm_ctx* c, const radmm_hyperparams* h, int k, int slot)
     rb += 8.0 * S.rows * (S.n_act + S.removed_now) + (S.primal ? 32.0 * S.n_act * S.n_act : 48.0 * S.rows * S.rows);
   }
   PhaseScope ps(c, RADMM_PHASE_REFACTOR, rb);
+  const bool trace = env_int("RADMM_TRACE_HOST", 0) != 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  const auto h0 = now();
   update_y_eff(c, changed);
+  const auto h1 = now();
   // dual sensors that stay dual keep a lagged data term (no full pass);
   // primal sensors (and the experimental fused sweeps) recompute it
   std::vector<int> exact;
@@ -2723,6 +2739,7 @@ uint64_t apply_screen(radmm_ctx* c, const radmm_hyperparams* h, int k, int slot)
   }
   event_prep(c, ej);
   data_terms(c, exact, h->mu);
+  const auto h2 = now();
   std::vector<int> rebuild, down;
   for (int q : changed) {
     Sensor& S = c->sensors[q];
@@ -2738,6 +2755,13 @@ uint64_t apply_screen(radmm_ctx* c, const radmm_hyperparams* h, int k, int slot)
   for (int q : rebuild) snapshot_base(c, c->sensors[q], true);
   full_rebuild(c, rebuild, h->mu, h->beta);
   downdate(c, down, h->mu);
+  if (trace) {
+    const auto h3 = now();
+    c->trace_us[0] += us(h0, h1);
+    c->trace_us[1] += us(h1, h2);
+    c->trace_us[2] += us(h2, h3);
+    ++c->trace_n;
+  }
   return notice;
 }
 
@@ -3469,9 +3493,19 @@ void do_run(radmm_ctx* c, const radmm_hyperparams* h, const radmm_run_options* o
     staged_trigger = f.trigger != 0;
   }
   if (fixed) sm.converged = f.converged;
-  if (trace_host && host_n)
+  if (trace_host && host_n) {
     std::fprintf(stderr, "[radmm host] %d re-issued rounds: events %.1f us, issue %.1f us per round\n", host_n,
                  host_ev_us / host_n, host_issue_us / host_n);
+    if (c->trace_n)
+      std::fprintf(stderr,
+                   "[radmm host] %d events: frozen echo %.1f us, bookkeeping launch %.1f us, downdates %.1f us "
+                   "(lazy append: prep %.1f, item table %.1f, column passes %.1f, border %.1f)\n",
+                   c->trace_n, c->trace_us[0] / c->trace_n, c->trace_us[1] / c->trace_n, c->trace_us[2] / c->trace_n,
+                   c->trace_us[3] / c->trace_n, c->trace_us[4] / c->trace_n, c->trace_us[5] / c->trace_n,
+                   c->trace_us[6] / c->trace_n);
+    for (double& t : c->trace_us) t = 0;
+    c->trace_n = 0;
+  }
   CK(cudaEventRecord(STEP(sm.iterations), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   check_deferred(c);
