@@ -552,6 +552,8 @@ def e2e_run(cfg, hyper, ys, to_tolerance=True, q0=0, q1=None, dist=None, reps=3)
     ys_all = [ys[q - q0] if q0 <= q < q1 else np.zeros(cfg.KM, dtype=np.complex128) for q in range(cfg.Q)]
     prob = api.Problem(ops, ys_all)
     try:
+        if reps > 1:  # one untimed call first (first-use kernel loading, first touch of the pinned pages)
+            _e2e_once(api, D, torch, prob, hyper, ys, ops, to_tolerance, q0, q1, dist, world)
         runs = [_e2e_once(api, D, torch, prob, hyper, ys, ops, to_tolerance, q0, q1, dist, world) for _ in range(reps)]
     finally:
         del prob, ops
@@ -561,7 +563,8 @@ def e2e_run(cfg, hyper, ys, to_tolerance=True, q0=0, q1=None, dist=None, reps=3)
     runs.sort(key=lambda r: r["ms"])
     med = dict(runs[len(runs) // 2])
     med["host_buffers"] = pinned_kind
-    med["repeats"] = {"n": reps, "statistic": "median of independent api.run calls (each a fresh context)",
+    med["repeats"] = {"n": reps, "statistic": "median of independent api.run calls (each a fresh context)"
+                                   + ("; one untimed call first" if reps > 1 else ""),
                       "values": sorted(r["value"] for r in runs)}
     return med
 
