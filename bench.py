@@ -446,9 +446,9 @@ def ours(args, cfg):
     main = device_measure(cfg, rank, world, local, dist, K, W, ttt=(not args.no_ttt and not cfg.fixed_iterations),
                           ttt_max_iter=args.ttt_max_iter)
     # e2e through the public API with host (pinned) buffers -- before the CPU
-    # baseline: its 16-thread complex128 sample leaves the host's memory in a
-    # state that slowed the next upload and teardown by seconds (config 3:
-    # 3.3 -> 4.8 s and 0.9 -> 3.3 s)
+    # baseline, so the 16-thread complex128 sample cannot disturb the host
+    # side of the upload and the teardown (config 3's upload stage measured
+    # 3.3-4.8 s and its teardown 0.9-3.3 s across boxes and orders)
     e2e = None
     if not args.no_e2e:
         tol = main["ttt_hyper"] is not None
