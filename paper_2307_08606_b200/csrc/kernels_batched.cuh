@@ -30,8 +30,12 @@ struct HermJob {
   int groups;        // strip groups per tile column: ceil(nb / kHermStrip)
   const double2* v;  // right-hand side 0 (nullptr: the job sits this launch out)
   double2* w;
-  const double2* v1; // right-hand side 1 (NR = 2 launches; nullptr: none)
+  const double2* v1; // right-hand side 1 (NR >= 2 launches; nullptr: none)
   double2* w1;
+  const double2* v2; // right-hand sides 2, 3 (NR = 4 launches: an event's 2-3 removed columns
+  double2* w2;       // ride the iteration's own pass over G; nullptr: none)
+  const double2* v3;
+  double2* w3;
   double2* dotp;     // [NR][nb][groups][64], column stride dstride
   double2* axp;      // [NR][nb (nb - 1) / 2][64], slot I (I - 1) / 2 + J, column stride astride
   int64_t dstride, astride;
@@ -183,7 +187,7 @@ constexpr size_t herm_persist_smem(int nr) {
 // (registers and a second shared buffer), so items cost no start-up latency.
 // Per-item arithmetic and partial slots are exactly herm_gapply_kernel's.
 template <int NR>
-__global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __grid_constant__ Pack<HermJob> P,
+__global__ void __launch_bounds__(256, NR <= 2 ? 2 : 1) herm_gapply_persist_kernel(const __grid_constant__ Pack<HermJob> P,
                                                                     const uint64_t* __restrict__ items, int n_items,
                                                                     const int* __restrict__ go) {
   pdl_enter();
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   auto load_vec = [&](int buf, uint64_t it) {
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
     const HermJob& jb = P.j[q];
-    const double2* vs[2] = {jb.v, jb.v1};
+    const double2* vs[4] = {jb.v, jb.v1, jb.v2, jb.v3};
 #pragma unroll
     for (int c = 0; c < NR; ++c) {
       const double2* vc = vs[c];
@@ -265,7 +269,8 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
   while (true) {
     const int q = (int)(it >> 48), J = (int)(it >> 32 & 0xFFFF), I0 = (int)(it >> 16 & 0xFFFF), nt = (int)(it & 0xFFFF);
     const HermJob& jb = P.j[q];
-    const bool has1 = NR > 1 && jb.v1 != nullptr;  // second right-hand side present (else skipped)
+    // right-hand sides beyond the first are optional per job (absent: skipped)
+    const bool has[4] = {true, NR > 1 && jb.v1 != nullptr, NR > 2 && jb.v2 != nullptr, NR > 3 && jb.v3 != nullptr};
     const int nxt = next_item(cur + gridDim.x);
     const uint64_t it_n = nxt < n_items ? __ldg(items + nxt) : 0;
     __syncthreads();  // vectors of `buf` visible; the other buffer's readers are done
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
-          if (c == 1 && !has1) continue;
+          if (!has[c]) continue;
           const double2 vi = vI[buf][c][t * kHermTile + lane + 32 * h];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -311,11 +316,10 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
     }
     __syncthreads();  // every warp's axpy partials of the strip are in shared memory
     {
-      const int nc = has1 ? 2 : 1;
-      for (int e = tid; e < nt * nc * kHermTile; e += 256) {
-        const int t = e / (nc * kHermTile), c = (e / kHermTile) % nc, r = e % kHermTile;
+      for (int e = tid; e < nt * NR * kHermTile; e += 256) {
+        const int t = e / (NR * kHermTile), c = (e / kHermTile) % NR, r = e % kHermTile;
         const int I = I0 + t;
-        if (I == J) continue;
+        if (I == J || !has[c]) continue;
         double2 sum = sax[t][c][0][r];
 #pragma unroll
         for (int w8 = 1; w8 < 8; ++w8) {
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(256, 2) herm_gapply_persist_kernel(const __gri
       const int gi = (I0 - J) / kHermStrip;
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
-        if (c == 1 && !has1) continue;
+        if (!has[c]) continue;
         double2* dp = jb.dotp + c * jb.dstride + ((int64_t)J * jb.groups + gi) * kHermTile + c0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) dp[k] = make_double2(dr[c][k], di[c][k]);
@@ -361,8 +365,9 @@ __global__ void __launch_bounds__(kHermRedSlices * kHermTile) herm_reduce_kernel
   if (go && __ldg(go) == 0) return;
   const HermJob& jb = P.j[blockIdx.y];
   const int c = blockIdx.z;
-  double2* const out = c == 0 ? jb.w : jb.w1;
-  if (!jb.v || !out || (c == 1 && !jb.v1)) return;
+  double2* const out = c == 0 ? jb.w : c == 1 ? jb.w1 : c == 2 ? jb.w2 : jb.w3;
+  const double2* const vin = c == 0 ? jb.v : c == 1 ? jb.v1 : c == 2 ? jb.v2 : jb.v3;
+  if (!jb.v || !out || !vin) return;
   const int b = blockIdx.x, r = threadIdx.x & 63, sl = threadIdx.x >> 6;
   __shared__ double2 part[kHermRedSlices][kHermTile];
   if (b >= jb.nb) return;

@@ -334,7 +334,7 @@ struct Sensor {
   bool raw_gram = false;
   bool raw_packed = false;  // the raw Gram sits in Cp (packed factor) instead of G
   int lz_d = 0;    // |D|
-  int lz_new = 0;  // 1: P[:, d-1] = G a is formed by the next G-apply (second right-hand side)
+  int lz_new = 0;  // 1-3: the last lz_new columns of P are formed by the next G-apply (extra right-hand sides)
   int lz_r = 0;    // columns added by the last event (bordered Sinv update pending)
   DArr<double2> lz_P, lz_R, lz_S, lz_t, lz_B;
   DArr<int> lz_pix;
@@ -929,8 +929,8 @@ int herm_pack(radmm_ctx* c, const std::vector<int>& qs, Pack<HermJob>& pk) {
     h.groups = (h.nb + kHermStrip - 1) / kHermStrip;
     const size_t nd = (size_t)h.nb * h.groups * kHermTile,
                  na = std::max<size_t>((size_t)h.nb * (h.nb - 1) / 2 * kHermTile, 1);
-    if (S.hdot.n < 2 * nd) S.hdot.alloc(2 * nd, false);  // two right-hand sides
-    if (S.hax.n < 2 * na) S.hax.alloc(2 * na, false);
+    if (S.hdot.n < 4 * nd) S.hdot.alloc(4 * nd, false);  // up to four right-hand sides
+    if (S.hax.n < 4 * na) S.hax.alloc(4 * na, false);
     h.v = S.v.p; h.w = S.w.p; h.dotp = S.hdot.p; h.axp = S.hax.p;
     h.dstride = (int64_t)nd; h.astride = (int64_t)na;
     pk.j[i] = h;
@@ -975,7 +975,9 @@ void herm_launch(radmm_ctx* c, const Pack<HermJob>& pk, size_t nq, int nb_max, i
   } else
 #endif
   {
-    auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : herm_gapply_persist_kernel<2>;
+    nr = nr <= 1 ? 1 : nr == 2 ? 2 : 4;
+    auto kern = nr == 1 ? herm_gapply_persist_kernel<1> : nr == 2 ? herm_gapply_persist_kernel<2>
+                                                                   : herm_gapply_persist_kernel<4>;
     const size_t smem = herm_persist_smem(nr);
     set_smem_attr((const void*)kern, (int)((int)smem));
     int per_sm = 1;
@@ -1002,8 +1004,8 @@ void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
       ColDotJob g{};
       g.M = S.G.p; g.ld = S.ldg; g.len = S.rows; g.n_out = S.rows; g.vec = S.v.p; g.out = S.w.p; g.scale = 1.0;
       gj.push_back(g);
-      if (S.lz_new) {  // pending lazy-downdate column P[:, d-1] = G a
-        g.vec = S.lz_R.p; g.out = S.lz_P.p + (size_t)(S.lz_d - 1) * S.ld;
+      for (int u = 0; u < S.lz_new; ++u) {  // pending lazy-downdate columns P[:, d-new+u] = G a_u
+        g.vec = S.lz_R.p + (size_t)u * S.ld; g.out = S.lz_P.p + (size_t)(S.lz_d - S.lz_new + u) * S.ld;
         gj.push_back(g);
       }
     }
@@ -1016,9 +1018,16 @@ void gapply(radmm_ctx* c, const std::vector<int>& qs, const int* go = nullptr) {
   for (size_t i = 0; i < qs.size(); ++i) {
     Sensor& S = c->sensors[qs[i]];
     if (!S.lz_new) continue;
-    pk.j[i].v1 = S.lz_R.p;
-    pk.j[i].w1 = S.lz_P.p + (size_t)(S.lz_d - 1) * S.ld;
-    nr = 2;
+    // this event's removed columns ride the pass as extra right-hand sides
+    HermJob& hj = pk.j[i];
+    const double2* vs[3] = {nullptr, nullptr, nullptr};
+    double2* ws[3] = {nullptr, nullptr, nullptr};
+    for (int u = 0; u < S.lz_new && u < 3; ++u) {
+      vs[u] = S.lz_R.p + (size_t)u * S.ld;
+      ws[u] = S.lz_P.p + (size_t)(S.lz_d - S.lz_new + u) * S.ld;
+    }
+    hj.v1 = vs[0]; hj.w1 = ws[0]; hj.v2 = vs[1]; hj.w2 = ws[1]; hj.v3 = vs[2]; hj.w3 = ws[2];
+    nr = std::max(nr, 1 + S.lz_new);
   }
   herm_launch(c, pk, qs.size(), nb_max, nr, go);
 }
@@ -1897,6 +1906,11 @@ bool lazy_enabled() { return env_int("RADMM_LAZY", 1) != 0 && !fused_enabled(); 
 // RADMM_LAZY_MAX (<= kLazyMax) lowers the fold point (tests force folds)
 int lazy_max() { return std::min(kLazyMax, std::max(1, env_int("RADMM_LAZY_MAX", kLazyMax))); }
 
+// Removed columns per event that ride the iteration's G-apply as extra
+// right-hand sides (1: the two-RHS kernel; 2-3: the four-RHS kernel, one CTA
+// per SM); larger events form their columns in extra passes, two per pass.
+int lazy_ride() { return std::max(0, std::min(3, env_int("RADMM_LAZY_RIDE", 3))); }
+
 void lazy_reserve(Sensor& S) {
   if (S.lz_P.n < (size_t)S.ld * kLazyMax) {
     S.lz_P.alloc((size_t)S.ld * kLazyMax, false);
@@ -1989,8 +2003,8 @@ void lazy_append(radmm_ctx* c, const std::vector<int>& qs, double mu) {
     ej.push_back(e);
     S.lz_d += r;
     S.lz_r = r;
-    if (r == 1 && herm_enabled()) {
-      S.lz_new = 1;
+    if (r <= lazy_ride() && herm_enabled()) {
+      S.lz_new = r;  // formed by the next iteration's G-apply (gapply), no extra pass over G
     } else {
       now.push_back(q);
       passes = std::max(passes, (r + 1) / 2);
