@@ -437,6 +437,8 @@ struct LazyJob {
   unsigned* cnt;        // arrival counter of the job's dot blocks (zero between launches)
   int ident;            // refinement residual: s = mu t (no Sinv), then dst += A_D s
   double2* dst;         //   (lazy_resid_axpy_kernel; w is only read)
+  double2* sum_into;    // correction pass: sum_into += w + mu P s instead of w += mu P s (w untouched);
+                        //   folds the refinement's final w = w1 + dw into the lazy term of dw
 };
 
 // s = mu Sinv t for one job by one block: four threads per row of Sinv,
@@ -545,7 +547,127 @@ __global__ void __launch_bounds__(256) lazy_axpy_kernel(const __grid_constant__ 
     im = fma(p.y, x.x, im);
   }
   const double2 u = jb.w[i];
-  jb.w[i] = make_double2(u.x + re, u.y + im);
+  if (jb.sum_into) {
+    const double2 a = jb.sum_into[i];
+    jb.sum_into[i] = make_double2(a.x + (u.x + re), a.y + (u.y + im));
+  } else {
+    jb.w[i] = make_double2(u.x + re, u.y + im);
+  }
+}
+
+// The lazy term in ONE launch for short operators (up to kLazyFusedRows rows,
+// where the two launches are pure latency: config 1 98 -> 88 us per iteration): a
+// cluster of kLazyCluster CTAs per sensor.  Each warp dots one eliminated
+// column with the vector (t = A_D^H u), the CTAs read each other's dots
+// through distributed shared memory, every CTA forms s = mu Sinv t (or mu t)
+// for itself, and then applies its share of the rows (w += P s, or
+// dst += A_D s for the refinement residual).  Replaces lazy_dot_kernel +
+// lazy_axpy_kernel / lazy_resid_axpy_kernel: one dependent launch instead of
+// two in every post-trigger iteration (three lazy terms per refined solve).
+constexpr int kLazyCluster = 8;
+constexpr int kLazyFusedRows = 1024;  // above this the dots want more than 8 CTAs per sensor (C2 geometry: 2 launches are faster)
+
+__device__ __forceinline__ double2 dsmem_ld_double2(const double2* p, unsigned cta) {
+  uint32_t ra;
+  double2 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+  return v;
+}
+
+__global__ void __cluster_dims__(kLazyCluster, 1, 1) __launch_bounds__(256)
+    lazy_fused_kernel(const __grid_constant__ Pack<LazyJob> P, double mu, const int* __restrict__ go) {
+  pdl_enter();
+  if (go && __ldg(go) == 0) return;  // cancelled speculative iteration (the whole cluster)
+  const LazyJob& jb = P.j[blockIdx.y];
+  const int d = jb.d;
+  if (d <= 0) return;
+  const unsigned rank = cluster_ctarank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ __align__(16) double2 t_loc[8];  // dots of columns rank * 8 + warp
+  __shared__ double2 t_all[kLazyMax];
+  __shared__ double2 sv[kLazyMax];
+  __shared__ int px[kLazyMax];
+  {
+    const int j = (int)rank * 8 + warp;
+    double re = 0.0, im = 0.0;
+    if (j < d) {
+      const float2* a = jb.A + (int64_t)jb.pix[j] * jb.ld;
+#pragma unroll 4
+      for (int i = lane; i < jb.rows; i += 32) {
+        const float2 x = a[i];
+        const double2 u = jb.w[i];
+        // conj(a) * u
+        re = fma((double)x.x, u.x, re);
+        re = fma((double)x.y, u.y, re);
+        im = fma((double)x.x, u.y, im);
+        im = fma(-(double)x.y, u.x, im);
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+    }
+    if (lane == 0) t_loc[warp] = make_double2(re, im);
+  }
+  cluster_sync_acqrel();  // every CTA's dots are written
+  if ((int)threadIdx.x < d) {
+    t_all[threadIdx.x] = dsmem_ld_double2(&t_loc[threadIdx.x & 7], threadIdx.x >> 3);
+    px[threadIdx.x] = jb.pix[threadIdx.x];
+  }
+  __syncthreads();
+  cluster_sync_acqrel();  // no CTA leaves while its dots may still be read
+  if (jb.ident) {
+    if ((int)threadIdx.x < d) sv[threadIdx.x] = make_double2(mu * t_all[threadIdx.x].x, mu * t_all[threadIdx.x].y);
+  } else {
+    lazy_s(jb, mu, t_all, sv);
+  }
+  __syncthreads();
+  // this CTA's rows
+  const int per = ((jb.rows + kLazyCluster - 1) / kLazyCluster + 31) & ~31;
+  const int i_end = min(jb.rows, ((int)rank + 1) * per);
+  for (int i = (int)rank * per + threadIdx.x; i < i_end; i += 256) {
+    double re = 0.0, im = 0.0;
+    if (jb.ident) {
+      for (int k = 0; k < d; ++k) {
+        const float2 a = jb.A[i + (int64_t)px[k] * jb.ld];
+        const double2 x = sv[k];
+        re = fma((double)a.x, x.x, re);
+        re = fma(-(double)a.y, x.y, re);
+        im = fma((double)a.x, x.y, im);
+        im = fma((double)a.y, x.x, im);
+      }
+      const double2 u = jb.dst[i];
+      jb.dst[i] = make_double2(u.x + re, u.y + im);
+    } else {
+      int k = 0;
+      for (; k + 8 <= d; k += 8) {  // eight independent loads in flight, summed in order
+        double2 p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = jb.P[i + (int64_t)(k + u) * jb.ld];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 x = sv[k + u];
+          re = fma(p[u].x, x.x, re);
+          re = fma(-p[u].y, x.y, re);
+          im = fma(p[u].x, x.y, im);
+          im = fma(p[u].y, x.x, im);
+        }
+      }
+      for (; k < d; ++k) {
+        const double2 p = jb.P[i + (int64_t)k * jb.ld], x = sv[k];
+        re = fma(p.x, x.x, re);
+        re = fma(-p.y, x.y, re);
+        im = fma(p.x, x.y, im);
+        im = fma(p.y, x.x, im);
+      }
+      const double2 u = jb.w[i];
+      if (jb.sum_into) {
+        const double2 a = jb.sum_into[i];
+        jb.sum_into[i] = make_double2(a.x + (u.x + re), a.y + (u.y + im));
+      } else {
+        jb.w[i] = make_double2(u.x + re, u.y + im);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

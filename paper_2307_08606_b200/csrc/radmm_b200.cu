@@ -1562,6 +1562,8 @@ void packed_update(radmm_ctx* c, const std::vector<PackedUpdJob>& jobs, double a
 }
 
 void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* go, bool on_dw = false);
+// The lazy terms in one cluster launch (RADMM_LAZY_FUSED=0: dot + axpy launches).
+bool lazy_fused(int rows_max) { return rows_max <= kLazyFusedRows && env_int("RADMM_LAZY_FUSED", 1) != 0; }
 
 // rho += mu A_D (A_D^H w) for sensors with accumulated lazy columns: the
 // residual against C_D = C - mu A_D A_D^H, the capacitance the lazy inverse
@@ -1583,6 +1585,10 @@ void lazy_resid(radmm_ctx* c, const std::vector<int>& qs, double mu, const int* 
     rmax = std::max(rmax, S.rows);
   }
   if (!nb) return;
+  if (lazy_fused(rmax)) {  // one cluster launch per batch (kernels_batched.cuh)
+    LAUNCH(c, lazy_fused_kernel, dim3(kLazyCluster, (unsigned)nb), 256, 0, pk, mu, go);
+    return;
+  }
   LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
   LAUNCH(c, lazy_resid_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, go);
 }
@@ -1672,6 +1678,7 @@ void refine(radmm_ctx* c, const std::vector<int>& gq, double mu, const int* go) 
     for (int q : part) {
       Sensor& S = c->sensors[q];
       if (herm && S.lz_d == 0) continue;  // already folded into the reduce
+      if (S.lz_d > 0) continue;           // folded into the lazy term (lazy_correct, sum_into)
       va.j[nva++] = VaddJob{S.w.p, S.dw.p, S.rows};
     }
     if (nva) LAUNCH(c, vadd_kernel, dim3((unsigned)((rows_max + 255) / 256), (unsigned)nva), 256, 0, va, go);
@@ -2069,6 +2076,8 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
     if (nb >= kMaxBatch) fail(RADMM_INVALID_ARGUMENT, "too many sensors in one lazy-downdate batch");
     pk.j[nb] = LazyJob{S.A.p, S.ld, S.rows, S.lz_pix.p, S.lz_d, S.lz_P.p, S.lz_S.p, kLazyMax,
                        on_dw ? S.dw.p : S.w.p, S.lz_t.p, c->lazy_cnt.p + nb};
+    // the refinement's correction: w += dw + lazy term in the same kernel (no separate w += dw)
+    if (on_dw) pk.j[nb].sum_into = S.w.p;
     ++nb;
     dmax = std::max(dmax, S.lz_d);
     rmax = std::max(rmax, S.rows);
@@ -2076,6 +2085,10 @@ void lazy_correct(radmm_ctx* c, const std::vector<int>& qs, double mu, const int
   if (!nb) return;
   if (c->lazy_cnt.n < (size_t)kMaxBatch) c->lazy_cnt.alloc(kMaxBatch);  // zeroed; the last blocks re-zero
   for (int i = 0; i < nb; ++i) pk.j[i].cnt = c->lazy_cnt.p + i;
+  if (lazy_fused(rmax)) {
+    LAUNCH(c, lazy_fused_kernel, dim3(kLazyCluster, (unsigned)nb), 256, 0, pk, mu, go);
+    return;
+  }
   LAUNCH(c, lazy_dot_kernel, dim3((unsigned)dmax, (unsigned)nb), 256, 0, pk, mu, go);
   LAUNCH(c, lazy_axpy_kernel, dim3((unsigned)((rmax + 255) / 256), (unsigned)nb), 256, 0, pk, mu, go);
 }
