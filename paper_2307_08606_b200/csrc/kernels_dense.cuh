@@ -635,7 +635,7 @@ __global__ void gemm_split_reduce(const __grid_constant__ Pack<GemmJob> jobs, in
 // if a pivot is not a positive finite real (the Cholesky-failure analogue of
 // solver_core.hpp:42-43).
 struct DiagJob {
-  const double2* M;
+  double2* M;      // the matrix being swept (read by the pivot / panel kernels, rewritten by gj_hfix_kernel)
   int64_t ld;
   int n;          // matrix order
   int k0, kb;     // pivot block
@@ -785,13 +785,13 @@ __global__ void gj_hfix_kernel(const __grid_constant__ Pack<DiagJob> jobs) {
     } else {
       v = jb.F[i + (int64_t)c * jb.ldf];
     }
-    const_cast<double2*>(jb.M)[i + (int64_t)(k0 + c) * jb.ld] = v;
+    jb.M[i + (int64_t)(k0 + c) * jb.ld] = v;
   }
   const int64_t up = (int64_t)k0 * kb;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < up; e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e % kb), i = (int)(e / kb);
     const double2 v = jb.F[i + (int64_t)c * jb.ldf];
-    const_cast<double2*>(jb.M)[(k0 + c) + (int64_t)i * jb.ld] = make_double2(v.x, -v.y);
+    jb.M[(k0 + c) + (int64_t)i * jb.ld] = make_double2(v.x, -v.y);
   }
 }
 
