@@ -269,6 +269,15 @@ typedef struct {
 int radmm_host_alloc(size_t bytes, void** out);
 int radmm_host_free(void* p);
 
+/* radmm_ctx_destroy returns once the context's device memory is back in the
+ * library's stream-ordered pool (the next context reuses it at once); the pool
+ * gives everything above RADMM_POOL_KEEP_GB back to the driver from a
+ * background thread (config 3: 172 GB, seconds of driver work).  This call
+ * waits for that thread and trims synchronously -- for callers that want the
+ * memory available to other allocators right away.  Not part of the reference
+ * API (the reference's host memory is freed by its destructors). */
+int radmm_pool_trim(int device);
+
 int radmm_set_profiling(radmm_ctx* ctx, int enabled);
 /* out[RADMM_PHASE_COUNT], accumulated over the last run. */
 int radmm_get_phase_stats(radmm_ctx* ctx, radmm_phase_stat* out);

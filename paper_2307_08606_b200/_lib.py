@@ -130,6 +130,7 @@ SIGNATURES = {
     "radmm_back_projection": (C.c_int, [_VP, _DP]),
     "radmm_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_VP)]),
     "radmm_host_free": (C.c_int, [_VP]),
+    "radmm_pool_trim": (C.c_int, [C.c_int]),
     "radmm_set_profiling": (C.c_int, [_VP, C.c_int]),
     "radmm_get_phase_stats": (C.c_int, [_VP, C.POINTER(PhaseStat)]),
     "radmm_get_iteration_stats": (C.c_int, [_VP, _DP, C.POINTER(C.c_int64), C.c_int]),

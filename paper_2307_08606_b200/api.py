@@ -502,6 +502,13 @@ def set_tuning(name: str, value: int | None) -> None:
     _lib.check(_lib.lib().radmm_set_tuning(name.encode(), int(value or 0), int(value is None)))
 
 
+def pool_trim(device: int = 0) -> None:
+    """Give the device memory of closed solvers back to the driver now
+    (radmm_pool_trim): ``Solver.close()`` returns as soon as the memory is back
+    in the library's pool and lets a background thread do this."""
+    _lib.check(_lib.lib().radmm_pool_trim(int(device)))
+
+
 class PinnedBuffer:
     """Page-locked host memory (radmm_host_alloc) viewed as a NumPy array --
     where callers stage large operators so uploads run at full host-link

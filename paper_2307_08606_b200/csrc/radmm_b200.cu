@@ -623,11 +623,53 @@ void set_device(radmm_ctx* c) { CK(cudaSetDevice(c->device)); }
 
 // Keep up to RADMM_POOL_KEEP_GB (default 16) of freed device memory reserved
 // in the device's default pool between contexts (0: release at every sync).
+// Returning a context's memory to the driver is slow and erratic (config 3:
+// 172 GB, measured 0.9-5.4 s inside radmm_ctx_destroy when the pool trimmed at
+// every synchronisation of the teardown).  So the pool never trims by itself
+// (release threshold = max): a destroyed context's blocks go back to the pool
+// at once -- the next context reuses them without driver calls -- and the
+// pool is trimmed down to RADMM_POOL_KEEP_GB by one background thread per
+// teardown, off the caller's critical path.  The thread is joined before the
+// next context is created (memory estimates must not race it), by
+// radmm_pool_trim() and at process exit.  RADMM_POOL_ASYNC_TRIM=0 restores the
+// synchronous behaviour (threshold = RADMM_POOL_KEEP_GB, trimming inside the
+// teardown's synchronisations).
+struct PoolReaper {
+  std::mutex mu;
+  std::thread th;
+};
+PoolReaper& pool_reaper() {
+  static PoolReaper* r = new PoolReaper;  // never destroyed: joined by the atexit hook instead
+  return *r;
+}
+void pool_reaper_join() {
+  PoolReaper& r = pool_reaper();
+  std::lock_guard<std::mutex> lk(r.mu);
+  if (r.th.joinable()) r.th.join();
+}
+uint64_t pool_keep_bytes() { return (uint64_t)std::max(0, env_int("RADMM_POOL_KEEP_GB", 16)) << 30; }
+bool pool_async_trim() { return env_int("RADMM_POOL_ASYNC_TRIM", 1) != 0; }
+
 void configure_pool(int device) {
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t keep = (uint64_t)std::max(0, env_int("RADMM_POOL_KEEP_GB", 16)) << 30;
+  uint64_t keep = pool_async_trim() ? ~0ull : pool_keep_bytes();
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+}
+
+void pool_trim_async(int device) {
+  if (!pool_async_trim()) return;
+  pool_reaper_join();
+  static std::once_flag once;
+  std::call_once(once, [] { std::atexit([] { pool_reaper_join(); }); });
+  const size_t keep = (size_t)pool_keep_bytes();
+  PoolReaper& r = pool_reaper();
+  std::lock_guard<std::mutex> lk(r.mu);
+  r.th = std::thread([device, keep] {
+    cudaMemPool_t pool;
+    if (cudaSetDevice(device) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, keep);
+  });
 }
 
 // Bytes an allocation can still get: free device memory plus what the
@@ -650,6 +692,7 @@ int occupancy(const void* func, int threads, size_t smem);
 void set_smem_attr(const void* func, int bytes);
 
 void init_ctx(radmm_ctx* c, int device, int n_pixels, int q_local) {
+  pool_reaper_join();  // a previous context's memory is back with the driver (or kept by the pool)
   c->device = device;
   CK(cudaSetDevice(device));
   configure_pool(device);
@@ -4039,7 +4082,20 @@ int radmm_ctx_destroy(radmm_ctx* ctx) {
                    ms(t1, t2), ms(t2, t3), ms(t3, t4));
       return;
     }
+    const int device = ctx ? ctx->device : -1;
     delete ctx;
+    if (device >= 0) pool_trim_async(device);
+  });
+}
+
+int radmm_pool_trim(int device) {
+  return guarded([&] {
+    pool_reaper_join();
+    cudaMemPool_t pool;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemPoolTrimTo(pool, (size_t)pool_keep_bytes()));
   });
 }
 
@@ -4442,7 +4498,11 @@ int radmm_solve_local(radmm_solve_cache* sc, const double* rhs, double* x) {
 }
 
 int radmm_solve_cache_destroy(radmm_solve_cache* sc) {
-  return guarded([&] { delete sc; });
+  return guarded([&] {
+    const int device = sc && sc->ctx ? sc->ctx->device : -1;
+    delete sc;
+    if (device >= 0) pool_trim_async(device);
+  });
 }
 
 int radmm_soft_threshold(int device, const double* v, int64_t n, double kappa, double* out) {

@@ -1028,3 +1028,25 @@ def test_sharded_observer_run_sees_every_iteration(monkeypatch):
     assert any(sz != seen_plain[0] for sz in seen_plain)  # eliminations happened
     assert [r.bytes_sent for r in rs.report.iterations] == [r.bytes_sent for r in rp.report.iterations]
     assert np.array_equal(rs.sigma, rp.sigma)
+
+
+def test_pool_trim_returns_memory_after_close():
+    """Solver.close() hands the device memory back to the library's pool and a
+    background thread returns it to the driver; api.pool_trim() waits for that
+    and trims synchronously, after which the driver sees the memory free."""
+    import torch
+    rng = np.random.default_rng(5)
+    n, rows, q = 4096, 1024, 24  # ~0.8 GB of operators
+    s = api.Solver(n, q)
+    a = (rng.normal(size=(rows, n)) + 1j * rng.normal(size=(rows, n))).astype(np.complex64)
+    for i in range(q):
+        s.set_operator(i, a)
+    used_free, _ = torch.cuda.mem_get_info()
+    s.close()
+    api.set_tuning("RADMM_POOL_KEEP_GB", 0)
+    try:
+        api.pool_trim(0)
+        free_after, _ = torch.cuda.mem_get_info()
+    finally:
+        api.set_tuning("RADMM_POOL_KEEP_GB", None)
+    assert free_after - used_free > 0.5 * q * a.nbytes, (used_free, free_after)

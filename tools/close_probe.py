@@ -1,5 +1,5 @@
 import time, sys, os, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
 from paper_2307_08606_b200 import api, scenario
