@@ -506,7 +506,10 @@ def _small_c1(**kw):
 
 DOWNDATE_VARIANTS = {
     "lazy": {},                        # default: columns accumulate in P = G A_D, folded at 64
-    "lazy_herm": {"RADMM_HERM_MIN_ROWS": "0"},  # single columns ride the triangle G-apply (NR = 2)
+    "lazy_herm": {"RADMM_HERM_MIN_ROWS": "0"},  # up to 3 columns ride the triangle G-apply (NR = 2 / 4)
+    "lazy_herm_ride1": {"RADMM_HERM_MIN_ROWS": "0", "RADMM_LAZY_RIDE": "1"},  # one rides, more in extra passes
+    "lazy_herm_no_ride": {"RADMM_HERM_MIN_ROWS": "0", "RADMM_LAZY_RIDE": "0"},  # every column in extra passes
+    "lazy_two_launch": {"RADMM_LAZY_FUSED": "0"},  # lazy terms as dot + axpy launches (not the cluster kernel)
     "lazy_folds": {"RADMM_LAZY_MAX": "3", "RADMM_HERM_MIN_ROWS": "0"},  # fold into G every few events
     "lazy_full_gapply": {"RADMM_HERM": "0"},  # every column through the column-dot G-apply
     "eager": {"RADMM_LAZY": "0"},      # G rewritten at every event
