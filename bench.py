@@ -322,7 +322,8 @@ def _cpu_compiled_iterations(cfg, sensors, ops64, fusion, budget_s, extrapolate_
         lu.build()
         ops64 = [np.asfortranarray(a, dtype=np.complex64) for a in ops64]
         out = {}
-        for key, nthreads in (("value_c_openmp", lu.threads()), ("value_c_openmp_1thread", 1)):
+        nmax = lu.threads()  # before any set_threads: omp_get_max_threads follows the last setting
+        for key, nthreads in (("value_c_openmp", nmax), ("value_c_openmp_1thread", 1)):
             lu.set_threads(nthreads)
             t = []
             while not t or (sum(t) < budget_s / 2 and len(t) < 50):
@@ -336,7 +337,7 @@ def _cpu_compiled_iterations(cfg, sensors, ops64, fusion, budget_s, extrapolate_
                 t.append(time.perf_counter() - t0)
             per = float(np.median(t))
             out[key] = 1.0 / (per if extrapolate_q is None else extrapolate_q * per + fusion_s)
-        lu.set_threads(lu.threads())
+        lu.set_threads(nmax)
         out["sample_c_openmp"] = ("the same iteration with each local update's two operator passes and its Cholesky "
                                   "solve compiled (oracle/local_update.c: gcc -O3, OpenMP over columns, complex64 "
                                   "operator streamed as stored, fp64 accumulation, column-oriented triangular sweeps)"
